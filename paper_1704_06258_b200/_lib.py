@@ -1,0 +1,333 @@
+"""ctypes binding of libhubgpu.so (include/hubgpu.h).
+
+The library is built in-tree (``make -C paper_1704_06258_b200/csrc``) and is
+the ONLY compute path of this package: there is no CPU fallback.  Loading it
+needs no GPU; every compute entry point raises ``RuntimeError`` when no CUDA
+device is visible.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+import weakref
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libhubgpu.so"
+
+HG_OK, HG_EARG, HG_ECUDA, HG_ENODEV, HG_ESTATE = 0, 1, 2, 3, 4
+HG_HOST, HG_DEVICE = 0, 1
+FLAG_SYMMETRIC, FLAG_WEIGHTS_EXACT = 1, 2
+
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+_u64p = C.POINTER(C.c_uint64)
+_u8p = C.POINTER(C.c_uint8)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+class GaParamsC(C.Structure):
+    _fields_ = [("islands_total", C.c_int32), ("island_lo", C.c_int32),
+                ("island_hi", C.c_int32), ("pop_size", C.c_int32),
+                ("strength", C.c_int32), ("strict_paper", C.c_int32),
+                ("seed", C.c_uint64)]
+
+
+# name -> (restype, argtypes); the exported surface of include/hubgpu.h
+SIGNATURES = {
+    "hg_last_error": (C.c_char_p, []),
+    "hg_version": (C.c_int, []),
+    "hg_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "hg_instance_create": (C.c_int, [C.c_int, C.c_int, C.c_int, _f64p, _f64p, _f64p, _f64p,
+                                     C.c_double, _i64p, C.c_double, C.c_double, C.c_double,
+                                     _vp, C.POINTER(_vp)]),
+    "hg_instance_free": (None, [_vp]),
+    "hg_instance_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int)]),
+    "hg_instance_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "hg_synchronize": (C.c_int, [_vp]),
+    "hg_allocate": (C.c_int, [_vp, C.c_int64, _i64p, _i64p]),
+    "hg_evaluate": (C.c_int, [_vp, C.c_int64, _i64p, _i64p, _f64p]),
+    "hg_pop_create": (C.c_int, [_vp, C.c_int64, C.POINTER(_vp)]),
+    "hg_pop_free": (None, [_vp]),
+    "hg_pop_load_hubs": (C.c_int, [_vp, C.c_int64, _vp, C.c_int]),
+    "hg_pop_evaluate": (C.c_int, [_vp, C.c_int64]),
+    "hg_pop_read": (C.c_int, [_vp, C.c_int64, _vp, C.c_int]),
+    "hg_pop_launches_per_evaluate": (C.c_int, [_vp]),
+    "hg_pop_last_fitness_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "hg_correct": (C.c_int, [_vp, C.c_int64, _u8p, _i64p]),
+    "hg_crossover": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _u8p, _i64p, _u8p, _u8p]),
+    "hg_swap": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _i64p, _i64p, _u8p]),
+    "hg_ga_create": (C.c_int, [_vp, C.POINTER(GaParamsC), C.POINTER(_vp)]),
+    "hg_ga_free": (None, [_vp]),
+    "hg_ga_begin_round": (C.c_int, [_vp, _i64p]),
+    "hg_ga_generations": (C.c_int, [_vp, C.c_int]),
+    "hg_ga_round_results": (C.c_int, [_vp, _f64p, _i64p]),
+    "hg_ga_last_children": (C.c_int, [_vp, _i64p, _f64p]),
+    "hg_ga_draw_counters": (C.c_int, [_vp, _u64p]),
+    "hg_ga_launches_per_generation": (C.c_int, [_vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load libhubgpu.so (once).  Raises if it was not built: there is no
+    fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with "
+                    "`make -C paper_1704_06258_b200/csrc` (or __graft_entry__.build())")
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+class HubGpuError(RuntimeError):
+    pass
+
+
+def check(rc: int) -> None:
+    if rc == HG_OK:
+        return
+    msg = load().hg_last_error().decode(errors="replace")
+    if rc == HG_EARG:
+        raise ValueError(msg)
+    if rc == HG_ENODEV:
+        raise HubGpuError(msg)
+    raise HubGpuError(f"libhubgpu error {rc}: {msg}")
+
+
+def device_count() -> int:
+    c = C.c_int(0)
+    check(load().hg_device_count(C.byref(c)))
+    return c.value
+
+
+_device = int(os.environ.get("HUBGPU_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def set_device(index: int) -> None:
+    """Select the CUDA device new device instances are created on."""
+    global _device
+    _device = int(index)
+
+
+def current_device() -> int:
+    return _device
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(ctype)
+
+
+# ---------------------------------------------------------------------------
+# device-resident instances, cached on the (immutable) Instance object
+# ---------------------------------------------------------------------------
+
+
+class DeviceInstance:
+    """Owns an hg_inst handle: HBM-resident dist / flow / derived vectors."""
+
+    def __init__(self, inst, device: int, stream=None):
+        lib = load()
+        self.n, self.p = inst.n, inst.p
+        self.device = device
+        h = _vp()
+        dist = np.ascontiguousarray(inst.dist, dtype=np.float64)
+        flow = np.ascontiguousarray(inst.flow, dtype=np.float64)
+        out_flow = np.ascontiguousarray(inst.out_flow, dtype=np.float64)
+        in_flow = np.ascontiguousarray(inst.in_flow, dtype=np.float64)
+        rank = np.ascontiguousarray(inst.middle_rank, dtype=np.int64)
+        check(lib.hg_instance_create(device, inst.n, inst.p, ptr(dist, _f64p), ptr(flow, _f64p),
+                                     ptr(out_flow, _f64p), ptr(in_flow, _f64p),
+                                     float(inst.total_flow), ptr(rank, _i64p),
+                                     float(inst.chi), float(inst.alpha), float(inst.delta),
+                                     stream, C.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.hg_instance_free, h)
+        n_, p_, flags = C.c_int(), C.c_int(), C.c_int()
+        check(lib.hg_instance_info(h, C.byref(n_), C.byref(p_), C.byref(flags)))
+        self.flags = flags.value
+
+    @property
+    def stream(self) -> int:
+        s = _vp()
+        check(load().hg_instance_stream(self.handle, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self) -> None:
+        check(load().hg_synchronize(self.handle))
+
+    def allocate(self, hubs: np.ndarray) -> np.ndarray:
+        hubs = np.ascontiguousarray(hubs, dtype=np.int64).reshape(-1, self.p)
+        out = np.empty((hubs.shape[0], self.n), dtype=np.int64)
+        check(load().hg_allocate(self.handle, hubs.shape[0], ptr(hubs, _i64p), ptr(out, _i64p)))
+        return out
+
+    def evaluate(self, hubs: np.ndarray, alloc: np.ndarray | None = None) -> np.ndarray:
+        hubs = np.ascontiguousarray(hubs, dtype=np.int64).reshape(-1, self.p)
+        B = hubs.shape[0]
+        out = np.empty((B, 4), dtype=np.float64)
+        ap = None
+        if alloc is not None:
+            alloc = np.ascontiguousarray(alloc, dtype=np.int64).reshape(B, self.n)
+            ap = ptr(alloc, _i64p)
+        check(load().hg_evaluate(self.handle, B, ptr(hubs, _i64p), ap, ptr(out, _f64p)))
+        return out
+
+    def correct(self, masks: np.ndarray) -> np.ndarray:
+        masks = np.ascontiguousarray(masks, dtype=np.uint8).reshape(-1, self.n)
+        out = np.empty((masks.shape[0], self.p), dtype=np.int64)
+        check(load().hg_correct(self.handle, masks.shape[0], ptr(masks, _u8p), ptr(out, _i64p)))
+        return out
+
+
+def device_instance(inst, device: int | None = None) -> DeviceInstance:
+    dev = _device if device is None else int(device)
+    cache = inst.__dict__.get("_hubgpu_dev")
+    if cache is None:
+        cache = {}
+        object.__setattr__(inst, "_hubgpu_dev", cache)
+    d = cache.get(dev)
+    if d is None:
+        d = DeviceInstance(inst, dev)
+        cache[dev] = d
+    return d
+
+
+# ---------------------------------------------------------------------------
+# population and GA handles
+# ---------------------------------------------------------------------------
+
+
+class DevicePopulation:
+    """A device-resident population buffer (hg_pop) bound to one instance."""
+
+    def __init__(self, dinst: DeviceInstance, capacity: int):
+        lib = load()
+        self.dinst = dinst
+        self.capacity = int(capacity)
+        h = _vp()
+        check(lib.hg_pop_create(dinst.handle, self.capacity, C.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.hg_pop_free, h)
+
+    def load_hubs(self, hubs32, where: int = HG_HOST, count: int | None = None) -> None:
+        """hubs32: int32 numpy array (host) or a device pointer (int) with where=HG_DEVICE."""
+        if where == HG_HOST:
+            hubs32 = np.ascontiguousarray(hubs32, dtype=np.int32).reshape(-1, self.dinst.p)
+            count = hubs32.shape[0]
+            p = hubs32.ctypes.data
+        else:
+            p = int(hubs32)
+        check(load().hg_pop_load_hubs(self.handle, int(count), p, where))
+
+    def evaluate(self, count: int) -> None:
+        check(load().hg_pop_evaluate(self.handle, int(count)))
+
+    def read(self, count: int, out=None, where: int = HG_HOST):
+        if where == HG_HOST:
+            if out is None:
+                out = np.empty((count, 4), dtype=np.float64)
+            check(load().hg_pop_read(self.handle, int(count), out.ctypes.data, HG_HOST))
+            return out
+        check(load().hg_pop_read(self.handle, int(count), int(out), HG_DEVICE))
+        return out
+
+    def last_fitness_ms(self) -> float:
+        v = C.c_float()
+        check(load().hg_pop_last_fitness_ms(self.handle, C.byref(v)))
+        return v.value
+
+    @property
+    def launches_per_evaluate(self) -> int:
+        return load().hg_pop_launches_per_evaluate(self.handle)
+
+
+class DeviceGa:
+    """Islands [lo, hi) of an island-GA run on one device (hg_ga)."""
+
+    def __init__(self, dinst: DeviceInstance, islands_total: int, lo: int, hi: int,
+                 pop_size: int, strength: int, strict: bool, seed: int):
+        lib = load()
+        self.dinst = dinst
+        self.lo, self.hi = lo, hi
+        self.pop = pop_size
+        prm = GaParamsC(islands_total, lo, hi, pop_size, strength, 1 if strict else 0,
+                        seed & ((1 << 64) - 1))
+        h = _vp()
+        check(lib.hg_ga_create(dinst.handle, C.byref(prm), C.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.hg_ga_free, h)
+
+    @property
+    def n_local(self) -> int:
+        return self.hi - self.lo
+
+    def begin_round(self, hubs: np.ndarray) -> None:
+        hubs = np.ascontiguousarray(hubs, dtype=np.int64)
+        check(load().hg_ga_begin_round(self.handle, ptr(hubs, _i64p)))
+
+    def generations(self, count: int) -> None:
+        check(load().hg_ga_generations(self.handle, int(count)))
+
+    def round_results(self):
+        raw = np.empty(self.n_local, dtype=np.float64)
+        hubs = np.empty((self.n_local, self.dinst.p), dtype=np.int64)
+        check(load().hg_ga_round_results(self.handle, ptr(raw, _f64p), ptr(hubs, _i64p)))
+        return raw, hubs
+
+    def last_children(self):
+        B = self.n_local * self.pop
+        hubs = np.empty((B, self.dinst.p), dtype=np.int64)
+        raw = np.empty(B, dtype=np.float64)
+        check(load().hg_ga_last_children(self.handle, ptr(hubs, _i64p), ptr(raw, _f64p)))
+        return hubs, raw
+
+    def draw_counters(self) -> np.ndarray:
+        out = np.empty((self.n_local, 3), dtype=np.uint64)
+        check(load().hg_ga_draw_counters(self.handle, ptr(out, _u64p)))
+        return out
+
+    @property
+    def launches_per_generation(self) -> int:
+        return load().hg_ga_launches_per_generation(self.handle)
+
+
+def crossover_masks(a: np.ndarray, b: np.ndarray, cuts: np.ndarray, device: int | None = None):
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    B, n = a.reshape(-1, a.shape[-1]).shape
+    cuts = np.ascontiguousarray(cuts, dtype=np.int64).reshape(B)
+    c1 = np.empty((B, n), dtype=np.uint8)
+    c2 = np.empty((B, n), dtype=np.uint8)
+    check(load().hg_crossover(_device if device is None else device, n, B, ptr(a, _u8p),
+                              ptr(b, _u8p), ptr(cuts, _i64p), ptr(c1, _u8p), ptr(c2, _u8p)))
+    return c1, c2
+
+
+def swap_masks(masks: np.ndarray, r_close: np.ndarray, r_open: np.ndarray,
+               device: int | None = None) -> np.ndarray:
+    masks = np.ascontiguousarray(masks, dtype=np.uint8)
+    B, n = masks.reshape(-1, masks.shape[-1]).shape
+    rc = np.ascontiguousarray(r_close, dtype=np.int64).reshape(B)
+    ro = np.ascontiguousarray(r_open, dtype=np.int64).reshape(B)
+    out = np.empty((B, n), dtype=np.uint8)
+    check(load().hg_swap(_device if device is None else device, n, B, ptr(masks, _u8p),
+                         ptr(rc, _i64p), ptr(ro, _i64p), ptr(out, _u8p)))
+    return out

@@ -1,0 +1,857 @@
+// C-ABI object layer of libhubgpu.so (see include/hubgpu.h).
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "hg_internal.cuh"
+
+namespace hg {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    int ensure(size_t need) {
+        if (need <= bytes) return HG_OK;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        size_t cap = need + need / 4 + 256;
+        HG_CUDA(cudaMalloc(&ptr, cap));
+        bytes = cap;
+        return HG_OK;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct hg_pop {
+    hg_inst* inst = nullptr;
+    int64_t cap = 0;
+    int32_t* hubs = nullptr;
+    uint8_t* cl = nullptr;
+    double* T = nullptr;
+    double* legs = nullptr;
+    double* part = nullptr;
+    double* out = nullptr;
+    DevBuf alloc;  // int32 [cap][n], on demand
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+struct hg_inst {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+    int flags = 0;
+    DevInst I{};
+    FitPlan plan{};
+    double* dC = nullptr;
+    double* dCt = nullptr;
+    double* dW = nullptr;
+    double* dO = nullptr;
+    double* dD = nullptr;
+    double* dwOD = nullptr;
+    int32_t* drank = nullptr;
+    hg_pop* scratch = nullptr;
+    DevBuf t1, t2, t3, t4;
+};
+
+namespace {
+
+int set_device(int dev) {
+    HG_CUDA(cudaSetDevice(dev));
+    return HG_OK;
+}
+
+void pop_release(hg_pop* P) {
+    if (!P) return;
+    cudaFree(P->hubs);
+    cudaFree(P->cl);
+    cudaFree(P->T);
+    cudaFree(P->legs);
+    cudaFree(P->part);
+    cudaFree(P->out);
+    P->alloc.release();
+    if (P->ev0) cudaEventDestroy(P->ev0);
+    if (P->ev1) cudaEventDestroy(P->ev1);
+    P->hubs = nullptr;
+    P->cl = nullptr;
+    P->T = nullptr;
+    P->legs = nullptr;
+    P->part = nullptr;
+    P->out = nullptr;
+    P->ev0 = P->ev1 = nullptr;
+    P->cap = 0;
+}
+
+int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
+    const DevInst& I = inst->I;
+    P->inst = inst;
+    P->cap = cap;
+    HG_CUDA(cudaMalloc(&P->hubs, (size_t)cap * I.p * sizeof(int32_t)));
+    HG_CUDA(cudaMalloc(&P->cl, (size_t)cap * I.npad));
+    HG_CUDA(cudaMalloc(&P->T, (size_t)cap * I.p * I.ps * sizeof(double)));
+    HG_CUDA(cudaMalloc(&P->legs, (size_t)cap * 2 * sizeof(double)));
+    HG_CUDA(cudaMalloc(&P->part, (size_t)cap * inst->plan.tiles * sizeof(double)));
+    HG_CUDA(cudaMalloc(&P->out, (size_t)cap * 4 * sizeof(double)));
+    HG_CUDA(cudaEventCreate(&P->ev0));
+    HG_CUDA(cudaEventCreate(&P->ev1));
+    return HG_OK;
+}
+
+int scratch_pop(hg_inst* inst, int64_t B, hg_pop** out) {
+    if (!inst->scratch) {
+        inst->scratch = new (std::nothrow) hg_pop();
+        if (!inst->scratch) {
+            set_error("out of host memory");
+            return HG_ECUDA;
+        }
+    }
+    hg_pop* P = inst->scratch;
+    if (P->cap < B) {
+        pop_release(P);
+        int64_t cap = B < 64 ? 64 : B;
+        HG_TRY(pop_alloc(P, inst, cap));
+    }
+    *out = P;
+    return HG_OK;
+}
+
+// queue K2 + K3 + finalise for B individuals whose int32 hubs are in P->hubs
+// (alloc32 == nullptr: nearest allocation; otherwise the given allocation)
+int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
+    hg_inst* inst = P->inst;
+    const DevInst& I = inst->I;
+    cudaStream_t s = inst->stream;
+    if (alloc32)
+        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, P->T, P->legs, s));
+    else
+        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->T, P->legs, nullptr, s));
+    HG_CUDA(cudaEventRecord(P->ev0, s));
+    HG_TRY(launch_fitness(I, inst->plan, B, P->cl, P->T, P->part,
+                          inst->sm_count * inst->plan.blocks_per_sm, s));
+    HG_CUDA(cudaEventRecord(P->ev1, s));
+    HG_TRY(launch_finalize(I, inst->plan, B, P->legs, P->part, P->out, s));
+    return HG_OK;
+}
+
+int h2d_i64_as_i32(hg_inst* inst, DevBuf& tmp, const int64_t* host, int64_t count, int32_t* dst) {
+    if (count <= 0) return HG_OK;
+    HG_TRY(tmp.ensure((size_t)count * sizeof(int64_t)));
+    HG_CUDA(cudaMemcpyAsync(tmp.ptr, host, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            inst->stream));
+    return launch_i64_to_i32(tmp.as<int64_t>(), dst, count, inst->stream);
+}
+
+int d2h_i32_as_i64(hg_inst* inst, DevBuf& tmp, const int32_t* dsrc, int64_t count, int64_t* host) {
+    if (count <= 0) return HG_OK;
+    HG_TRY(tmp.ensure((size_t)count * sizeof(int64_t)));
+    HG_TRY(launch_i32_to_i64(dsrc, tmp.as<int64_t>(), count, inst->stream));
+    HG_CUDA(cudaMemcpyAsync(host, tmp.ptr, (size_t)count * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            inst->stream));
+    return HG_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// exported API
+// ============================================================================
+
+extern "C" {
+
+const char* hg_last_error(void) { return hg::g_err; }
+
+int hg_version(void) { return 100; }
+
+int hg_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    if (count) *count = c;
+    return HG_OK;
+}
+
+int hg_instance_create(int device, int n, int p, const double* dist, const double* flow,
+                       const double* out_flow, const double* in_flow, double total_flow,
+                       const int64_t* middle_rank, double chi, double alpha, double delta,
+                       void* stream, hg_inst** out) {
+    (void)total_flow;
+    HG_ARG(out != nullptr, "out is NULL");
+    *out = nullptr;
+    HG_ARG(n >= 1, "node count must be positive, got %d", n);
+    HG_ARG(p >= 1 && p <= n, "hub count p=%d outside [1, %d]", p, n);
+    HG_ARG(p <= kMaxP, "p=%d exceeds the supported maximum %d", p, kMaxP);
+    HG_ARG(n <= kMaxNga, "n=%d exceeds the supported maximum %d", n, kMaxNga);
+    HG_ARG(dist && flow && out_flow && in_flow && middle_rank, "NULL instance array");
+    int ndev = 0;
+    hg_device_count(&ndev);
+    if (ndev <= 0) {
+        set_error("no CUDA device visible: libhubgpu needs a B200 (sm_100a)");
+        return HG_ENODEV;
+    }
+    HG_ARG(device >= 0 && device < ndev, "device %d outside [0, %d)", device, ndev);
+    HG_TRY(set_device(device));
+
+    hg_inst* inst = new (std::nothrow) hg_inst();
+    if (!inst) {
+        set_error("out of host memory");
+        return HG_ECUDA;
+    }
+    inst->device = device;
+    int rc = HG_OK;
+    do {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+            set_error("cudaGetDeviceProperties failed");
+            rc = HG_ECUDA;
+            break;
+        }
+        inst->sm_count = prop.multiProcessorCount;
+        if (stream) {
+            inst->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            if (cudaStreamCreateWithFlags(&inst->stream, cudaStreamNonBlocking) != cudaSuccess) {
+                set_error("cudaStreamCreate failed");
+                rc = HG_ECUDA;
+                break;
+            }
+            inst->own_stream = true;
+        }
+        const size_t nn = (size_t)n * n;
+        cudaStream_t s = inst->stream;
+        auto chk = [&](cudaError_t e, const char* what) {
+            if (e != cudaSuccess && rc == HG_OK) {
+                set_error("%s: %s", what, cudaGetErrorString(e));
+                rc = HG_ECUDA;
+            }
+        };
+        chk(cudaMalloc(&inst->dC, nn * 8), "cudaMalloc(dist)");
+        chk(cudaMalloc(&inst->dW, nn * 8), "cudaMalloc(flow)");
+        chk(cudaMalloc(&inst->dO, (size_t)n * 8), "cudaMalloc");
+        chk(cudaMalloc(&inst->dD, (size_t)n * 8), "cudaMalloc");
+        chk(cudaMalloc(&inst->dwOD, (size_t)n * 8), "cudaMalloc");
+        chk(cudaMalloc(&inst->drank, (size_t)n * 4), "cudaMalloc");
+        if (rc) break;
+        chk(cudaMemcpyAsync(inst->dC, dist, nn * 8, cudaMemcpyHostToDevice, s), "H2D dist");
+        chk(cudaMemcpyAsync(inst->dW, flow, nn * 8, cudaMemcpyHostToDevice, s), "H2D flow");
+        chk(cudaMemcpyAsync(inst->dO, out_flow, (size_t)n * 8, cudaMemcpyHostToDevice, s), "H2D");
+        chk(cudaMemcpyAsync(inst->dD, in_flow, (size_t)n * 8, cudaMemcpyHostToDevice, s), "H2D");
+        // correction weights O_i + D_i (hm/operators.py:94), exactness of order-free sums
+        std::vector<double> w(n);
+        std::vector<int32_t> rk(n);
+        bool exact = true;
+        double tot = 0.0;
+        for (int i = 0; i < n; ++i) {
+            w[i] = out_flow[i] + in_flow[i];
+            if (!(w[i] == std::floor(w[i])) || w[i] < 0) exact = false;
+            tot += w[i];
+            rk[i] = (int32_t)middle_rank[i];
+        }
+        if (!(tot < 9007199254740992.0)) exact = false;
+        chk(cudaMemcpyAsync(inst->dwOD, w.data(), (size_t)n * 8, cudaMemcpyHostToDevice, s),
+            "H2D");
+        chk(cudaMemcpyAsync(inst->drank, rk.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s),
+            "H2D");
+        int* dflag = nullptr;
+        chk(cudaMalloc(&dflag, sizeof(int)), "cudaMalloc");
+        if (rc) break;
+        int one = 1;
+        chk(cudaMemcpyAsync(dflag, &one, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+        if (rc == HG_OK) rc = launch_check_symmetric(inst->dC, n, dflag, s);
+        int sym = 0;
+        chk(cudaMemcpyAsync(&sym, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+        chk(cudaStreamSynchronize(s), "sync");
+        cudaFree(dflag);
+        if (rc) break;
+        if (sym) {
+            inst->dCt = inst->dC;
+        } else {
+            chk(cudaMalloc(&inst->dCt, nn * 8), "cudaMalloc(dist^T)");
+            if (rc) break;
+            rc = launch_transpose(inst->dC, inst->dCt, n, s);
+            if (rc) break;
+        }
+        inst->flags = (sym ? HG_FLAG_SYMMETRIC : 0) | (exact ? HG_FLAG_WEIGHTS_EXACT : 0);
+
+        DevInst& I = inst->I;
+        I.n = n;
+        I.p = p;
+        I.nw = (n + 31) / 32;
+        I.ps = (p + 1) & ~1;
+        I.weights_exact = exact ? 1 : 0;
+        I.chi = chi;
+        I.alpha = alpha;
+        I.delta = delta;
+        I.C = inst->dC;
+        I.Ct = inst->dCt;
+        I.W = inst->dW;
+        I.O = inst->dO;
+        I.D = inst->dD;
+        I.wOD = inst->dwOD;
+        I.rank = inst->drank;
+        I.npad = 16;  // provisional for the plan
+        inst->plan = fitness_plan(I, inst->sm_count);
+        int64_t q = inst->plan.tr > inst->plan.tc ? inst->plan.tr : inst->plan.tc;
+        if (q < 16) q = 16;
+        I.npad = (int)round_up(n, q);
+        rc = prepare_fitness(inst->plan);
+        if (rc) break;
+        chk(cudaStreamSynchronize(s), "sync");
+    } while (0);
+    if (rc != HG_OK) {
+        hg_instance_free(inst);
+        return rc;
+    }
+    *out = inst;
+    return HG_OK;
+}
+
+void hg_instance_free(hg_inst* inst) {
+    if (!inst) return;
+    cudaSetDevice(inst->device);
+    if (inst->stream) cudaStreamSynchronize(inst->stream);
+    if (inst->scratch) {
+        pop_release(inst->scratch);
+        delete inst->scratch;
+    }
+    if (inst->dCt && inst->dCt != inst->dC) cudaFree(inst->dCt);
+    cudaFree(inst->dC);
+    cudaFree(inst->dW);
+    cudaFree(inst->dO);
+    cudaFree(inst->dD);
+    cudaFree(inst->dwOD);
+    cudaFree(inst->drank);
+    inst->t1.release();
+    inst->t2.release();
+    inst->t3.release();
+    inst->t4.release();
+    if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
+    delete inst;
+}
+
+int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    if (n) *n = inst->I.n;
+    if (p) *p = inst->I.p;
+    if (flags) *flags = inst->flags;
+    return HG_OK;
+}
+
+int hg_instance_stream(const hg_inst* inst, void** stream) {
+    HG_ARG(inst != nullptr && stream != nullptr, "NULL argument");
+    *stream = inst->stream;
+    return HG_OK;
+}
+
+int hg_synchronize(hg_inst* inst) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    HG_TRY(set_device(inst->device));
+    HG_CUDA(cudaStreamSynchronize(inst->stream));
+    return HG_OK;
+}
+
+int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    HG_ARG(B >= 0, "negative batch");
+    if (B == 0) return HG_OK;
+    HG_ARG(hubs && alloc, "NULL buffer");
+    HG_TRY(set_device(inst->device));
+    hg_pop* P;
+    HG_TRY(scratch_pop(inst, B, &P));
+    const DevInst& I = inst->I;
+    HG_TRY(h2d_i64_as_i32(inst, inst->t1, hubs, B * I.p, P->hubs));
+    HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
+    HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->T, P->legs, P->alloc.as<int32_t>(),
+                           inst->stream));
+    HG_TRY(d2h_i32_as_i64(inst, inst->t2, P->alloc.as<int32_t>(), B * I.n, alloc));
+    HG_CUDA(cudaStreamSynchronize(inst->stream));
+    return HG_OK;
+}
+
+int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* alloc,
+                double* out) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    HG_ARG(B >= 0, "negative batch");
+    if (B == 0) return HG_OK;
+    HG_ARG(hubs && out, "NULL buffer");
+    HG_TRY(set_device(inst->device));
+    hg_pop* P;
+    HG_TRY(scratch_pop(inst, B, &P));
+    const DevInst& I = inst->I;
+    HG_TRY(h2d_i64_as_i32(inst, inst->t1, hubs, B * I.p, P->hubs));
+    const int32_t* a32 = nullptr;
+    if (alloc) {
+        HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
+        HG_TRY(h2d_i64_as_i32(inst, inst->t2, alloc, B * I.n, P->alloc.as<int32_t>()));
+        a32 = P->alloc.as<int32_t>();
+    }
+    HG_TRY(pop_eval_queue(P, B, a32));
+    HG_CUDA(cudaMemcpyAsync(out, P->out, (size_t)B * 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                            inst->stream));
+    HG_CUDA(cudaStreamSynchronize(inst->stream));
+    return HG_OK;
+}
+
+int hg_pop_create(hg_inst* inst, int64_t capacity, hg_pop** out) {
+    HG_ARG(inst && out, "NULL argument");
+    HG_ARG(capacity >= 1, "capacity must be >= 1");
+    HG_TRY(set_device(inst->device));
+    hg_pop* P = new (std::nothrow) hg_pop();
+    if (!P) {
+        set_error("out of host memory");
+        return HG_ECUDA;
+    }
+    int rc = pop_alloc(P, inst, capacity);
+    if (rc) {
+        pop_release(P);
+        delete P;
+        return rc;
+    }
+    *out = P;
+    return HG_OK;
+}
+
+void hg_pop_free(hg_pop* pop) {
+    if (!pop) return;
+    cudaSetDevice(pop->inst->device);
+    cudaStreamSynchronize(pop->inst->stream);
+    pop_release(pop);
+    delete pop;
+}
+
+int hg_pop_load_hubs(hg_pop* pop, int64_t B, const int32_t* hubs, int where) {
+    HG_ARG(pop && hubs, "NULL argument");
+    HG_ARG(B >= 0 && B <= pop->cap, "batch %lld outside [0, %lld]", (long long)B,
+           (long long)pop->cap);
+    HG_TRY(set_device(pop->inst->device));
+    const size_t bytes = (size_t)B * pop->inst->I.p * sizeof(int32_t);
+    HG_CUDA(cudaMemcpyAsync(pop->hubs, hubs, bytes,
+                            where == HG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            pop->inst->stream));
+    return HG_OK;
+}
+
+int hg_pop_evaluate(hg_pop* pop, int64_t B) {
+    HG_ARG(pop != nullptr, "NULL population");
+    HG_ARG(B >= 0 && B <= pop->cap, "batch outside capacity");
+    if (B == 0) return HG_OK;
+    HG_TRY(set_device(pop->inst->device));
+    return pop_eval_queue(pop, B, nullptr);
+}
+
+int hg_pop_read(hg_pop* pop, int64_t B, double* out, int where) {
+    HG_ARG(pop && out, "NULL argument");
+    HG_ARG(B >= 0 && B <= pop->cap, "batch outside capacity");
+    HG_TRY(set_device(pop->inst->device));
+    HG_CUDA(cudaMemcpyAsync(out, pop->out, (size_t)B * 4 * sizeof(double),
+                            where == HG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            pop->inst->stream));
+    if (where != HG_DEVICE) HG_CUDA(cudaStreamSynchronize(pop->inst->stream));
+    return HG_OK;
+}
+
+int hg_pop_launches_per_evaluate(const hg_pop* pop) {
+    (void)pop;
+    return 3;
+}
+
+int hg_pop_last_fitness_ms(hg_pop* pop, float* ms) {
+    HG_ARG(pop && ms, "NULL argument");
+    HG_TRY(set_device(pop->inst->device));
+    HG_CUDA(cudaEventSynchronize(pop->ev1));
+    HG_CUDA(cudaEventElapsedTime(ms, pop->ev0, pop->ev1));
+    return HG_OK;
+}
+
+int hg_correct(hg_inst* inst, int64_t B, const uint8_t* masks, int64_t* hubs_out) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    HG_ARG(B >= 0, "negative batch");
+    if (B == 0) return HG_OK;
+    HG_ARG(masks && hubs_out, "NULL buffer");
+    HG_TRY(set_device(inst->device));
+    const DevInst& I = inst->I;
+    cudaStream_t s = inst->stream;
+    HG_TRY(inst->t1.ensure((size_t)B * I.n));
+    HG_TRY(inst->t2.ensure((size_t)B * I.nw * 4));
+    HG_TRY(inst->t3.ensure((size_t)B * I.p * 4));
+    HG_CUDA(cudaMemcpyAsync(inst->t1.ptr, masks, (size_t)B * I.n, cudaMemcpyHostToDevice, s));
+    HG_TRY(launch_bytes_to_bits(inst->t1.as<uint8_t>(), inst->t2.as<uint32_t>(), B, I.n, I.nw, s));
+    HG_TRY(launch_correct(I, B, inst->t2.as<uint32_t>(), I.n, inst->t3.as<int32_t>(), s));
+    HG_TRY(d2h_i32_as_i64(inst, inst->t4, inst->t3.as<int32_t>(), B * I.p, hubs_out));
+    HG_CUDA(cudaStreamSynchronize(s));
+    return HG_OK;
+}
+
+// per-device scratch for the instance-free operators (serialised by a mutex)
+struct OpScratch {
+    bool init = false;
+    cudaStream_t stream = nullptr;
+    DevBuf t1, t2, t3;
+};
+static std::mutex g_op_mutex;
+static OpScratch g_op[64];
+
+static int op_scratch(int device, OpScratch** out) {
+    int ndev = 0;
+    hg_device_count(&ndev);
+    if (ndev <= 0) {
+        set_error("no CUDA device visible: libhubgpu needs a B200 (sm_100a)");
+        return HG_ENODEV;
+    }
+    HG_ARG(device >= 0 && device < ndev && device < 64, "device %d outside [0, %d)", device, ndev);
+    HG_TRY(set_device(device));
+    OpScratch& S = g_op[device];
+    if (!S.init) {
+        HG_CUDA(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+        S.init = true;
+    }
+    *out = &S;
+    return HG_OK;
+}
+
+int hg_crossover(int device, int n, int64_t B, const uint8_t* a, const uint8_t* b,
+                 const int64_t* cuts, uint8_t* child1, uint8_t* child2) {
+    HG_ARG(n >= 1, "mask length must be positive");
+    HG_ARG(B >= 0, "negative batch");
+    if (B == 0) return HG_OK;
+    HG_ARG(a && b && cuts && child1 && child2, "NULL buffer");
+    for (int64_t x = 0; x < B; ++x)
+        HG_ARG(cuts[x] >= 1 && cuts[x] <= n, "cut %lld outside [1, %d]", (long long)cuts[x], n);
+    std::lock_guard<std::mutex> lock(g_op_mutex);
+    OpScratch* S;
+    HG_TRY(op_scratch(device, &S));
+    const int nw = (n + 31) / 32;
+    cudaStream_t s = S->stream;
+    const size_t mb = (size_t)B * n, W = (size_t)B * nw;
+    HG_TRY(S->t1.ensure(2 * mb));
+    HG_TRY(S->t2.ensure(4 * W * 4));
+    HG_TRY(S->t3.ensure((size_t)B * 8));
+    uint8_t* dbytes = S->t1.as<uint8_t>();
+    uint32_t* dbits = S->t2.as<uint32_t>();
+    HG_CUDA(cudaMemcpyAsync(dbytes, a, mb, cudaMemcpyHostToDevice, s));
+    HG_CUDA(cudaMemcpyAsync(dbytes + mb, b, mb, cudaMemcpyHostToDevice, s));
+    HG_CUDA(cudaMemcpyAsync(S->t3.ptr, cuts, (size_t)B * 8, cudaMemcpyHostToDevice, s));
+    HG_TRY(launch_bytes_to_bits(dbytes, dbits, B, n, nw, s));
+    HG_TRY(launch_bytes_to_bits(dbytes + mb, dbits + W, B, n, nw, s));
+    HG_TRY(launch_splice(B, n, nw, dbits, dbits + W, S->t3.as<int64_t>(), dbits + 2 * W,
+                         dbits + 3 * W, s));
+    HG_TRY(launch_bits_to_bytes(dbits + 2 * W, dbytes, B, n, nw, s));
+    HG_TRY(launch_bits_to_bytes(dbits + 3 * W, dbytes + mb, B, n, nw, s));
+    HG_CUDA(cudaMemcpyAsync(child1, dbytes, mb, cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaMemcpyAsync(child2, dbytes + mb, mb, cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    return HG_OK;
+}
+
+int hg_swap(int device, int n, int64_t B, const uint8_t* masks, const int64_t* r_close,
+            const int64_t* r_open, uint8_t* out) {
+    HG_ARG(n >= 1, "mask length must be positive");
+    HG_ARG(B >= 0, "negative batch");
+    if (B == 0) return HG_OK;
+    HG_ARG(masks && r_close && r_open && out, "NULL buffer");
+    for (int64_t x = 0; x < B; ++x) {
+        if (r_close[x] < 0) continue;
+        int64_t on = 0;
+        for (int i = 0; i < n; ++i) on += masks[x * n + i] ? 1 : 0;
+        HG_ARG(on > 0 && on < n, "swap on an all-open/all-closed mask needs r_close < 0");
+        HG_ARG(r_close[x] < on && r_open[x] >= 0 && r_open[x] < n - on,
+               "swap draw outside its bound");
+    }
+    std::lock_guard<std::mutex> lock(g_op_mutex);
+    OpScratch* S;
+    HG_TRY(op_scratch(device, &S));
+    const int nw = (n + 31) / 32;
+    cudaStream_t s = S->stream;
+    const size_t mb = (size_t)B * n;
+    HG_TRY(S->t1.ensure(mb));
+    HG_TRY(S->t2.ensure((size_t)B * nw * 4));
+    HG_TRY(S->t3.ensure((size_t)B * 16));
+    int64_t* dr = S->t3.as<int64_t>();
+    HG_CUDA(cudaMemcpyAsync(S->t1.ptr, masks, mb, cudaMemcpyHostToDevice, s));
+    HG_CUDA(cudaMemcpyAsync(dr, r_close, (size_t)B * 8, cudaMemcpyHostToDevice, s));
+    HG_CUDA(cudaMemcpyAsync(dr + B, r_open, (size_t)B * 8, cudaMemcpyHostToDevice, s));
+    HG_TRY(launch_bytes_to_bits(S->t1.as<uint8_t>(), S->t2.as<uint32_t>(), B, n, nw, s));
+    HG_TRY(launch_swap_given(B, n, nw, S->t2.as<uint32_t>(), dr, dr + B, s));
+    HG_TRY(launch_bits_to_bytes(S->t2.as<uint32_t>(), S->t1.as<uint8_t>(), B, n, nw, s));
+    HG_CUDA(cudaMemcpyAsync(out, S->t1.ptr, mb, cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    return HG_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// island GA
+// ============================================================================
+
+struct hg_ga {
+    hg_inst* inst = nullptr;
+    hg_pop* pop = nullptr;
+    hg_ga_params prm{};
+    GaDev G{};
+    int64_t B = 0;
+    int32_t* inc = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<void*> bufs;
+};
+
+namespace {
+
+template <class T>
+int ga_alloc(hg_ga* ga, T** p, size_t count) {
+    void* v = nullptr;
+    HG_CUDA(cudaMalloc(&v, count * sizeof(T) + 16));
+    ga->bufs.push_back(v);
+    *p = static_cast<T*>(v);
+    return HG_OK;
+}
+
+int ga_queue_generation(hg_ga* ga) {
+    hg_inst* inst = ga->inst;
+    cudaStream_t s = inst->stream;
+    const GaDev& G = ga->G;
+    HG_TRY(launch_build_pop(G, s));
+    HG_TRY(launch_crossover(G, s));
+    HG_TRY(launch_mut_scan(G, s));
+    HG_TRY(launch_mutate(G, s));
+    HG_TRY(launch_correct(inst->I, ga->B, G.kids, 2 * G.p, G.khubs, s));
+    HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->T,
+                           ga->pop->legs, nullptr, s));
+    HG_TRY(launch_fitness(inst->I, inst->plan, ga->B, ga->pop->cl, ga->pop->T, ga->pop->part,
+                          inst->sm_count * inst->plan.blocks_per_sm, s));
+    HG_TRY(launch_finalize(inst->I, inst->plan, ga->B, ga->pop->legs, ga->pop->part,
+                           ga->pop->out, s));
+    HG_TRY(launch_select(G, s));
+    return HG_OK;
+}
+
+constexpr int kGaLaunches = 9;
+
+void ga_release(hg_ga* ga) {
+    if (ga->exec) cudaGraphExecDestroy(ga->exec);
+    if (ga->graph) cudaGraphDestroy(ga->graph);
+    for (void* v : ga->bufs) cudaFree(v);
+    ga->bufs.clear();
+    if (ga->pop) {
+        pop_release(ga->pop);
+        delete ga->pop;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
+    HG_ARG(inst && prm && out, "NULL argument");
+    *out = nullptr;
+    const DevInst& I = inst->I;
+    HG_ARG(prm->islands_total >= 1, "islands must be >= 1, got %d", prm->islands_total);
+    HG_ARG(prm->island_lo >= 0 && prm->island_lo < prm->island_hi &&
+               prm->island_hi <= prm->islands_total,
+           "island range [%d, %d) invalid for %d islands", prm->island_lo, prm->island_hi,
+           prm->islands_total);
+    HG_ARG(prm->pop_size >= 2 && prm->pop_size % 2 == 0,
+           "pop_size must be even for pairwise crossover, got %d", prm->pop_size);
+    HG_ARG(prm->strength >= 1 && prm->strength <= I.p, "perturb_strength %d exceeds p=%d",
+           prm->strength, I.p);
+    HG_TRY(set_device(inst->device));
+    hg_ga* ga = new (std::nothrow) hg_ga();
+    if (!ga) {
+        set_error("out of host memory");
+        return HG_ECUDA;
+    }
+    ga->inst = inst;
+    ga->prm = *prm;
+    const int nloc = prm->island_hi - prm->island_lo;
+    ga->B = (int64_t)nloc * prm->pop_size;
+    int rc = HG_OK;
+    do {
+        ga->pop = new (std::nothrow) hg_pop();
+        if (!ga->pop) {
+            set_error("out of host memory");
+            rc = HG_ECUDA;
+            break;
+        }
+        if ((rc = pop_alloc(ga->pop, inst, ga->B))) break;
+        GaDev& G = ga->G;
+        G.n = I.n;
+        G.p = I.p;
+        G.nw = I.nw;
+        G.nloc = nloc;
+        G.pop = prm->pop_size;
+        G.strength = prm->strength;
+        G.strict_mode = prm->strict_paper ? 1 : 0;
+        G.island_lo = prm->island_lo;
+        const size_t B = (size_t)ga->B, nw = (size_t)I.nw, p = (size_t)I.p;
+        if ((rc = ga_alloc(ga, &G.anc, nloc * nw))) break;
+        if ((rc = ga_alloc(ga, &G.popbits, B * nw))) break;
+        if ((rc = ga_alloc(ga, &G.kids, B * nw))) break;
+        if ((rc = ga_alloc(ga, &G.kcount, B))) break;
+        if ((rc = ga_alloc(ga, &G.moff, B))) break;
+        if ((rc = ga_alloc(ga, &G.nondeg, (size_t)nloc))) break;
+        if ((rc = ga_alloc(ga, &G.champ_raw, (size_t)nloc))) break;
+        if ((rc = ga_alloc(ga, &G.champ_hubs, nloc * p))) break;
+        if ((rc = ga_alloc(ga, &G.best_raw, (size_t)nloc))) break;
+        if ((rc = ga_alloc(ga, &G.best_hubs, nloc * p))) break;
+        if ((rc = ga_alloc(ga, &G.st, (size_t)nloc * 3))) break;
+        if ((rc = ga_alloc(ga, &G.ctr, (size_t)nloc * 3))) break;
+        if ((rc = ga_alloc(ga, &ga->inc, p))) break;
+        G.khubs = ga->pop->hubs;
+        G.kraw = ga->pop->out;
+        G.inc = ga->inc;
+        // streams derive_stream(seed, island, role) keyed by the GLOBAL island
+        std::vector<uint64_t> st((size_t)nloc * 3), zero((size_t)nloc * 3, 0);
+        for (int li = 0; li < nloc; ++li)
+            for (int role = 0; role < 3; ++role) {
+                uint64_t keys[2] = {(uint64_t)(prm->island_lo + li), (uint64_t)role};
+                st[(size_t)li * 3 + role] = host_stream_key(prm->seed, keys, 2);
+            }
+        cudaStream_t s = inst->stream;
+        if (cudaMemcpyAsync(G.st, st.data(), st.size() * 8, cudaMemcpyHostToDevice, s) ||
+            cudaMemcpyAsync(G.ctr, zero.data(), zero.size() * 8, cudaMemcpyHostToDevice, s) ||
+            cudaStreamSynchronize(s)) {
+            set_error("GA state upload failed");
+            rc = HG_ECUDA;
+            break;
+        }
+        // capture one generation as a CUDA graph
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            set_error("cudaStreamBeginCapture failed");
+            rc = HG_ECUDA;
+            break;
+        }
+        int qrc = ga_queue_generation(ga);
+        cudaError_t ce = cudaStreamEndCapture(s, &ga->graph);
+        if (qrc) {
+            rc = qrc;
+            break;
+        }
+        if (ce != cudaSuccess) {
+            set_error("cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+            rc = HG_ECUDA;
+            break;
+        }
+        ce = cudaGraphInstantiate(&ga->exec, ga->graph, 0);
+        if (ce != cudaSuccess) {
+            set_error("cudaGraphInstantiate: %s", cudaGetErrorString(ce));
+            rc = HG_ECUDA;
+            break;
+        }
+    } while (0);
+    if (rc) {
+        ga_release(ga);
+        delete ga;
+        return rc;
+    }
+    *out = ga;
+    return HG_OK;
+}
+
+void hg_ga_free(hg_ga* ga) {
+    if (!ga) return;
+    cudaSetDevice(ga->inst->device);
+    cudaStreamSynchronize(ga->inst->stream);
+    ga_release(ga);
+    delete ga;
+}
+
+int hg_ga_begin_round(hg_ga* ga, const int64_t* ancestor_hubs) {
+    HG_ARG(ga && ancestor_hubs, "NULL argument");
+    HG_TRY(set_device(ga->inst->device));
+    const int p = ga->inst->I.p, n = ga->inst->I.n;
+    std::vector<int32_t> h(p);
+    for (int k = 0; k < p; ++k) {
+        HG_ARG(ancestor_hubs[k] >= 0 && ancestor_hubs[k] < n, "ancestor hub out of range");
+        HG_ARG(k == 0 || ancestor_hubs[k] > ancestor_hubs[k - 1], "ancestor hubs must be sorted");
+        h[k] = (int32_t)ancestor_hubs[k];
+    }
+    HG_CUDA(cudaMemcpyAsync(ga->inc, h.data(), p * 4, cudaMemcpyHostToDevice, ga->inst->stream));
+    HG_TRY(launch_round_begin(ga->G, ga->inst->stream));
+    // the pageable H2D above is staged before return, h may go out of scope
+    HG_CUDA(cudaStreamSynchronize(ga->inst->stream));
+    return HG_OK;
+}
+
+int hg_ga_generations(hg_ga* ga, int count) {
+    HG_ARG(ga != nullptr, "NULL GA");
+    HG_ARG(count >= 0, "negative generation count");
+    HG_TRY(set_device(ga->inst->device));
+    for (int g = 0; g < count; ++g) HG_CUDA(cudaGraphLaunch(ga->exec, ga->inst->stream));
+    return HG_OK;
+}
+
+int hg_ga_round_results(hg_ga* ga, double* raw, int64_t* hubs) {
+    HG_ARG(ga && raw && hubs, "NULL argument");
+    HG_TRY(set_device(ga->inst->device));
+    const GaDev& G = ga->G;
+    const bool strict = ga->prm.strict_paper != 0;
+    cudaStream_t s = ga->inst->stream;
+    std::vector<int32_t> h((size_t)G.nloc * G.p);
+    HG_CUDA(cudaMemcpyAsync(raw, strict ? G.champ_raw : G.best_raw, (size_t)G.nloc * 8,
+                            cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaMemcpyAsync(h.data(), strict ? G.champ_hubs : G.best_hubs, h.size() * 4,
+                            cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    for (size_t x = 0; x < h.size(); ++x) hubs[x] = h[x];
+    return HG_OK;
+}
+
+int hg_ga_last_children(hg_ga* ga, int64_t* hubs, double* raw) {
+    HG_ARG(ga && hubs && raw, "NULL argument");
+    HG_TRY(set_device(ga->inst->device));
+    cudaStream_t s = ga->inst->stream;
+    const int p = ga->inst->I.p;
+    std::vector<int32_t> h((size_t)ga->B * p);
+    std::vector<double> o((size_t)ga->B * 4);
+    HG_CUDA(cudaMemcpyAsync(h.data(), ga->pop->hubs, h.size() * 4, cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaMemcpyAsync(o.data(), ga->pop->out, o.size() * 8, cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    for (size_t x = 0; x < h.size(); ++x) hubs[x] = h[x];
+    for (int64_t b = 0; b < ga->B; ++b) raw[b] = o[(size_t)b * 4 + 3];
+    return HG_OK;
+}
+
+int hg_ga_draw_counters(hg_ga* ga, uint64_t* counters) {
+    HG_ARG(ga && counters, "NULL argument");
+    HG_TRY(set_device(ga->inst->device));
+    HG_CUDA(cudaMemcpyAsync(counters, ga->G.ctr, (size_t)ga->G.nloc * 3 * 8,
+                            cudaMemcpyDeviceToHost, ga->inst->stream));
+    HG_CUDA(cudaStreamSynchronize(ga->inst->stream));
+    return HG_OK;
+}
+
+int hg_ga_launches_per_generation(const hg_ga* ga) {
+    (void)ga;
+    return kGaLaunches;
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+// Internal declarations shared by the libhubgpu translation units.
+//
+// Device data layout (all row-major, one allocation per array):
+//   C   [n][n]   fp64  dist: C[i][k] = unit cost i -> k           (hm/model.py:45)
+//   Ct  [n][n]   fp64  C transposed (aliases C when symmetric) -- allocation
+//                      reads Ct[h][i] so a warp's 32 nodes are one 256 B line
+//   W   [n][n]   fp64  flow
+//   O, D, wOD [n] fp64 out/in flow and their sum (correction weights)
+//   rank [n]     int32 middle-node order (hm/model.py:96-105)
+// Population (capacity Bcap), see hg_pop:
+//   hubs [B][p]       int32 sorted hub ids
+//   cl   [B][npad]    uint8 cluster of node i = position of its hub in hubs
+//                     (padding to npad is zero so padded lanes hit T row 0)
+//   T    [B][p][ps]   fp64 hub-to-hub cost table T[k][l] = C[h_k][h_l]
+//   legs [B][2]       fp64 sum_i O_i*leg_i, sum_i D_i*leg_i (leg_i = C[i][a_i])
+//   part [B][tiles]   fp64 per-W-tile partial of sum_ij W_ij T[c_i][c_j]
+//   out  [B][4]       fp64 collection, transfer, distribution, raw
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdarg>
+
+#include "../../include/hubgpu.h"
+
+namespace hg {
+
+void set_error(const char* fmt, ...);
+
+#define HG_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            ::hg::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),     \
+                            __FILE__, __LINE__);                                        \
+            return HG_ECUDA;                                                            \
+        }                                                                               \
+    } while (0)
+
+#define HG_ARG(cond, ...)                                                               \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            ::hg::set_error(__VA_ARGS__);                                               \
+            return HG_EARG;                                                             \
+        }                                                                               \
+    } while (0)
+
+#define HG_TRY(expr)                                                                    \
+    do {                                                                                \
+        int s_ = (expr);                                                                \
+        if (s_ != HG_OK) return s_;                                                     \
+    } while (0)
+
+constexpr int kMaxP = 255;          // cluster ids are uint8
+constexpr int kMaxNga = 32768;      // GA mask kernels keep one mask per warp in smem
+
+struct DevInst {
+    int n, p;
+    int nw;        // 32-bit words per hub mask
+    int ps;        // row stride (doubles) of T tables: p rounded up to even
+    int npad;      // row stride (bytes) of cluster-id rows
+    int weights_exact;
+    double chi, alpha, delta;
+    const double* C;
+    const double* Ct;
+    const double* W;
+    const double* O;
+    const double* D;
+    const double* wOD;
+    const int32_t* rank;
+};
+
+// fitness tiling chosen per instance (see fitness_plan)
+struct FitPlan {
+    int variant;      // index into the kernel table
+    int rw, cj;       // rows per warp, columns per lane
+    int tr, tc;       // tile rows (16*rw) / columns (32*cj)
+    int trn, tcn, tiles;
+    int g;            // individuals per pipeline stage
+    int blocks_per_sm;
+    size_t smem;
+};
+
+FitPlan fitness_plan(const DevInst& I, int sm_count);
+int prepare_fitness(const FitPlan& P);
+
+// ---- launchers (k_eval.cu) -------------------------------------------------
+int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStream_t s);
+int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s);
+int launch_transpose(const double* src, double* dst, int n, cudaStream_t s);
+int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s);
+int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, double* T,
+                    double* legs, int32_t* alloc, cudaStream_t s);
+int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
+                      uint8_t* cl, double* T, double* legs, cudaStream_t s);
+int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
+                   const double* T, double* part, int grid, cudaStream_t s);
+int launch_finalize(const DevInst& I, const FitPlan& P, int64_t B, const double* legs,
+                    const double* part, double* out, cudaStream_t s);
+
+// ---- launchers (k_ga.cu) ---------------------------------------------------
+int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n, int nw,
+                         cudaStream_t s);
+int launch_bits_to_bytes(const uint32_t* bits, uint8_t* bytes, int64_t B, int n, int nw,
+                         cudaStream_t s);
+int launch_correct(const DevInst& I, int64_t B, const uint32_t* bits, int hmax, int32_t* hubs,
+                   cudaStream_t s);
+int launch_splice(int64_t B, int n, int nw, const uint32_t* a, const uint32_t* b,
+                  const int64_t* cuts, uint32_t* c1, uint32_t* c2, cudaStream_t s);
+int launch_swap_given(int64_t B, int n, int nw, uint32_t* bits, const int64_t* r_close,
+                      const int64_t* r_open, cudaStream_t s);
+
+struct GaDev {
+    int n, p, nw;
+    int nloc, pop, strength, strict_mode;
+    int island_lo;
+    uint32_t* anc;        // [nloc][nw]
+    uint32_t* popbits;    // [B][nw]
+    uint32_t* kids;       // [B][nw]
+    int32_t* kcount;      // [B]
+    int32_t* moff;        // [B]
+    int32_t* nondeg;      // [nloc]
+    int32_t* khubs;       // [B][p]   (the population's hubs buffer)
+    const double* kraw;   // [B][4]   (the population's out buffer)
+    double* champ_raw;    // [nloc]
+    int32_t* champ_hubs;  // [nloc][p]
+    double* best_raw;     // [nloc]
+    int32_t* best_hubs;   // [nloc][p]
+    uint64_t* st;         // [nloc][3] stream states
+    uint64_t* ctr;        // [nloc][3] draws consumed
+    const int32_t* inc;   // [p] round ancestor
+};
+
+int launch_round_begin(const GaDev& G, cudaStream_t s);
+int launch_build_pop(const GaDev& G, cudaStream_t s);
+int launch_crossover(const GaDev& G, cudaStream_t s);
+int launch_mut_scan(const GaDev& G, cudaStream_t s);
+int launch_mutate(const GaDev& G, cudaStream_t s);
+int launch_select(const GaDev& G, cudaStream_t s);
+
+// ---- SplitMix64 (hm/rng.py:43-48, 84-89) --------------------------------------
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// k-th output (1-based) of the stream whose state is s
+__host__ __device__ __forceinline__ uint64_t sm_draw(uint64_t s, uint64_t k) {
+    return mix64(s + k * kGolden);
+}
+
+// int(random() * bound) with random() = (x >> 11) * 2^-53 (hm/rng.py:74-82)
+__device__ __forceinline__ int below(uint64_t x, int bound) {
+    double u = __dmul_rn((double)(x >> 11), 0x1p-53);
+    return (int)__dmul_rn(u, (double)bound);
+}
+
+inline uint64_t host_stream_key(uint64_t seed, const uint64_t* keys, int nkeys) {
+    uint64_t s = mix64(seed);
+    for (int i = 0; i < nkeys; ++i) s = mix64(s ^ mix64(keys[i] + kGolden));
+    return s;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+}  // namespace hg

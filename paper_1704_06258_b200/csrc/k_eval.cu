@@ -1,0 +1,608 @@
+// K2 (nearest-hub allocation + spoke legs + hub-cost tables) and K3 (population
+// fitness: sum_ij W_ij T_b[c_b(i)][c_b(j)]) for sm_100a.
+//
+// Reference: allocate_to_nearest (hm/model.py:202-207) and _components
+// (hm/evaluation.py:103-120).  The transfer term is evaluated in its gather
+// form S_T = sum_ij W_ij C[a_i][a_j] (the reference's own batched screen uses
+// the same formulation, hm/oracle.py:126-127); it equals sum_kl F_kl C[h_k][h_l]
+// up to fp64 summation order.
+
+#include <cooperative_groups.h>
+#include <cuda_pipeline.h>
+
+#include "hg_internal.cuh"
+
+namespace hg {
+
+// ----------------------------------------------------------------------------
+// small utilities
+// ----------------------------------------------------------------------------
+
+__global__ void k_i64_to_i32(const int64_t* __restrict__ s, int32_t* __restrict__ d, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = (int32_t)s[i];
+}
+
+__global__ void k_i32_to_i64(const int32_t* __restrict__ s, int64_t* __restrict__ d, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
+static int grid_for(int64_t m, int block) {
+    int64_t g = ceil_div(m, block);
+    if (g > 148 * 32) g = 148 * 32;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStream_t s) {
+    if (count <= 0) return HG_OK;
+    k_i64_to_i32<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s) {
+    if (count <= 0) return HG_OK;
+    k_i32_to_i64<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// 32x32 smem-tiled transpose (padding column against bank conflicts)
+__global__ void k_transpose(const double* __restrict__ a, double* __restrict__ t, int n) {
+    __shared__ double tile[32][33];
+    int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        int i = by + r, j = bx + threadIdx.x;
+        if (i < n && j < n) tile[r][threadIdx.x] = a[(size_t)i * n + j];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        int i = bx + r, j = by + threadIdx.x;
+        if (i < n && j < n) t[(size_t)i * n + j] = tile[threadIdx.x][r];
+    }
+}
+
+int launch_transpose(const double* src, double* dst, int n, cudaStream_t s) {
+    dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
+    k_transpose<<<grid, dim3(32, 8), 0, s>>>(src, dst, n);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+__global__ void k_check_symmetric(const double* __restrict__ C, int n, int* flag) {
+    int64_t total = (int64_t)n * n;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int i = (int)(x / n), j = (int)(x % n);
+        if (j > i && C[x] != C[(size_t)j * n + i]) *flag = 0;
+    }
+}
+
+int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s) {
+    k_check_symmetric<<<grid_for((int64_t)n * n, 256), 256, 0, s>>>(C, n, flag);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// block reduction of two doubles in a fixed order (deterministic)
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int NT>
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch) {
+    constexpr int NWARP = NT / 32;
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+        scratch[warp] = a;
+        scratch[NWARP + warp] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sa = 0.0, sb = 0.0;
+        for (int w = 0; w < NWARP; ++w) {
+            sa += scratch[w];
+            sb += scratch[NWARP + w];
+        }
+        a = sa;
+        b = sb;
+    }
+}
+
+// ----------------------------------------------------------------------------
+// K2 -- nearest-hub allocation (hm/model.py:202-207)
+//   one CTA per individual; thread owns nodes i = tid, tid+NT, ...;
+//   argmin over the p hubs reads Ct[h][i] (coalesced in i), strict '<' keeps
+//   the first (lowest-index) minimum, then a hub node is forced onto itself.
+//   Emits the cluster ids, the per-individual hub-cost table T and the two
+//   spoke-leg sums.
+// ----------------------------------------------------------------------------
+
+constexpr int kAllocThreads = 256;
+
+__global__ void __launch_bounds__(kAllocThreads)
+k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
+           double* __restrict__ T, double* __restrict__ legs, int32_t* __restrict__ alloc) {
+    extern __shared__ int32_t hs[];  // p
+    __shared__ double scratch[2 * (kAllocThreads / 32)];
+    const int n = I.n, p = I.p;
+    const int64_t b = blockIdx.x;
+    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = hubs[b * p + k];
+    __syncthreads();
+
+    double so = 0.0, sd = 0.0;
+    uint8_t* clb = cl + b * I.npad;
+    for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
+        int c = 0;
+        if (i < n) {
+            int h0 = hs[0];
+            double best = I.Ct[(size_t)h0 * n + i];
+            int bk = 0, self = (h0 == i) ? 0 : -1;
+#pragma unroll 4
+            for (int k = 1; k < p; ++k) {
+                int h = hs[k];
+                double d = I.Ct[(size_t)h * n + i];
+                if (d < best) {
+                    best = d;
+                    bk = k;
+                }
+                if (h == i) self = k;
+            }
+            double leg = best;
+            if (self >= 0) {  // hubs serve themselves; C[h][h] == 0
+                bk = self;
+                leg = 0.0;
+            }
+            so += I.O[i] * leg;
+            sd += I.D[i] * leg;
+            c = bk;
+            if (alloc) alloc[b * n + i] = hs[bk];
+        }
+        clb[i] = (uint8_t)c;
+    }
+    double* Tb = T + b * (int64_t)p * I.ps;
+    for (int x = threadIdx.x; x < p * p; x += kAllocThreads) {
+        int k = x / p, l = x - k * p;
+        Tb[k * I.ps + l] = I.C[(size_t)hs[k] * n + hs[l]];
+    }
+    block_sum2<kAllocThreads>(so, sd, scratch);
+    if (threadIdx.x == 0) {
+        legs[2 * b] = so;
+        legs[2 * b + 1] = sd;
+    }
+}
+
+int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, double* T,
+                    double* legs, int32_t* alloc, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    k_allocate<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, cl, T, legs,
+                                                                          alloc);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// same products for an arbitrary feasible allocation (objective() of any
+// Solution, hm/evaluation.py:86-120): cluster = position of alloc[i] in hubs
+__global__ void __launch_bounds__(kAllocThreads)
+k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restrict__ alloc,
+             uint8_t* __restrict__ cl, double* __restrict__ T, double* __restrict__ legs) {
+    extern __shared__ int32_t hs[];
+    __shared__ double scratch[2 * (kAllocThreads / 32)];
+    const int n = I.n, p = I.p;
+    const int64_t b = blockIdx.x;
+    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = hubs[b * p + k];
+    __syncthreads();
+    double so = 0.0, sd = 0.0;
+    uint8_t* clb = cl + b * I.npad;
+    for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
+        int c = 0;
+        if (i < n) {
+            int a = alloc[b * n + i];
+            int lo = 0, hi = p - 1;  // hubs sorted; a is one of them (validated by caller)
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (hs[mid] < a) lo = mid + 1; else hi = mid;
+            }
+            c = lo;
+            double leg = I.C[(size_t)i * n + a];
+            so += I.O[i] * leg;
+            sd += I.D[i] * leg;
+        }
+        clb[i] = (uint8_t)c;
+    }
+    double* Tb = T + b * (int64_t)p * I.ps;
+    for (int x = threadIdx.x; x < p * p; x += kAllocThreads) {
+        int k = x / p, l = x - k * p;
+        Tb[k * I.ps + l] = I.C[(size_t)hs[k] * n + hs[l]];
+    }
+    block_sum2<kAllocThreads>(so, sd, scratch);
+    if (threadIdx.x == 0) {
+        legs[2 * b] = so;
+        legs[2 * b + 1] = sd;
+    }
+}
+
+int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
+                      uint8_t* cl, double* T, double* legs, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    k_from_alloc<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, alloc, cl, T,
+                                                                            legs);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// K3 -- population fitness, transfer term.
+//
+// A CTA of 16 warps owns a W tile of TR = 16*RW rows x TC = 32*CJ columns held
+// in REGISTERS (warp w: rows i0+w*RW.., lane: columns j0+lane*CJ..), and streams
+// individuals through it.  Per individual b the pipeline stages into smem
+//   Ts[r][0..p) = T_b[c_b(i0+r)][.]   (the tile rows' hub-cost rows, TR x ps)
+//   Cs[0..TC)   = c_b(j0..j0+TC)       (column cluster ids)
+// with cp.async (3 stages x G individuals), and every element costs one
+// smem gather Ts[r][c_b(j)] + one DFMA.  Per (b, tile) the CTA reduces in a
+// fixed order and writes one partial; k_finalize sums the partials of b in a
+// fixed order, so results do not depend on batch size, grid or placement.
+//
+// Work = (tile, group of G individuals) units, ordered chunk-major so the T
+// tables of the individuals in flight stay L2-resident; each CTA takes one
+// contiguous range of units (balanced to within one unit), reloading its W
+// registers only when the tile changes.
+// ----------------------------------------------------------------------------
+
+constexpr int kFitWarps = 16;
+constexpr int kFitThreads = kFitWarps * 32;
+constexpr int kFitStages = 3;
+constexpr int kFitMaxG = 8;
+
+struct FitArgs {
+    DevInst I;
+    const uint8_t* cl;
+    const double* T;
+    double* part;
+    int64_t B;
+    int tcn, tiles;
+    int G;
+    int64_t chunk;         // individuals per chunk (multiple of G)
+    int64_t full_chunks;   // B / chunk
+    int64_t gpc;           // groups per full chunk per tile = chunk / G
+    int64_t gl;            // groups per tile in the last (partial) chunk
+    int64_t q_full;        // units in the full chunks
+    int64_t q_total;
+};
+
+struct Unit {
+    int tile;
+    int64_t b0;
+    int cnt;
+};
+
+__device__ __forceinline__ Unit decode_unit(const FitArgs& A, int64_t q) {
+    Unit u;
+    if (q < A.q_full) {
+        int64_t per = (int64_t)A.tiles * A.gpc;
+        int64_t c = q / per, r = q - c * per;
+        u.tile = (int)(r / A.gpc);
+        int64_t gq = r - (int64_t)u.tile * A.gpc;
+        u.b0 = c * A.chunk + gq * A.G;
+        u.cnt = A.G;
+    } else {
+        int64_t r = q - A.q_full;
+        u.tile = (int)(r / A.gl);
+        int64_t gq = r - (int64_t)u.tile * A.gl;
+        u.b0 = A.full_chunks * A.chunk + gq * A.G;
+        int64_t left = A.B - u.b0;
+        u.cnt = (int)(left < A.G ? left : A.G);
+    }
+    return u;
+}
+
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+    __pipeline_memcpy_async(dst, src, 16);
+}
+
+template <int RW, int CJ>
+__device__ __forceinline__ void issue_unit(const FitArgs& A, const Unit& u, double* Ts,
+                                           uint8_t* Cs) {
+    constexpr int TR = kFitWarps * RW, TC = 32 * CJ;
+    const int ps = A.I.ps, p = A.I.p, npad = A.I.npad;
+    const int tr = u.tile / A.tcn, tc = u.tile - tr * A.tcn;
+    const int i0 = tr * TR, j0 = tc * TC;
+    const int rowchunks = ps >> 1;           // 16 B chunks per T row
+    const int tchunks = TR * rowchunks;
+    constexpr int cchunks = TC / 16 > 0 ? TC / 16 : 1;
+    const int per = tchunks + cchunks;
+    const int total = u.cnt * per;
+    for (int x = threadIdx.x; x < total; x += kFitThreads) {
+        int g = x / per, y = x - g * per;
+        int64_t b = u.b0 + g;
+        if (y < tchunks) {
+            int r = y / rowchunks, part = y - r * rowchunks;
+            int cid = A.cl[b * npad + i0 + r];
+            const double* src = A.T + ((b * p + cid) * (int64_t)ps + part * 2);
+            cp16(Ts + ((size_t)(g * TR + r) * ps + part * 2), src);
+        } else {
+            int k = y - tchunks;
+            if (TC >= 16) {
+                cp16(Cs + g * TC + k * 16, A.cl + b * npad + j0 + k * 16);
+            }
+        }
+    }
+    if (TC < 16) {  // CJ == 0 never; kept for completeness
+        for (int x = threadIdx.x; x < u.cnt * TC; x += kFitThreads) {
+            int g = x / TC, k = x - g * TC;
+            Cs[g * TC + k] = A.cl[(u.b0 + g) * npad + j0 + k];
+        }
+    }
+}
+
+template <int CJ>
+__device__ __forceinline__ void load_cids(const uint8_t* p, uint32_t (&cw)[(CJ + 3) / 4]) {
+    if constexpr (CJ >= 16) {
+#pragma unroll
+        for (int v = 0; v < CJ / 16; ++v) {
+            uint4 x = reinterpret_cast<const uint4*>(p)[v];
+            cw[4 * v + 0] = x.x;
+            cw[4 * v + 1] = x.y;
+            cw[4 * v + 2] = x.z;
+            cw[4 * v + 3] = x.w;
+        }
+    } else if constexpr (CJ == 8) {
+        uint2 x = *reinterpret_cast<const uint2*>(p);
+        cw[0] = x.x;
+        cw[1] = x.y;
+    } else if constexpr (CJ == 4) {
+        cw[0] = *reinterpret_cast<const uint32_t*>(p);
+    } else if constexpr (CJ == 2) {
+        cw[0] = *reinterpret_cast<const uint16_t*>(p);
+    } else {
+        cw[0] = *p;
+    }
+}
+
+template <int RW, int CJ>
+__global__ void __launch_bounds__(kFitThreads, 1) k_fitness(FitArgs A) {
+    constexpr int TR = kFitWarps * RW, TC = 32 * CJ;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int ps = A.I.ps, n = A.I.n;
+    const int G = A.G;
+    const size_t ts_stage = (size_t)G * TR * ps;      // doubles
+    double* Ts0 = reinterpret_cast<double*>(smem);
+    uint8_t* Cs0 = reinterpret_cast<uint8_t*>(Ts0 + kFitStages * ts_stage);
+    double* red = reinterpret_cast<double*>(Cs0 + kFitStages * G * TC + 16);  // [2][G][16]
+    red = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red) + 15) & ~uintptr_t(15));
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t q0 = A.q_total * blockIdx.x / gridDim.x;
+    const int64_t q1 = A.q_total * (blockIdx.x + 1) / gridDim.x;
+    if (q0 >= q1) return;
+
+    // prologue
+#pragma unroll
+    for (int s = 0; s < kFitStages - 1; ++s) {
+        if (q0 + s < q1) {
+            Unit u = decode_unit(A, q0 + s);
+            issue_unit<RW, CJ>(A, u, Ts0 + s * ts_stage, Cs0 + s * G * TC);
+        }
+        __pipeline_commit();
+    }
+
+    double w[RW][CJ];
+    int cur_tile = -1;
+    Unit prev;
+    prev.cnt = 0;
+    prev.tile = 0;
+    prev.b0 = 0;
+
+    for (int64_t k = 0; q0 + k < q1; ++k) {
+        const Unit u = decode_unit(A, q0 + k);
+        if (u.tile != cur_tile) {
+            cur_tile = u.tile;
+            const int tr = u.tile / A.tcn, tc = u.tile - tr * A.tcn;
+            const int jb = tc * TC + lane * CJ;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const int i = tr * TR + warp * RW + r;
+#pragma unroll
+                for (int q = 0; q < CJ; ++q) {
+                    const int j = jb + q;
+                    w[r][q] = (i < n && j < n) ? __ldg(A.I.W + (size_t)i * n + j) : 0.0;
+                }
+            }
+        }
+        __pipeline_wait_prior(kFitStages - 2);
+        __syncthreads();
+
+        // finish the previous unit's reduction (its red buffer is complete)
+        if (prev.cnt > 0 && threadIdx.x < prev.cnt) {
+            const double* rp = red + ((k - 1) & 1) * kFitMaxG * kFitWarps + threadIdx.x * kFitWarps;
+            double s = 0.0;
+#pragma unroll
+            for (int x = 0; x < kFitWarps; ++x) s += rp[x];
+            A.part[(prev.b0 + threadIdx.x) * A.tiles + prev.tile] = s;
+        }
+
+        const int st = (int)(k % kFitStages);
+        const double* Ts = Ts0 + st * ts_stage;
+        const uint8_t* Cs = Cs0 + st * G * TC;
+        double* rk = red + (k & 1) * kFitMaxG * kFitWarps;
+        for (int g = 0; g < u.cnt; ++g) {
+            uint32_t cw[(CJ + 3) / 4];
+            load_cids<CJ>(Cs + g * TC + lane * CJ, cw);
+            // two independent DFMA chains per row keep the FP64 pipe fed
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const double* Tr = Ts + (size_t)(g * TR + warp * RW + r) * ps;
+#pragma unroll
+                for (int q = 0; q < CJ; ++q) {
+                    const uint32_t cid = (cw[q >> 2] >> ((q & 3) * 8)) & 0xffu;
+                    if (q & 1) acc1 = fma(w[r][q], Tr[cid], acc1);
+                    else acc0 = fma(w[r][q], Tr[cid], acc0);
+                }
+            }
+            double acc = warp_sum(acc0 + acc1);
+            if (lane == 0) rk[g * kFitWarps + warp] = acc;
+        }
+        prev = u;
+
+        // refill the stage consumed in the previous iteration
+        const int64_t qn = q0 + k + kFitStages - 1;
+        if (qn < q1) {
+            const int sn = (int)((k + kFitStages - 1) % kFitStages);
+            Unit un = decode_unit(A, qn);
+            issue_unit<RW, CJ>(A, un, Ts0 + sn * ts_stage, Cs0 + sn * G * TC);
+        }
+        __pipeline_commit();
+    }
+    __syncthreads();
+    if (prev.cnt > 0 && threadIdx.x < prev.cnt) {
+        const int64_t kl = q1 - q0 - 1;
+        const double* rp = red + (kl & 1) * kFitMaxG * kFitWarps + threadIdx.x * kFitWarps;
+        double s = 0.0;
+#pragma unroll
+        for (int x = 0; x < kFitWarps; ++x) s += rp[x];
+        A.part[(prev.b0 + threadIdx.x) * A.tiles + prev.tile] = s;
+    }
+}
+
+// kernel table: (RW, CJ)
+using FitKernel = void (*)(FitArgs);
+struct FitVariant {
+    int rw, cj;
+    FitKernel fn;
+};
+static const FitVariant kVariants[] = {
+    {2, 16, k_fitness<2, 16>},  // 32 x 512 tiles: n >= ~400
+    {2, 8, k_fitness<2, 8>},    // 32 x 256
+    {2, 4, k_fitness<2, 4>},    // 32 x 128
+    {1, 2, k_fitness<1, 2>},    // 16 x 64
+    {1, 1, k_fitness<1, 1>},    // 16 x 32: tiny instances
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+static size_t fit_smem(int rw, int cj, int g, int ps) {
+    size_t tr = kFitWarps * rw, tc = 32 * cj;
+    size_t bytes = kFitStages * (size_t)g * tr * ps * sizeof(double);
+    bytes += kFitStages * (size_t)g * tc + 16;
+    bytes = (bytes + 15) & ~size_t(15);
+    bytes += 2 * kFitMaxG * kFitWarps * sizeof(double);
+    return bytes;
+}
+
+int prepare_fitness(const FitPlan& P) {
+    HG_CUDA(cudaFuncSetAttribute(kVariants[P.variant].fn,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    return HG_OK;
+}
+
+FitPlan fitness_plan(const DevInst& I, int sm_count) {
+    (void)sm_count;
+    // pick the variant with the least padded area; ties -> the wider tile
+    int best = 0;
+    double best_cost = 1e300;
+    for (int v = 0; v < kNumVariants; ++v) {
+        int tr = kFitWarps * kVariants[v].rw, tc = 32 * kVariants[v].cj;
+        double area = (double)round_up(I.n, tr) * (double)round_up(I.n, tc);
+        // mild preference for wide tiles: T-row traffic per element ~ ps / tc
+        double cost = area * (1.0 + 0.5 * (double)I.ps / (double)tc);
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best = v;
+        }
+    }
+    FitPlan P{};
+    P.variant = best;
+    P.rw = kVariants[best].rw;
+    P.cj = kVariants[best].cj;
+    P.tr = kFitWarps * P.rw;
+    P.tc = 32 * P.cj;
+    P.g = kFitMaxG;
+    while (P.g > 1 && fit_smem(P.rw, P.cj, P.g, I.ps) > 200 * 1024) P.g >>= 1;
+    P.smem = fit_smem(P.rw, P.cj, P.g, I.ps);
+    P.trn = (int)ceil_div(I.n, P.tr);
+    P.tcn = (int)(round_up(I.n, P.tc) / P.tc);
+    P.tiles = P.trn * P.tcn;
+    P.blocks_per_sm = 1;
+    return P;
+}
+
+int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
+                   const double* T, double* part, int grid, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    FitArgs A;
+    A.I = I;
+    A.cl = cl;
+    A.T = T;
+    A.part = part;
+    A.B = B;
+    A.tcn = P.tcn;
+    A.tiles = P.tiles;
+    A.G = P.g;
+    // keep the T tables + cluster rows of one chunk within ~48 MB of L2
+    const double per_ind = (double)I.p * I.ps * 8.0 + (double)I.npad;
+    int64_t chunk = (int64_t)(48.0 * 1024 * 1024 / per_ind);
+    chunk = chunk / P.g * P.g;
+    if (chunk < P.g) chunk = P.g;
+    if (chunk > round_up(B, P.g)) chunk = round_up(B, P.g);
+    A.chunk = chunk;
+    A.full_chunks = B / chunk;
+    A.gpc = chunk / P.g;
+    const int64_t rem = B - A.full_chunks * chunk;
+    A.gl = ceil_div(rem, P.g);
+    A.q_full = A.full_chunks * (int64_t)P.tiles * A.gpc;
+    A.q_total = A.q_full + (int64_t)P.tiles * A.gl;
+    int g = grid;
+    if (g > A.q_total) g = (int)A.q_total;
+    FitKernel fn = kVariants[P.variant].fn;
+    fn<<<g, kFitThreads, P.smem, s>>>(A);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// finalise: S_T(b) = sum over tiles in a fixed order; raw = (coll + tran) + dist
+// (hm/evaluation.py:93, 110-119).  One warp per individual.
+// ----------------------------------------------------------------------------
+
+__global__ void k_finalize(DevInst I, int64_t B, int tiles, const double* __restrict__ legs,
+                           const double* __restrict__ part, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (b >= B) return;
+    double s = 0.0;
+    for (int t = lane; t < tiles; t += 32) s += part[b * tiles + t];
+    s = warp_sum(s);
+    if (lane == 0) {
+        const double coll = I.chi * legs[2 * b];
+        const double dist = I.delta * legs[2 * b + 1];
+        const double tran = I.alpha * s;
+        out[4 * b + 0] = coll;
+        out[4 * b + 1] = tran;
+        out[4 * b + 2] = dist;
+        out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
+    }
+}
+
+int launch_finalize(const DevInst& I, const FitPlan& P, int64_t B, const double* legs,
+                    const double* part, double* out, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    const int threads = 256;
+    const int64_t blocks = ceil_div(B * 32, threads);
+    k_finalize<<<(unsigned)blocks, threads, 0, s>>>(I, B, P.tiles, legs, part, out);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+}  // namespace hg

@@ -1,0 +1,571 @@
+// K4a-c, K5: island-GA operators on bit-packed hub masks, sm_100a.
+//
+// Reference: _run_island (hm/engine.py:138-167) and the operators
+// crossover_hub_arrays / swap_random_hub_spoke / correct_hub_set
+// (hm/operators.py:41-124).  Every random draw is replayed by INDEX on the
+// counter-based SplitMix64 streams of the reference (hm/rng.py:84-89):
+//   population stream: individual m (m >= 1 elitist, m >= 0 strict), swap s
+//                      uses draws ctr + 2*((m-e)*strength + s) + {1, 2}
+//                      (none when p == n: the swap is the identity);
+//   crossover stream:  pair j uses draw ctr + j + 1 (none when n == 1);
+//   mutation stream:   child c uses draws ctr + 2*o_c + {1, 2} where o_c counts
+//                      the non-degenerate children before c (a child that is
+//                      all-open or all-closed consumes nothing).
+// so islands, pairs and children are processed in parallel yet consume
+// exactly the reference's draw sequence.
+
+#include <cub/block/block_scan.cuh>
+
+#include "hg_internal.cuh"
+
+namespace hg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// r-th (0-based) set bit (want_set) or clear bit (!want_set) among [0, n) of
+// an nw-word mask in shared memory; uniform across the warp.
+__device__ int warp_select(const uint32_t* m, int nw, int n, int r, bool want_set, int lane) {
+    int base = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+        const int w = w0 + lane;
+        uint32_t word = 0;
+        if (w < nw) {
+            word = m[w];
+            if (!want_set) {
+                word = ~word;
+                if (w == nw - 1 && (n & 31)) word &= (1u << (n & 31)) - 1u;
+            }
+        }
+        const int c = __popc(word);
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const int total = __shfl_sync(kFull, inc, 31);
+        if (r < base + total) {
+            const unsigned hit = __ballot_sync(kFull, r < base + inc);
+            const int L = __ffs(hit) - 1;
+            const int excl = __shfl_sync(kFull, inc - c, L);
+            uint32_t wd = __shfl_sync(kFull, word, L);
+            int k = r - base - excl;
+            for (int t = 0; t < k; ++t) wd &= wd - 1u;
+            return (w0 + L) * 32 + (__ffs(wd) - 1);
+        }
+        base += total;
+    }
+    return -1;
+}
+
+// ---------------------------------------------------------------------------
+// byte masks <-> bit masks
+// ---------------------------------------------------------------------------
+
+__global__ void k_bytes_to_bits(const uint8_t* __restrict__ bytes, uint32_t* __restrict__ bits,
+                                int64_t B, int n, int nw) {
+    const int64_t total = B * nw;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = x / nw;
+        const int w = (int)(x - b * nw);
+        uint32_t v = 0;
+        for (int t = 0; t < 32; ++t) {
+            const int i = w * 32 + t;
+            if (i < n && bytes[b * n + i]) v |= 1u << t;
+        }
+        bits[x] = v;
+    }
+}
+
+__global__ void k_bits_to_bytes(const uint32_t* __restrict__ bits, uint8_t* __restrict__ bytes,
+                                int64_t B, int n, int nw) {
+    const int64_t total = B * n;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = x / n;
+        const int i = (int)(x - b * n);
+        bytes[x] = (bits[b * nw + (i >> 5)] >> (i & 31)) & 1u;
+    }
+}
+
+static int grid_for(int64_t m, int block) {
+    int64_t g = ceil_div(m, block);
+    if (g > 148 * 32) g = 148 * 32;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n, int nw,
+                         cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    k_bytes_to_bits<<<grid_for(B * nw, 256), 256, 0, s>>>(bytes, bits, B, n, nw);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+int launch_bits_to_bytes(const uint32_t* bits, uint8_t* bytes, int64_t B, int n, int nw,
+                         cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    k_bits_to_bytes<<<grid_for(B * n, 256), 256, 0, s>>>(bits, bytes, B, n, nw);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K4c -- correction (hm/operators.py:69-101), one CTA per mask.
+// ---------------------------------------------------------------------------
+
+constexpr int kCorrThreads = 128;
+using CorrScan = cub::BlockScan<int, kCorrThreads>;
+
+// extract the set bits of the smem mask, in order, into H; returns the count
+__device__ int block_extract(const uint32_t* mask, int nw, int32_t* H,
+                             typename CorrScan::TempStorage& tmp, int* bcast) {
+    int base = 0;
+    for (int w0 = 0; w0 < nw; w0 += kCorrThreads) {
+        const int w = w0 + threadIdx.x;
+        const uint32_t word = w < nw ? mask[w] : 0u;
+        int off, total;
+        CorrScan(tmp).ExclusiveSum(__popc(word), off, total);
+        uint32_t v = word;
+        int k = base + off;
+        while (v) {
+            H[k++] = w * 32 + (__ffs(v) - 1);
+            v &= v - 1u;
+        }
+        base += total;
+        __syncthreads();
+    }
+    (void)bcast;
+    return base;
+}
+
+__global__ void __launch_bounds__(kCorrThreads)
+k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __restrict__ hubs_out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ typename CorrScan::TempStorage tmp;
+    __shared__ int s_kill;
+    const int n = I.n, p = I.p, nw = I.nw;
+    const int64_t b = blockIdx.x;
+    double* carried = reinterpret_cast<double*>(sm);                 // [hmax]
+    uint32_t* mask = reinterpret_cast<uint32_t*>(carried + hmax);     // [nw]
+    int32_t* H = reinterpret_cast<int32_t*>(mask + nw);               // [hmax]
+    int16_t* cls = reinterpret_cast<int16_t*>(H + hmax);              // [n] (inexact weights only)
+
+    int cnt = 0;
+    for (int w = threadIdx.x; w < nw; w += kCorrThreads) {
+        const uint32_t v = bits[b * nw + w];
+        mask[w] = v;
+        cnt += __popc(v);
+    }
+    int h;
+    {
+        int dummy;
+        CorrScan(tmp).ExclusiveSum(cnt, dummy, h);
+        __syncthreads();
+    }
+
+    if (h < p) {
+        // deficit: open closed nodes in middle-rank order (hm/operators.py:84-93)
+        int need = p - h;
+        for (int base = 0; need > 0 && base < n; base += kCorrThreads) {
+            const int r = base + threadIdx.x;
+            const int node = r < n ? I.rank[r] : -1;
+            const int closed = (node >= 0 && !((mask[node >> 5] >> (node & 31)) & 1u)) ? 1 : 0;
+            int pre, total;
+            CorrScan(tmp).ExclusiveSum(closed, pre, total);
+            if (closed && pre < need) atomicOr(&mask[node >> 5], 1u << (node & 31));
+            need -= total < need ? total : need;
+            __syncthreads();
+        }
+    }
+    h = block_extract(mask, nw, H, tmp, nullptr);
+    __syncthreads();
+
+    // excess: close the least-loaded hub, one at a time (hm/operators.py:94-100)
+    while (h > p) {
+        for (int k = threadIdx.x; k < h; k += kCorrThreads) carried[k] = 0.0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += kCorrThreads) {
+            int h0 = H[0];
+            double best = I.Ct[(size_t)h0 * n + i];
+            int bk = 0, self = (h0 == i) ? 0 : -1;
+            for (int k = 1; k < h; ++k) {
+                const int hk = H[k];
+                const double d = I.Ct[(size_t)hk * n + i];
+                if (d < best) {
+                    best = d;
+                    bk = k;
+                }
+                if (hk == i) self = k;
+            }
+            if (self >= 0) bk = self;
+            if (I.weights_exact)
+                atomicAdd(&carried[bk], I.wOD[i]);  // integer-valued: order-free, exact
+            else
+                cls[i] = (int16_t)bk;
+        }
+        __syncthreads();
+        if (!I.weights_exact) {
+            // index-ordered accumulation per hub, as np.bincount does
+            for (int k = threadIdx.x; k < h; k += kCorrThreads) {
+                double acc = 0.0;
+                for (int i = 0; i < n; ++i)
+                    if (cls[i] == k) acc += I.wOD[i];
+                carried[k] = acc;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x < 32) {
+            // first minimum of carried[0..h)
+            double bv = 0.0;
+            int bi = -1;
+            for (int k = threadIdx.x; k < h; k += 32) {
+                const double v = carried[k];
+                if (bi < 0 || v < bv) {
+                    bv = v;
+                    bi = k;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(kFull, bv, o);
+                const int oi = __shfl_xor_sync(kFull, bi, o);
+                if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            if (threadIdx.x == 0) s_kill = bi;
+        }
+        __syncthreads();
+        // delete H[kill] (np.delete keeps the order); h is small, shift serially
+        if (threadIdx.x == 0)
+            for (int k = s_kill; k < h - 1; ++k) H[k] = H[k + 1];
+        __syncthreads();
+        --h;
+    }
+    for (int k = threadIdx.x; k < p; k += kCorrThreads) hubs_out[b * p + k] = H[k];
+}
+
+int launch_correct(const DevInst& I, int64_t B, const uint32_t* bits, int hmax, int32_t* hubs,
+                   cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    if (hmax < I.p) hmax = I.p;
+    size_t smem = (size_t)hmax * 8 + (size_t)I.nw * 4 + (size_t)hmax * 4;
+    smem = (smem + 7) & ~size_t(7);
+    if (!I.weights_exact) smem += (size_t)I.n * 2;
+    if (smem > 48 * 1024)
+        HG_CUDA(cudaFuncSetAttribute(k_correct, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    k_correct<<<(unsigned)B, kCorrThreads, smem, s>>>(I, bits, hmax, hubs);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// explicit-draw operators (single-solution API and tests)
+// ---------------------------------------------------------------------------
+
+__global__ void k_splice(int64_t B, int n, int nw, const uint32_t* __restrict__ a,
+                         const uint32_t* __restrict__ bb, const int64_t* __restrict__ cuts,
+                         uint32_t* __restrict__ c1, uint32_t* __restrict__ c2) {
+    const int64_t total = B * nw;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = x / nw;
+        const int w = (int)(x - b * nw);
+        const int64_t cut = cuts[b];
+        const int64_t lo = (int64_t)w * 32;
+        uint32_t m;
+        if (cut >= lo + 32) m = kFull;
+        else if (cut <= lo) m = 0u;
+        else m = (1u << (cut - lo)) - 1u;
+        const uint32_t va = a[x], vb = bb[x];
+        c1[x] = (va & m) | (vb & ~m);
+        c2[x] = (vb & m) | (va & ~m);
+    }
+}
+
+int launch_splice(int64_t B, int n, int nw, const uint32_t* a, const uint32_t* b,
+                  const int64_t* cuts, uint32_t* c1, uint32_t* c2, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    k_splice<<<grid_for(B * nw, 256), 256, 0, s>>>(B, n, nw, a, b, cuts, c1, c2);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+constexpr int kWarpsPerBlock = 8;
+
+__global__ void k_swap_given(int64_t B, int n, int nw, uint32_t* __restrict__ bits,
+                             const int64_t* __restrict__ rc, const int64_t* __restrict__ ro) {
+    extern __shared__ uint32_t wsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+    if (b >= B) return;
+    uint32_t* m = wsm + warp * nw;
+    for (int w = lane; w < nw; w += 32) m[w] = bits[b * nw + w];
+    __syncwarp();
+    if (rc[b] >= 0) {
+        const int pc = warp_select(m, nw, n, (int)rc[b], true, lane);
+        const int po = warp_select(m, nw, n, (int)ro[b], false, lane);
+        if (lane == 0) {
+            m[pc >> 5] &= ~(1u << (pc & 31));
+            m[po >> 5] |= 1u << (po & 31);
+        }
+        __syncwarp();
+    }
+    for (int w = lane; w < nw; w += 32) bits[b * nw + w] = m[w];
+}
+
+int launch_swap_given(int64_t B, int n, int nw, uint32_t* bits, const int64_t* r_close,
+                      const int64_t* r_open, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    const unsigned blocks = (unsigned)ceil_div(B, kWarpsPerBlock);
+    k_swap_given<<<blocks, kWarpsPerBlock * 32, kWarpsPerBlock * nw * 4, s>>>(B, n, nw, bits,
+                                                                             r_close, r_open);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K4a -- population build (hm/engine.py:148-153): individual 0 is the local
+// ancestor (elitist), the others `strength` swaps of it.  One warp each.
+// ---------------------------------------------------------------------------
+
+__global__ void k_round_begin(GaDev G) {
+    const int li = blockIdx.x;
+    if (li >= G.nloc) return;
+    for (int w = threadIdx.x; w < G.nw; w += blockDim.x) G.anc[(int64_t)li * G.nw + w] = 0u;
+    __syncthreads();
+    for (int k = threadIdx.x; k < G.p; k += blockDim.x) {
+        const int h = G.inc[k];
+        atomicOr(&G.anc[(int64_t)li * G.nw + (h >> 5)], 1u << (h & 31));
+    }
+    if (threadIdx.x == 0) G.best_raw[li] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+}
+
+int launch_round_begin(const GaDev& G, cudaStream_t s) {
+    k_round_begin<<<G.nloc, 128, 0, s>>>(G);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+__global__ void k_build_pop(GaDev G) {
+    extern __shared__ uint32_t wsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gid = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+    const int64_t B = (int64_t)G.nloc * G.pop;
+    if (gid >= B) return;
+    const int li = (int)(gid / G.pop), m = (int)(gid - (int64_t)li * G.pop);
+    const int nw = G.nw, n = G.n, p = G.p;
+    uint32_t* mk = wsm + warp * nw;
+    for (int w = lane; w < nw; w += 32) mk[w] = G.anc[(int64_t)li * nw + w];
+    __syncwarp();
+    const int e = G.strict_mode ? 0 : 1;
+    if (m >= e && p < n) {
+        const uint64_t s = G.st[li * 3 + 0];
+        const uint64_t base = G.ctr[li * 3 + 0] + (uint64_t)(m - e) * G.strength * 2;
+        for (int k = 0; k < G.strength; ++k) {
+            const int r1 = below(sm_draw(s, base + 2 * k + 1), p);
+            const int r2 = below(sm_draw(s, base + 2 * k + 2), n - p);
+            const int pc = warp_select(mk, nw, n, r1, true, lane);
+            const int po = warp_select(mk, nw, n, r2, false, lane);
+            if (lane == 0) {
+                mk[pc >> 5] &= ~(1u << (pc & 31));
+                mk[po >> 5] |= 1u << (po & 31);
+            }
+            __syncwarp();
+        }
+    }
+    for (int w = lane; w < nw; w += 32) G.popbits[gid * nw + w] = mk[w];
+}
+
+int launch_build_pop(const GaDev& G, cudaStream_t s) {
+    const int64_t B = (int64_t)G.nloc * G.pop;
+    const unsigned blocks = (unsigned)ceil_div(B, kWarpsPerBlock);
+    k_build_pop<<<blocks, kWarpsPerBlock * 32, kWarpsPerBlock * G.nw * 4, s>>>(G);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K4b -- crossover (hm/operators.py:41-57) of pairs (2j, 2j+1), one warp each
+// ---------------------------------------------------------------------------
+
+__global__ void k_crossover(GaDev G) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int half = G.pop / 2;
+    const int64_t gid = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+    if (gid >= (int64_t)G.nloc * half) return;
+    const int li = (int)(gid / half), j = (int)(gid - (int64_t)li * half);
+    const int n = G.n, nw = G.nw;
+    int cut = n;  // n == 1: both children are copies, no draw
+    if (n > 1) cut = 1 + below(sm_draw(G.st[li * 3 + 1], G.ctr[li * 3 + 1] + j + 1), n - 1);
+    const int64_t ia = (int64_t)li * G.pop + 2 * j;
+    const uint32_t* a = G.popbits + ia * nw;
+    const uint32_t* bb = a + nw;
+    uint32_t* c1 = G.kids + ia * nw;
+    uint32_t* c2 = c1 + nw;
+    int n1 = 0, n2 = 0;
+    for (int w = lane; w < nw; w += 32) {
+        const int lo = w * 32;
+        uint32_t m;
+        if (cut >= lo + 32) m = kFull;
+        else if (cut <= lo) m = 0u;
+        else m = (1u << (cut - lo)) - 1u;
+        const uint32_t va = a[w], vb = bb[w];
+        const uint32_t x1 = (va & m) | (vb & ~m), x2 = (vb & m) | (va & ~m);
+        c1[w] = x1;
+        c2[w] = x2;
+        n1 += __popc(x1);
+        n2 += __popc(x2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n1 += __shfl_xor_sync(kFull, n1, o);
+        n2 += __shfl_xor_sync(kFull, n2, o);
+    }
+    if (lane == 0) {
+        G.kcount[ia] = n1;
+        G.kcount[ia + 1] = n2;
+    }
+}
+
+int launch_crossover(const GaDev& G, cudaStream_t s) {
+    const int64_t P = (int64_t)G.nloc * (G.pop / 2);
+    const unsigned blocks = (unsigned)ceil_div(P, kWarpsPerBlock);
+    k_crossover<<<blocks, kWarpsPerBlock * 32, 0, s>>>(G);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// per island: exclusive count of non-degenerate children before each child
+constexpr int kScanThreads = 256;
+using MutScan = cub::BlockScan<int, kScanThreads>;
+
+__global__ void k_mut_scan(GaDev G) {
+    __shared__ typename MutScan::TempStorage tmp;
+    const int li = blockIdx.x;
+    int base = 0;
+    for (int m0 = 0; m0 < G.pop; m0 += kScanThreads) {
+        const int m = m0 + threadIdx.x;
+        int flag = 0;
+        if (m < G.pop) {
+            const int c = G.kcount[(int64_t)li * G.pop + m];
+            flag = (c != 0 && c != G.n) ? 1 : 0;
+        }
+        int off, total;
+        MutScan(tmp).ExclusiveSum(flag, off, total);
+        if (m < G.pop) G.moff[(int64_t)li * G.pop + m] = base + off;
+        base += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) G.nondeg[li] = base;
+}
+
+int launch_mut_scan(const GaDev& G, cudaStream_t s) {
+    k_mut_scan<<<G.nloc, kScanThreads, 0, s>>>(G);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// swap mutation of every child (hm/operators.py:113-124, engine.py:157)
+__global__ void k_mutate(GaDev G) {
+    extern __shared__ uint32_t wsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gid = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+    const int64_t B = (int64_t)G.nloc * G.pop;
+    if (gid >= B) return;
+    const int cnt = G.kcount[gid];
+    const int n = G.n, nw = G.nw;
+    if (cnt == 0 || cnt == n) return;  // identity, no draws
+    const int li = (int)(gid / G.pop);
+    uint32_t* mk = wsm + warp * nw;
+    uint32_t* g = G.kids + gid * nw;
+    for (int w = lane; w < nw; w += 32) mk[w] = g[w];
+    __syncwarp();
+    const uint64_t s = G.st[li * 3 + 2];
+    const uint64_t base = G.ctr[li * 3 + 2] + 2ull * (uint64_t)G.moff[gid];
+    const int r1 = below(sm_draw(s, base + 1), cnt);
+    const int r2 = below(sm_draw(s, base + 2), n - cnt);
+    const int pc = warp_select(mk, nw, n, r1, true, lane);
+    const int po = warp_select(mk, nw, n, r2, false, lane);  // closed list before closing
+    if (lane == 0) {
+        mk[pc >> 5] &= ~(1u << (pc & 31));
+        mk[po >> 5] |= 1u << (po & 31);
+    }
+    __syncwarp();
+    for (int w = lane; w < nw; w += 32) g[w] = mk[w];
+}
+
+int launch_mutate(const GaDev& G, cudaStream_t s) {
+    const int64_t B = (int64_t)G.nloc * G.pop;
+    const unsigned blocks = (unsigned)ceil_div(B, kWarpsPerBlock);
+    k_mutate<<<blocks, kWarpsPerBlock * 32, kWarpsPerBlock * G.nw * 4, s>>>(G);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K5 -- island selection (hm/engine.py:162-166): champion = first strict
+// minimum in child order; the local ancestor becomes the champion; the island
+// best keeps the earliest strict minimum across generations.  Also advances
+// the three stream counters by what this generation consumed.
+// ---------------------------------------------------------------------------
+
+__global__ void k_select(GaDev G) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int li = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (li >= G.nloc) return;
+    const int pop = G.pop, p = G.p, nw = G.nw;
+    double bv = 0.0;
+    int bi = -1;
+    for (int m = lane; m < pop; m += 32) {
+        const double v = G.kraw[((int64_t)li * pop + m) * 4 + 3];
+        if (bi < 0 || v < bv) {
+            bv = v;
+            bi = m;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, bv, o);
+        const int oi = __shfl_xor_sync(kFull, bi, o);
+        if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    const int32_t* ch = G.khubs + ((int64_t)li * pop + bi) * p;
+    uint32_t* anc = G.anc + (int64_t)li * nw;
+    for (int w = lane; w < nw; w += 32) anc[w] = 0u;
+    __syncwarp();
+    for (int k = lane; k < p; k += 32) {
+        const int h = ch[k];
+        atomicOr(&anc[h >> 5], 1u << (h & 31));
+        G.champ_hubs[(int64_t)li * p + k] = h;
+    }
+    const bool better = bv < G.best_raw[li];
+    __syncwarp();
+    if (better)
+        for (int k = lane; k < p; k += 32) G.best_hubs[(int64_t)li * p + k] = ch[k];
+    if (lane == 0) {
+        G.champ_raw[li] = bv;
+        if (better) G.best_raw[li] = bv;
+        const int e = G.strict_mode ? 0 : 1;
+        if (p < G.n) G.ctr[li * 3 + 0] += (uint64_t)(pop - e) * G.strength * 2;
+        if (G.n > 1) G.ctr[li * 3 + 1] += (uint64_t)(pop / 2);
+        G.ctr[li * 3 + 2] += 2ull * (uint64_t)G.nondeg[li];
+    }
+}
+
+int launch_select(const GaDev& G, cudaStream_t s) {
+    const int wpb = 4;
+    k_select<<<(unsigned)ceil_div(G.nloc, wpb), wpb * 32, 0, s>>>(G);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+}  // namespace hg

@@ -1,0 +1,280 @@
+"""Parity of the CUDA path against the reference's golden vectors and the
+oracle (needs a B200: marked gpu).
+
+Bars: allocations, corrected hub sets, crossover / swap masks and GA hub
+sets are bit-exact; fp64 costs agree with the reference within 1e-12
+relative (the north star asks 1e-9); GA raw values and traces within 1e-12.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import EVAL_LABELS, GA_LABELS, golden, orc, params_of
+
+import paper_1704_06258_b200 as hg
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+
+
+def inst_from(g, prefix) -> hg.Instance:
+    n, p, chi, alpha, delta = g[f"{prefix}_meta"]
+    return hg.Instance(int(n), int(p), g[f"{prefix}_dist"], g[f"{prefix}_flow"], float(chi),
+                       float(alpha), float(delta))
+
+
+def close(a, b, rel=REL):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.all(np.abs(a - b) <= rel * np.maximum(np.abs(b), 1e-300) + 1e-300)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if hg.device_count() < 1:
+        pytest.fail("no CUDA device: the gpu tests must run on a B200")
+
+
+class TestAllocation:
+    @pytest.mark.parametrize("label", EVAL_LABELS + ["tie", "ovr"])
+    def test_bit_exact_vs_reference(self, label):
+        g = golden("evaluation")
+        inst = inst_from(g, label)
+        got = hg.nearest_allocations(inst, g[f"{label}_hubs"])
+        assert np.array_equal(got, g[f"{label}_alloc"])
+
+    def test_single_api(self):
+        g = golden("evaluation")
+        inst = inst_from(g, "ap")
+        sol = hg.nearest_allocation(g["ap_hubs"][3], inst)
+        assert np.array_equal(sol.alloc, g["ap_alloc"][3])
+        assert hg.validate(sol, inst).ok
+        with pytest.raises(ValueError, match="expected p=10"):
+            hg.nearest_allocation([1, 2], inst)
+
+    def test_ur_vs_oracle(self):
+        inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
+        pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+        pop = hg.random_population(1000, 20, 64)
+        got = hg.nearest_allocations(inst, pop)
+        for b in range(64):
+            assert np.array_equal(got[b], orc.nearest(pr.C, pop[b]))
+
+
+class TestObjective:
+    @pytest.mark.parametrize("label", EVAL_LABELS)
+    def test_population_components(self, label):
+        g = golden("evaluation")
+        inst = inst_from(g, label)
+        out = hg.evaluate_population(inst, g[f"{label}_hubs"])
+        assert close(out, g[f"{label}_comp"])
+
+    @pytest.mark.parametrize("label", EVAL_LABELS)
+    def test_arbitrary_feasible_allocations(self, label):
+        g = golden("evaluation")
+        inst = inst_from(g, label)
+        for hubs, alloc, comp in zip(g[f"{label}_rhubs"], g[f"{label}_ralloc"],
+                                     g[f"{label}_rcomp"]):
+            hub = np.zeros(inst.n, dtype=bool)
+            hub[hubs] = True
+            bd = hg.objective(inst, hg.Solution(hub=hub, alloc=alloc))
+            assert close([bd.collection_cost, bd.transfer_cost, bd.distribution_cost,
+                          bd.raw_total], comp)
+
+    def test_modes_exact(self):
+        g = golden("evaluation")
+        inst = inst_from(g, "cab")
+        sol = hg.nearest_allocation(g["cab_hubs"][0], inst)
+        raw = hg.objective(inst, sol).raw_total
+        assert hg.fitness(inst, sol, hg.FitnessMode.STANDARD_MILLI) == raw * 1e-3
+        assert hg.fitness(inst, sol, hg.FitnessMode.CAB_NORMALIZED) == raw / inst.total_flow
+
+    def test_batch_invariance_bitwise(self):
+        """A hub set's score does not depend on its batch or position."""
+        inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
+        pop = hg.random_population(1000, 20, 300)
+        full = hg.evaluate_population(inst, pop)
+        part = hg.evaluate_population(inst, pop[123:140])
+        assert np.array_equal(full[123:140], part)
+        rev = hg.evaluate_population(inst, pop[::-1])
+        assert np.array_equal(full, rev[::-1])
+
+    @pytest.mark.parametrize("n,p,f", [(1000, 20, (1.0, 0.75, 1.0)), (200, 10, (3.0, 0.75, 2.0)),
+                                       (333, 7, (1.0, 0.5, 2.0)), (25, 3, (1.0, 0.2, 1.0)),
+                                       (90, 50, (1.0, 0.75, 1.0))])
+    def test_vs_oracle_random_configs(self, n, p, f):
+        inst = hg.generate_urand(n, p, 77, f)
+        pr = orc.Problem(n, p, inst.dist, inst.flow, *f)
+        pop = hg.random_population(n, p, 40, key=5)
+        out = hg.evaluate_population(inst, pop)
+        ref = np.array([list(orc.cost_terms(pr, h, orc.nearest(pr.C, h))) for h in pop])
+        ref = np.concatenate([ref, (ref[:, 0] + ref[:, 1] + ref[:, 2])[:, None]], axis=1)
+        assert close(out, ref)
+
+    def test_asymmetric_self_flow(self):
+        pr = orc.stream_problem(24, 40, 6, symmetric=False, self_flow=True, chi=3.0, alpha=0.75,
+                                delta=2.0)
+        inst = hg.Instance(40, 6, pr.C, pr.W, 3.0, 0.75, 2.0)
+        pop = hg.random_population(40, 6, 30, key=9)
+        out = hg.evaluate_population(inst, pop)
+        for b in range(30):
+            a = orc.nearest(pr.C, pop[b])
+            assert np.array_equal(hg.nearest_allocations(inst, pop[b:b + 1])[0], a)
+            assert close(out[b, 3], orc.path_sum(pr, a), rel=1e-9)
+
+    def test_big_instance_linearity(self):
+        """n=6000, p=50 (BASELINE config 4): the transfer term is linear in
+        alpha and in W; check against the oracle on a few individuals."""
+        inst = hg.generate_urand(6000, 50, 1704, (1.0, 0.75, 1.0))
+        pop = hg.random_population(6000, 50, 3)
+        out = hg.evaluate_population(inst, pop)
+        pr = orc.Problem(6000, 50, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+        for b in range(3):
+            a = orc.nearest(pr.C, pop[b])
+            st = 0.75 * orc.transfer_gather(pr, pop[b], a)
+            assert close(out[b, 1], st, rel=1e-11)
+        inst2 = inst.with_factors(alpha=1.5)
+        out2 = hg.evaluate_population(inst2, pop)
+        assert close(out2[:, 1], 2.0 * out[:, 1], rel=1e-14)
+        assert np.array_equal(out2[:, 0], out[:, 0])
+
+
+class TestOperators:
+    def test_correction_vs_reference(self):
+        g = golden("operators")
+        inst = inst_from(g, "op")
+        assert np.array_equal(hg.correct_hub_sets(inst=inst, masks=g["corr_masks"]),
+                              g["corr_hubs"])
+        inst = inst_from(g, "opbig")
+        assert np.array_equal(hg.correct_hub_sets(inst=inst, masks=g["corrbig_masks"]),
+                              g["corrbig_hubs"])
+        assert np.array_equal(hg.correct_hub_set(g["corrbig_masks"][5], inst),
+                              g["corrbig_hubs"][5])
+
+    def test_correction_inexact_weights(self):
+        """Non-integer flows: carried loads are summed in index order (np.bincount)."""
+        pr = orc.stream_problem(31, 30, 4)
+        W = pr.W * 0.1 + 1e-3
+        pr2 = orc.Problem(30, 4, pr.C, W, 1.0, 0.75, 1.0)
+        inst = hg.Instance(30, 4, pr.C, W, 1.0, 0.75, 1.0)
+        rng = np.random.default_rng(3)
+        masks = rng.random((200, 30)) < 0.4
+        got = hg.correct_hub_sets(masks, inst)
+        for m, h in zip(masks, got):
+            assert np.array_equal(h, orc.repair(m, pr2))
+
+    def test_crossover_and_swap_replay(self):
+        g = golden("operators")
+        st = hg.derive_stream(15)
+        for cr, sw in zip(g["xs_cross"], g["xs_swap"]):
+            c1, c2 = hg.crossover_hub_arrays(g["xs_a"], g["xs_b"], st)
+            assert np.array_equal(c1, cr[0]) and np.array_equal(c2, cr[1])
+            assert np.array_equal(hg.swap_random_hub_spoke(c1, st), sw)
+        assert st.state == int(g["xs_state_after"][0])
+
+    def test_perturb_matches_mutation_composition(self):
+        pr = orc.stream_problem(57, 10, 4)
+        inst = hg.Instance(10, 4, pr.C, pr.W, 1.0, 0.75, 1.0)
+        sol = hg.nearest_allocation({0, 2, 5, 8}, inst)
+        got = hg.perturb(sol, inst, hg.derive_stream(14), strength=3)
+        exp = sol
+        rng = hg.derive_stream(14)
+        for _ in range(3):
+            exp = hg.mutation(exp, inst, rng)
+        assert got == exp
+
+    def test_closure_pipelines(self):
+        """crossover -> swap -> correction always yields a feasible solution
+        (reference acceptance criterion 7, batched on the device)."""
+        rng = np.random.default_rng(7)
+        for n, p in ((9, 3), (64, 5), (300, 40)):
+            inst = hg.generate_urand(n, p, 5, (1.0, 0.75, 1.0))
+            masks = rng.random((2000, n)) < rng.random((2000, 1))
+            hubs = hg.correct_hub_sets(masks, inst)
+            assert (np.diff(hubs, axis=1) > 0).all() and hubs.min() >= 0 and hubs.max() < n
+            pr = orc.Problem(n, p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+            for k in range(0, 2000, 97):
+                assert np.array_equal(hubs[k], orc.repair(masks[k], pr))
+
+
+class TestGa:
+    @pytest.mark.parametrize("label", GA_LABELS)
+    def test_solve_replays_reference(self, label):
+        g = golden("ga")
+        inst = inst_from(g, label)
+        params = hg.GaParams(**params_of(g, label))
+        mode = hg.FitnessMode.from_string(str(g[f"{label}_mode"]))
+        rep = hg.solve(inst, params, mode)
+        assert np.array_equal(rep.best_solution.hubs, g[f"{label}_hubs"])
+        assert np.array_equal(rep.best_solution.alloc, g[f"{label}_alloc"])
+        assert close([rep.raw_objective, rep.scaled_fitness], g[f"{label}_raw"])
+        assert close(rep.trace, g[f"{label}_trace"])
+        assert rep.evaluations == int(g[f"{label}_evals"][0])
+        assert not rep.interrupted
+
+    def test_audit_sees_every_evaluation_and_interrupt(self):
+        pr = orc.stream_problem(86, 9, 3)
+        inst = hg.Instance(9, 3, pr.C, pr.W, 1.0, 0.75, 1.0)
+        seen = []
+        params = hg.GaParams(islands=2, pop_size=4, inner_iters=3, outer_iters=2, seed=9)
+        rep = hg.solve(inst, params, hg.FitnessMode.RAW, workers=1,
+                       audit=lambda s: seen.append(hg.validate(s, inst).ok))
+        assert all(seen) and len(seen) == rep.evaluations + 1
+
+        calls = {"k": 0}
+
+        def stop(_s):
+            calls["k"] += 1
+            if calls["k"] > 40:
+                raise KeyboardInterrupt
+
+        pr = orc.stream_problem(93, 9, 3)
+        inst = hg.Instance(9, 3, pr.C, pr.W, 1.0, 0.75, 1.0)
+        params = hg.GaParams(islands=2, pop_size=4, inner_iters=5, outer_iters=5, seed=6)
+        rep = hg.solve(inst, params, hg.FitnessMode.RAW, workers=1, audit=stop)
+        assert rep.interrupted and hg.validate(rep.best_solution, inst).ok
+        assert len(rep.trace) < params.outer_iters
+
+    def test_reaches_restricted_optimum(self):
+        """Reference acceptance criterion 1 on a sample of its instance family."""
+        hits = 0
+        for k in range(20):
+            meta = orc.Stream(orc.stream_key(777, k))
+            n = 5 + meta.below(5)
+            p = 2 + meta.below(2)
+            inst = hg.generate_urand(n, p, 1000 + k, (1.0, 0.75, 1.0))
+            pr = orc.Problem(n, p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+            _, rr = orc.restricted_best(pr)
+            rep = hg.solve(inst, hg.GaParams(islands=8, pop_size=16, inner_iters=20,
+                                             outer_iters=5, seed=k, perturb_strength=2),
+                           hg.FitnessMode.STANDARD_MILLI)
+            hits += abs(rep.raw_objective - rr) <= 1e-12 * rr
+            assert all(b <= a for a, b in zip(rep.trace, rep.trace[1:]))
+        assert hits >= 19
+
+    def test_virtual_shards_identical(self):
+        """Island sharding across devices reproduces the 1-device run: shards
+        of [0, R) run one after another on this GPU with the same exchange."""
+        from paper_1704_06258_b200 import engine
+
+        inst = hg.generate_urand(200, 10, 1704, (3.0, 0.75, 2.0))
+        params = hg.GaParams(islands=12, pop_size=16, inner_iters=4, outer_iters=3, seed=3)
+        ref = hg.solve(inst, params, hg.FitnessMode.STANDARD_MILLI)
+        for world in (2, 3, 4):
+            shards = [engine.DeviceIslands(inst, params, params.resolved_strength(inst.p),
+                                           *hg.island_shard(12, r, world)) for r in range(world)]
+
+            class Joined:
+                def run_round(self, anc, audit=None):
+                    parts = [s.run_round(anc) for s in shards]
+                    return (np.concatenate([q[0] for q in parts]),
+                            np.concatenate([q[1] for q in parts]))
+
+            rep = engine._solve(inst, params, hg.FitnessMode.STANDARD_MILLI, None,
+                                lambda *a: Joined(), None)
+            assert rep.raw_objective == ref.raw_objective
+            assert rep.trace == ref.trace
+            assert rep.best_solution == ref.best_solution

@@ -1,0 +1,162 @@
+"""Host-side logic of the package and the C-ABI boundary (CPU only)."""
+
+from __future__ import annotations
+
+import hashlib
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden, orc
+
+import paper_1704_06258_b200 as hg
+from paper_1704_06258_b200 import _lib
+
+
+class TestLibraryBoundary:
+    def test_library_exports_every_header_symbol(self):
+        header = (ROOT / "include" / "hubgpu.h").read_text()
+        declared = set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(hg_\w+)\(", header, re.M))
+        assert len(declared) >= 25
+        lib = _lib.load()
+        for name in declared:
+            assert hasattr(lib, name), name
+        assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
+
+    def test_version(self):
+        assert _lib.load().hg_version() == 100
+
+    def test_fails_loudly_without_a_device(self):
+        if _lib.device_count() > 0:
+            pytest.skip("a GPU is visible")
+        inst = hg.generate_urand(8, 2, 1, (1.0, 0.75, 1.0))
+        with pytest.raises(_lib.HubGpuError, match="no CUDA device"):
+            hg.nearest_allocation([0, 1], inst)
+        with pytest.raises(_lib.HubGpuError):
+            hg.objective(inst, hg.Solution(hub=np.eye(8, dtype=bool)[0] | np.eye(8, dtype=bool)[1],
+                                           alloc=np.array([0, 1, 0, 0, 0, 0, 0, 0])))
+
+
+class TestInstance:
+    def test_derived_vectors(self):
+        inst = hg.Instance(n=2, p=1, dist=np.array([[0.0, 1.0], [1.0, 0.0]]),
+                           flow=np.array([[0.0, 5.0], [3.0, 2.0]]), chi=1.0, alpha=0.5, delta=1.0)
+        assert inst.out_flow.tolist() == [5.0, 5.0]
+        assert inst.in_flow.tolist() == [3.0, 7.0]
+        assert inst.total_flow == 10.0
+
+    @pytest.mark.parametrize("kw,match", [
+        (dict(dist=np.array([[1.0, 1.0], [1.0, 0.0]])), "diagonal"),
+        (dict(dist=np.array([[0.0, -1.0], [1.0, 0.0]])), "negative"),
+        (dict(flow=np.array([[0.0, np.inf], [0.0, 0.0]])), "non-finite"),
+        (dict(p=3), "hub count"),
+        (dict(chi=0.0), "chi must be a positive"),
+        (dict(dist=np.zeros((3, 3))), "dist must be 2x2"),
+    ])
+    def test_rejections(self, kw, match):
+        args = dict(n=2, p=1, dist=np.zeros((2, 2)), flow=np.zeros((2, 2)), chi=1, alpha=1,
+                    delta=1)
+        args.update(kw)
+        with pytest.raises(ValueError, match=match):
+            hg.Instance(**args)
+
+    def test_read_only_and_middle_rank(self):
+        g = golden("instances")
+        for idx in range(3):
+            inst = hg.Instance(*[int(v) for v in g[f"mk{idx}_meta"][:2]], g[f"mk{idx}_dist"],
+                               g[f"mk{idx}_flow"], *[float(v) for v in g[f"mk{idx}_meta"][2:]])
+            assert np.array_equal(inst.middle_rank, g[f"mk{idx}_rank"])
+            with pytest.raises(ValueError):
+                inst.dist[0, 1] = 7.0
+        assert np.array_equal(hg.middle_nodes(inst, 3), g["mk2_rank"][:3])
+        with pytest.raises(ValueError):
+            hg.middle_nodes(inst, 0)
+
+
+class TestGenerator:
+    @pytest.mark.parametrize("idx", range(4))
+    def test_small_bitwise(self, idx):
+        g = golden("instances")
+        n, p, seed, *f = g[f"urand{idx}_args"]
+        inst = hg.generate_urand(int(n), int(p), int(seed), tuple(f))
+        assert np.array_equal(inst.dist, g[f"urand{idx}_dist"])
+        assert np.array_equal(inst.flow, g[f"urand{idx}_flow"])
+
+    def test_ur_digest(self):
+        g = golden("instances")
+        n, p, seed, *f = g["big1_args"]
+        inst = hg.generate_urand(int(n), int(p), int(seed), tuple(f))
+        assert hashlib.sha256(inst.dist.tobytes()).hexdigest() == str(g["big1_sha"][0])
+        assert hashlib.sha256(inst.flow.tobytes()).hexdigest() == str(g["big1_sha"][1])
+        assert inst.total_flow == float(g["big1_total"][0])
+
+    def test_population_matches_oracle(self):
+        for n, p in ((25, 3), (200, 10), (70, 40), (5, 5)):
+            assert np.array_equal(hg.random_population(n, p, 40),
+                                  orc.bench_population(n, p, 40))
+        assert np.array_equal(hg.random_population(200, 10, 48),
+                              golden("evaluation")["ap_hubs"])
+
+
+class TestRng:
+    def test_streams_match_reference(self):
+        g = golden("rng")
+        assert hg.mix64(0x9E3779B97F4A7C15) == int(g["kat"][0])
+        st = hg.derive_stream(1704, 1000, 20)
+        ref = orc.Stream(orc.stream_key(1704, 1000, 20))
+        assert [st.next_u64() for _ in range(50)] == [ref.u64() for _ in range(50)]
+        a, b = hg.RngStream(11), hg.RngStream(11)
+        assert a.randint_block(64, 7).tolist() == [b.randint(7) for _ in range(64)]
+        with pytest.raises(ValueError):
+            hg.RngStream(1).randint(0)
+
+    def test_resolve_rng_keys(self):
+        a = hg.resolve_rng(42, 3, hg.Role.MUTATION)
+        assert a.state == orc.stream_key(42, 3, 2)
+
+
+class TestParamsAndScaling:
+    def test_ga_params(self):
+        with pytest.raises(ValueError, match="even"):
+            hg.GaParams(pop_size=15)
+        with pytest.raises(ValueError):
+            hg.GaParams(islands=0)
+        assert hg.GaParams().resolved_strength(2) == 2
+        assert hg.GaParams().resolved_strength(10) == 3
+        with pytest.raises(ValueError, match="exceeds p"):
+            hg.GaParams(perturb_strength=5).resolved_strength(2)
+
+    def test_scale_identities(self):
+        raw = 167493060.0
+        assert hg.scale(raw, hg.FitnessMode.STANDARD_MILLI, 1.0) == raw * 1e-3 == 167493.06
+        assert hg.scale(raw, hg.FitnessMode.CAB_NORMALIZED, 7.0) == raw / 7.0
+        with pytest.raises(hg.ZeroTotalFlowError):
+            hg.scale(raw, hg.FitnessMode.CAB_NORMALIZED, 0.0)
+        assert hg.FitnessMode.from_string("CAB") is hg.FitnessMode.CAB_NORMALIZED
+        with pytest.raises(ValueError):
+            hg.FitnessMode.from_string("bogus")
+
+    def test_island_shards_cover_in_order(self):
+        for R in (1, 7, 64, 128):
+            for world in (1, 2, 3, 4, 8):
+                spans = [hg.island_shard(R, r, world) for r in range(world)]
+                assert spans[0][0] == 0 and spans[-1][1] == R
+                assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+class TestValidate:
+    def test_messages(self):
+        inst = hg.Instance(n=3, p=2, dist=np.zeros((3, 3)), flow=np.ones((3, 3)), chi=1, alpha=1,
+                           delta=1)
+        sol = hg.Solution(hub=np.array([True, True, False]), alloc=np.array([0, 1, 2]))
+        res = hg.validate(sol, inst)
+        assert not res.ok and any("node 3" in v and "closed" in v for v in res.violations)
+        sol = hg.Solution(hub=np.array([True, True, False]), alloc=np.array([1, 1, 1]))
+        assert any("hub 1 not allocated to itself" in v for v in hg.validate(sol, inst).violations)
+        with pytest.raises(hg.StructureError):
+            hg.validate(hg.Solution(hub=np.array([True, False, False]),
+                                    alloc=np.array([0, 0, 5])), inst)
+        with pytest.raises(hg.InfeasibleSolutionError):
+            hg.objective(inst, hg.Solution(hub=np.array([True, False, False]),
+                                           alloc=np.array([0, 0, 0])))
