@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -61,6 +62,7 @@ struct hg_pop {
 };
 
 struct hg_inst {
+    std::atomic<int> refs{1};  // the handle itself + every hg_pop / hg_ga built on it
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -333,8 +335,7 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
     return HG_OK;
 }
 
-void hg_instance_free(hg_inst* inst) {
-    if (!inst) return;
+static void inst_destroy(hg_inst* inst) {
     cudaSetDevice(inst->device);
     if (inst->stream) cudaStreamSynchronize(inst->stream);
     if (inst->scratch) {
@@ -355,6 +356,12 @@ void hg_instance_free(hg_inst* inst) {
     if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
     delete inst;
 }
+
+static void inst_release(hg_inst* inst) {
+    if (inst && inst->refs.fetch_sub(1) == 1) inst_destroy(inst);
+}
+
+void hg_instance_free(hg_inst* inst) { inst_release(inst); }
 
 int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags) {
     HG_ARG(inst != nullptr, "instance is NULL");
@@ -434,16 +441,19 @@ int hg_pop_create(hg_inst* inst, int64_t capacity, hg_pop** out) {
         delete P;
         return rc;
     }
+    inst->refs.fetch_add(1);
     *out = P;
     return HG_OK;
 }
 
 void hg_pop_free(hg_pop* pop) {
     if (!pop) return;
-    cudaSetDevice(pop->inst->device);
-    cudaStreamSynchronize(pop->inst->stream);
+    hg_inst* inst = pop->inst;
+    cudaSetDevice(inst->device);
+    cudaStreamSynchronize(inst->stream);
     pop_release(pop);
     delete pop;
+    inst_release(inst);
 }
 
 int hg_pop_load_hubs(hg_pop* pop, int64_t B, const int32_t* hubs, int where) {
@@ -772,16 +782,19 @@ int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
         delete ga;
         return rc;
     }
+    inst->refs.fetch_add(1);
     *out = ga;
     return HG_OK;
 }
 
 void hg_ga_free(hg_ga* ga) {
     if (!ga) return;
-    cudaSetDevice(ga->inst->device);
-    cudaStreamSynchronize(ga->inst->stream);
+    hg_inst* inst = ga->inst;
+    cudaSetDevice(inst->device);
+    cudaStreamSynchronize(inst->stream);
     ga_release(ga);
     delete ga;
+    inst_release(inst);
 }
 
 int hg_ga_begin_round(hg_ga* ga, const int64_t* ancestor_hubs) {
