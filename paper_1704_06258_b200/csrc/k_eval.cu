@@ -131,9 +131,24 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch
 
 constexpr int kAllocThreads = 256;
 
+// hub-cost table of one individual as two 32-bit planes (hi words, lo words
+// of each fp64 C[h_k][h_l]): [hi: p x ps][lo: p x ps].  A warp gathering one
+// T row at 32 lane-specific columns then touches <= p distinct 4-byte banks
+// per plane -- conflict-free for p <= 32, where an 8-byte gather conflicts
+// between columns c and c+16.
+__device__ __forceinline__ void write_T(const DevInst& I, const int32_t* hs, uint32_t* Tb) {
+    const int p = I.p, n = I.n;
+    for (int x = threadIdx.x; x < p * p; x += kAllocThreads) {
+        const int k = x / p, l = x - k * p;
+        const double v = I.C[(size_t)hs[k] * n + hs[l]];
+        Tb[k * I.ps + l] = (uint32_t)__double2hiint(v);
+        Tb[(p + k) * I.ps + l] = (uint32_t)__double2loint(v);
+    }
+}
+
 __global__ void __launch_bounds__(kAllocThreads)
 k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
-           double* __restrict__ T, double* __restrict__ legs, int32_t* __restrict__ alloc) {
+           uint32_t* __restrict__ T, double* __restrict__ legs, int32_t* __restrict__ alloc) {
     extern __shared__ int32_t hs[];  // p
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
@@ -171,11 +186,7 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
         }
         clb[i] = (uint8_t)c;
     }
-    double* Tb = T + b * (int64_t)p * I.ps;
-    for (int x = threadIdx.x; x < p * p; x += kAllocThreads) {
-        int k = x / p, l = x - k * p;
-        Tb[k * I.ps + l] = I.C[(size_t)hs[k] * n + hs[l]];
-    }
+    write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
     block_sum2<kAllocThreads>(so, sd, scratch);
     if (threadIdx.x == 0) {
         legs[2 * b] = so;
@@ -183,7 +194,7 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
     }
 }
 
-int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, double* T,
+int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint32_t* T,
                     double* legs, int32_t* alloc, cudaStream_t s) {
     if (B <= 0) return HG_OK;
     k_allocate<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, cl, T, legs,
@@ -196,7 +207,7 @@ int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* c
 // Solution, hm/evaluation.py:86-120): cluster = position of alloc[i] in hubs
 __global__ void __launch_bounds__(kAllocThreads)
 k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restrict__ alloc,
-             uint8_t* __restrict__ cl, double* __restrict__ T, double* __restrict__ legs) {
+             uint8_t* __restrict__ cl, uint32_t* __restrict__ T, double* __restrict__ legs) {
     extern __shared__ int32_t hs[];
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
@@ -221,11 +232,7 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
         }
         clb[i] = (uint8_t)c;
     }
-    double* Tb = T + b * (int64_t)p * I.ps;
-    for (int x = threadIdx.x; x < p * p; x += kAllocThreads) {
-        int k = x / p, l = x - k * p;
-        Tb[k * I.ps + l] = I.C[(size_t)hs[k] * n + hs[l]];
-    }
+    write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
     block_sum2<kAllocThreads>(so, sd, scratch);
     if (threadIdx.x == 0) {
         legs[2 * b] = so;
@@ -234,7 +241,7 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
 }
 
 int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
-                      uint8_t* cl, double* T, double* legs, cudaStream_t s) {
+                      uint8_t* cl, uint32_t* T, double* legs, cudaStream_t s) {
     if (B <= 0) return HG_OK;
     k_from_alloc<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, alloc, cl, T,
                                                                             legs);
@@ -248,7 +255,8 @@ int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const in
 // A CTA of 16 warps owns a W tile of TR = 16*RW rows x TC = 32*CJ columns held
 // in REGISTERS (warp w: rows i0+w*RW.., lane: columns j0+lane*CJ..), and streams
 // individuals through it.  Per individual b the pipeline stages into smem
-//   Ts[r][0..p) = T_b[c_b(i0+r)][.]   (the tile rows' hub-cost rows, TR x ps)
+//   Ts[r] = T_b[c_b(i0+r)][.]   (the tile rows' hub-cost rows as hi/lo word
+//                                planes, TR x 2 x ps uint32)
 //   Cs[0..TC)   = c_b(j0..j0+TC)       (column cluster ids)
 // with cp.async (3 stages x G individuals), and every element costs one
 // smem gather Ts[r][c_b(j)] + one DFMA.  Per (b, tile) the CTA reduces in a
@@ -269,7 +277,7 @@ constexpr int kFitMaxG = 8;
 struct FitArgs {
     DevInst I;
     const uint8_t* cl;
-    const double* T;
+    const uint32_t* T;
     double* part;
     int64_t B;
     int tcn, tiles;
@@ -313,36 +321,31 @@ __device__ __forceinline__ void cp16(void* dst, const void* src) {
 }
 
 template <int RW, int CJ>
-__device__ __forceinline__ void issue_unit(const FitArgs& A, const Unit& u, double* Ts,
+__device__ __forceinline__ void issue_unit(const FitArgs& A, const Unit& u, uint32_t* Ts,
                                            uint8_t* Cs) {
     constexpr int TR = kFitWarps * RW, TC = 32 * CJ;
+    static_assert(TC % 16 == 0, "column tile must be a multiple of 16 bytes");
     const int ps = A.I.ps, p = A.I.p, npad = A.I.npad;
     const int tr = u.tile / A.tcn, tc = u.tile - tr * A.tcn;
     const int i0 = tr * TR, j0 = tc * TC;
-    const int rowchunks = ps >> 1;           // 16 B chunks per T row
-    const int tchunks = TR * rowchunks;
-    constexpr int cchunks = TC / 16 > 0 ? TC / 16 : 1;
+    const int rowchunks = ps >> 2;           // 16 B chunks per plane row
+    const int tchunks = TR * 2 * rowchunks;  // hi + lo rows
+    constexpr int cchunks = TC / 16;
     const int per = tchunks + cchunks;
     const int total = u.cnt * per;
     for (int x = threadIdx.x; x < total; x += kFitThreads) {
-        int g = x / per, y = x - g * per;
-        int64_t b = u.b0 + g;
+        const int g = x / per, y = x - g * per;
+        const int64_t b = u.b0 + g;
         if (y < tchunks) {
-            int r = y / rowchunks, part = y - r * rowchunks;
-            int cid = A.cl[b * npad + i0 + r];
-            const double* src = A.T + ((b * p + cid) * (int64_t)ps + part * 2);
-            cp16(Ts + ((size_t)(g * TR + r) * ps + part * 2), src);
+            const int r = y / (2 * rowchunks), z = y - r * 2 * rowchunks;
+            const int plane = z >= rowchunks, part = z - plane * rowchunks;
+            const int cid = A.cl[b * npad + i0 + r];
+            const uint32_t* src =
+                A.T + (((b * 2 + plane) * p + cid) * (int64_t)ps + part * 4);
+            cp16(Ts + ((size_t)(g * TR + r) * 2 + plane) * ps + part * 4, src);
         } else {
-            int k = y - tchunks;
-            if (TC >= 16) {
-                cp16(Cs + g * TC + k * 16, A.cl + b * npad + j0 + k * 16);
-            }
-        }
-    }
-    if (TC < 16) {  // CJ == 0 never; kept for completeness
-        for (int x = threadIdx.x; x < u.cnt * TC; x += kFitThreads) {
-            int g = x / TC, k = x - g * TC;
-            Cs[g * TC + k] = A.cl[(u.b0 + g) * npad + j0 + k];
+            const int k = y - tchunks;
+            cp16(Cs + g * TC + k * 16, A.cl + b * npad + j0 + k * 16);
         }
     }
 }
@@ -377,8 +380,8 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fitness(FitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int ps = A.I.ps, n = A.I.n;
     const int G = A.G;
-    const size_t ts_stage = (size_t)G * TR * ps;      // doubles
-    double* Ts0 = reinterpret_cast<double*>(smem);
+    const size_t ts_stage = (size_t)G * TR * 2 * ps;  // uint32 words
+    uint32_t* Ts0 = reinterpret_cast<uint32_t*>(smem);
     uint8_t* Cs0 = reinterpret_cast<uint8_t*>(Ts0 + kFitStages * ts_stage);
     double* red = reinterpret_cast<double*>(Cs0 + kFitStages * G * TC + 16);  // [2][G][16]
     red = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red) + 15) & ~uintptr_t(15));
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fitness(FitArgs A) {
         }
 
         const int st = (int)(k % kFitStages);
-        const double* Ts = Ts0 + st * ts_stage;
+        const uint32_t* Ts = Ts0 + st * ts_stage;
         const uint8_t* Cs = Cs0 + st * G * TC;
         double* rk = red + (k & 1) * kFitMaxG * kFitWarps;
         for (int g = 0; g < u.cnt; ++g) {
@@ -444,12 +447,14 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fitness(FitArgs A) {
             double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
             for (int r = 0; r < RW; ++r) {
-                const double* Tr = Ts + (size_t)(g * TR + warp * RW + r) * ps;
+                const uint32_t* Th = Ts + (size_t)(g * TR + warp * RW + r) * 2 * ps;
+                const uint32_t* Tl = Th + ps;
 #pragma unroll
                 for (int q = 0; q < CJ; ++q) {
                     const uint32_t cid = (cw[q >> 2] >> ((q & 3) * 8)) & 0xffu;
-                    if (q & 1) acc1 = fma(w[r][q], Tr[cid], acc1);
-                    else acc0 = fma(w[r][q], Tr[cid], acc0);
+                    const double t = __hiloint2double((int)Th[cid], (int)Tl[cid]);
+                    if (q & 1) acc1 = fma(w[r][q], t, acc1);
+                    else acc0 = fma(w[r][q], t, acc0);
                 }
             }
             double acc = warp_sum(acc0 + acc1);
@@ -494,7 +499,7 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 static size_t fit_smem(int rw, int cj, int g, int ps) {
     size_t tr = kFitWarps * rw, tc = 32 * cj;
-    size_t bytes = kFitStages * (size_t)g * tr * ps * sizeof(double);
+    size_t bytes = kFitStages * (size_t)g * tr * 2 * ps * sizeof(uint32_t);
     bytes += kFitStages * (size_t)g * tc + 16;
     bytes = (bytes + 15) & ~size_t(15);
     bytes += 2 * kFitMaxG * kFitWarps * sizeof(double);
@@ -539,7 +544,7 @@ FitPlan fitness_plan(const DevInst& I, int sm_count) {
 }
 
 int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
-                   const double* T, double* part, int grid, cudaStream_t s) {
+                   const uint32_t* T, double* part, int grid, cudaStream_t s) {
     if (B <= 0) return HG_OK;
     FitArgs A;
     A.I = I;
@@ -551,7 +556,7 @@ int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t*
     A.tiles = P.tiles;
     A.G = P.g;
     // keep the T tables + cluster rows of one chunk within ~48 MB of L2
-    const double per_ind = (double)I.p * I.ps * 8.0 + (double)I.npad;
+    const double per_ind = (double)I.p * I.ps * 8.0 + (double)I.npad;  // 2 planes x 4 B
     int64_t chunk = (int64_t)(48.0 * 1024 * 1024 / per_ind);
     chunk = chunk / P.g * P.g;
     if (chunk < P.g) chunk = P.g;
