@@ -53,6 +53,7 @@ struct hg_pop {
     int64_t cap = 0;
     int32_t* hubs = nullptr;
     uint8_t* cl = nullptr;
+    uint16_t* co = nullptr;
     uint32_t* T = nullptr;
     double* legs = nullptr;
     double* part = nullptr;
@@ -92,6 +93,7 @@ void pop_release(hg_pop* P) {
     if (!P) return;
     cudaFree(P->hubs);
     cudaFree(P->cl);
+    cudaFree(P->co);
     cudaFree(P->T);
     cudaFree(P->legs);
     cudaFree(P->part);
@@ -101,6 +103,7 @@ void pop_release(hg_pop* P) {
     if (P->ev1) cudaEventDestroy(P->ev1);
     P->hubs = nullptr;
     P->cl = nullptr;
+    P->co = nullptr;
     P->T = nullptr;
     P->legs = nullptr;
     P->part = nullptr;
@@ -115,6 +118,7 @@ int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     P->cap = cap;
     HG_CUDA(cudaMalloc(&P->hubs, (size_t)cap * I.p * sizeof(int32_t)));
     HG_CUDA(cudaMalloc(&P->cl, (size_t)cap * I.npad));
+    HG_CUDA(cudaMalloc(&P->co, (size_t)cap * I.npad * sizeof(uint16_t)));
     HG_CUDA(cudaMalloc(&P->T, (size_t)cap * 2 * I.p * I.ps * sizeof(uint32_t)));
     HG_CUDA(cudaMalloc(&P->legs, (size_t)cap * 2 * sizeof(double)));
     HG_CUDA(cudaMalloc(&P->part, (size_t)cap * inst->plan.tiles * sizeof(double)));
@@ -149,11 +153,11 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
     if (alloc32)
-        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, P->T, P->legs, s));
+        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, P->co, P->T, P->legs, s));
     else
-        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->T, P->legs, nullptr, s));
+        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, P->legs, nullptr, s));
     HG_CUDA(cudaEventRecord(P->ev0, s));
-    HG_TRY(launch_fitness(I, inst->plan, B, P->cl, P->T, P->part,
+    HG_TRY(launch_fitness(I, inst->plan, B, P->cl, P->co, P->T, P->part,
                           inst->sm_count * inst->plan.blocks_per_sm, s));
     HG_CUDA(cudaEventRecord(P->ev1, s));
     HG_TRY(launch_finalize(I, inst->plan, B, P->legs, P->part, P->out, s));
@@ -395,7 +399,7 @@ int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc) {
     const DevInst& I = inst->I;
     HG_TRY(h2d_i64_as_i32(inst, inst->t1, hubs, B * I.p, P->hubs));
     HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
-    HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->T, P->legs, P->alloc.as<int32_t>(),
+    HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, P->legs, P->alloc.as<int32_t>(),
                            inst->stream));
     HG_TRY(d2h_i32_as_i64(inst, inst->t2, P->alloc.as<int32_t>(), B * I.n, alloc));
     HG_CUDA(cudaStreamSynchronize(inst->stream));
@@ -653,9 +657,10 @@ int ga_queue_generation(hg_ga* ga) {
     HG_TRY(launch_mut_scan(G, s));
     HG_TRY(launch_mutate(G, s));
     HG_TRY(launch_correct(inst->I, ga->B, G.kids, 2 * G.p, G.khubs, s));
-    HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->T,
+    HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->co, ga->pop->T,
                            ga->pop->legs, nullptr, s));
-    HG_TRY(launch_fitness(inst->I, inst->plan, ga->B, ga->pop->cl, ga->pop->T, ga->pop->part,
+    HG_TRY(launch_fitness(inst->I, inst->plan, ga->B, ga->pop->cl, ga->pop->co, ga->pop->T,
+                          ga->pop->part,
                           inst->sm_count * inst->plan.blocks_per_sm, s));
     HG_TRY(launch_finalize(inst->I, inst->plan, ga->B, ga->pop->legs, ga->pop->part,
                            ga->pop->out, s));

@@ -11,6 +11,7 @@
 //   hubs [B][p]       int32 sorted hub ids
 //   cl   [B][npad]    uint8 cluster of node i = position of its hub in hubs
 //                     (padding to npad is zero so padded lanes hit T row 0)
+//   co   [B][npad]    uint16 4*cl: byte offset of the column in a T plane row
 //   T    [B][2][p][ps] uint32 hub-to-hub cost table T[k][l] = C[h_k][h_l] as
 //                     a plane of hi words and a plane of lo words
 //   legs [B][2]       fp64 sum_i O_i*leg_i, sum_i D_i*leg_i (leg_i = C[i][a_i])
@@ -90,12 +91,12 @@ int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStrea
 int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s);
 int launch_transpose(const double* src, double* dst, int n, cudaStream_t s);
 int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s);
-int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint32_t* T,
-                    double* legs, int32_t* alloc, cudaStream_t s);
+int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
+                    uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s);
 int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
-                      uint8_t* cl, uint32_t* T, double* legs, cudaStream_t s);
+                      uint8_t* cl, uint16_t* co, uint32_t* T, double* legs, cudaStream_t s);
 int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
-                   const uint32_t* T, double* part, int grid, cudaStream_t s);
+                   const uint16_t* co, const uint32_t* T, double* part, int grid, cudaStream_t s);
 int launch_finalize(const DevInst& I, const FitPlan& P, int64_t B, const double* legs,
                     const double* part, double* out, cudaStream_t s);
 

@@ -148,7 +148,7 @@ __device__ __forceinline__ void write_T(const DevInst& I, const int32_t* hs, uin
 
 __global__ void __launch_bounds__(kAllocThreads)
 k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
-           uint32_t* __restrict__ T, double* __restrict__ legs, int32_t* __restrict__ alloc) {
+           uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs, int32_t* __restrict__ alloc) {
     extern __shared__ int32_t hs[];  // p
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
@@ -158,6 +158,7 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
 
     double so = 0.0, sd = 0.0;
     uint8_t* clb = cl + b * I.npad;
+    uint16_t* cob = co + b * I.npad;
     for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
         int c = 0;
         if (i < n) {
@@ -185,6 +186,7 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
             if (alloc) alloc[b * n + i] = hs[bk];
         }
         clb[i] = (uint8_t)c;
+        cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
     }
     write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
     block_sum2<kAllocThreads>(so, sd, scratch);
@@ -194,10 +196,10 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
     }
 }
 
-int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint32_t* T,
-                    double* legs, int32_t* alloc, cudaStream_t s) {
+int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
+                    uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s) {
     if (B <= 0) return HG_OK;
-    k_allocate<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, cl, T, legs,
+    k_allocate<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, cl, co, T, legs,
                                                                           alloc);
     HG_CUDA(cudaGetLastError());
     return HG_OK;
@@ -207,7 +209,8 @@ int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* c
 // Solution, hm/evaluation.py:86-120): cluster = position of alloc[i] in hubs
 __global__ void __launch_bounds__(kAllocThreads)
 k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restrict__ alloc,
-             uint8_t* __restrict__ cl, uint32_t* __restrict__ T, double* __restrict__ legs) {
+             uint8_t* __restrict__ cl, uint16_t* __restrict__ co, uint32_t* __restrict__ T,
+             double* __restrict__ legs) {
     extern __shared__ int32_t hs[];
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
@@ -216,6 +219,7 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
     __syncthreads();
     double so = 0.0, sd = 0.0;
     uint8_t* clb = cl + b * I.npad;
+    uint16_t* cob = co + b * I.npad;
     for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
         int c = 0;
         if (i < n) {
@@ -231,6 +235,7 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
             sd += I.D[i] * leg;
         }
         clb[i] = (uint8_t)c;
+        cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
     }
     write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
     block_sum2<kAllocThreads>(so, sd, scratch);
@@ -241,10 +246,10 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
 }
 
 int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
-                      uint8_t* cl, uint32_t* T, double* legs, cudaStream_t s) {
+                      uint8_t* cl, uint16_t* co, uint32_t* T, double* legs, cudaStream_t s) {
     if (B <= 0) return HG_OK;
-    k_from_alloc<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, alloc, cl, T,
-                                                                            legs);
+    k_from_alloc<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, alloc, cl, co,
+                                                                            T, legs);
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }
@@ -273,10 +278,15 @@ constexpr int kFitWarps = 16;
 constexpr int kFitThreads = kFitWarps * 32;
 constexpr int kFitStages = 3;
 constexpr int kFitMaxG = 8;
+// The lo-word plane of the staged hub-cost rows sits at a FIXED byte offset
+// from the hi-word plane, so both gathers of an element share one address
+// register (LDS [R+UR] and [R+UR+kLoOff]).
+constexpr int kLoOff = 96 * 1024;
 
 struct FitArgs {
     DevInst I;
     const uint8_t* cl;
+    const uint16_t* co;
     const uint32_t* T;
     double* part;
     int64_t B;
@@ -322,7 +332,7 @@ __device__ __forceinline__ void cp16(void* dst, const void* src) {
 
 template <int RW, int CJ>
 __device__ __forceinline__ void issue_unit(const FitArgs& A, const Unit& u, uint32_t* Ts,
-                                           uint8_t* Cs) {
+                                           uint16_t* Cs) {
     constexpr int TR = kFitWarps * RW, TC = 32 * CJ;
     static_assert(TC % 16 == 0, "column tile must be a multiple of 16 bytes");
     const int ps = A.I.ps, p = A.I.p, npad = A.I.npad;
@@ -330,7 +340,7 @@ __device__ __forceinline__ void issue_unit(const FitArgs& A, const Unit& u, uint
     const int i0 = tr * TR, j0 = tc * TC;
     const int rowchunks = ps >> 2;           // 16 B chunks per plane row
     const int tchunks = TR * 2 * rowchunks;  // hi + lo rows
-    constexpr int cchunks = TC / 16;
+    constexpr int cchunks = TC * 2 / 16;
     const int per = tchunks + cchunks;
     const int total = u.cnt * per;
     for (int x = threadIdx.x; x < total; x += kFitThreads) {
@@ -342,33 +352,33 @@ __device__ __forceinline__ void issue_unit(const FitArgs& A, const Unit& u, uint
             const int cid = A.cl[b * npad + i0 + r];
             const uint32_t* src =
                 A.T + (((b * 2 + plane) * p + cid) * (int64_t)ps + part * 4);
-            cp16(Ts + ((size_t)(g * TR + r) * 2 + plane) * ps + part * 4, src);
+            cp16(reinterpret_cast<char*>(Ts + (size_t)(g * TR + r) * ps + part * 4) +
+                     plane * kLoOff, src);
         } else {
             const int k = y - tchunks;
-            cp16(Cs + g * TC + k * 16, A.cl + b * npad + j0 + k * 16);
+            cp16(Cs + g * TC + k * 8, A.co + b * npad + j0 + k * 8);
         }
     }
 }
 
+// CJ 16-bit column offsets of one lane, packed two per word
 template <int CJ>
-__device__ __forceinline__ void load_cids(const uint8_t* p, uint32_t (&cw)[(CJ + 3) / 4]) {
-    if constexpr (CJ >= 16) {
+__device__ __forceinline__ void load_offs(const uint16_t* p, uint32_t (&cw)[(CJ + 1) / 2]) {
+    if constexpr (CJ >= 8) {
 #pragma unroll
-        for (int v = 0; v < CJ / 16; ++v) {
-            uint4 x = reinterpret_cast<const uint4*>(p)[v];
+        for (int v = 0; v < CJ / 8; ++v) {
+            const uint4 x = reinterpret_cast<const uint4*>(p)[v];
             cw[4 * v + 0] = x.x;
             cw[4 * v + 1] = x.y;
             cw[4 * v + 2] = x.z;
             cw[4 * v + 3] = x.w;
         }
-    } else if constexpr (CJ == 8) {
-        uint2 x = *reinterpret_cast<const uint2*>(p);
+    } else if constexpr (CJ == 4) {
+        const uint2 x = *reinterpret_cast<const uint2*>(p);
         cw[0] = x.x;
         cw[1] = x.y;
-    } else if constexpr (CJ == 4) {
-        cw[0] = *reinterpret_cast<const uint32_t*>(p);
     } else if constexpr (CJ == 2) {
-        cw[0] = *reinterpret_cast<const uint16_t*>(p);
+        cw[0] = *reinterpret_cast<const uint32_t*>(p);
     } else {
         cw[0] = *p;
     }
@@ -380,13 +390,15 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fitness(FitArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int ps = A.I.ps, n = A.I.n;
     const int G = A.G;
-    const size_t ts_stage = (size_t)G * TR * 2 * ps;  // uint32 words
-    uint32_t* Ts0 = reinterpret_cast<uint32_t*>(smem);
-    uint8_t* Cs0 = reinterpret_cast<uint8_t*>(Ts0 + kFitStages * ts_stage);
-    double* red = reinterpret_cast<double*>(Cs0 + kFitStages * G * TC + 16);  // [2][G][16]
+    const size_t ts_stage = (size_t)G * TR * ps;  // uint32 words per plane
+    uint32_t* Ts0 = reinterpret_cast<uint32_t*>(smem);  // hi plane; lo plane at +kLoOff
+    uint16_t* Cs0 = reinterpret_cast<uint16_t*>(smem + 2 * kLoOff);
+    double* red = reinterpret_cast<double*>(Cs0 + kFitStages * G * TC + 8);  // [2][G][16]
     red = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red) + 15) & ~uintptr_t(15));
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    // warp index made provably warp-uniform so row bases live in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int64_t q0 = A.q_total * blockIdx.x / gridDim.x;
     const int64_t q1 = A.q_total * (blockIdx.x + 1) / gridDim.x;
     if (q0 >= q1) return;
@@ -438,21 +450,23 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fitness(FitArgs A) {
 
         const int st = (int)(k % kFitStages);
         const uint32_t* Ts = Ts0 + st * ts_stage;
-        const uint8_t* Cs = Cs0 + st * G * TC;
+        const uint16_t* Cs = Cs0 + st * G * TC;
         double* rk = red + (k & 1) * kFitMaxG * kFitWarps;
         for (int g = 0; g < u.cnt; ++g) {
-            uint32_t cw[(CJ + 3) / 4];
-            load_cids<CJ>(Cs + g * TC + lane * CJ, cw);
-            // two independent DFMA chains per row keep the FP64 pipe fed
+            uint32_t cw[(CJ + 1) / 2];
+            load_offs<CJ>(Cs + g * TC + lane * CJ, cw);
+            // two independent DFMA chains keep the FP64 pipe fed
             double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
             for (int r = 0; r < RW; ++r) {
-                const uint32_t* Th = Ts + (size_t)(g * TR + warp * RW + r) * 2 * ps;
-                const uint32_t* Tl = Th + ps;
+                const char* Th = reinterpret_cast<const char*>(
+                    Ts + (size_t)(g * TR + warp * RW + r) * ps);
+                const char* Tl = Th + kLoOff;
 #pragma unroll
                 for (int q = 0; q < CJ; ++q) {
-                    const uint32_t cid = (cw[q >> 2] >> ((q & 3) * 8)) & 0xffu;
-                    const double t = __hiloint2double((int)Th[cid], (int)Tl[cid]);
+                    const uint32_t off = (q & 1) ? (cw[q >> 1] >> 16) : (cw[q >> 1] & 0xffffu);
+                    const double t = __hiloint2double(*reinterpret_cast<const int*>(Th + off),
+                                                      *reinterpret_cast<const int*>(Tl + off));
                     if (q & 1) acc1 = fma(w[r][q], t, acc1);
                     else acc0 = fma(w[r][q], t, acc0);
                 }
@@ -497,10 +511,14 @@ static const FitVariant kVariants[] = {
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
+static size_t fit_hi_bytes(int rw, int g, int ps) {
+    return kFitStages * (size_t)g * kFitWarps * rw * ps * sizeof(uint32_t);
+}
+
 static size_t fit_smem(int rw, int cj, int g, int ps) {
-    size_t tr = kFitWarps * rw, tc = 32 * cj;
-    size_t bytes = kFitStages * (size_t)g * tr * 2 * ps * sizeof(uint32_t);
-    bytes += kFitStages * (size_t)g * tc + 16;
+    size_t tc = 32 * cj;
+    size_t bytes = 2 * (size_t)kLoOff;
+    bytes += kFitStages * (size_t)g * tc * 2 + 16;
     bytes = (bytes + 15) & ~size_t(15);
     bytes += 2 * kFitMaxG * kFitWarps * sizeof(double);
     return bytes;
@@ -534,7 +552,9 @@ FitPlan fitness_plan(const DevInst& I, int sm_count) {
     P.tr = kFitWarps * P.rw;
     P.tc = 32 * P.cj;
     P.g = kFitMaxG;
-    while (P.g > 1 && fit_smem(P.rw, P.cj, P.g, I.ps) > 200 * 1024) P.g >>= 1;
+    while (P.g > 1 && (fit_hi_bytes(P.rw, P.g, I.ps) > (size_t)kLoOff ||
+                       fit_smem(P.rw, P.cj, P.g, I.ps) > 226 * 1024))
+        P.g >>= 1;
     P.smem = fit_smem(P.rw, P.cj, P.g, I.ps);
     P.trn = (int)ceil_div(I.n, P.tr);
     P.tcn = (int)(round_up(I.n, P.tc) / P.tc);
@@ -544,11 +564,12 @@ FitPlan fitness_plan(const DevInst& I, int sm_count) {
 }
 
 int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
-                   const uint32_t* T, double* part, int grid, cudaStream_t s) {
+                   const uint16_t* co, const uint32_t* T, double* part, int grid, cudaStream_t s) {
     if (B <= 0) return HG_OK;
     FitArgs A;
     A.I = I;
     A.cl = cl;
+    A.co = co;
     A.T = T;
     A.part = part;
     A.B = B;
@@ -556,7 +577,7 @@ int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t*
     A.tiles = P.tiles;
     A.G = P.g;
     // keep the T tables + cluster rows of one chunk within ~48 MB of L2
-    const double per_ind = (double)I.p * I.ps * 8.0 + (double)I.npad;  // 2 planes x 4 B
+    const double per_ind = (double)I.p * I.ps * 8.0 + 3.0 * I.npad;  // 2 planes x 4 B
     int64_t chunk = (int64_t)(48.0 * 1024 * 1024 / per_ind);
     chunk = chunk / P.g * P.g;
     if (chunk < P.g) chunk = P.g;
