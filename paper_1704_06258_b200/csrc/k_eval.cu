@@ -10,6 +10,8 @@
 #include <cooperative_groups.h>
 #include <cuda_pipeline.h>
 
+#include <cstdlib>
+
 #include "hg_internal.cuh"
 
 namespace hg {
@@ -356,17 +358,32 @@ __device__ __forceinline__ void issue_unit(const FitArgs& A, const Unit& u, uint
                      plane * kLoOff, src);
         } else {
             const int k = y - tchunks;
-            cp16(Cs + g * TC + k * 8, A.co + b * npad + j0 + k * 8);
+            // chunk k (8 columns) belongs to lane k / (CJ/8); store the v-th chunk
+            // of every lane contiguously so a warp's LDS.128 is conflict-free
+            int slot = k;
+            if constexpr (CJ >= 16) slot = (k % (CJ / 8)) * 32 + k / (CJ / 8);
+            cp16(Cs + g * TC + slot * 8, A.co + b * npad + j0 + k * 8);
         }
     }
 }
 
 // CJ 16-bit column offsets of one lane, packed two per word
 template <int CJ>
-__device__ __forceinline__ void load_offs(const uint16_t* p, uint32_t (&cw)[(CJ + 1) / 2]) {
-    if constexpr (CJ >= 8) {
+__device__ __forceinline__ void load_offs(const uint16_t* base, int lane,
+                                          uint32_t (&cw)[(CJ + 1) / 2]) {
+    const uint16_t* p = base + lane * CJ;
+    if constexpr (CJ >= 16) {
 #pragma unroll
         for (int v = 0; v < CJ / 8; ++v) {
+            const uint4 x = reinterpret_cast<const uint4*>(base)[v * 32 + lane];
+            cw[4 * v + 0] = x.x;
+            cw[4 * v + 1] = x.y;
+            cw[4 * v + 2] = x.z;
+            cw[4 * v + 3] = x.w;
+        }
+    } else if constexpr (CJ == 8) {
+        {
+            const int v = 0;
             const uint4 x = reinterpret_cast<const uint4*>(p)[v];
             cw[4 * v + 0] = x.x;
             cw[4 * v + 1] = x.y;
@@ -454,7 +471,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) k_fitness(FitArgs A) {
         double* rk = red + (k & 1) * kFitMaxG * kFitWarps;
         for (int g = 0; g < u.cnt; ++g) {
             uint32_t cw[(CJ + 1) / 2];
-            load_offs<CJ>(Cs + g * TC + lane * CJ, cw);
+            load_offs<CJ>(Cs + g * TC, lane, cw);
             // two independent DFMA chains keep the FP64 pipe fed
             double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
@@ -504,6 +521,9 @@ struct FitVariant {
 };
 static const FitVariant kVariants[] = {
     {2, 16, k_fitness<2, 16>},  // 32 x 512 tiles: n >= ~400
+    {1, 32, k_fitness<1, 32>},  // 16 x 1024
+    {1, 16, k_fitness<1, 16>},  // 16 x 512
+    {4, 8, k_fitness<4, 8>},    // 64 x 256
     {2, 8, k_fitness<2, 8>},    // 32 x 256
     {2, 4, k_fitness<2, 4>},    // 32 x 128
     {1, 2, k_fitness<1, 2>},    // 16 x 64
@@ -544,6 +564,10 @@ FitPlan fitness_plan(const DevInst& I, int sm_count) {
             best_cost = cost;
             best = v;
         }
+    }
+    if (const char* ov = getenv("HUBGPU_FIT_VARIANT")) {  // tuning override
+        const int v = atoi(ov);
+        if (v >= 0 && v < kNumVariants) best = v;
     }
     FitPlan P{};
     P.variant = best;
