@@ -552,15 +552,19 @@ int prepare_fitness(const FitPlan& P) {
 
 FitPlan fitness_plan(const DevInst& I, int sm_count) {
     (void)sm_count;
-    // pick the variant with the least padded area; ties -> the wider tile
+    // pick the variant with the least (padded area x measured per-element cost);
+    // per-element costs relative to (2,16), measured on B200 at n=1000 with
+    // p=20 and p=50 (tools/sweep_variants.sh, profiles/ROUND1.md)
+    static const double kCostSmallP[] = {1.00, 1.13, 1.30, 1.31, 1.40, 2.35, 7.0, 13.1};
+    static const double kCostLargeP[] = {1.14, 1.00, 1.17, 1.60, 1.69, 2.9, 6.0, 11.3};
+    static_assert(sizeof(kCostSmallP) / sizeof(double) == kNumVariants, "cost table");
     int best = 0;
     double best_cost = 1e300;
     for (int v = 0; v < kNumVariants; ++v) {
-        int tr = kFitWarps * kVariants[v].rw, tc = 32 * kVariants[v].cj;
-        double area = (double)round_up(I.n, tr) * (double)round_up(I.n, tc);
-        // mild preference for wide tiles: T-row traffic per element ~ ps / tc
-        double cost = area * (1.0 + 0.5 * (double)I.ps / (double)tc);
-        if (cost < best_cost * 0.999) {
+        const int tr = kFitWarps * kVariants[v].rw, tc = 32 * kVariants[v].cj;
+        const double area = (double)round_up(I.n, tr) * (double)round_up(I.n, tc);
+        const double cost = area * (I.p > 32 ? kCostLargeP[v] : kCostSmallP[v]);
+        if (cost < best_cost) {
             best_cost = cost;
             best = v;
         }
