@@ -41,6 +41,12 @@ extern "C" {
 /* instance flags reported by hg_instance_info */
 #define HG_FLAG_SYMMETRIC 1    /* dist == dist^T exactly: one matrix serves both */
 #define HG_FLAG_WEIGHTS_EXACT 2 /* out+in flow integer-valued, total < 2^53      */
+#define HG_FLAG_TENSOR_OK 4     /* flows integers in [0,255]: exact u8 tensor path */
+
+/* fitness kernel choice (hg_instance_set_fitness) */
+#define HG_FIT_AUTO 0      /* tensor cores when exact, else the fp64 gather   */
+#define HG_FIT_FP64 1      /* K3: fp64 smem-gather kernel (any flows)          */
+#define HG_FIT_TENSOR 2    /* K3-TC: u8 tcgen05 GEMM + fp64 epilogue           */
 
 typedef struct hg_inst hg_inst;
 typedef struct hg_pop hg_pop;
@@ -61,6 +67,11 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
                        void* stream, hg_inst** out);
 void hg_instance_free(hg_inst* inst);
 int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags);
+/* select / query the transfer-term kernel used by hg_evaluate, hg_pop_* and
+ * GA objects created afterwards (both give the same values within fp64
+ * summation-order rounding) */
+int hg_instance_set_fitness(hg_inst* inst, int kind);
+int hg_instance_fitness(const hg_inst* inst, int* kind);
 /* the cudaStream_t all device work of this instance is queued on */
 int hg_instance_stream(const hg_inst* inst, void** stream);
 int hg_synchronize(hg_inst* inst);

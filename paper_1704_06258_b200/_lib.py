@@ -20,7 +20,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libhubgpu.so"
 
 HG_OK, HG_EARG, HG_ECUDA, HG_ENODEV, HG_ESTATE = 0, 1, 2, 3, 4
 HG_HOST, HG_DEVICE = 0, 1
-FLAG_SYMMETRIC, FLAG_WEIGHTS_EXACT = 1, 2
+FLAG_SYMMETRIC, FLAG_WEIGHTS_EXACT, FLAG_TENSOR_OK = 1, 2, 4
+FIT_AUTO, FIT_FP64, FIT_TENSOR = 0, 1, 2
 
 _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
@@ -49,6 +50,8 @@ SIGNATURES = {
     "hg_instance_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                    C.POINTER(C.c_int)]),
     "hg_instance_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "hg_instance_set_fitness": (C.c_int, [_vp, C.c_int]),
+    "hg_instance_fitness": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "hg_synchronize": (C.c_int, [_vp]),
     "hg_allocate": (C.c_int, [_vp, C.c_int64, _i64p, _i64p]),
     "hg_evaluate": (C.c_int, [_vp, C.c_int64, _i64p, _i64p, _f64p]),
@@ -119,6 +122,17 @@ def device_count() -> int:
 
 
 _device = int(os.environ.get("HUBGPU_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+# transfer-term kernel for new device instances: auto (tensor cores when the
+# flows allow the exact u8 GEMM), fp64 (K3 gather) or tensor (K3-TC)
+_fit_default = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR}[
+    os.environ.get("HUBGPU_FITNESS", "auto")]
+
+
+def set_fitness_default(kind: str) -> None:
+    """'auto' | 'fp64' | 'tensor' for device instances created from now on
+    ('tensor' falls back to fp64 where the flows are not u8 integers)."""
+    global _fit_default
+    _fit_default = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR}[kind]
 
 
 def set_device(index: int) -> None:
@@ -163,6 +177,17 @@ class DeviceInstance:
         n_, p_, flags = C.c_int(), C.c_int(), C.c_int()
         check(lib.hg_instance_info(h, C.byref(n_), C.byref(p_), C.byref(flags)))
         self.flags = flags.value
+        if _fit_default == FIT_FP64 or (_fit_default == FIT_TENSOR and self.flags & FLAG_TENSOR_OK):
+            self.set_fitness(_fit_default)
+
+    def set_fitness(self, kind: int) -> None:
+        check(load().hg_instance_set_fitness(self.handle, int(kind)))
+
+    @property
+    def fitness_kernel(self) -> str:
+        k = C.c_int()
+        check(load().hg_instance_fitness(self.handle, C.byref(k)))
+        return {FIT_FP64: "fp64", FIT_TENSOR: "tensor"}[k.value]
 
     @property
     def stream(self) -> int:

@@ -63,7 +63,11 @@ struct hg_pop {
 };
 
 struct hg_inst {
-    std::atomic<int> refs{1};  // the handle itself + every hg_pop / hg_ga built on it
+    std::atomic<int> refs{1};
+    alignas(64) unsigned char wmap[128];  // CUtensorMap of W8 (K3-TC)
+    uint8_t* dW8 = nullptr;                // u8 copy of W, [npad_tc][npad_tc], when exact
+    bool tc_ok = false;                    // flows are integers in [0, 255] and p fits
+    int fit_kind = HG_FIT_AUTO;  // the handle itself + every hg_pop / hg_ga built on it
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -121,7 +125,8 @@ int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     HG_CUDA(cudaMalloc(&P->co, (size_t)cap * I.npad * sizeof(uint16_t)));
     HG_CUDA(cudaMalloc(&P->T, (size_t)cap * 2 * I.p * I.ps * sizeof(uint32_t)));
     HG_CUDA(cudaMalloc(&P->legs, (size_t)cap * 2 * sizeof(double)));
-    HG_CUDA(cudaMalloc(&P->part, (size_t)cap * inst->plan.tiles * sizeof(double)));
+    const int tiles = inst->plan.tiles > tc_tiles(I.n) ? inst->plan.tiles : tc_tiles(I.n);
+    HG_CUDA(cudaMalloc(&P->part, (size_t)cap * tiles * sizeof(double)));
     HG_CUDA(cudaMalloc(&P->out, (size_t)cap * 4 * sizeof(double)));
     HG_CUDA(cudaEventCreate(&P->ev0));
     HG_CUDA(cudaEventCreate(&P->ev1));
@@ -146,6 +151,25 @@ int scratch_pop(hg_inst* inst, int64_t B, hg_pop** out) {
     return HG_OK;
 }
 
+// K3 (fp64 gather) or K3-TC (tensor cores) + finalise, by the instance's choice
+int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* co,
+                  const uint32_t* T, double* part, const double* legs, double* out) {
+    const DevInst& I = inst->I;
+    cudaStream_t s = inst->stream;
+    const bool tc = inst->fit_kind == HG_FIT_TENSOR ||
+                    (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok);
+    int tiles;
+    if (tc) {
+        HG_TRY(launch_fitness_tc(I, inst->wmap, B, cl, T, part, inst->sm_count, s));
+        tiles = tc_tiles(I.n);
+    } else {
+        HG_TRY(launch_fitness(I, inst->plan, B, cl, co, T, part,
+                              inst->sm_count * inst->plan.blocks_per_sm, s));
+        tiles = inst->plan.tiles;
+    }
+    return launch_finalize(I, tiles, B, legs, part, out, s);
+}
+
 // queue K2 + K3 + finalise for B individuals whose int32 hubs are in P->hubs
 // (alloc32 == nullptr: nearest allocation; otherwise the given allocation)
 int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
@@ -157,10 +181,8 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
     else
         HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, P->legs, nullptr, s));
     HG_CUDA(cudaEventRecord(P->ev0, s));
-    HG_TRY(launch_fitness(I, inst->plan, B, P->cl, P->co, P->T, P->part,
-                          inst->sm_count * inst->plan.blocks_per_sm, s));
+    HG_TRY(queue_fitness(inst, B, P->cl, P->co, P->T, P->part, P->legs, P->out));
     HG_CUDA(cudaEventRecord(P->ev1, s));
-    HG_TRY(launch_finalize(I, inst->plan, B, P->legs, P->part, P->out, s));
     return HG_OK;
 }
 
@@ -325,10 +347,30 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.npad = 16;  // provisional for the plan
         inst->plan = fitness_plan(I, inst->sm_count);
         int64_t q = inst->plan.tr > inst->plan.tc ? inst->plan.tr : inst->plan.tc;
-        if (q < 16) q = 16;
+        if (q < 128) q = 128;  // K3-TC reads 128-wide K blocks of cluster ids
         I.npad = (int)round_up(n, q);
         rc = prepare_fitness(inst->plan);
         if (rc) break;
+        // K3-TC eligibility: every flow an integer in [0, 255] -> exact u8 GEMM
+        bool u8 = tc_supported(p);
+        for (size_t x = 0; u8 && x < nn; ++x) {
+            const double v = flow[x];
+            if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v))) u8 = false;
+        }
+        if (u8) {
+            const int nt = (int)round_up(n, 128);
+            std::vector<uint8_t> w8((size_t)nt * nt, 0);
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) w8[(size_t)i * nt + j] = (uint8_t)flow[(size_t)i * n + j];
+            chk(cudaMalloc(&inst->dW8, w8.size()), "cudaMalloc(W8)");
+            chk(cudaMemcpy(inst->dW8, w8.data(), w8.size(), cudaMemcpyHostToDevice), "H2D W8");
+            if (rc) break;
+            rc = tc_make_wmap(inst->dW8, nt, inst->wmap);
+            if (rc) break;
+            rc = prepare_fitness_tc(p);
+            if (rc) break;
+            inst->tc_ok = true;
+        }
         chk(cudaStreamSynchronize(s), "sync");
     } while (0);
     if (rc != HG_OK) {
@@ -353,6 +395,7 @@ static void inst_destroy(hg_inst* inst) {
     cudaFree(inst->dD);
     cudaFree(inst->dwOD);
     cudaFree(inst->drank);
+    cudaFree(inst->dW8);
     inst->t1.release();
     inst->t2.release();
     inst->t3.release();
@@ -371,7 +414,25 @@ int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags) {
     HG_ARG(inst != nullptr, "instance is NULL");
     if (n) *n = inst->I.n;
     if (p) *p = inst->I.p;
-    if (flags) *flags = inst->flags;
+    if (flags) *flags = inst->flags | (inst->tc_ok ? HG_FLAG_TENSOR_OK : 0);
+    return HG_OK;
+}
+
+int hg_instance_set_fitness(hg_inst* inst, int kind) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    HG_ARG(kind == HG_FIT_AUTO || kind == HG_FIT_FP64 || kind == HG_FIT_TENSOR,
+           "unknown fitness kernel %d", kind);
+    HG_ARG(kind != HG_FIT_TENSOR || inst->tc_ok,
+           "tensor-core fitness needs integer flows in [0, 255] and p <= 128");
+    inst->fit_kind = kind;
+    return HG_OK;
+}
+
+int hg_instance_fitness(const hg_inst* inst, int* kind) {
+    HG_ARG(inst && kind, "NULL argument");
+    *kind = (inst->fit_kind == HG_FIT_TENSOR || (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok))
+                ? HG_FIT_TENSOR
+                : HG_FIT_FP64;
     return HG_OK;
 }
 
@@ -659,11 +720,8 @@ int ga_queue_generation(hg_ga* ga) {
     HG_TRY(launch_correct(inst->I, ga->B, G.kids, 2 * G.p, G.khubs, s));
     HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->co, ga->pop->T,
                            ga->pop->legs, nullptr, s));
-    HG_TRY(launch_fitness(inst->I, inst->plan, ga->B, ga->pop->cl, ga->pop->co, ga->pop->T,
-                          ga->pop->part,
-                          inst->sm_count * inst->plan.blocks_per_sm, s));
-    HG_TRY(launch_finalize(inst->I, inst->plan, ga->B, ga->pop->legs, ga->pop->part,
-                           ga->pop->out, s));
+    HG_TRY(queue_fitness(inst, ga->B, ga->pop->cl, ga->pop->co, ga->pop->T, ga->pop->part,
+                         ga->pop->legs, ga->pop->out));
     HG_TRY(launch_select(G, s));
     return HG_OK;
 }

@@ -97,8 +97,17 @@ int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const in
                       uint8_t* cl, uint16_t* co, uint32_t* T, double* legs, cudaStream_t s);
 int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
                    const uint16_t* co, const uint32_t* T, double* part, int grid, cudaStream_t s);
-int launch_finalize(const DevInst& I, const FitPlan& P, int64_t B, const double* legs,
+int launch_finalize(const DevInst& I, int tiles, int64_t B, const double* legs,
                     const double* part, double* out, cudaStream_t s);
+
+// ---- K3-TC (k_fitness_tc.cu): tensor-core transfer term for u8 flows ------
+bool tc_supported(int p);
+int tc_tiles(int n);
+size_t tc_smem_bytes(int p);
+int prepare_fitness_tc(int p);
+int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out);  // map_out: CUtensorMap (128 B)
+int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
+                      const uint32_t* T, double* part, int grid, cudaStream_t s);
 
 // ---- launchers (k_ga.cu) ---------------------------------------------------
 int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n, int nw,

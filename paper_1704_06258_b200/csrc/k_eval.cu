@@ -649,12 +649,12 @@ __global__ void k_finalize(DevInst I, int64_t B, int tiles, const double* __rest
     }
 }
 
-int launch_finalize(const DevInst& I, const FitPlan& P, int64_t B, const double* legs,
+int launch_finalize(const DevInst& I, int tiles, int64_t B, const double* legs,
                     const double* part, double* out, cudaStream_t s) {
     if (B <= 0) return HG_OK;
     const int threads = 256;
     const int64_t blocks = ceil_div(B * 32, threads);
-    k_finalize<<<(unsigned)blocks, threads, 0, s>>>(I, B, P.tiles, legs, part, out);
+    k_finalize<<<(unsigned)blocks, threads, 0, s>>>(I, B, tiles, legs, part, out);
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }

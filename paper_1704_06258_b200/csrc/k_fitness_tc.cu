@@ -1,0 +1,389 @@
+// K3-TC: population fitness (transfer term) on the 5th-generation tensor cores.
+//
+// When every flow W_ij is an integer in [0, 255] (all synthetic instances of
+// the reference generator, hm/io.py:203, are integers in [0, 100]) the
+// transfer term factors EXACTLY through an integer GEMM:
+//
+//   G_b[i][l]  = sum_j W[i][j] * [c_b(j) == l]          (u8 x u8 -> s32, exact)
+//   S_T(b)     = sum_i sum_l G_b[i][l] * T_b[c_b(i)][l]  (fp64 epilogue)
+//
+// which equals sum_ij W_ij C[a_i][a_j] of hm/evaluation.py:113-119 up to fp64
+// summation order.  Batched over the population, G is one GEMM
+//   D[i][(b,l)] = W[i][:] . OneHot[(b,l)][:]
+// with M = nodes i (128 per tile), N = (individual, hub) pairs (ipt
+// individuals x p, <= 256), K = nodes j.
+//
+// Per CTA (256 threads, one per SM): TMEM holds the 128 x N s32 accumulator;
+// W tiles (A operand, K-major, SWIZZLE_128B) arrive by TMA; the one-hot B
+// operand is generated in shared memory from the cluster-id bytes by all
+// threads (same canonical SWIZZLE_128B K-major layout), fenced to the async
+// proxy, and consumed by tcgen05.mma.kind::i8 issued by one thread; K-blocks
+// are double-buffered so generation of block k+1 overlaps the MMAs of block k.
+// The epilogue reads the accumulator with tcgen05.ld, converts exactly to
+// fp64 and contracts with the staged hub-cost tables; one partial per
+// (individual, 128-row tile) in a fixed reduction order.
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "hg_internal.cuh"
+
+namespace hg {
+
+namespace {
+
+constexpr int kTcThreads = 256;
+constexpr int kTcTmemCols = 512;
+constexpr int kAStage = 128 * 128;   // bytes: 128 rows x 128 K (u8)
+constexpr int kBStage = 256 * 128;   // bytes: up to 256 rows x 128 K
+constexpr int kSmemT = 2 * kAStage + 2 * kBStage;  // offset of the T staging area
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
+// K-major, SWIZZLE_128B canonical layout: 8-row x 128 B atoms, 1024 B apart
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);  // start address
+    d |= (uint64_t)1 << 16;                   // leading byte offset (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;         // stride byte offset: next 8-row group
+    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// byte-wise (x == l) -> 0x01 / 0x00, exact (no cross-byte carries)
+__device__ __forceinline__ uint32_t onehot4(uint32_t x, uint32_t lrep) {
+    const uint32_t y = x ^ lrep;
+    const uint32_t t = ((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y;
+    return (~t >> 7) & 0x01010101u;
+}
+
+}  // namespace
+
+struct TcArgs {
+    const uint8_t* cl;
+    const uint32_t* T;
+    double* part;
+    int64_t B;
+    int n, p, ps, npad;
+    int ipt;      // individuals per N tile
+    int N;        // MMA N (multiple of 16, <= 256)
+    int64_t NT;   // N tiles
+    int MT, KB;   // 128-row tiles, 128-wide K blocks
+    int pss;      // smem row stride of staged T planes (odd)
+    uint32_t idesc;
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-align the operand area (SWIZZLE_128B atoms)
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* sA = smem;                          // 2 x 16 KB
+    unsigned char* sB = smem + 2 * kAStage;            // 2 x 32 KB
+    uint32_t* sT = reinterpret_cast<uint32_t*>(smem + kSmemT);
+    const int tsz = A.ipt * 2 * A.p * A.pss;           // words
+    double* red = reinterpret_cast<double*>(sT + ((tsz + 1) & ~1));  // [8 warps][ipt]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * A.ipt);   // tma[2], mma[2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t bar_tma0 = smem_u32(bars), bar_mma0 = smem_u32(bars + 2);
+
+    if (tid == 0) {
+        mbar_init(bar_tma0, 1);
+        mbar_init(bar_tma0 + 8, 1);
+        mbar_init(bar_mma0, 1);
+        mbar_init(bar_mma0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(kTcTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t units = A.NT * A.MT;
+    const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+    uint32_t n_tma[2] = {0, 0}, n_mma[2] = {0, 0};
+    int64_t cur_nt = -1;
+    const int p = A.p;
+    const int half = (A.ipt + 1) / 2;
+
+    for (int64_t u = u0; u < u1; ++u) {
+        const int64_t nt = u / A.MT;
+        const int mt = (int)(u - nt * A.MT);
+        const int64_t bbase = nt * A.ipt;
+        if (nt != cur_nt) {
+            // stage the hub-cost tables (hi/lo planes) of this N tile's individuals
+            cur_nt = nt;
+            const int per = 2 * p * p;
+            for (int x = tid; x < A.ipt * per; x += kTcThreads) {
+                const int bl = x / per, y = x - bl * per;
+                const int row = y / p, l = y - row * p;  // row = plane * p + c
+                const int64_t b = bbase + bl;
+                uint32_t v = 0;
+                if (b < A.B) v = A.T[(b * 2 * p + row) * (int64_t)A.ps + l];
+                sT[(bl * 2 * p + row) * A.pss + l] = v;
+            }
+        }
+        for (int kb = 0; kb < A.KB; ++kb) {
+            const int s = kb & 1;
+            if (kb >= 2) mbar_wait(bar_mma0 + 8 * s, (n_mma[s] - 1) & 1);
+            unsigned char* a_st = sA + s * kAStage;
+            unsigned char* b_st = sB + s * kBStage;
+            if (tid == 0) {
+                mbar_expect_tx(bar_tma0 + 8 * s, kAStage);
+                tma_load_2d(smem_u32(a_st), &tmW, kb * 128, mt * 128, bar_tma0 + 8 * s);
+            }
+            n_tma[s]++;
+            // one-hot B tile: row r = (individual bl, hub l), 128 K bytes, swizzled
+            for (int it = tid; it < A.N * 8; it += kTcThreads) {
+                const int r = it >> 3, c = it & 7;
+                const int bl = r / p, l = r - bl * p;
+                const int64_t b = bbase + bl;
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (bl < A.ipt && b < A.B) {
+                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(
+                        A.cl + b * A.npad + kb * 128 + c * 16));
+                    const uint32_t lrep = (uint32_t)l * 0x01010101u;
+                    v.x = onehot4(x.x, lrep);
+                    v.y = onehot4(x.y, lrep);
+                    v.z = onehot4(x.z, lrep);
+                    v.w = onehot4(x.w, lrep);
+                }
+                *reinterpret_cast<uint4*>(b_st + (r >> 3) * 1024 + (r & 7) * 128 +
+                                          ((c ^ (r & 7)) << 4)) = v;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                mbar_wait(bar_tma0 + 8 * s, (n_tma[s] - 1) & 1);
+                tc_fence_after();
+                const uint64_t ad = sw128_desc(smem_u32(a_st));
+                const uint64_t bd = sw128_desc(smem_u32(b_st));
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)  // K = 32 bytes per MMA: +2 in 16 B units
+                    mma_i8(tmem, ad + 2 * ks, bd + 2 * ks, A.idesc, (kb | ks) != 0);
+                mma_commit(bar_mma0 + 8 * s);
+            }
+            n_mma[s]++;
+        }
+        // accumulator complete
+        const int sl = (A.KB - 1) & 1;
+        mbar_wait(bar_mma0 + 8 * sl, (n_mma[sl] - 1) & 1);
+        tc_fence_after();
+
+        // epilogue: warp quadrant q owns TMEM lanes / rows 32q..32q+31; the two
+        // warp halves split the individuals
+        const int q = warp & 3, h = warp >> 2;
+        const int i = mt * 128 + q * 32 + lane;
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+        const int bl_lo = h * half, bl_hi = min(A.ipt, (h + 1) * half);
+        for (int bl = bl_lo; bl < bl_hi; ++bl) {
+            const int64_t b = bbase + bl;
+            double acc = 0.0;
+            if (b < A.B) {  // warp-uniform
+                const int c = (i < A.npad) ? A.cl[b * A.npad + i] : 0;
+                const uint32_t* th = sT + (bl * 2 * p + c) * A.pss;
+                const uint32_t* tl = sT + (bl * 2 * p + p + c) * A.pss;
+                for (int l0 = 0; l0 < p; l0 += 8) {
+                    uint32_t d[8];
+                    tmem_ld8(trow + (uint32_t)(bl * p + l0), d);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (l0 + k < p) {
+                            // exact u32 -> fp64: 2^52 + d, then subtract 2^52
+                            const double dd = __hiloint2double(0x43300000, (int)d[k]) -
+                                              4503599627370496.0;
+                            const double t = __hiloint2double((int)th[l0 + k], (int)tl[l0 + k]);
+                            acc = fma(dd, t, acc);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) red[warp * A.ipt + bl] = acc;
+        }
+        tc_fence_before();
+        __syncthreads();
+        if (tid < A.ipt) {
+            const int64_t b = bbase + tid;
+            if (b < A.B) {
+                const int hh = tid / half;
+                double s4 = 0.0;
+                for (int qq = 0; qq < 4; ++qq) s4 += red[(hh * 4 + qq) * A.ipt + tid];
+                A.part[b * A.MT + mt] = s4;
+            }
+        }
+        // red is rewritten only after the next unit's K loop (its __syncthreads)
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(kTcTmemCols)
+                     : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out) {
+    auto enc = get_encode();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return HG_ECUDA;
+    }
+    CUtensorMap* m = static_cast<CUtensorMap*>(map_out);
+    cuuint64_t dims[2] = {(cuuint64_t)npad_tc, (cuuint64_t)npad_tc};
+    cuuint64_t strides[1] = {(cuuint64_t)npad_tc};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)W8, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return HG_ECUDA;
+    }
+    return HG_OK;
+}
+
+static int tc_pss(int p) { return p | 1; }
+
+size_t tc_smem_bytes(int p) {
+    const int ipt = 256 / p;
+    size_t t = (size_t)ipt * 2 * p * tc_pss(p) * 4;
+    t = (t + 7) & ~size_t(7);
+    return 1024 + kSmemT + t + 8 * ipt * 8 + 4 * 8 + 16;
+}
+
+bool tc_supported(int p) { return p >= 1 && p <= 128 && tc_smem_bytes(p) <= 227 * 1024; }
+
+int tc_tiles(int n) { return (int)(round_up(n, 128) / 128); }
+
+int prepare_fitness_tc(int p) {
+    HG_CUDA(cudaFuncSetAttribute(k_fitness_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tc_smem_bytes(p)));
+    return HG_OK;
+}
+
+int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
+                      const uint32_t* T, double* part, int grid, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    TcArgs A;
+    A.cl = cl;
+    A.T = T;
+    A.part = part;
+    A.B = B;
+    A.n = I.n;
+    A.p = I.p;
+    A.ps = I.ps;
+    A.npad = I.npad;
+    A.ipt = 256 / I.p;
+    A.N = (int)round_up((int64_t)A.ipt * I.p, 16);
+    A.NT = ceil_div(B, A.ipt);
+    A.MT = tc_tiles(I.n);
+    A.KB = A.MT;
+    A.pss = tc_pss(I.p);
+    // kind::i8 instruction descriptor: D s32, A/B u8, both K-major, N, M=128
+    A.idesc = (2u << 4) | ((uint32_t)(A.N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int64_t units = A.NT * A.MT;
+    int g = grid;
+    if (g > units) g = (int)units;
+    CUtensorMap map = *static_cast<const CUtensorMap*>(wmap);
+    k_fitness_tc<<<g, kTcThreads, tc_smem_bytes(I.p), s>>>(map, A);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+}  // namespace hg

@@ -38,6 +38,17 @@ def _need_gpu():
         pytest.fail("no CUDA device: the gpu tests must run on a B200")
 
 
+@pytest.fixture(params=["fp64", "tensor"])
+def kernel(request):
+    """Run a test once with the fp64 gather kernel (K3) and once with the
+    tensor-core kernel (K3-TC, used wherever the flows are u8 integers)."""
+    from paper_1704_06258_b200 import _lib
+
+    _lib.set_fitness_default(request.param)
+    yield request.param
+    _lib.set_fitness_default("auto")
+
+
 class TestAllocation:
     @pytest.mark.parametrize("label", EVAL_LABELS + ["tie", "ovr"])
     def test_bit_exact_vs_reference(self, label):
@@ -66,14 +77,14 @@ class TestAllocation:
 
 class TestObjective:
     @pytest.mark.parametrize("label", EVAL_LABELS)
-    def test_population_components(self, label):
+    def test_population_components(self, label, kernel):
         g = golden("evaluation")
         inst = inst_from(g, label)
         out = hg.evaluate_population(inst, g[f"{label}_hubs"])
         assert close(out, g[f"{label}_comp"])
 
     @pytest.mark.parametrize("label", EVAL_LABELS)
-    def test_arbitrary_feasible_allocations(self, label):
+    def test_arbitrary_feasible_allocations(self, label, kernel):
         g = golden("evaluation")
         inst = inst_from(g, label)
         for hubs, alloc, comp in zip(g[f"{label}_rhubs"], g[f"{label}_ralloc"],
@@ -92,7 +103,7 @@ class TestObjective:
         assert hg.fitness(inst, sol, hg.FitnessMode.STANDARD_MILLI) == raw * 1e-3
         assert hg.fitness(inst, sol, hg.FitnessMode.CAB_NORMALIZED) == raw / inst.total_flow
 
-    def test_batch_invariance_bitwise(self):
+    def test_batch_invariance_bitwise(self, kernel):
         """A hub set's score does not depend on its batch or position."""
         inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
         pop = hg.random_population(1000, 20, 300)
@@ -105,7 +116,7 @@ class TestObjective:
     @pytest.mark.parametrize("n,p,f", [(1000, 20, (1.0, 0.75, 1.0)), (200, 10, (3.0, 0.75, 2.0)),
                                        (333, 7, (1.0, 0.5, 2.0)), (25, 3, (1.0, 0.2, 1.0)),
                                        (90, 50, (1.0, 0.75, 1.0))])
-    def test_vs_oracle_random_configs(self, n, p, f):
+    def test_vs_oracle_random_configs(self, n, p, f, kernel):
         inst = hg.generate_urand(n, p, 77, f)
         pr = orc.Problem(n, p, inst.dist, inst.flow, *f)
         pop = hg.random_population(n, p, 40, key=5)
@@ -114,7 +125,7 @@ class TestObjective:
         ref = np.concatenate([ref, (ref[:, 0] + ref[:, 1] + ref[:, 2])[:, None]], axis=1)
         assert close(out, ref)
 
-    def test_asymmetric_self_flow(self):
+    def test_asymmetric_self_flow(self, kernel):
         pr = orc.stream_problem(24, 40, 6, symmetric=False, self_flow=True, chi=3.0, alpha=0.75,
                                 delta=2.0)
         inst = hg.Instance(40, 6, pr.C, pr.W, 3.0, 0.75, 2.0)
@@ -125,7 +136,7 @@ class TestObjective:
             assert np.array_equal(hg.nearest_allocations(inst, pop[b:b + 1])[0], a)
             assert close(out[b, 3], orc.path_sum(pr, a), rel=1e-9)
 
-    def test_big_instance_linearity(self):
+    def test_big_instance_linearity(self, kernel):
         """n=6000, p=50 (BASELINE config 4): the transfer term is linear in
         alpha and in W; check against the oracle on a few individuals."""
         inst = hg.generate_urand(6000, 50, 1704, (1.0, 0.75, 1.0))
@@ -140,6 +151,30 @@ class TestObjective:
         out2 = hg.evaluate_population(inst2, pop)
         assert close(out2[:, 1], 2.0 * out[:, 1], rel=1e-14)
         assert np.array_equal(out2[:, 0], out[:, 0])
+
+
+class TestKernels:
+    def test_tensor_path_is_selected_for_u8_flows(self):
+        inst = hg.generate_urand(300, 20, 3, (1.0, 0.75, 1.0))
+        d = inst.device()
+        assert d.flags & 4 and d.fitness_kernel == "tensor"
+        frac = hg.Instance(inst.n, inst.p, inst.dist, inst.flow * 0.5, 1.0, 0.75, 1.0)
+        assert frac.device().fitness_kernel == "fp64"
+        with pytest.raises(ValueError, match="tensor-core"):
+            frac.device().set_fitness(2)
+
+    @pytest.mark.parametrize("n,p", [(1000, 20), (200, 10), (129, 50), (77, 3), (256, 1),
+                                     (300, 17)])
+    def test_tensor_equals_fp64(self, n, p):
+        inst = hg.generate_urand(n, p, 21, (2.0, 0.6, 1.5))
+        pop = hg.random_population(n, p, 300, key=4)
+        d = inst.device()
+        d.set_fitness(2)
+        tc = hg.evaluate_population(inst, pop)
+        d.set_fitness(1)
+        fp = hg.evaluate_population(inst, pop)
+        assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
+        assert close(tc, fp, rel=1e-13)
 
 
 class TestOperators:
@@ -202,7 +237,7 @@ class TestOperators:
 
 class TestGa:
     @pytest.mark.parametrize("label", GA_LABELS)
-    def test_solve_replays_reference(self, label):
+    def test_solve_replays_reference(self, label, kernel):
         g = golden("ga")
         inst = inst_from(g, label)
         params = hg.GaParams(**params_of(g, label))
@@ -255,7 +290,7 @@ class TestGa:
             assert all(b <= a for a, b in zip(rep.trace, rep.trace[1:]))
         assert hits >= 19
 
-    def test_virtual_shards_identical(self):
+    def test_virtual_shards_identical(self, kernel):
         """Island sharding across devices reproduces the 1-device run: shards
         of [0, R) run one after another on this GPU with the same exchange."""
         from paper_1704_06258_b200 import engine
