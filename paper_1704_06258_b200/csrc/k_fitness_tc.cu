@@ -10,21 +10,24 @@
 // which equals sum_ij W_ij C[a_i][a_j] of hm/evaluation.py:113-119 up to fp64
 // summation order.  Batched over the population, G is one GEMM
 //   D[i][(b,l)] = W[i][:] . OneHot[(b,l)][:]
-// with M = nodes i (128 per tile), N = (individual, hub) pairs (ipt
-// individuals x p, <= 256), K = nodes j.
+// with M = nodes i, N = (individual, hub) pairs (ipt individuals x p <= 256),
+// K = nodes j.
 //
-// Per CTA (256 threads, one per SM): TMEM holds the 128 x N s32 accumulator;
-// W tiles (A operand, K-major, SWIZZLE_128B) arrive by TMA; the one-hot B
-// operand is generated in shared memory from the cluster-id bytes by all
-// threads (same canonical SWIZZLE_128B K-major layout), fenced to the async
-// proxy, and consumed by tcgen05.mma.kind::i8 issued by one thread; K-blocks
-// are double-buffered so generation of block k+1 overlaps the MMAs of block k.
-// The epilogue reads the accumulator with tcgen05.ld, converts exactly to
-// fp64 and contracts with the staged hub-cost tables; one partial per
-// (individual, 128-row tile) in a fixed reduction order.
+// Work unit = (N tile of ipt individuals, PAIR of 128-row M tiles).  Per CTA
+// (512 threads, one per SM) TMEM holds the two 128 x N s32 accumulators
+// (columns 0 and 256).  Per 128-wide K block: the two W tiles (A operands,
+// K-major, SWIZZLE_128B) arrive by TMA; the one-hot B tile is generated ONCE
+// in shared memory (same canonical layout) from cluster ids staged by
+// cp.async one K block ahead, fenced to the async proxy, and consumed by the
+// 8 tcgen05.mma.kind::i8 of both accumulators (issued by one thread); K
+// blocks are double-buffered so generation of block k+1 overlaps the MMAs of
+// block k.  The epilogue reads the accumulators with tcgen05.ld, converts
+// exactly to fp64 and contracts with the staged hub-cost tables; one partial
+// per (individual, 128-row tile) in a fixed reduction order.
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_pipeline.h>
 
 #include "hg_internal.cuh"
 
@@ -32,11 +35,18 @@ namespace hg {
 
 namespace {
 
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 512;
+constexpr int kTcWarps = kTcThreads / 32;
 constexpr int kTcTmemCols = 512;
-constexpr int kAStage = 128 * 128;   // bytes: 128 rows x 128 K (u8)
+constexpr int kAStage = 128 * 128;   // bytes: 128 rows x 128 K (u8), one M tile
 constexpr int kBStage = 256 * 128;   // bytes: up to 256 rows x 128 K
-constexpr int kSmemT = 2 * kAStage + 2 * kBStage;  // offset of the T staging area
+constexpr int kMaxIpt = 64;  // caps the per-tile staging for tiny p
+
+// shared memory map (offsets from the 1024-aligned base)
+constexpr int kOffA = 0;                            // [2 stages][2 tiles] x 16 KB
+constexpr int kOffB = kOffA + 4 * kAStage;          // [2 stages] x 32 KB
+constexpr int kOffRowInfo = kOffB + 2 * kBStage;    // [256] int: (bl << 16) | l
+constexpr int kOffVar = kOffRowInfo + 256 * 4;      // variable part
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -105,12 +115,15 @@ __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
           "=r"(r[7])
         : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
@@ -132,27 +145,38 @@ struct TcArgs {
     int ipt;      // individuals per N tile
     int N;        // MMA N (multiple of 16, <= 256)
     int64_t NT;   // N tiles
-    int MT, KB;   // 128-row tiles, 128-wide K blocks
-    int pss;      // smem row stride of staged T planes (odd)
+    int MT, MP;   // 128-row tiles, tile pairs
+    int KB;       // 128-wide K blocks
+    int pss;      // smem row stride of staged T planes (odd -> conflict-free)
     uint32_t idesc;
 };
+
+__host__ __device__ inline int tc_var_T(int ipt, int p, int pss) {
+    return ((ipt * 2 * p * pss * 4) + 15) & ~15;
+}
 
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-align the operand area (SWIZZLE_128B atoms)
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* sA = smem;                          // 2 x 16 KB
-    unsigned char* sB = smem + 2 * kAStage;            // 2 x 32 KB
-    uint32_t* sT = reinterpret_cast<uint32_t*>(smem + kSmemT);
-    const int tsz = A.ipt * 2 * A.p * A.pss;           // words
-    double* red = reinterpret_cast<double*>(sT + ((tsz + 1) & ~1));  // [8 warps][ipt]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * A.ipt);   // tma[2], mma[2]
+    const int p = A.p, ipt = A.ipt;
+    int* rowinfo = reinterpret_cast<int*>(smem + kOffRowInfo);
+    unsigned char* var = smem + kOffVar;
+    uint32_t* sT = reinterpret_cast<uint32_t*>(var);                  // [ipt][2][p][pss]
+    var += tc_var_T(ipt, p, A.pss);
+    uint8_t* cbuf = var;                                              // [2][ipt][128]
+    var += 2 * ((ipt * 128 + 15) & ~15);
+    uint8_t* rc = var;                                                // [ipt][256] row cids
+    var += (ipt * 256 + 15) & ~15;
+    double* red = reinterpret_cast<double*>(var);                     // [16 warps][2][ipt]
+    var += kTcWarps * 2 * ipt * 8;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(var);                // tma[2], mma[2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t bar_tma0 = smem_u32(bars), bar_mma0 = smem_u32(bars + 2);
+    const int cstride = (ipt * 128 + 15) & ~15;
 
     if (tid == 0) {
         mbar_init(bar_tma0, 1);
@@ -161,6 +185,10 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         mbar_init(bar_mma0 + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    }
+    for (int r = tid; r < 256; r += kTcThreads) {
+        const int bl = r / p;
+        rowinfo[r] = (r < A.N && bl < ipt) ? ((bl << 16) | (r - bl * p)) : -1;
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -174,50 +202,82 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const int64_t units = A.NT * A.MT;
+    const int64_t units = A.NT * A.MP;
     const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
     uint32_t n_tma[2] = {0, 0}, n_mma[2] = {0, 0};
     int64_t cur_nt = -1;
-    const int p = A.p;
-    const int half = (A.ipt + 1) / 2;
 
     for (int64_t u = u0; u < u1; ++u) {
-        const int64_t nt = u / A.MT;
-        const int mt = (int)(u - nt * A.MT);
-        const int64_t bbase = nt * A.ipt;
+        const int64_t nt = u / A.MP;
+        const int mp = (int)(u - nt * A.MP);
+        const int m0 = 2 * mp;
+        const bool has1 = m0 + 1 < A.MT;
+        const int64_t bbase = nt * ipt;
+        const int nind = (int)min<int64_t>(ipt, A.B - bbase);
         if (nt != cur_nt) {
-            // stage the hub-cost tables (hi/lo planes) of this N tile's individuals
+            // hub-cost tables (hi/lo planes) of this N tile's individuals
             cur_nt = nt;
             const int per = 2 * p * p;
-            for (int x = tid; x < A.ipt * per; x += kTcThreads) {
+            for (int x = tid; x < ipt * per; x += kTcThreads) {
                 const int bl = x / per, y = x - bl * per;
                 const int row = y / p, l = y - row * p;  // row = plane * p + c
-                const int64_t b = bbase + bl;
                 uint32_t v = 0;
-                if (b < A.B) v = A.T[(b * 2 * p + row) * (int64_t)A.ps + l];
+                if (bl < nind) v = A.T[((bbase + bl) * 2 * p + row) * (int64_t)A.ps + l];
                 sT[(bl * 2 * p + row) * A.pss + l] = v;
             }
         }
+        // row cluster ids of the pair's 256 rows (epilogue)
+        for (int x = tid; x < ipt * 16; x += kTcThreads) {
+            const int bl = x >> 4, k = x & 15;
+            const int i0 = m0 * 128 + k * 16;
+            if (bl < nind && i0 < A.npad)
+                __pipeline_memcpy_async(rc + bl * 256 + k * 16, A.cl + (bbase + bl) * A.npad + i0,
+                                        16);
+        }
+        // cluster ids of K block 0
+        for (int x = tid; x < nind * 8; x += kTcThreads) {
+            const int bl = x >> 3, k = x & 7;
+            __pipeline_memcpy_async(cbuf + bl * 128 + k * 16,
+                                    A.cl + (bbase + bl) * A.npad + k * 16, 16);
+        }
+        __pipeline_commit();
+
         for (int kb = 0; kb < A.KB; ++kb) {
             const int s = kb & 1;
             if (kb >= 2) mbar_wait(bar_mma0 + 8 * s, (n_mma[s] - 1) & 1);
-            unsigned char* a_st = sA + s * kAStage;
-            unsigned char* b_st = sB + s * kBStage;
+            unsigned char* a_st = smem + kOffA + s * 2 * kAStage;
+            unsigned char* b_st = smem + kOffB + s * kBStage;
             if (tid == 0) {
-                mbar_expect_tx(bar_tma0 + 8 * s, kAStage);
-                tma_load_2d(smem_u32(a_st), &tmW, kb * 128, mt * 128, bar_tma0 + 8 * s);
+                mbar_expect_tx(bar_tma0 + 8 * s, has1 ? 2 * kAStage : kAStage);
+                tma_load_2d(smem_u32(a_st), &tmW, kb * 128, m0 * 128, bar_tma0 + 8 * s);
+                if (has1)
+                    tma_load_2d(smem_u32(a_st + kAStage), &tmW, kb * 128, (m0 + 1) * 128,
+                                bar_tma0 + 8 * s);
             }
             n_tma[s]++;
+            // prefetch cluster ids of K block kb+1 into the other buffer
+            if (kb + 1 < A.KB) {
+                uint8_t* nb = cbuf + (s ^ 1) * cstride;
+                for (int x = tid; x < nind * 8; x += kTcThreads) {
+                    const int bl = x >> 3, k = x & 7;
+                    __pipeline_memcpy_async(nb + bl * 128 + k * 16,
+                                            A.cl + (bbase + bl) * A.npad + (kb + 1) * 128 + k * 16,
+                                            16);
+                }
+            }
+            __pipeline_commit();
+            __pipeline_wait_prior(1);
+            __syncthreads();
             // one-hot B tile: row r = (individual bl, hub l), 128 K bytes, swizzled
+            const uint8_t* cb = cbuf + s * cstride;
             for (int it = tid; it < A.N * 8; it += kTcThreads) {
                 const int r = it >> 3, c = it & 7;
-                const int bl = r / p, l = r - bl * p;
-                const int64_t b = bbase + bl;
+                const int info = rowinfo[r];
+                const int bl = info >> 16;
                 uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                if (bl < A.ipt && b < A.B) {
-                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(
-                        A.cl + b * A.npad + kb * 128 + c * 16));
-                    const uint32_t lrep = (uint32_t)l * 0x01010101u;
+                if (info >= 0 && bl < nind) {
+                    const uint4 x = *reinterpret_cast<const uint4*>(cb + bl * 128 + c * 16);
+                    const uint32_t lrep = (uint32_t)(info & 0xffff) * 0x01010101u;
                     v.x = onehot4(x.x, lrep);
                     v.y = onehot4(x.y, lrep);
                     v.z = onehot4(x.z, lrep);
@@ -231,64 +291,73 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             if (tid == 0) {
                 mbar_wait(bar_tma0 + 8 * s, (n_tma[s] - 1) & 1);
                 tc_fence_after();
-                const uint64_t ad = sw128_desc(smem_u32(a_st));
+                const uint64_t a0 = sw128_desc(smem_u32(a_st));
+                const uint64_t a1 = sw128_desc(smem_u32(a_st + kAStage));
                 const uint64_t bd = sw128_desc(smem_u32(b_st));
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)  // K = 32 bytes per MMA: +2 in 16 B units
-                    mma_i8(tmem, ad + 2 * ks, bd + 2 * ks, A.idesc, (kb | ks) != 0);
+                    mma_i8(tmem, a0 + 2 * ks, bd + 2 * ks, A.idesc, (kb | ks) != 0);
+                if (has1) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        mma_i8(tmem + 256, a1 + 2 * ks, bd + 2 * ks, A.idesc, (kb | ks) != 0);
+                }
                 mma_commit(bar_mma0 + 8 * s);
             }
             n_mma[s]++;
         }
-        // accumulator complete
+        // accumulators complete
         const int sl = (A.KB - 1) & 1;
         mbar_wait(bar_mma0 + 8 * sl, (n_mma[sl] - 1) & 1);
         tc_fence_after();
 
-        // epilogue: warp quadrant q owns TMEM lanes / rows 32q..32q+31; the two
-        // warp halves split the individuals
-        const int q = warp & 3, h = warp >> 2;
-        const int i = mt * 128 + q * 32 + lane;
-        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-        const int bl_lo = h * half, bl_hi = min(A.ipt, (h + 1) * half);
-        for (int bl = bl_lo; bl < bl_hi; ++bl) {
-            const int64_t b = bbase + bl;
-            double acc = 0.0;
-            if (b < A.B) {  // warp-uniform
-                const int c = (i < A.npad) ? A.cl[b * A.npad + i] : 0;
+        // epilogue: warp w reads TMEM lanes (rows) 32*(w&3)..; the 4 warp
+        // groups g = w>>2 take individuals bl = g, g+4, ...
+        const int q = warp & 3, g = warp >> 2;
+        for (int a = 0; a < (has1 ? 2 : 1); ++a) {
+            const int rloc = a * 128 + q * 32 + lane;  // row within the pair
+            const uint32_t trow = tmem + (uint32_t)(a * 256) + ((uint32_t)(q * 32) << 16);
+            for (int bl = g; bl < nind; bl += 4) {
+                const int c = rc[bl * 256 + rloc];
                 const uint32_t* th = sT + (bl * 2 * p + c) * A.pss;
                 const uint32_t* tl = sT + (bl * 2 * p + p + c) * A.pss;
-                for (int l0 = 0; l0 < p; l0 += 8) {
-                    uint32_t d[8];
-                    tmem_ld8(trow + (uint32_t)(bl * p + l0), d);
+                double acc0 = 0.0, acc1 = 0.0;
+                for (int l0 = 0; l0 < p; l0 += 32) {
+                    uint32_t d[32];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
+                    for (int k8 = 0; k8 < 4; ++k8)
+                        if (l0 + 8 * k8 < p) tmem_ld8(trow + (uint32_t)(bl * p + l0 + 8 * k8), d + 8 * k8);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
                         if (l0 + k < p) {
-                            // exact u32 -> fp64: 2^52 + d, then subtract 2^52
+                            // exact u32 -> fp64: (2^52 + d) - 2^52
                             const double dd = __hiloint2double(0x43300000, (int)d[k]) -
                                               4503599627370496.0;
-                            const double t = __hiloint2double((int)th[l0 + k], (int)tl[l0 + k]);
-                            acc = fma(dd, t, acc);
+                            const double t =
+                                __hiloint2double((int)th[l0 + k], (int)tl[l0 + k]);
+                            if (k & 1) acc1 = fma(dd, t, acc1);
+                            else acc0 = fma(dd, t, acc0);
                         }
                     }
                 }
-            }
+                double acc = acc0 + acc1;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) red[warp * A.ipt + bl] = acc;
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) red[(warp * 2 + a) * ipt + bl] = acc;
+            }
         }
         tc_fence_before();
         __syncthreads();
-        if (tid < A.ipt) {
-            const int64_t b = bbase + tid;
-            if (b < A.B) {
-                const int hh = tid / half;
-                double s4 = 0.0;
-                for (int qq = 0; qq < 4; ++qq) s4 += red[(hh * 4 + qq) * A.ipt + tid];
-                A.part[b * A.MT + mt] = s4;
-            }
+        for (int x = tid; x < 2 * nind; x += kTcThreads) {
+            const int a = x / nind, bl = x - a * nind;
+            if (a == 1 && !has1) continue;
+            const int gg = bl & 3;
+            double s4 = 0.0;
+            for (int qq = 0; qq < 4; ++qq) s4 += red[((gg * 4 + qq) * 2 + a) * ipt + bl];
+            A.part[(bbase + bl) * A.MT + m0 + a] = s4;
         }
-        // red is rewritten only after the next unit's K loop (its __syncthreads)
+        // red / rc / cbuf are rewritten only after the next unit's first __syncthreads
     }
     tc_fence_before();
     __syncthreads();
@@ -340,11 +409,17 @@ int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out) {
 
 static int tc_pss(int p) { return p | 1; }
 
+static int tc_ipt(int p) { return 256 / p < kMaxIpt ? 256 / p : kMaxIpt; }
+
 size_t tc_smem_bytes(int p) {
-    const int ipt = 256 / p;
-    size_t t = (size_t)ipt * 2 * p * tc_pss(p) * 4;
-    t = (t + 7) & ~size_t(7);
-    return 1024 + kSmemT + t + 8 * ipt * 8 + 4 * 8 + 16;
+    const int ipt = tc_ipt(p);
+    size_t b = 1024 + kOffVar;
+    b += tc_var_T(ipt, p, tc_pss(p));
+    b += 2 * ((ipt * 128 + 15) & ~15);
+    b += (ipt * 256 + 15) & ~15;
+    b += kTcWarps * 2 * ipt * 8;
+    b += 4 * 8 + 16;
+    return b;
 }
 
 bool tc_supported(int p) { return p >= 1 && p <= 128 && tc_smem_bytes(p) <= 227 * 1024; }
@@ -369,15 +444,16 @@ int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8
     A.p = I.p;
     A.ps = I.ps;
     A.npad = I.npad;
-    A.ipt = 256 / I.p;
+    A.ipt = tc_ipt(I.p);
     A.N = (int)round_up((int64_t)A.ipt * I.p, 16);
     A.NT = ceil_div(B, A.ipt);
     A.MT = tc_tiles(I.n);
+    A.MP = (A.MT + 1) / 2;
     A.KB = A.MT;
     A.pss = tc_pss(I.p);
     // kind::i8 instruction descriptor: D s32, A/B u8, both K-major, N, M=128
     A.idesc = (2u << 4) | ((uint32_t)(A.N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    const int64_t units = A.NT * A.MT;
+    const int64_t units = A.NT * A.MP;
     int g = grid;
     if (g > units) g = (int)units;
     CUtensorMap map = *static_cast<const CUtensorMap*>(wmap);
