@@ -213,7 +213,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         const int m0 = 2 * mp;
         const bool has1 = m0 + 1 < A.MT;
         const int64_t bbase = nt * ipt;
-        const int nind = (int)min<int64_t>(ipt, A.B - bbase);
+        const int nind = (int)(A.B - bbase < ipt ? A.B - bbase : ipt);
         if (nt != cur_nt) {
             // hub-cost tables (hi/lo planes) of this N tile's individuals
             cur_nt = nt;
