@@ -409,10 +409,7 @@ int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out) {
 
 static int tc_pss(int p) { return p | 1; }
 
-static int tc_ipt(int p) { return 256 / p < kMaxIpt ? 256 / p : kMaxIpt; }
-
-size_t tc_smem_bytes(int p) {
-    const int ipt = tc_ipt(p);
+static size_t tc_smem_for(int p, int ipt) {
     size_t b = 1024 + kOffVar;
     b += tc_var_T(ipt, p, tc_pss(p));
     b += 2 * ((ipt * 128 + 15) & ~15);
@@ -421,6 +418,15 @@ size_t tc_smem_bytes(int p) {
     b += 4 * 8 + 16;
     return b;
 }
+
+// individuals per N tile: as many as fit N <= 256 and the shared memory
+static int tc_ipt(int p) {
+    int ipt = 256 / p < kMaxIpt ? 256 / p : kMaxIpt;
+    while (ipt > 1 && tc_smem_for(p, ipt) > 227 * 1024) --ipt;
+    return ipt;
+}
+
+size_t tc_smem_bytes(int p) { return tc_smem_for(p, tc_ipt(p)); }
 
 bool tc_supported(int p) { return p >= 1 && p <= 128 && tc_smem_bytes(p) <= 227 * 1024; }
 
