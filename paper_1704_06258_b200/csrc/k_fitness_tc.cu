@@ -422,6 +422,10 @@ static size_t tc_smem_for(int p, int ipt) {
 // individuals per N tile: as many as fit N <= 256 and the shared memory
 static int tc_ipt(int p) {
     int ipt = 256 / p < kMaxIpt ? 256 / p : kMaxIpt;
+    // the epilogue reads 8 accumulator columns at a time: the last individual's
+    // reads must stay inside its 256-column accumulator
+    const int p8 = (p + 7) & ~7;
+    while (ipt > 1 && (ipt - 1) * p + p8 > 256) --ipt;
     while (ipt > 1 && tc_smem_for(p, ipt) > 227 * 1024) --ipt;
     return ipt;
 }
