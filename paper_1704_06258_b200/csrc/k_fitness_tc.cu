@@ -127,11 +127,13 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// byte-wise (x == l) -> 0x01 / 0x00, exact (no cross-byte carries)
+// byte-wise (x == l) -> 0x80 / 0x00, exact (no cross-byte carries).  The
+// one-hot value is 128 (u8) instead of 1: the GEMM yields 128*G exactly
+// (< 2^31) and the 2^-7 is folded into the staged hub-cost tables.
 __device__ __forceinline__ uint32_t onehot4(uint32_t x, uint32_t lrep) {
     const uint32_t y = x ^ lrep;
-    const uint32_t t = ((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y;
-    return (~t >> 7) & 0x01010101u;
+    const uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+    return ~(t | y) & 0x80808080u;
 }
 
 }  // namespace
@@ -147,23 +149,27 @@ struct TcArgs {
     int64_t NT;   // N tiles
     int MT, MP;   // 128-row tiles, tile pairs
     int KB;       // 128-wide K blocks
-    int pss;      // smem row stride of staged T planes (odd -> conflict-free)
+    int pss;      // smem row stride (doubles) of the staged T rows: even, pss/2 odd
     uint32_t idesc;
 };
 
+// staged T: ipt x p rows of pss doubles (16-byte aligned rows, and an odd
+// number of 16-byte chunks per row so a quarter-warp's LDS.128 of 8 different
+// rows hit 8 different bank groups)
 __host__ __device__ inline int tc_var_T(int ipt, int p, int pss) {
-    return ((ipt * 2 * p * pss * 4) + 15) & ~15;
+    return ((ipt * p * pss * 8) + 15) & ~15;
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-align by pointer arithmetic on the shared array itself, so the
+    // compiler keeps every access in the shared window (LDS/STS, not LD/ST.E)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int p = A.p, ipt = A.ipt;
     int* rowinfo = reinterpret_cast<int*>(smem + kOffRowInfo);
     unsigned char* var = smem + kOffVar;
-    uint32_t* sT = reinterpret_cast<uint32_t*>(var);                  // [ipt][2][p][pss]
+    double* sT = reinterpret_cast<double*>(var);                      // [ipt][p][pss] T * 2^-7
     var += tc_var_T(ipt, p, A.pss);
     uint8_t* cbuf = var;                                              // [2][ipt][128]
     var += 2 * ((ipt * 128 + 15) & ~15);
@@ -215,15 +221,20 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         const int64_t bbase = nt * ipt;
         const int nind = (int)(A.B - bbase < ipt ? A.B - bbase : ipt);
         if (nt != cur_nt) {
-            // hub-cost tables (hi/lo planes) of this N tile's individuals
+            // hub-cost tables of this N tile's individuals as fp64 x 2^-7 (exact
+            // power-of-two scaling: undoes the one-hot value 128)
             cur_nt = nt;
-            const int per = 2 * p * p;
+            const int per = p * p;
             for (int x = tid; x < ipt * per; x += kTcThreads) {
                 const int bl = x / per, y = x - bl * per;
-                const int row = y / p, l = y - row * p;  // row = plane * p + c
-                uint32_t v = 0;
-                if (bl < nind) v = A.T[((bbase + bl) * 2 * p + row) * (int64_t)A.ps + l];
-                sT[(bl * 2 * p + row) * A.pss + l] = v;
+                const int c = y / p, l = y - c * p;
+                double v = 0.0;
+                if (bl < nind) {
+                    const uint32_t* tb = A.T + (bbase + bl) * 2 * p * (int64_t)A.ps;
+                    v = __hiloint2double((int)tb[c * A.ps + l], (int)tb[(p + c) * A.ps + l]) *
+                        0.0078125;
+                }
+                sT[(bl * p + c) * A.pss + l] = v;
             }
         }
         // row cluster ids of the pair's 256 rows (epilogue)
@@ -319,14 +330,19 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             const uint32_t trow = tmem + (uint32_t)(a * 256) + ((uint32_t)(q * 32) << 16);
             for (int bl = g; bl < nind; bl += 4) {
                 const int c = rc[bl * 256 + rloc];
-                const uint32_t* th = sT + (bl * 2 * p + c) * A.pss;
-                const uint32_t* tl = sT + (bl * 2 * p + p + c) * A.pss;
+                const double2* tr = reinterpret_cast<const double2*>(sT + (bl * p + c) * A.pss);
                 double acc0 = 0.0, acc1 = 0.0;
                 for (int l0 = 0; l0 < p; l0 += 32) {
                     uint32_t d[32];
+                    double2 t[16];
 #pragma unroll
                     for (int k8 = 0; k8 < 4; ++k8)
                         if (l0 + 8 * k8 < p) tmem_ld8(trow + (uint32_t)(bl * p + l0 + 8 * k8), d + 8 * k8);
+                    // the thread's T row (c fixed per row and individual) while the
+                    // TMEM loads are in flight; rows padded to an even stride
+#pragma unroll
+                    for (int k2 = 0; k2 < 16; ++k2)
+                        if (l0 + 2 * k2 < p) t[k2] = tr[(l0 >> 1) + k2];
                     tmem_wait_ld();
 #pragma unroll
                     for (int k = 0; k < 32; ++k) {
@@ -334,10 +350,9 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                             // exact u32 -> fp64: (2^52 + d) - 2^52
                             const double dd = __hiloint2double(0x43300000, (int)d[k]) -
                                               4503599627370496.0;
-                            const double t =
-                                __hiloint2double((int)th[l0 + k], (int)tl[l0 + k]);
-                            if (k & 1) acc1 = fma(dd, t, acc1);
-                            else acc0 = fma(dd, t, acc0);
+                            const double tv = (k & 1) ? t[k >> 1].y : t[k >> 1].x;
+                            if (k & 1) acc1 = fma(dd, tv, acc1);
+                            else acc0 = fma(dd, tv, acc0);
                         }
                     }
                 }
@@ -407,7 +422,7 @@ int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out) {
     return HG_OK;
 }
 
-static int tc_pss(int p) { return p | 1; }
+static int tc_pss(int p) { return (((p + 1) / 2) | 1) * 2; }
 
 static size_t tc_smem_for(int p, int ipt) {
     size_t b = 1024 + kOffVar;
