@@ -173,8 +173,9 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
     var += tc_var_T(ipt, p, A.pss);
     uint8_t* cbuf = var;                                              // [2][ipt][128]
     var += 2 * ((ipt * 128 + 15) & ~15);
-    uint8_t* rc = var;                                                // [ipt][256] row cids
-    var += (ipt * 256 + 15) & ~15;
+    uint8_t* rc = var;                                                // [2][ipt][256] row cids
+    const int rcstride = (ipt * 256 + 15) & ~15;
+    var += 2 * rcstride;
     double* red = reinterpret_cast<double*>(var);                     // [16 warps][2][ipt]
     var += kTcWarps * 2 * ipt * 8;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);                // tma[2], mma[2]
@@ -213,17 +214,69 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
     uint32_t n_tma[2] = {0, 0}, n_mma[2] = {0, 0};
     int64_t cur_nt = -1;
 
+    struct UnitInfo {
+        int64_t nt, bbase;
+        int m0, nind;
+        bool has1;
+    };
+    auto unit_info = [&](int64_t u) {
+        UnitInfo U;
+        U.nt = u / A.MP;
+        U.m0 = 2 * (int)(u - U.nt * A.MP);
+        U.has1 = U.m0 + 1 < A.MT;
+        U.bbase = U.nt * ipt;
+        U.nind = (int)(A.B - U.bbase < ipt ? A.B - U.bbase : ipt);
+        return U;
+    };
+    // thread 0: the two W tiles of K block kb into A stage s
+    auto issue_A = [&](const UnitInfo& U, int kb, int s) {
+        unsigned char* a_st = smem + kOffA + s * 2 * kAStage;
+        mbar_expect_tx(bar_tma0 + 8 * s, U.has1 ? 2 * kAStage : kAStage);
+        tma_load_2d(smem_u32(a_st), &tmW, kb * 128, U.m0 * 128, bar_tma0 + 8 * s);
+        if (U.has1)
+            tma_load_2d(smem_u32(a_st + kAStage), &tmW, kb * 128, (U.m0 + 1) * 128,
+                        bar_tma0 + 8 * s);
+    };
+    auto fetch_cids = [&](const UnitInfo& U, int kb, uint8_t* dst) {
+        for (int x = tid; x < U.nind * 8; x += kTcThreads) {
+            const int bl = x >> 3, k = x & 7;
+            __pipeline_memcpy_async(dst + bl * 128 + k * 16,
+                                    A.cl + (U.bbase + bl) * A.npad + kb * 128 + k * 16, 16);
+        }
+    };
+    auto fetch_rc = [&](const UnitInfo& U, uint8_t* dst) {  // row cids of the pair's 256 rows
+        for (int x = tid; x < U.nind * 16; x += kTcThreads) {
+            const int bl = x >> 4, k = x & 15;
+            const int i0 = U.m0 * 128 + k * 16;
+            if (i0 < A.npad)
+                __pipeline_memcpy_async(dst + bl * 256 + k * 16,
+                                        A.cl + (U.bbase + bl) * A.npad + i0, 16);
+        }
+    };
+
+    // prologue: first unit's K block 0 (stage 0) and epilogue row ids
+    uint32_t gk = 0;  // K blocks issued by this CTA so far (stage = gk & 1)
+    if (u0 < u1) {
+        const UnitInfo U = unit_info(u0);
+        if (tid == 0) issue_A(U, 0, 0);
+        n_tma[0]++;
+        fetch_cids(U, 0, cbuf);
+        fetch_rc(U, rc);
+        __pipeline_commit();
+        __pipeline_wait_prior(0);
+        __syncthreads();
+    }
+
     for (int64_t u = u0; u < u1; ++u) {
-        const int64_t nt = u / A.MP;
-        const int mp = (int)(u - nt * A.MP);
-        const int m0 = 2 * mp;
-        const bool has1 = m0 + 1 < A.MT;
-        const int64_t bbase = nt * ipt;
-        const int nind = (int)(A.B - bbase < ipt ? A.B - bbase : ipt);
-        if (nt != cur_nt) {
+        const UnitInfo U = unit_info(u);
+        const int m0 = U.m0, nind = U.nind;
+        const bool has1 = U.has1;
+        const int64_t bbase = U.bbase;
+        const uint8_t* rcu = rc + ((u - u0) & 1) * rcstride;
+        if (U.nt != cur_nt) {
             // hub-cost tables of this N tile's individuals as fp64 x 2^-7 (exact
             // power-of-two scaling: undoes the one-hot value 128)
-            cur_nt = nt;
+            cur_nt = U.nt;
             const int per = p * p;
             for (int x = tid; x < ipt * per; x += kTcThreads) {
                 const int bl = x / per, y = x - bl * per;
@@ -237,48 +290,15 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                 sT[(bl * p + c) * A.pss + l] = v;
             }
         }
-        // row cluster ids of the pair's 256 rows (epilogue)
-        for (int x = tid; x < ipt * 16; x += kTcThreads) {
-            const int bl = x >> 4, k = x & 15;
-            const int i0 = m0 * 128 + k * 16;
-            if (bl < nind && i0 < A.npad)
-                __pipeline_memcpy_async(rc + bl * 256 + k * 16, A.cl + (bbase + bl) * A.npad + i0,
-                                        16);
-        }
-        // cluster ids of K block 0
-        for (int x = tid; x < nind * 8; x += kTcThreads) {
-            const int bl = x >> 3, k = x & 7;
-            __pipeline_memcpy_async(cbuf + bl * 128 + k * 16,
-                                    A.cl + (bbase + bl) * A.npad + k * 16, 16);
-        }
-        __pipeline_commit();
 
-        for (int kb = 0; kb < A.KB; ++kb) {
-            const int s = kb & 1;
-            if (kb >= 2) mbar_wait(bar_mma0 + 8 * s, (n_mma[s] - 1) & 1);
+        for (int kb = 0; kb < A.KB; ++kb, ++gk) {
+            const int s = gk & 1;
+            // B stage s is free once the MMAs of K block gk-2 are done
+            if (gk >= 2) mbar_wait(bar_mma0 + 8 * s, (n_mma[s] - 1) & 1);
             unsigned char* a_st = smem + kOffA + s * 2 * kAStage;
             unsigned char* b_st = smem + kOffB + s * kBStage;
-            if (tid == 0) {
-                mbar_expect_tx(bar_tma0 + 8 * s, has1 ? 2 * kAStage : kAStage);
-                tma_load_2d(smem_u32(a_st), &tmW, kb * 128, m0 * 128, bar_tma0 + 8 * s);
-                if (has1)
-                    tma_load_2d(smem_u32(a_st + kAStage), &tmW, kb * 128, (m0 + 1) * 128,
-                                bar_tma0 + 8 * s);
-            }
-            n_tma[s]++;
-            // prefetch cluster ids of K block kb+1 into the other buffer
-            if (kb + 1 < A.KB) {
-                uint8_t* nb = cbuf + (s ^ 1) * cstride;
-                for (int x = tid; x < nind * 8; x += kTcThreads) {
-                    const int bl = x >> 3, k = x & 7;
-                    __pipeline_memcpy_async(nb + bl * 128 + k * 16,
-                                            A.cl + (bbase + bl) * A.npad + (kb + 1) * 128 + k * 16,
-                                            16);
-                }
-            }
+            if (kb + 1 < A.KB) fetch_cids(U, kb + 1, cbuf + (s ^ 1) * cstride);
             __pipeline_commit();
-            __pipeline_wait_prior(1);
-            __syncthreads();
             // one-hot B tile: row r = (individual bl, hub l), 128 K bytes, swizzled
             const uint8_t* cb = cbuf + s * cstride;
             for (int it = tid; it < A.N * 8; it += kTcThreads) {
@@ -298,6 +318,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                                           ((c ^ (r & 7)) << 4)) = v;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __pipeline_wait_prior(0);  // cluster ids of the next K block have landed
             __syncthreads();
             if (tid == 0) {
                 mbar_wait(bar_tma0 + 8 * s, (n_tma[s] - 1) & 1);
@@ -314,13 +335,29 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                         mma_i8(tmem + 256, a1 + 2 * ks, bd + 2 * ks, A.idesc, (kb | ks) != 0);
                 }
                 mma_commit(bar_mma0 + 8 * s);
+                // the next K block's W tiles go into stage s^1 as soon as the MMAs of
+                // K block gk-1 (its previous user) are done: a full block of lead time
+                if (kb + 1 < A.KB) {
+                    if (gk >= 1) mbar_wait(bar_mma0 + 8 * (s ^ 1), (n_mma[s ^ 1] - 1) & 1);
+                    issue_A(U, kb + 1, s ^ 1);
+                }
             }
             n_mma[s]++;
+            if (kb + 1 < A.KB) n_tma[s ^ 1]++;
         }
-        // accumulators complete
-        const int sl = (A.KB - 1) & 1;
+        // accumulators complete (MMAs retire in order)
+        const int sl = (gk - 1) & 1;
         mbar_wait(bar_mma0 + 8 * sl, (n_mma[sl] - 1) & 1);
         tc_fence_after();
+        // prefetch the next unit's first K block and row ids under the epilogue
+        if (u + 1 < u1) {
+            const UnitInfo Un = unit_info(u + 1);
+            if (tid == 0) issue_A(Un, 0, gk & 1);
+            n_tma[gk & 1]++;
+            fetch_cids(Un, 0, cbuf + (gk & 1) * cstride);
+            fetch_rc(Un, rc + ((u + 1 - u0) & 1) * rcstride);
+        }
+        __pipeline_commit();
 
         // epilogue: warp w reads TMEM lanes (rows) 32*(w&3)..; the 4 warp
         // groups g = w>>2 take individuals bl = g, g+4, ...
@@ -329,23 +366,24 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             const int rloc = a * 128 + q * 32 + lane;  // row within the pair
             const uint32_t trow = tmem + (uint32_t)(a * 256) + ((uint32_t)(q * 32) << 16);
             for (int bl = g; bl < nind; bl += 4) {
-                const int c = rc[bl * 256 + rloc];
+                const int c = rcu[bl * 256 + rloc];
                 const double2* tr = reinterpret_cast<const double2*>(sT + (bl * p + c) * A.pss);
                 double acc0 = 0.0, acc1 = 0.0;
-                for (int l0 = 0; l0 < p; l0 += 32) {
-                    uint32_t d[32];
-                    double2 t[16];
+                for (int l0 = 0; l0 < p; l0 += 16) {
+                    uint32_t d[16];
+                    double2 t[8];
 #pragma unroll
-                    for (int k8 = 0; k8 < 4; ++k8)
-                        if (l0 + 8 * k8 < p) tmem_ld8(trow + (uint32_t)(bl * p + l0 + 8 * k8), d + 8 * k8);
+                    for (int k8 = 0; k8 < 2; ++k8)
+                        if (l0 + 8 * k8 < p)
+                            tmem_ld8(trow + (uint32_t)(bl * p + l0 + 8 * k8), d + 8 * k8);
                     // the thread's T row (c fixed per row and individual) while the
                     // TMEM loads are in flight; rows padded to an even stride
 #pragma unroll
-                    for (int k2 = 0; k2 < 16; ++k2)
+                    for (int k2 = 0; k2 < 8; ++k2)
                         if (l0 + 2 * k2 < p) t[k2] = tr[(l0 >> 1) + k2];
                     tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) {
+                    for (int k = 0; k < 16; ++k) {
                         if (l0 + k < p) {
                             // exact u32 -> fp64: (2^52 + d) - 2^52
                             const double dd = __hiloint2double(0x43300000, (int)d[k]) -
@@ -363,6 +401,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             }
         }
         tc_fence_before();
+        __pipeline_wait_prior(0);  // next unit's prefetch has landed
         __syncthreads();
         for (int x = tid; x < 2 * nind; x += kTcThreads) {
             const int a = x / nind, bl = x - a * nind;
@@ -428,7 +467,7 @@ static size_t tc_smem_for(int p, int ipt) {
     size_t b = 1024 + kOffVar;
     b += tc_var_T(ipt, p, tc_pss(p));
     b += 2 * ((ipt * 128 + 15) & ~15);
-    b += (ipt * 256 + 15) & ~15;
+    b += 2 * ((ipt * 256 + 15) & ~15);
     b += kTcWarps * 2 * ipt * 8;
     b += 4 * 8 + 16;
     return b;
