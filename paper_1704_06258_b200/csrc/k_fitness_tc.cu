@@ -167,11 +167,12 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
     // compiler keeps every access in the shared window (LDS/STS, not LD/ST.E)
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int p = A.p, ipt = A.ipt;
-    int* rowinfo = reinterpret_cast<int*>(smem + kOffRowInfo);
     unsigned char* var = smem + kOffVar;
     double* sT = reinterpret_cast<double*>(var);                      // [ipt][p][pss] T * 2^-7
     var += tc_var_T(ipt, p, A.pss);
-    uint8_t* cbuf = var;                                              // [2][ipt][128]
+    uint8_t* cbuf = var;                                              // [2][ipt][128] next cids
+    var += 2 * ((ipt * 128 + 15) & ~15);
+    uint8_t* sc = var;                  // [2][ipt][128] cids currently set in B stage s (0xFF: none)
     var += 2 * ((ipt * 128 + 15) & ~15);
     uint8_t* rc = var;                                                // [2][ipt][256] row cids
     const int rcstride = (ipt * 256 + 15) & ~15;
@@ -193,10 +194,10 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
     }
-    for (int r = tid; r < 256; r += kTcThreads) {
-        const int bl = r / p;
-        rowinfo[r] = (r < A.N && bl < ipt) ? ((bl << 16) | (r - bl * p)) : -1;
-    }
+    // B stages start all-zero; afterwards only the bytes that change are written
+    for (int x = tid; x < 2 * kBStage / 16; x += kTcThreads)
+        reinterpret_cast<uint4*>(smem + kOffB)[x] = make_uint4(0u, 0u, 0u, 0u);
+    for (int x = tid; x < 2 * cstride; x += kTcThreads) sc[x] = 0xFF;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -276,13 +277,16 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         if (U.nt != cur_nt) {
             // hub-cost tables of this N tile's individuals as fp64 x 2^-7 (exact
             // power-of-two scaling: undoes the one-hot value 128)
+            // power-of-two scaling: undoes the one-hot value 128); row tails up to
+            // pss are zero so the epilogue runs whole 8-column chunks unguarded
             cur_nt = U.nt;
-            const int per = p * p;
+            const int pss = A.pss;
+            const int per = p * pss;
             for (int x = tid; x < ipt * per; x += kTcThreads) {
                 const int bl = x / per, y = x - bl * per;
-                const int c = y / p, l = y - c * p;
+                const int c = y / pss, l = y - c * pss;
                 double v = 0.0;
-                if (bl < nind) {
+                if (bl < nind && l < p) {
                     const uint32_t* tb = A.T + (bbase + bl) * 2 * p * (int64_t)A.ps;
                     v = __hiloint2double((int)tb[c * A.ps + l], (int)tb[(p + c) * A.ps + l]) *
                         0.0078125;
@@ -299,23 +303,40 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             unsigned char* b_st = smem + kOffB + s * kBStage;
             if (kb + 1 < A.KB) fetch_cids(U, kb + 1, cbuf + (s ^ 1) * cstride);
             __pipeline_commit();
-            // one-hot B tile: row r = (individual bl, hub l), 128 K bytes, swizzled
-            const uint8_t* cb = cbuf + s * cstride;
-            for (int it = tid; it < A.N * 8; it += kTcThreads) {
-                const int r = it >> 3, c = it & 7;
-                const int info = rowinfo[r];
-                const int bl = info >> 16;
-                uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                if (info >= 0 && bl < nind) {
-                    const uint4 x = *reinterpret_cast<const uint4*>(cb + bl * 128 + c * 16);
-                    const uint32_t lrep = (uint32_t)(info & 0xffff) * 0x01010101u;
-                    v.x = onehot4(x.x, lrep);
-                    v.y = onehot4(x.y, lrep);
-                    v.z = onehot4(x.z, lrep);
-                    v.w = onehot4(x.w, lrep);
+            // one-hot B tile, row r = (individual bl, hub l), 128 K bytes, SW128
+            // swizzled.  Column j of individual bl has exactly one 0x80, in row
+            // bl*p + c_bl(j): update the stage by diffing against the cluster ids
+            // it currently holds (sc) -- clear the old byte, set the new one.
+            {
+                const uint8_t* cb = cbuf + s * cstride;
+                uint8_t* scs = sc + s * cstride;
+                for (int it = tid; it < ipt * 32; it += kTcThreads) {
+                    const int bl = it >> 5, w = it & 31;
+                    const uint32_t nw = bl < nind
+                                            ? *reinterpret_cast<const uint32_t*>(cb + bl * 128 + 4 * w)
+                                            : 0xFFFFFFFFu;
+                    uint32_t* op = reinterpret_cast<uint32_t*>(scs + bl * 128 + 4 * w);
+                    const uint32_t ow = *op;
+                    if (ow != nw) {
+                        const int cch = w >> 2;  // 16-byte chunk of the row
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t o = (ow >> (8 * k)) & 0xFFu, v = (nw >> (8 * k)) & 0xFFu;
+                            if (o == v) continue;
+                            const int jb = (4 * w + k) & 15;
+                            if (o != 0xFFu) {
+                                const int r = bl * p + (int)o;
+                                b_st[(r >> 3) * 1024 + (r & 7) * 128 + ((cch ^ (r & 7)) << 4) + jb] = 0;
+                            }
+                            if (v != 0xFFu) {
+                                const int r = bl * p + (int)v;
+                                b_st[(r >> 3) * 1024 + (r & 7) * 128 + ((cch ^ (r & 7)) << 4) + jb] =
+                                    0x80;
+                            }
+                        }
+                        *op = nw;
+                    }
                 }
-                *reinterpret_cast<uint4*>(b_st + (r >> 3) * 1024 + (r & 7) * 128 +
-                                          ((c ^ (r & 7)) << 4)) = v;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __pipeline_wait_prior(0);  // cluster ids of the next K block have landed
@@ -369,29 +390,25 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                 const int c = rcu[bl * 256 + rloc];
                 const double2* tr = reinterpret_cast<const double2*>(sT + (bl * p + c) * A.pss);
                 double acc0 = 0.0, acc1 = 0.0;
-                for (int l0 = 0; l0 < p; l0 += 16) {
-                    uint32_t d[16];
-                    double2 t[8];
-#pragma unroll
-                    for (int k8 = 0; k8 < 2; ++k8)
-                        if (l0 + 8 * k8 < p)
-                            tmem_ld8(trow + (uint32_t)(bl * p + l0 + 8 * k8), d + 8 * k8);
+                for (int l0 = 0; l0 < p; l0 += 8) {
+                    // 8 accumulator columns (the tail beyond p belongs to the next
+                    // individual or is unused: it meets zero T entries)
+                    uint32_t d[8];
+                    tmem_ld8(trow + (uint32_t)(bl * p + l0), d);
                     // the thread's T row (c fixed per row and individual) while the
-                    // TMEM loads are in flight; rows padded to an even stride
+                    // TMEM load is in flight
+                    double2 t[4];
 #pragma unroll
-                    for (int k2 = 0; k2 < 8; ++k2)
-                        if (l0 + 2 * k2 < p) t[k2] = tr[(l0 >> 1) + k2];
+                    for (int k2 = 0; k2 < 4; ++k2) t[k2] = tr[(l0 >> 1) + k2];
                     tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        if (l0 + k < p) {
-                            // exact u32 -> fp64: (2^52 + d) - 2^52
-                            const double dd = __hiloint2double(0x43300000, (int)d[k]) -
-                                              4503599627370496.0;
-                            const double tv = (k & 1) ? t[k >> 1].y : t[k >> 1].x;
-                            if (k & 1) acc1 = fma(dd, tv, acc1);
-                            else acc0 = fma(dd, tv, acc0);
-                        }
+                    for (int k = 0; k < 8; ++k) {
+                        // exact u32 -> fp64: (2^52 + d) - 2^52
+                        const double dd =
+                            __hiloint2double(0x43300000, (int)d[k]) - 4503599627370496.0;
+                        const double tv = (k & 1) ? t[k >> 1].y : t[k >> 1].x;
+                        if (k & 1) acc1 = fma(dd, tv, acc1);
+                        else acc0 = fma(dd, tv, acc0);
                     }
                 }
                 double acc = acc0 + acc1;
@@ -461,12 +478,14 @@ int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out) {
     return HG_OK;
 }
 
-static int tc_pss(int p) { return (((p + 1) / 2) | 1) * 2; }
+// row stride (doubles) of staged T: >= p rounded up to 8 (zero tail), with an
+// odd number of 16-byte chunks per row (conflict-free LDS.128 across rows)
+static int tc_pss(int p) { return ((p + 7) & ~7) + 2; }
 
 static size_t tc_smem_for(int p, int ipt) {
     size_t b = 1024 + kOffVar;
     b += tc_var_T(ipt, p, tc_pss(p));
-    b += 2 * ((ipt * 128 + 15) & ~15);
+    b += 4 * ((ipt * 128 + 15) & ~15);  // cbuf + sc
     b += 2 * ((ipt * 256 + 15) & ~15);
     b += kTcWarps * 2 * ipt * 8;
     b += 4 * 8 + 16;
