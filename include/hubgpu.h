@@ -108,6 +108,10 @@ int hg_pop_launches_per_evaluate(const hg_pop* pop);
  * measured with CUDA events on the instance stream (synchronises) */
 int hg_pop_last_fitness_ms(hg_pop* pop, float* ms);
 
+/* tuning aid: per-phase cycle counters of K3-TC when the process runs with
+ * HUBGPU_TC_TIMING=1 (32 counters, read and reset); HG_EARG otherwise */
+int hg_debug_tc_timing(unsigned long long* out32);
+
 /* K4c -- correction.  Replaces correct_hub_set (hm/operators.py:69-101) for
  * B raw hub masks (B x n bytes): deficit opens closed nodes in middle-rank
  * order; excess closes, one at a time, the hub whose nearest-allocated nodes

@@ -62,6 +62,7 @@ SIGNATURES = {
     "hg_pop_read": (C.c_int, [_vp, C.c_int64, _vp, C.c_int]),
     "hg_pop_launches_per_evaluate": (C.c_int, [_vp]),
     "hg_pop_last_fitness_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "hg_debug_tc_timing": (C.c_int, [_u64p]),
     "hg_correct": (C.c_int, [_vp, C.c_int64, _u8p, _i64p]),
     "hg_crossover": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _u8p, _i64p, _u8p, _u8p]),
     "hg_swap": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _i64p, _i64p, _u8p]),

@@ -552,6 +552,11 @@ int hg_pop_read(hg_pop* pop, int64_t B, double* out, int where) {
     return HG_OK;
 }
 
+int hg_debug_tc_timing(unsigned long long* out32) {
+    HG_ARG(out32 != nullptr, "NULL buffer");
+    return tc_timing_read(out32);
+}
+
 int hg_pop_launches_per_evaluate(const hg_pop* pop) {
     (void)pop;
     return 3;

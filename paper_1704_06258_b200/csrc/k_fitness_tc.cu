@@ -29,6 +29,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_pipeline.h>
 
+#include <cstdlib>
+
 #include "hg_internal.cuh"
 
 namespace hg {
@@ -151,6 +153,7 @@ struct TcArgs {
     int KB;       // 128-wide K blocks
     int pss;      // smem row stride (doubles) of the staged T rows: even, pss/2 odd
     uint32_t idesc;
+    unsigned long long* timing;  // optional per-phase cycle counters (tuning builds)
 };
 
 // staged T: ipt x p rows of pss doubles (16-byte aligned rows, and an odd
@@ -185,6 +188,18 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t bar_tma0 = smem_u32(bars), bar_mma0 = smem_u32(bars + 2);
     const int cstride = (ipt * 128 + 15) & ~15;
+    // phase timing (only when A.timing is set): thread 0 (MMA issuer) and thread 32
+    const bool timed = A.timing != nullptr && (tid == 0 || tid == 32);
+    unsigned long long tph[12] = {0};
+    long long tlast = timed ? clock64() : 0;
+#define TC_T(ph)                                   \
+    do {                                           \
+        if (timed) {                               \
+            const long long now_ = clock64();      \
+            tph[ph] += (unsigned long long)(now_ - tlast); \
+            tlast = now_;                          \
+        }                                          \
+    } while (0)
 
     if (tid == 0) {
         mbar_init(bar_tma0, 1);
@@ -274,6 +289,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         const bool has1 = U.has1;
         const int64_t bbase = U.bbase;
         const uint8_t* rcu = rc + ((u - u0) & 1) * rcstride;
+        TC_T(11);
         if (U.nt != cur_nt) {
             // hub-cost tables of this N tile's individuals as fp64 x 2^-7 (exact
             // power-of-two scaling: undoes the one-hot value 128)
@@ -295,10 +311,12 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             }
         }
 
+        TC_T(0);
         for (int kb = 0; kb < A.KB; ++kb, ++gk) {
             const int s = gk & 1;
             // B stage s is free once the MMAs of K block gk-2 are done
             if (gk >= 2) mbar_wait(bar_mma0 + 8 * s, (n_mma[s] - 1) & 1);
+            TC_T(1);
             unsigned char* a_st = smem + kOffA + s * 2 * kAStage;
             unsigned char* b_st = smem + kOffB + s * kBStage;
             if (kb + 1 < A.KB) fetch_cids(U, kb + 1, cbuf + (s ^ 1) * cstride);
@@ -338,11 +356,14 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                     }
                 }
             }
+            TC_T(2);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __pipeline_wait_prior(0);  // cluster ids of the next K block have landed
             __syncthreads();
+            TC_T(3);
             if (tid == 0) {
                 mbar_wait(bar_tma0 + 8 * s, (n_tma[s] - 1) & 1);
+                TC_T(4);
                 tc_fence_after();
                 const uint64_t a0 = sw128_desc(smem_u32(a_st));
                 const uint64_t a1 = sw128_desc(smem_u32(a_st + kAStage));
@@ -356,12 +377,14 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                         mma_i8(tmem + 256, a1 + 2 * ks, bd + 2 * ks, A.idesc, (kb | ks) != 0);
                 }
                 mma_commit(bar_mma0 + 8 * s);
+                TC_T(5);
                 // the next K block's W tiles go into stage s^1 as soon as the MMAs of
                 // K block gk-1 (its previous user) are done: a full block of lead time
                 if (kb + 1 < A.KB) {
                     if (gk >= 1) mbar_wait(bar_mma0 + 8 * (s ^ 1), (n_mma[s ^ 1] - 1) & 1);
                     issue_A(U, kb + 1, s ^ 1);
                 }
+                TC_T(6);
             }
             n_mma[s]++;
             if (kb + 1 < A.KB) n_tma[s ^ 1]++;
@@ -370,6 +393,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         const int sl = (gk - 1) & 1;
         mbar_wait(bar_mma0 + 8 * sl, (n_mma[sl] - 1) & 1);
         tc_fence_after();
+        TC_T(7);
         // prefetch the next unit's first K block and row ids under the epilogue
         if (u + 1 < u1) {
             const UnitInfo Un = unit_info(u + 1);
@@ -379,6 +403,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             fetch_rc(Un, rc + ((u + 1 - u0) & 1) * rcstride);
         }
         __pipeline_commit();
+        TC_T(8);
 
         // epilogue: warp w reads TMEM lanes (rows) 32*(w&3)..; the 4 warp
         // groups g = w>>2 take individuals bl = g, g+4, ...
@@ -417,6 +442,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
                 if (lane == 0) red[(warp * 2 + a) * ipt + bl] = acc;
             }
         }
+        TC_T(9);
         tc_fence_before();
         __pipeline_wait_prior(0);  // next unit's prefetch has landed
         __syncthreads();
@@ -430,6 +456,10 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
         }
         // red / rc / cbuf are rewritten only after the next unit's first __syncthreads
     }
+    TC_T(10);
+    if (timed)
+        for (int k = 0; k < 12; ++k) atomicAdd(A.timing + (tid ? 16 : 0) + k, tph[k]);
+#undef TC_T
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -443,6 +473,29 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+
+// HUBGPU_TC_TIMING=1: per-phase cycle counters of K3-TC (tuning only)
+static unsigned long long* tc_timing_buffer() {
+    static int on = -1;
+    static unsigned long long* buf = nullptr;
+    if (on < 0) {
+        const char* e = getenv("HUBGPU_TC_TIMING");
+        on = (e && e[0] == '1') ? 1 : 0;
+        if (on && cudaMalloc(&buf, 32 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(buf, 0, 32 * sizeof(unsigned long long));
+        else
+            buf = nullptr;
+    }
+    return buf;
+}
+
+int tc_timing_read(unsigned long long* out32) {
+    unsigned long long* b = tc_timing_buffer();
+    if (!b) return HG_EARG;
+    HG_CUDA(cudaMemcpy(out32, b, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    HG_CUDA(cudaMemset(b, 0, 32 * sizeof(unsigned long long)));
+    return HG_OK;
+}
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -536,6 +589,7 @@ int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8
     A.pss = tc_pss(I.p);
     // kind::i8 instruction descriptor: D s32, A/B u8, both K-major, N, M=128
     A.idesc = (2u << 4) | ((uint32_t)(A.N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    A.timing = tc_timing_buffer();
     const int64_t units = A.NT * A.MP;
     int g = grid;
     if (g > units) g = (int)units;

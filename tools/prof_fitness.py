@@ -22,3 +22,14 @@ for _ in range(reps):
     pop.evaluate(B)
 d.synchronize()
 print("fitness ms (last):", pop.last_fitness_ms())
+
+if __import__("os").environ.get("HUBGPU_TC_TIMING") == "1":
+    from paper_1704_06258_b200 import _lib
+
+    buf = np.zeros(32, dtype=np.uint64)
+    _lib.check(_lib.load().hg_debug_tc_timing(buf.ctypes.data_as(_lib._u64p)))
+    names = ["Tstage", "waitB", "gen", "bar", "tmaW", "mmaIss", "waitMMA+A", "finalW", "prefetch",
+             "epilog", "end", "unitTop"]
+    for who, off in (("thread0", 0), ("thread32", 16)):
+        tot = buf[off:off + 12].sum()
+        print(who, " ".join(f"{nm}={100 * buf[off + k] / max(tot, 1):.1f}%" for k, nm in enumerate(names)))
