@@ -63,11 +63,11 @@ struct hg_pop {
 };
 
 struct hg_inst {
-    std::atomic<int> refs{1};
+    std::atomic<int> refs{1};  // the handle itself + every hg_pop / hg_ga built on it
     alignas(64) unsigned char wmap[128];  // CUtensorMap of W8 (K3-TC)
     uint8_t* dW8 = nullptr;                // u8 copy of W, [npad_tc][npad_tc], when exact
     bool tc_ok = false;                    // flows are integers in [0, 255] and p fits
-    int fit_kind = HG_FIT_AUTO;  // the handle itself + every hg_pop / hg_ga built on it
+    int fit_kind = HG_FIT_AUTO;
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -82,6 +82,7 @@ struct hg_inst {
     double* dD = nullptr;
     double* dwOD = nullptr;
     int32_t* drank = nullptr;
+    uint16_t* dCq = nullptr;
     hg_pop* scratch = nullptr;
     DevBuf t1, t2, t3, t4;
 };
@@ -326,6 +327,19 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             rc = launch_transpose(inst->dC, inst->dCt, n, s);
             if (rc) break;
         }
+        {
+            // 16-bit monotone quantisation of Ct: exact pre-filter for allocation
+            double cmin = dist[0], cmax = dist[0];
+            for (size_t x = 1; x < nn; ++x) {
+                cmin = dist[x] < cmin ? dist[x] : cmin;
+                cmax = dist[x] > cmax ? dist[x] : cmax;
+            }
+            const double scale = cmax > cmin ? 65535.0 / (cmax - cmin) : 0.0;
+            chk(cudaMalloc(&inst->dCq, nn * sizeof(uint16_t)), "cudaMalloc(Cq)");
+            if (rc) break;
+            rc = launch_quantize(inst->dCt, inst->dCq, (int64_t)nn, cmin, scale, s);
+            if (rc) break;
+        }
         inst->flags = (sym ? HG_FLAG_SYMMETRIC : 0) | (exact ? HG_FLAG_WEIGHTS_EXACT : 0);
 
         DevInst& I = inst->I;
@@ -344,6 +358,7 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.D = inst->dD;
         I.wOD = inst->dwOD;
         I.rank = inst->drank;
+        I.Cq = inst->dCq;
         I.npad = 16;  // provisional for the plan
         inst->plan = fitness_plan(I, inst->sm_count);
         int64_t q = inst->plan.tr > inst->plan.tc ? inst->plan.tr : inst->plan.tc;
@@ -395,6 +410,7 @@ static void inst_destroy(hg_inst* inst) {
     cudaFree(inst->dD);
     cudaFree(inst->dwOD);
     cudaFree(inst->drank);
+    cudaFree(inst->dCq);
     cudaFree(inst->dW8);
     inst->t1.release();
     inst->t2.release();

@@ -84,6 +84,25 @@ __global__ void k_check_symmetric(const double* __restrict__ C, int n, int* flag
     }
 }
 
+// monotone 16-bit quantisation (x - cmin) * scale, floored and clamped: both
+// IEEE operations are monotone non-decreasing, so q(a) < q(b) => a < b
+__global__ void k_quantize(const double* __restrict__ Ct, uint16_t* __restrict__ Cq, int64_t m,
+                           double cmin, double scale) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        double v = floor((Ct[x] - cmin) * scale);
+        v = v < 0.0 ? 0.0 : (v > 65535.0 ? 65535.0 : v);
+        Cq[x] = (uint16_t)v;
+    }
+}
+
+int launch_quantize(const double* Ct, uint16_t* Cq, int64_t count, double cmin, double scale,
+                    cudaStream_t s) {
+    k_quantize<<<grid_for(count, 256), 256, 0, s>>>(Ct, Cq, count, cmin, scale);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
 int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s) {
     k_check_symmetric<<<grid_for((int64_t)n * n, 256), 256, 0, s>>>(C, n, flag);
     HG_CUDA(cudaGetLastError());
@@ -164,18 +183,34 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
     for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
         int c = 0;
         if (i < n) {
-            int h0 = hs[0];
-            double best = I.Ct[(size_t)h0 * n + i];
-            int bk = 0, self = (h0 == i) ? 0 : -1;
+            // exact argmin through the monotone 16-bit pre-filter: the fp64
+            // minimum is among the hubs tied at the minimal quantised value
+            int bk = 0, self = -1, ties = 0;
+            unsigned qmin = 0xFFFFFFFFu;
 #pragma unroll 4
-            for (int k = 1; k < p; ++k) {
-                int h = hs[k];
-                double d = I.Ct[(size_t)h * n + i];
-                if (d < best) {
-                    best = d;
+            for (int k = 0; k < p; ++k) {
+                const int h = hs[k];
+                const unsigned q = I.Cq[(size_t)h * n + i];
+                if (q < qmin) {
+                    qmin = q;
                     bk = k;
+                    ties = 0;
+                } else if (q == qmin) {
+                    ++ties;
                 }
                 if (h == i) self = k;
+            }
+            double best = I.Ct[(size_t)hs[bk] * n + i];
+            if (ties) {  // resolve in fp64, first minimum among the tied hubs
+                for (int k = bk + 1; k < p; ++k) {
+                    const int h = hs[k];
+                    if (I.Cq[(size_t)h * n + i] != qmin) continue;
+                    const double d = I.Ct[(size_t)h * n + i];
+                    if (d < best) {
+                        best = d;
+                        bk = k;
+                    }
+                }
             }
             double leg = best;
             if (self >= 0) {  // hubs serve themselves; C[h][h] == 0

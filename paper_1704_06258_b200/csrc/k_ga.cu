@@ -188,17 +188,31 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
         for (int k = threadIdx.x; k < h; k += kCorrThreads) carried[k] = 0.0;
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += kCorrThreads) {
-            int h0 = H[0];
-            double best = I.Ct[(size_t)h0 * n + i];
-            int bk = 0, self = (h0 == i) ? 0 : -1;
-            for (int k = 1; k < h; ++k) {
+            // first fp64 minimum over H via the exact 16-bit pre-filter (see k_allocate)
+            int bk = 0, self = -1, ties = 0;
+            unsigned qmin = 0xFFFFFFFFu;
+            for (int k = 0; k < h; ++k) {
                 const int hk = H[k];
-                const double d = I.Ct[(size_t)hk * n + i];
-                if (d < best) {
-                    best = d;
+                const unsigned q = I.Cq[(size_t)hk * n + i];
+                if (q < qmin) {
+                    qmin = q;
                     bk = k;
+                    ties = 0;
+                } else if (q == qmin) {
+                    ++ties;
                 }
                 if (hk == i) self = k;
+            }
+            if (ties) {
+                double best = I.Ct[(size_t)H[bk] * n + i];
+                for (int k = bk + 1; k < h; ++k) {
+                    if (I.Cq[(size_t)H[k] * n + i] != qmin) continue;
+                    const double d = I.Ct[(size_t)H[k] * n + i];
+                    if (d < best) {
+                        best = d;
+                        bk = k;
+                    }
+                }
             }
             if (self >= 0) bk = self;
             if (I.weights_exact)
