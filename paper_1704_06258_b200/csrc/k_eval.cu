@@ -169,8 +169,10 @@ __device__ __forceinline__ void write_T(const DevInst& I, const int32_t* hs, uin
 
 __global__ void __launch_bounds__(kAllocThreads)
 k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
-           uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs, int32_t* __restrict__ alloc) {
-    extern __shared__ int32_t hs[];  // p
+           uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
+           int32_t* __restrict__ alloc) {
+    constexpr int NPT = 8;  // nodes per thread per pass (i, i+256, ...)
+    __shared__ int32_t hs[kMaxP + 1];
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
     const int64_t b = blockIdx.x;
@@ -180,50 +182,71 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
     double so = 0.0, sd = 0.0;
     uint8_t* clb = cl + b * I.npad;
     uint16_t* cob = co + b * I.npad;
-    for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
-        int c = 0;
-        if (i < n) {
-            // exact argmin through the monotone 16-bit pre-filter: the fp64
-            // minimum is among the hubs tied at the minimal quantised value
-            int bk = 0, self = -1, ties = 0;
-            unsigned qmin = 0xFFFFFFFFu;
-#pragma unroll 4
-            for (int k = 0; k < p; ++k) {
-                const int h = hs[k];
-                const unsigned q = I.Cq[(size_t)h * n + i];
-                if (q < qmin) {
-                    qmin = q;
-                    bk = k;
-                    ties = 0;
-                } else if (q == qmin) {
-                    ++ties;
-                }
-                if (h == i) self = k;
-            }
-            double best = I.Ct[(size_t)hs[bk] * n + i];
-            if (ties) {  // resolve in fp64, first minimum among the tied hubs
-                for (int k = bk + 1; k < p; ++k) {
-                    const int h = hs[k];
-                    if (I.Cq[(size_t)h * n + i] != qmin) continue;
-                    const double d = I.Ct[(size_t)h * n + i];
-                    if (d < best) {
-                        best = d;
-                        bk = k;
+    for (int base = 0; base < I.npad; base += kAllocThreads * NPT) {
+        const int i0 = base + threadIdx.x;
+        unsigned qmin[NPT];
+        int bk[NPT], ties[NPT];
+#pragma unroll
+        for (int t = 0; t < NPT; ++t) {
+            qmin[t] = 0xFFFFFFFFu;
+            bk[t] = 0;
+            ties[t] = 0;
+        }
+        // exact argmin through the monotone 16-bit pre-filter: the fp64
+        // minimum is among the hubs tied at the minimal quantised value
+        for (int k = 0; k < p; ++k) {
+            const uint16_t* row = I.Cq + (size_t)hs[k] * n + i0;
+#pragma unroll
+            for (int t = 0; t < NPT; ++t) {
+                if (i0 + t * kAllocThreads < n) {
+                    const unsigned q = row[t * kAllocThreads];
+                    if (q < qmin[t]) {
+                        qmin[t] = q;
+                        bk[t] = k;
+                        ties[t] = 0;
+                    } else if (q == qmin[t]) {
+                        ties[t] = 1;
                     }
                 }
             }
-            double leg = best;
-            if (self >= 0) {  // hubs serve themselves; C[h][h] == 0
-                bk = self;
-                leg = 0.0;
-            }
-            so += I.O[i] * leg;
-            sd += I.D[i] * leg;
-            c = bk;
-            if (alloc) alloc[b * n + i] = hs[bk];
         }
-        clb[i] = (uint8_t)c;
-        cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
+#pragma unroll
+        for (int t = 0; t < NPT; ++t) {
+            const int i = i0 + t * kAllocThreads;
+            if (i >= I.npad) break;
+            int c = 0;
+            if (i < n) {
+                int kk = bk[t];
+                double best = I.Ct[(size_t)hs[kk] * n + i];
+                if (ties[t]) {  // resolve in fp64, first minimum among the tied hubs
+                    for (int k = kk + 1; k < p; ++k) {
+                        const int h = hs[k];
+                        if (I.Cq[(size_t)h * n + i] != qmin[t]) continue;
+                        const double d = I.Ct[(size_t)h * n + i];
+                        if (d < best) {
+                            best = d;
+                            kk = k;
+                        }
+                    }
+                }
+                // a hub's own row attains the minimum 0 (C[h][h] == 0), so its leg
+                // is 0 whichever hub the argmin picked; its cluster is fixed below
+                so += I.O[i] * best;
+                sd += I.D[i] * best;
+                c = kk;
+                if (alloc) alloc[b * n + i] = hs[kk];
+            }
+            clb[i] = (uint8_t)c;
+            cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
+        }
+    }
+    __syncthreads();
+    // hubs serve themselves (hm/model.py:206)
+    for (int k = threadIdx.x; k < p; k += kAllocThreads) {
+        const int h = hs[k];
+        clb[h] = (uint8_t)k;
+        cob[h] = (uint16_t)(k * 4);
+        if (alloc) alloc[b * n + h] = h;
     }
     write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
     block_sum2<kAllocThreads>(so, sd, scratch);
@@ -236,8 +259,7 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
 int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
                     uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s) {
     if (B <= 0) return HG_OK;
-    k_allocate<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, cl, co, T, legs,
-                                                                          alloc);
+    k_allocate<<<(unsigned)B, kAllocThreads, 0, s>>>(I, hubs, cl, co, T, legs, alloc);
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }
