@@ -335,7 +335,8 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
                 cmax = dist[x] > cmax ? dist[x] : cmax;
             }
             const double scale = cmax > cmin ? 65535.0 / (cmax - cmin) : 0.0;
-            chk(cudaMalloc(&inst->dCq, nn * sizeof(uint16_t)), "cudaMalloc(Cq)");
+            // padded by 8*256 entries: K2 reads 8 strided nodes per hub row unguarded
+            chk(cudaMalloc(&inst->dCq, (nn + 2048) * sizeof(uint16_t)), "cudaMalloc(Cq)");
             if (rc) break;
             rc = launch_quantize(inst->dCt, inst->dCq, (int64_t)nn, cmin, scale, s);
             if (rc) break;

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kAllocThreads)
 k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
            uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
            int32_t* __restrict__ alloc) {
-    constexpr int NPT = 8;  // nodes per thread per pass (i, i+256, ...)
+    constexpr int NPT = 4;  // nodes per thread per pass (i, i+256, ...)
     __shared__ int32_t hs[kMaxP + 1];
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
@@ -194,20 +194,19 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
         }
         // exact argmin through the monotone 16-bit pre-filter: the fp64
         // minimum is among the hubs tied at the minimal quantised value
+        // Cq rows are padded (allocation + npad) so the NPT loads of a hub row are
+        // issued unconditionally and batched; out-of-range nodes are masked
         for (int k = 0; k < p; ++k) {
             const uint16_t* row = I.Cq + (size_t)hs[k] * n + i0;
+            unsigned q[NPT];
+#pragma unroll
+            for (int t = 0; t < NPT; ++t) q[t] = row[t * kAllocThreads];
 #pragma unroll
             for (int t = 0; t < NPT; ++t) {
-                if (i0 + t * kAllocThreads < n) {
-                    const unsigned q = row[t * kAllocThreads];
-                    if (q < qmin[t]) {
-                        qmin[t] = q;
-                        bk[t] = k;
-                        ties[t] = 0;
-                    } else if (q == qmin[t]) {
-                        ties[t] = 1;
-                    }
-                }
+                const unsigned qt = (i0 + t * kAllocThreads < n) ? q[t] : 0xFFFFFFFEu;
+                ties[t] = (qt == qmin[t]) ? 1 : (qt < qmin[t] ? 0 : ties[t]);
+                bk[t] = qt < qmin[t] ? k : bk[t];
+                qmin[t] = qt < qmin[t] ? qt : qmin[t];
             }
         }
 #pragma unroll
