@@ -83,6 +83,7 @@ struct hg_inst {
     double* dwOD = nullptr;
     int32_t* drank = nullptr;
     uint16_t* dCq = nullptr;
+    int* derr = nullptr;  // input-validation flag (DevInst::err)
     hg_pop* scratch = nullptr;
     DevBuf t1, t2, t3, t4;
 };
@@ -193,6 +194,34 @@ int h2d_i64_as_i32(hg_inst* inst, DevBuf& tmp, const int64_t* host, int64_t coun
     HG_CUDA(cudaMemcpyAsync(tmp.ptr, host, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice,
                             inst->stream));
     return launch_i64_to_i32(tmp.as<int64_t>(), dst, count, inst->stream);
+}
+
+// host hub sets / allocations in, validated on the device (see k_hubs_in)
+int h2d_hubs_checked(hg_inst* inst, DevBuf& tmp, const int64_t* host, int64_t B, int32_t* dst) {
+    const int64_t count = B * inst->I.p;
+    HG_TRY(tmp.ensure((size_t)count * sizeof(int64_t)));
+    HG_CUDA(cudaMemcpyAsync(tmp.ptr, host, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            inst->stream));
+    return launch_hubs_in(tmp.as<int64_t>(), dst, B, inst->I.p, inst->I.n, inst->derr,
+                          inst->stream);
+}
+
+int h2d_alloc_checked(hg_inst* inst, DevBuf& tmp, const int64_t* host, int64_t B, int32_t* dst) {
+    const int64_t count = B * inst->I.n;
+    HG_TRY(tmp.ensure((size_t)count * sizeof(int64_t)));
+    HG_CUDA(cudaMemcpyAsync(tmp.ptr, host, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            inst->stream));
+    return launch_idx_in(tmp.as<int64_t>(), dst, count, inst->I.n, inst->derr, inst->stream);
+}
+
+// after the stream is synchronised: report (and clear) a validation failure
+int check_input_flag(hg_inst* inst, int host_flag, const char* what) {
+    if (host_flag == 0) return HG_OK;
+    HG_CUDA(cudaMemsetAsync(inst->derr, 0, sizeof(int), inst->stream));
+    HG_CUDA(cudaStreamSynchronize(inst->stream));
+    set_error("%s %lld: indices must be sorted ascending, distinct and in [0, %d)", what,
+              (long long)(0x7ffffffe - host_flag), inst->I.n);
+    return HG_EARG;
 }
 
 int d2h_i32_as_i64(hg_inst* inst, DevBuf& tmp, const int32_t* dsrc, int64_t count, int64_t* host) {
@@ -360,6 +389,9 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.wOD = inst->dwOD;
         I.rank = inst->drank;
         I.Cq = inst->dCq;
+        chk(cudaMalloc(&inst->derr, sizeof(int)), "cudaMalloc(err)");
+        chk(cudaMemsetAsync(inst->derr, 0, sizeof(int), s), "memset(err)");
+        I.err = inst->derr;
         I.npad = 16;  // provisional for the plan
         inst->plan = fitness_plan(I, inst->sm_count);
         int64_t q = inst->plan.tr > inst->plan.tc ? inst->plan.tr : inst->plan.tc;
@@ -412,6 +444,7 @@ static void inst_destroy(hg_inst* inst) {
     cudaFree(inst->dwOD);
     cudaFree(inst->drank);
     cudaFree(inst->dCq);
+    cudaFree(inst->derr);
     cudaFree(inst->dW8);
     inst->t1.release();
     inst->t2.release();
@@ -475,13 +508,15 @@ int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc) {
     hg_pop* P;
     HG_TRY(scratch_pop(inst, B, &P));
     const DevInst& I = inst->I;
-    HG_TRY(h2d_i64_as_i32(inst, inst->t1, hubs, B * I.p, P->hubs));
+    HG_TRY(h2d_hubs_checked(inst, inst->t1, hubs, B, P->hubs));
     HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
     HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, P->legs, P->alloc.as<int32_t>(),
                            inst->stream));
     HG_TRY(d2h_i32_as_i64(inst, inst->t2, P->alloc.as<int32_t>(), B * I.n, alloc));
+    int flag = 0;
+    HG_CUDA(cudaMemcpyAsync(&flag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost, inst->stream));
     HG_CUDA(cudaStreamSynchronize(inst->stream));
-    return HG_OK;
+    return check_input_flag(inst, flag, "hub set");
 }
 
 int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* alloc,
@@ -494,18 +529,20 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
     hg_pop* P;
     HG_TRY(scratch_pop(inst, B, &P));
     const DevInst& I = inst->I;
-    HG_TRY(h2d_i64_as_i32(inst, inst->t1, hubs, B * I.p, P->hubs));
+    HG_TRY(h2d_hubs_checked(inst, inst->t1, hubs, B, P->hubs));
     const int32_t* a32 = nullptr;
     if (alloc) {
         HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
-        HG_TRY(h2d_i64_as_i32(inst, inst->t2, alloc, B * I.n, P->alloc.as<int32_t>()));
+        HG_TRY(h2d_alloc_checked(inst, inst->t2, alloc, B, P->alloc.as<int32_t>()));
         a32 = P->alloc.as<int32_t>();
     }
     HG_TRY(pop_eval_queue(P, B, a32));
     HG_CUDA(cudaMemcpyAsync(out, P->out, (size_t)B * 4 * sizeof(double), cudaMemcpyDeviceToHost,
                             inst->stream));
+    int flag = 0;
+    HG_CUDA(cudaMemcpyAsync(&flag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost, inst->stream));
     HG_CUDA(cudaStreamSynchronize(inst->stream));
-    return HG_OK;
+    return check_input_flag(inst, flag, alloc ? "solution" : "hub set");
 }
 
 int hg_pop_create(hg_inst* inst, int64_t capacity, hg_pop** out) {

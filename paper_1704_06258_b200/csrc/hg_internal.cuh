@@ -73,6 +73,8 @@ struct DevInst {
     // Ct quantised monotonically to 16 bits: Cq = min(65535, floor((Ct - cmin) * s)).
     // q(a) < q(b) implies a < b, so it filters the allocation argmin exactly.
     const uint16_t* Cq;
+    // input-validation flag of the current host call (0 = ok, else 0x7ffffffe - bad row)
+    const int* err;
 };
 
 // fitness tiling chosen per instance (see fitness_plan)
@@ -91,6 +93,10 @@ int prepare_fitness(const FitPlan& P);
 
 // ---- launchers (k_eval.cu) -------------------------------------------------
 int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStream_t s);
+int launch_hubs_in(const int64_t* src, int32_t* dst, int64_t B, int p, int n, int* err,
+                   cudaStream_t s);
+int launch_idx_in(const int64_t* src, int32_t* dst, int64_t count, int n, int* err,
+                  cudaStream_t s);
 int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s);
 int launch_transpose(const double* src, double* dst, int n, cudaStream_t s);
 int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s);

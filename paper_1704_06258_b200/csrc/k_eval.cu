@@ -39,6 +39,51 @@ static int grid_for(int64_t m, int block) {
     return (int)g;
 }
 
+// hub sets in (int64, B x p) -> int32, validated: each row strictly increasing
+// within [0, n).  *err (0 = ok) records the FIRST bad row as 0x7ffffffe - row
+// via atomicMax; K2 then treats the whole batch as hubs 0..p-1 (stays in bounds)
+__global__ void k_hubs_in(const int64_t* __restrict__ s, int32_t* __restrict__ d, int64_t B,
+                          int p, int n, int* err) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < B * p;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = x / p;
+        const int k = (int)(x - b * p);
+        const int64_t v = s[x];
+        bool ok = v >= 0 && v < n;
+        if (k > 0) ok = ok && s[x - 1] < v;
+        if (!ok) atomicMax(err, (int)(0x7ffffffe - (b < 0x7ffffffe ? b : 0x7ffffffd)));
+        d[x] = (int32_t)v;
+    }
+}
+
+// indices in [0, n) (allocations); a bad entry records its row like k_hubs_in
+__global__ void k_idx_in(const int64_t* __restrict__ s, int32_t* __restrict__ d, int64_t count,
+                         int n, int* err) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = s[x];
+        const bool ok = v >= 0 && v < n;
+        if (!ok) atomicMax(err, (int)(0x7ffffffe - (x / n < 0x7ffffffe ? x / n : 0x7ffffffd)));
+        d[x] = ok ? (int32_t)v : 0;
+    }
+}
+
+int launch_hubs_in(const int64_t* src, int32_t* dst, int64_t B, int p, int n, int* err,
+                   cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    k_hubs_in<<<grid_for(B * p, 256), 256, 0, s>>>(src, dst, B, p, n, err);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+int launch_idx_in(const int64_t* src, int32_t* dst, int64_t count, int n, int* err,
+                  cudaStream_t s) {
+    if (count <= 0) return HG_OK;
+    k_idx_in<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count, n, err);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
 int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStream_t s) {
     if (count <= 0) return HG_OK;
     k_i64_to_i32<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count);
@@ -176,7 +221,8 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
     const int64_t b = blockIdx.x;
-    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = hubs[b * p + k];
+    const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
+    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = bad ? k : hubs[b * p + k];
     __syncthreads();
 
     double so = 0.0, sd = 0.0;
@@ -273,7 +319,8 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
     __shared__ double scratch[2 * (kAllocThreads / 32)];
     const int n = I.n, p = I.p;
     const int64_t b = blockIdx.x;
-    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = hubs[b * p + k];
+    const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
+    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = bad ? k : hubs[b * p + k];
     __syncthreads();
     double so = 0.0, sd = 0.0;
     uint8_t* clb = cl + b * I.npad;
@@ -281,7 +328,7 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
     for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
         int c = 0;
         if (i < n) {
-            int a = alloc[b * n + i];
+            int a = bad ? 0 : alloc[b * n + i];
             int lo = 0, hi = p - 1;  // hubs sorted; a is one of them (validated by caller)
             while (lo < hi) {
                 int mid = (lo + hi) >> 1;

@@ -103,6 +103,22 @@ class TestObjective:
         assert hg.fitness(inst, sol, hg.FitnessMode.STANDARD_MILLI) == raw * 1e-3
         assert hg.fitness(inst, sol, hg.FitnessMode.CAB_NORMALIZED) == raw / inst.total_flow
 
+    def test_device_side_input_validation(self):
+        inst = hg.generate_urand(300, 7, 9, (1.0, 0.75, 1.0))
+        pop = hg.random_population(300, 7, 50)
+        good = hg.evaluate_population(inst, pop)
+        for bad_row, mutate in ((17, lambda h: h.__setitem__(2, h[1])),      # repeat
+                                (3, lambda h: h.__setitem__(0, -1)),         # negative
+                                (40, lambda h: h.__setitem__(6, 300))):      # >= n
+            bad = pop.copy()
+            mutate(bad[bad_row])
+            with pytest.raises(ValueError, match=f"hub set {bad_row}:"):
+                hg.evaluate_population(inst, bad)
+            # the instance is usable afterwards and results are unchanged
+            assert np.array_equal(hg.evaluate_population(inst, pop), good)
+        with pytest.raises(ValueError, match="hub set 0:"):
+            hg.nearest_allocations(inst, pop[:1, ::-1])
+
     def test_batch_invariance_bitwise(self, kernel):
         """A hub set's score does not depend on its batch or position."""
         inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
