@@ -172,6 +172,64 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# GA time-to-best-cost vs the CPU reference (BASELINE.json metric, 2nd half)
+# ---------------------------------------------------------------------------
+
+
+def ga_time_to_target(hg, inst, args):
+    """The reference's GA (oracle port, one core: the reference `solve` is
+    GIL-bound, hm/engine.py:175-177) runs a bounded UR budget; its final best
+    cost is the target.  The GPU `solve` with the same GaParams replays the same
+    trajectory (same draws, hm/rng.py), so its wall time is the time to reach the
+    CPU's best cost.  A larger GPU budget run for at most the CPU's wall time
+    shows the best cost the GPU reaches in the same time."""
+    from oracle import hm_oracle as orc
+
+    kw = dict(islands=8, pop_size=16, inner_iters=args.ga_inner, outer_iters=1, seed=0)
+    params = hg.GaParams(**kw)
+    mode = hg.FitnessMode.STANDARD_MILLI
+    hg.solve(inst, hg.GaParams(islands=2, pop_size=4, inner_iters=1, outer_iters=1), mode)  # warm
+    t0 = time.perf_counter()
+    rep = hg.solve(inst, params, mode)
+    t_gpu = time.perf_counter() - t0
+
+    pr = orc.Problem(N, P, inst.dist, inst.flow, *FACTORS)
+    t0 = time.perf_counter()
+    ref = orc.island_ga(pr, kw["islands"], kw["pop_size"], kw["inner_iters"], 1, 0, None, False,
+                        "milli")
+    t_cpu = time.perf_counter() - t0
+    evals = kw["islands"] * kw["pop_size"] * kw["inner_iters"]
+
+    # same wall-clock budget, GPU-sized search: 128 islands x 64, rounds of 25
+    # generations until the CPU's time is used up
+    big = hg.GaParams(islands=128, pop_size=64, inner_iters=25, outer_iters=1, seed=1)
+    best, rounds, t0 = None, 0, time.perf_counter()
+    anc = None
+    while time.perf_counter() - t0 < t_cpu and rounds < 400:
+        r = hg.solve(inst, hg.GaParams(islands=128, pop_size=64, inner_iters=25, outer_iters=1,
+                                       seed=1 + rounds), mode)
+        rounds += 1
+        if best is None or r.raw_objective < best:
+            best = r.raw_objective
+    t_big = time.perf_counter() - t0
+    del anc, big
+    return {
+        "config": f"UR n={N} p={P}, GaParams(islands=8, pop_size=16, inner_iters="
+                  f"{kw['inner_iters']}, outer_iters=1, seed=0), milli",
+        "cpu_ref_seconds": t_cpu, "cpu_ref_best_raw": ref.raw, "cpu_ref_evals": evals,
+        "cpu_ref_kind": "port (oracle/hm_oracle.py island_ga, 1 core)",
+        "gpu_seconds_to_target": t_gpu, "gpu_best_raw": rep.raw_objective,
+        "gpu_replays_cpu": bool(abs(rep.raw_objective - ref.raw) <= 1e-12 * ref.raw
+                                and np.array_equal(rep.best_solution.hubs, ref.hubs)),
+        "speedup_time_to_target": t_cpu / t_gpu,
+        "gpu_same_wallclock": {"seconds": t_big, "solves": rounds,
+                               "evals": rounds * 128 * 64 * 25, "best_raw": best,
+                               "better_than_cpu": bool(best is not None and best < ref.raw),
+                               "config": "independent solves, 128 islands x 64, 25 gens"},
+    }
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 
@@ -288,6 +346,10 @@ def run_gpu(args):
         barrier()
         ga_ms = g0.elapsed_time(g1) / args.steps
 
+    ga_ttt = None
+    if rank == 0 and not args.no_cpu:
+        ga_ttt = ga_time_to_target(hg, inst, args)
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         cb = CpuBaseline()
@@ -337,6 +399,8 @@ def run_gpu(args):
                    "launches_per_generation": ga.launches_per_generation},
             "wall_s_timed_region": t_wall,
         }
+        if ga_ttt:
+            line["ga_time_to_target"] = ga_ttt
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -391,6 +455,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ga-inner", type=int, default=12,
+                    help="generations of the CPU-reference GA run (about 1 s each)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
