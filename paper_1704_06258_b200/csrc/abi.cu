@@ -67,6 +67,7 @@ struct hg_inst {
     alignas(64) unsigned char wmap[128];  // CUtensorMap of W8 (K3-TC)
     uint8_t* dW8 = nullptr;                // u8 copy of W, [npad_tc][npad_tc], when exact
     bool tc_ok = false;                    // flows are integers in [0, 255] and p fits
+    bool tcy_ok = false;                   // ... and n <= 1024: one-hot resident in TMEM
     int fit_kind = HG_FIT_AUTO;
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -161,7 +162,10 @@ int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* c
     const bool tc = inst->fit_kind == HG_FIT_TENSOR ||
                     (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok);
     int tiles;
-    if (tc) {
+    if (tc && inst->tcy_ok) {
+        HG_TRY(launch_fitness_tcy(I, inst->wmap, B, cl, T, part, inst->sm_count, s));
+        tiles = 1;
+    } else if (tc) {
         HG_TRY(launch_fitness_tc(I, inst->wmap, B, cl, T, part, inst->sm_count, s));
         tiles = tc_tiles(I.n);
     } else {
@@ -418,6 +422,12 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             rc = prepare_fitness_tc(p);
             if (rc) break;
             inst->tc_ok = true;
+            const char* var = getenv("HUBGPU_TC_VARIANT");  // tuning override: "x" | "y"
+            if (tcy_supported(n, p, I.npad) && !(var && var[0] == 'x')) {
+                rc = prepare_fitness_tcy(p, I.npad);
+                if (rc) break;
+                inst->tcy_ok = true;
+            }
         }
         chk(cudaStreamSynchronize(s), "sync");
     } while (0);

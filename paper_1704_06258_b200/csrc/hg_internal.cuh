@@ -120,6 +120,12 @@ int tc_timing_read(unsigned long long* out32);
 int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out);  // map_out: CUtensorMap (128 B)
 int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
                       const uint32_t* T, double* part, int grid, cudaStream_t s);
+// K3-TC/Y (k_fitness_tcy.cu): one-hot resident in TMEM, n <= 1024
+bool tcy_supported(int n, int p, int npad);
+size_t tcy_smem_bytes(int p, int npad);
+int prepare_fitness_tcy(int p, int npad);
+int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
+                       const uint32_t* T, double* part, int grid, cudaStream_t s);
 
 // ---- launchers (k_ga.cu) ---------------------------------------------------
 int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n, int nw,

@@ -322,37 +322,30 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
             if (kb + 1 < A.KB) fetch_cids(U, kb + 1, cbuf + (s ^ 1) * cstride);
             __pipeline_commit();
             // one-hot B tile, row r = (individual bl, hub l), 128 K bytes, SW128
-            // swizzled.  Column j of individual bl has exactly one 0x80, in row
-            // bl*p + c_bl(j): update the stage by diffing against the cluster ids
-            // it currently holds (sc) -- clear the old byte, set the new one.
+            // swizzled: thread (r, half) builds 64 bytes of row r by byte-wise
+            // compares of the staged cluster ids with l -- branch-free, 4
+            // independent 16-byte chunks per thread (latency hidden by ILP)
             {
                 const uint8_t* cb = cbuf + s * cstride;
-                uint8_t* scs = sc + s * cstride;
-                for (int it = tid; it < ipt * 32; it += kTcThreads) {
-                    const int bl = it >> 5, w = it & 31;
-                    const uint32_t nw = bl < nind
-                                            ? *reinterpret_cast<const uint32_t*>(cb + bl * 128 + 4 * w)
-                                            : 0xFFFFFFFFu;
-                    uint32_t* op = reinterpret_cast<uint32_t*>(scs + bl * 128 + 4 * w);
-                    const uint32_t ow = *op;
-                    if (ow != nw) {
-                        const int cch = w >> 2;  // 16-byte chunk of the row
+                for (int it = tid; it < A.N * 2; it += kTcThreads) {
+                    const int r = it >> 1, h2 = it & 1;
+                    const int bl = r / p, l = r - bl * p;
+                    const bool live = bl < nind;
+                    const uint32_t lrep = (uint32_t)l * 0x01010101u;
+                    const uint4* src = reinterpret_cast<const uint4*>(cb + bl * 128 + h2 * 64);
+                    unsigned char* dst = b_st + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const uint32_t o = (ow >> (8 * k)) & 0xFFu, v = (nw >> (8 * k)) & 0xFFu;
-                            if (o == v) continue;
-                            const int jb = (4 * w + k) & 15;
-                            if (o != 0xFFu) {
-                                const int r = bl * p + (int)o;
-                                b_st[(r >> 3) * 1024 + (r & 7) * 128 + ((cch ^ (r & 7)) << 4) + jb] = 0;
-                            }
-                            if (v != 0xFFu) {
-                                const int r = bl * p + (int)v;
-                                b_st[(r >> 3) * 1024 + (r & 7) * 128 + ((cch ^ (r & 7)) << 4) + jb] =
-                                    0x80;
-                            }
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = h2 * 4 + q;
+                        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                        if (live) {
+                            const uint4 x = src[q];
+                            v.x = onehot4(x.x, lrep);
+                            v.y = onehot4(x.y, lrep);
+                            v.z = onehot4(x.z, lrep);
+                            v.w = onehot4(x.w, lrep);
                         }
-                        *op = nw;
+                        *reinterpret_cast<uint4*>(dst + ((c ^ (r & 7)) << 4)) = v;
                     }
                 }
             }

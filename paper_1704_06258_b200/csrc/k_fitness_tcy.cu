@@ -1,0 +1,410 @@
+// K3-TC/Y: population fitness (transfer term) on tcgen05 with the one-hot
+// operand RESIDENT IN TENSOR MEMORY (n <= 1024).
+//
+// Same exact factorisation as k_fitness_tc.cu (hm/evaluation.py:113-119):
+//   D[(b,l)][i] = sum_j OneHot[(b,l)][j] * W[i][j]  = 128 * G_b[i][l]   (u8 x u8 -> s32)
+//   S_T(b)      = sum_i sum_l G_b[i][l] * T_b[c_b(i)][l]
+// but with the roles swapped: the one-hot rows (individual b, hub l) are the
+// A operand -- M = 128 TMEM lanes, all K = n columns of it generated ONCE per
+// unit straight into TMEM with tcgen05.st -- and W is the B operand, streamed
+// by TMA through a 6-deep shared-memory ring.  Shared memory then carries only
+// W (TMA write + MMA read), a third of the traffic of the smem-resident one-hot
+// design.  TMEM: A in columns [0, 256), two N=128 accumulators in [256, 512):
+// the epilogue of one 128-row W tile overlaps the MMAs of the next.
+//
+// Warp roles (20 warps): warp 0 = MMA issuer, warp 1 = TMA producer, warps
+// 4..19 = generators + epilogue (warp w reads TMEM lane quadrant w % 4, and
+// the 4 warps of a quadrant split the 128 accumulator columns).
+
+#include <cuda.h>
+#include <cuda_pipeline.h>
+
+#include "hg_internal.cuh"
+
+namespace hg {
+
+namespace {
+
+constexpr int kYThreads = 640;
+constexpr int kYWarps = kYThreads / 32;
+constexpr int kYEpiWarp0 = 4;                 // first epilogue warp
+constexpr int kYEpiThreads = kYThreads - 128; // 512
+constexpr int kYStages = 6;                   // W ring depth
+constexpr int kYStageBytes = 128 * 128;       // 128 W rows x 128 K (u8)
+constexpr int kYMaxIpt = 32;
+constexpr int kYTmemCols = 512;
+constexpr int kYAcc0 = 256;                   // first accumulator column
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAITY_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAITY_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                      uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T, kind::i8
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+        : "memory");
+}
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void epi_sync() {  // named barrier over the 16 epilogue warps
+    asm volatile("bar.sync 1, %0;" ::"n"(kYEpiThreads) : "memory");
+}
+// byte-wise (x == l) -> 0x80 / 0x00 (see k_fitness_tc.cu)
+__device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
+    const uint32_t y = x ^ lrep;
+    const uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+    return ~(t | y) & 0x80808080u;
+}
+
+}  // namespace
+
+struct YArgs {
+    const uint8_t* cl;
+    const uint32_t* T;
+    double* part;     // [B][1]: S_T complete per individual
+    int64_t B;
+    int n, p, ps, npad;
+    int ipt;          // individuals per unit (ipt * p <= 128)
+    int64_t units;
+    int IT;           // 128-row W tiles (= K blocks)
+    int acols;        // TMEM columns of A = IT * 32
+    int pss;          // staged T row stride (doubles)
+    uint32_t idesc;   // kind::i8, M=128, N=128, K-major both
+};
+
+__host__ __device__ inline size_t y_T_bytes(int ipt, int p, int pss) {
+    return ((size_t)ipt * p * pss * 8 + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t y_C_bytes(int ipt, int npad) {
+    return ((size_t)ipt * npad + 15) & ~size_t(15);
+}
+
+__global__ void __launch_bounds__(kYThreads, 1)
+k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    const int p = A.p, ipt = A.ipt, IT = A.IT;
+    unsigned char* ring = smem;                                          // W stages
+    unsigned char* var = smem + kYStages * kYStageBytes;
+    const size_t tb = y_T_bytes(ipt, p, A.pss), cb = y_C_bytes(ipt, A.npad);
+    double* sT[2] = {reinterpret_cast<double*>(var), reinterpret_cast<double*>(var + tb)};
+    var += 2 * tb;
+    uint8_t* sC[2] = {var, var + cb};
+    var += 2 * cb;
+    double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
+    var += 4 * 128 * 8;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(var);
+    // bars: full[6] empty[6] accfull[2] accempty[2] aready[1]
+    const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kYStages,
+                   b_accf = b_empty + 8 * kYStages, b_acce = b_accf + 16, b_ard = b_acce + 16;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kYStages + 5);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < kYStages; ++s) {
+            mb_init(b_full + 8 * s, 1);
+            mb_init(b_empty + 8 * s, 1);
+        }
+        for (int d = 0; d < 2; ++d) {
+            mb_init(b_accf + 8 * d, 1);
+            mb_init(b_acce + 8 * d, kYWarps - kYEpiWarp0);
+        }
+        mb_init(b_ard, kYWarps - kYEpiWarp0);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(tmem_slot)),
+                     "r"(kYTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t u0 = A.units * blockIdx.x / gridDim.x;
+    const int64_t u1 = A.units * (blockIdx.x + 1) / gridDim.x;
+
+    if (warp == 1) {
+        // ---------------- TMA producer: W tiles (it, kb), same order every unit
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (int64_t u = u0; u < u1; ++u)
+                for (int it = 0; it < IT; ++it)
+                    for (int kb = 0; kb < IT; ++kb, ++g) {
+                        const int s = g % kYStages;
+                        if (g >= kYStages) mb_wait(b_empty + 8 * s, ((g / kYStages) - 1) & 1);
+                        mb_expect_tx(b_full + 8 * s, kYStageBytes);
+                        tma2d(su32(ring + s * kYStageBytes), &tmW, kb * 128, it * 128,
+                              b_full + 8 * s);
+                    }
+        }
+    } else if (warp == 0) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            uint32_t g = 0, t = 0;
+            for (int64_t u = u0; u < u1; ++u) {
+                mb_wait(b_ard, (uint32_t)((u - u0) & 1));  // A of this unit is in TMEM
+                fence_after();
+                for (int it = 0; it < IT; ++it, ++t) {
+                    const int d = t & 1;
+                    if (t >= 2) mb_wait(b_acce + 8 * d, ((t >> 1) - 1) & 1);
+                    fence_after();
+                    const uint32_t dcol = tmem + kYAcc0 + d * 128;
+                    for (int kb = 0; kb < IT; ++kb, ++g) {
+                        const int s = g % kYStages;
+                        mb_wait(b_full + 8 * s, (g / kYStages) & 1);
+                        fence_after();
+                        const uint64_t bd = sw128(su32(ring + s * kYStageBytes));
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns of A
+                            mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
+                                   (kb | ks) != 0);
+                        commit(b_empty + 8 * s);
+                    }
+                    commit(b_accf + 8 * d);
+                }
+            }
+        }
+    } else if (warp >= kYEpiWarp0) {
+        // ---------------- generators + epilogue (16 warps)
+        const int et = tid - kYEpiWarp0 * 32;           // 0..511
+        const int q = warp & 3;                         // TMEM lane quadrant
+        const int sub = (warp - kYEpiWarp0) >> 2;       // 0..3: column quarter
+        const int r = q * 32 + lane;                    // A row / accumulator lane
+        const int bl = r / p, l = r - bl * p;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        uint32_t t = 0;
+        for (int64_t u = u0; u < u1; ++u) {
+            const int buf = (int)((u - u0) & 1);
+            const int64_t bbase = u * ipt;
+            const int nind = (int)(A.B - bbase < ipt ? A.B - bbase : ipt);
+            double* Ts = sT[buf];
+            uint8_t* Cs = sC[buf];
+            // stage this unit's T tables (x 2^-7, zero tails) and cluster rows
+            {
+                const int pss = A.pss, per = p * pss;
+                for (int x = et; x < ipt * per; x += kYEpiThreads) {
+                    const int b2 = x / per, y = x - b2 * per;
+                    const int c = y / pss, ll = y - c * pss;
+                    double v = 0.0;
+                    if (b2 < nind && ll < p) {
+                        const uint32_t* tbp = A.T + (bbase + b2) * 2 * p * (int64_t)A.ps;
+                        v = __hiloint2double((int)tbp[c * A.ps + ll], (int)tbp[(p + c) * A.ps + ll]) *
+                            0.0078125;
+                    }
+                    Ts[(b2 * p + c) * pss + ll] = v;
+                }
+                const int chunks = A.npad / 16;
+                for (int x = et; x < ipt * chunks; x += kYEpiThreads) {
+                    const int b2 = x / chunks, k = x - b2 * chunks;
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if (b2 < nind)
+                        v = __ldg(reinterpret_cast<const uint4*>(A.cl + (bbase + b2) * A.npad) + k);
+                    reinterpret_cast<uint4*>(Cs + (size_t)b2 * A.npad)[k] = v;
+                }
+            }
+            epi_sync();
+            // the previous unit's MMAs (which read A) are complete: its last
+            // accumulator was consumed below before we got here
+            // generate A: row r = (bl, l), K = nodes; this warp writes columns
+            // [sub * acols/4, (sub+1) * acols/4) of its quadrant's lanes
+            {
+                const bool live = r < ipt * p && bl < nind;
+                const uint32_t lrep = (uint32_t)l * 0x01010101u;
+                const int cq = A.acols / 4;
+                const uint4* crow = reinterpret_cast<const uint4*>(Cs + (size_t)(live ? bl : 0) * A.npad);
+                for (int c0 = sub * cq; c0 < (sub + 1) * cq; c0 += 8) {
+                    uint32_t v[8];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint4 x = crow[(c0 >> 2) + h];  // 16 cluster ids = 4 columns
+                        v[4 * h + 0] = live ? oh4(x.x, lrep) : 0u;
+                        v[4 * h + 1] = live ? oh4(x.y, lrep) : 0u;
+                        v[4 * h + 2] = live ? oh4(x.z, lrep) : 0u;
+                        v[4 * h + 3] = live ? oh4(x.w, lrep) : 0u;
+                    }
+                    st8(tmem + lane_base + (uint32_t)c0, v);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mb_arrive(b_ard);
+            }
+            // epilogue over the 128-row W tiles
+            double acc0 = 0.0, acc1 = 0.0;
+            const double* trow = Ts + (size_t)(r < ipt * p ? bl * p : 0) * A.pss + l;
+            const uint8_t* crow = Cs + (size_t)(bl < ipt ? bl : 0) * A.npad;
+            for (int it = 0; it < IT; ++it, ++t) {
+                const int d = t & 1;
+                mb_wait(b_accf + 8 * d, (t >> 1) & 1);
+                fence_after();
+                const uint32_t dcol = tmem + lane_base + kYAcc0 + d * 128 + sub * 32;
+                uint32_t v0[16], v1[16];
+                ld16(dcol, v0);
+                ld16(dcol + 16, v1);
+                // cluster ids of the 32 columns i = it*128 + sub*32 + k
+                const uint4 ca = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32)[0];
+                const uint4 cc = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32)[1];
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mb_arrive(b_acce + 8 * d);  // accumulator may be overwritten
+                const uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const uint32_t c = (cw[k >> 2] >> ((k & 3) * 8)) & 0xffu;
+                    const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
+                    const double dd = __hiloint2double(0x43300000, (int)dv) - 4503599627370496.0;
+                    const double tv = trow[c * A.pss];
+                    if (k & 1) acc1 = fma(dd, tv, acc1);
+                    else acc0 = fma(dd, tv, acc0);
+                }
+            }
+            // per-individual sum over its p rows and the 4 column quarters (fixed order)
+            red[sub * 128 + r] = acc0 + acc1;
+            epi_sync();
+            for (int b2 = et; b2 < nind; b2 += kYEpiThreads) {
+                double s = 0.0;
+                for (int sq = 0; sq < 4; ++sq)
+                    for (int ll = 0; ll < p; ++ll) s += red[sq * 128 + b2 * p + ll];
+                A.part[bbase + b2] = s;
+            }
+            epi_sync();
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(kYTmemCols)
+                     : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static int y_pss(int p) { return ((p + 7) & ~7) + 2; }
+
+static int y_ipt(int p) {
+    int ipt = 128 / p;
+    return ipt > kYMaxIpt ? kYMaxIpt : ipt;
+}
+
+size_t tcy_smem_bytes(int p, int npad) {
+    const int ipt = y_ipt(p);
+    size_t b = 1024 + (size_t)kYStages * kYStageBytes;
+    b += 2 * y_T_bytes(ipt, p, y_pss(p)) + 2 * y_C_bytes(ipt, npad);
+    b += 4 * 128 * 8 + (2 * kYStages + 5) * 8 + 16;
+    return b;
+}
+
+bool tcy_supported(int n, int p, int npad) {
+    return p >= 1 && p <= 128 && round_up(n, 128) <= 1024 && npad <= 1024 &&
+           tcy_smem_bytes(p, npad) <= 227 * 1024;
+}
+
+int prepare_fitness_tcy(int p, int npad) {
+    HG_CUDA(cudaFuncSetAttribute(k_fitness_tcy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tcy_smem_bytes(p, npad)));
+    return HG_OK;
+}
+
+int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
+                       const uint32_t* T, double* part, int grid, cudaStream_t s) {
+    if (B <= 0) return HG_OK;
+    YArgs A;
+    A.cl = cl;
+    A.T = T;
+    A.part = part;
+    A.B = B;
+    A.n = I.n;
+    A.p = I.p;
+    A.ps = I.ps;
+    A.npad = I.npad;
+    A.ipt = y_ipt(I.p);
+    A.units = ceil_div(B, A.ipt);
+    A.IT = (int)(round_up(I.n, 128) / 128);
+    A.acols = A.IT * 32;
+    A.pss = y_pss(I.p);
+    A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    int g = grid;
+    if (g > A.units) g = (int)A.units;
+    CUtensorMap map = *static_cast<const CUtensorMap*>(wmap);
+    k_fitness_tcy<<<g, kYThreads, tcy_smem_bytes(I.p, I.npad), s>>>(map, A);
+    HG_CUDA(cudaGetLastError());
+    return HG_OK;
+}
+
+}  // namespace hg
