@@ -143,6 +143,9 @@ __host__ __device__ inline size_t y_T_bytes(int ipt, int p, int pss) {
 __host__ __device__ inline size_t y_C_bytes(int ipt, int npad) {
     return ((size_t)ipt * npad + 15) & ~size_t(15);
 }
+__host__ __device__ inline size_t y_O_bytes(int ipt, int npad) {  // u16 T-row offsets
+    return ((size_t)ipt * npad * 2 + 15) & ~size_t(15);
+}
 
 __global__ void __launch_bounds__(kYThreads, 1)
 k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
@@ -156,6 +159,9 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
     var += 2 * tb;
     uint8_t* sC[2] = {var, var + cb};
     var += 2 * cb;
+    const size_t ob = y_O_bytes(ipt, A.npad);
+    uint16_t* sO[2] = {reinterpret_cast<uint16_t*>(var), reinterpret_cast<uint16_t*>(var + ob)};
+    var += 2 * ob;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
@@ -249,6 +255,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             const int nind = (int)(A.B - bbase < ipt ? A.B - bbase : ipt);
             double* Ts = sT[buf];
             uint8_t* Cs = sC[buf];
+            uint16_t* Os = sO[buf];
             // stage this unit's T tables (x 2^-7, zero tails) and cluster rows
             {
                 const int pss = A.pss, per = p * pss;
@@ -270,6 +277,18 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                     if (b2 < nind)
                         v = __ldg(reinterpret_cast<const uint4*>(A.cl + (bbase + b2) * A.npad) + k);
                     reinterpret_cast<uint4*>(Cs + (size_t)b2 * A.npad)[k] = v;
+                    // T-row offsets (in doubles) of these 16 columns for the epilogue
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                    uint32_t o[8];
+#pragma unroll
+                    for (int h = 0; h < 8; ++h) {
+                        const uint32_t c0 = (w[h >> 1] >> ((h & 1) * 16)) & 0xffu;
+                        const uint32_t c1 = (w[h >> 1] >> ((h & 1) * 16 + 8)) & 0xffu;
+                        o[h] = (c0 * A.pss) | ((c1 * A.pss) << 16);
+                    }
+                    uint4* od = reinterpret_cast<uint4*>(Os + (size_t)b2 * A.npad + k * 16);
+                    od[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                    od[1] = make_uint4(o[4], o[5], o[6], o[7]);
                 }
             }
             epi_sync();
@@ -300,9 +319,9 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 if (lane == 0) mb_arrive(b_ard);
             }
             // epilogue over the 128-row W tiles
-            double acc0 = 0.0, acc1 = 0.0;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
             const double* trow = Ts + (size_t)(r < ipt * p ? bl * p : 0) * A.pss + l;
-            const uint8_t* crow = Cs + (size_t)(bl < ipt ? bl : 0) * A.npad;
+            const uint16_t* orow = Os + (size_t)(bl < ipt ? bl : 0) * A.npad;
             for (int it = 0; it < IT; ++it, ++t) {
                 const int d = t & 1;
                 mb_wait(b_accf + 8 * d, (t >> 1) & 1);
@@ -311,24 +330,24 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 uint32_t v0[16], v1[16];
                 ld16(dcol, v0);
                 ld16(dcol + 16, v1);
-                // cluster ids of the 32 columns i = it*128 + sub*32 + k
-                const uint4 ca = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32)[0];
-                const uint4 cc = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32)[1];
+                // T-row offsets of the 32 columns i = it*128 + sub*32 + k
+                const uint4* op = reinterpret_cast<const uint4*>(orow + it * 128 + sub * 32);
+                const uint4 o0 = op[0], o1 = op[1], o2 = op[2], o3 = op[3];
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mb_arrive(b_acce + 8 * d);  // accumulator may be overwritten
-                const uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cc.x, cc.y, cc.z, cc.w};
+                const uint32_t ow[16] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w,
+                                         o2.x, o2.y, o2.z, o2.w, o3.x, o3.y, o3.z, o3.w};
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    const uint32_t c = (cw[k >> 2] >> ((k & 3) * 8)) & 0xffu;
+                    const uint32_t off = (k & 1) ? (ow[k >> 1] >> 16) : (ow[k >> 1] & 0xffffu);
                     const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
                     const double dd = __hiloint2double(0x43300000, (int)dv) - 4503599627370496.0;
-                    const double tv = trow[c * A.pss];
-                    if (k & 1) acc1 = fma(dd, tv, acc1);
-                    else acc0 = fma(dd, tv, acc0);
+                    acc[k & 3] = fma(dd, trow[off], acc[k & 3]);
                 }
             }
+            const double acc0 = acc[0] + acc[1], acc1 = acc[2] + acc[3];
             // per-individual sum over its p rows and the 4 column quarters (fixed order)
             red[sub * 128 + r] = acc0 + acc1;
             epi_sync();
@@ -365,7 +384,7 @@ static int y_ipt(int p) {
 size_t tcy_smem_bytes(int p, int npad) {
     const int ipt = y_ipt(p);
     size_t b = 1024 + (size_t)kYStages * kYStageBytes;
-    b += 2 * y_T_bytes(ipt, p, y_pss(p)) + 2 * y_C_bytes(ipt, npad);
+    b += 2 * y_T_bytes(ipt, p, y_pss(p)) + 2 * y_C_bytes(ipt, npad) + 2 * y_O_bytes(ipt, npad);
     b += 4 * 128 * 8 + (2 * kYStages + 5) * 8 + 16;
     return b;
 }
