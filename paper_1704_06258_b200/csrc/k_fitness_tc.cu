@@ -468,7 +468,7 @@ k_fitness_tc(const __grid_constant__ CUtensorMap tmW, TcArgs A) {
 // ---------------------------------------------------------------------------
 
 // HUBGPU_TC_TIMING=1: per-phase cycle counters of K3-TC (tuning only)
-static unsigned long long* tc_timing_buffer() {
+unsigned long long* tc_timing_buffer() {
     static int on = -1;
     static unsigned long long* buf = nullptr;
     if (on < 0) {

@@ -135,6 +135,7 @@ struct YArgs {
     int acols;        // TMEM columns of A = IT * 32
     int pss;          // staged T row stride (doubles)
     uint32_t idesc;   // kind::i8, M=128, N=128, K-major both
+    unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
 };
 
 __host__ __device__ inline size_t y_T_bytes(int ipt, int p, int pss) {
@@ -217,17 +218,28 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
         // ---------------- MMA issuer
         if (lane == 0) {
             uint32_t g = 0, t = 0;
+            unsigned long long w_a = 0, w_e = 0, w_f = 0, w_i = 0;
+            long long c0 = clock64();
+#define YT(acc_)                                    \
+    do {                                            \
+        const long long c1_ = clock64();            \
+        acc_ += (unsigned long long)(c1_ - c0);     \
+        c0 = c1_;                                   \
+    } while (0)
             for (int64_t u = u0; u < u1; ++u) {
                 mb_wait(b_ard, (uint32_t)((u - u0) & 1));  // A of this unit is in TMEM
+                YT(w_a);
                 fence_after();
                 for (int it = 0; it < IT; ++it, ++t) {
                     const int d = t & 1;
                     if (t >= 2) mb_wait(b_acce + 8 * d, ((t >> 1) - 1) & 1);
+                    YT(w_e);
                     fence_after();
                     const uint32_t dcol = tmem + kYAcc0 + d * 128;
                     for (int kb = 0; kb < IT; ++kb, ++g) {
                         const int s = g % kYStages;
                         mb_wait(b_full + 8 * s, (g / kYStages) & 1);
+                        YT(w_f);
                         fence_after();
                         const uint64_t bd = sw128(su32(ring + s * kYStageBytes));
 #pragma unroll
@@ -235,9 +247,16 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                             mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
                                    (kb | ks) != 0);
                         commit(b_empty + 8 * s);
+                        YT(w_i);
                     }
                     commit(b_accf + 8 * d);
                 }
+            }
+            if (A.timing) {
+                atomicAdd(A.timing + 0, w_a);
+                atomicAdd(A.timing + 1, w_e);
+                atomicAdd(A.timing + 2, w_f);
+                atomicAdd(A.timing + 3, w_i);
             }
         }
     } else if (warp >= kYEpiWarp0) {
@@ -249,6 +268,17 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
         const int bl = r / p, l = r - bl * p;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         uint32_t t = 0;
+        const bool timed = A.timing != nullptr && tid == kYEpiWarp0 * 32;
+        unsigned long long e_st = 0, e_gen = 0, e_wait = 0, e_cmp = 0, e_red = 0;
+        long long c0 = timed ? clock64() : 0;
+#define ET(acc_)                                    \
+    do {                                            \
+        if (timed) {                                \
+            const long long c1_ = clock64();        \
+            acc_ += (unsigned long long)(c1_ - c0); \
+            c0 = c1_;                               \
+        }                                           \
+    } while (0)
         for (int64_t u = u0; u < u1; ++u) {
             const int buf = (int)((u - u0) & 1);
             const int64_t bbase = u * ipt;
@@ -292,6 +322,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 }
             }
             epi_sync();
+            ET(e_st);
             // the previous unit's MMAs (which read A) are complete: its last
             // accumulator was consumed below before we got here
             // generate A: row r = (bl, l), K = nodes; this warp writes columns
@@ -318,6 +349,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 __syncwarp();
                 if (lane == 0) mb_arrive(b_ard);
             }
+            ET(e_gen);
             // epilogue over the 128-row W tiles
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             const double* trow = Ts + (size_t)(r < ipt * p ? bl * p : 0) * A.pss + l;
@@ -325,6 +357,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             for (int it = 0; it < IT; ++it, ++t) {
                 const int d = t & 1;
                 mb_wait(b_accf + 8 * d, (t >> 1) & 1);
+                ET(e_wait);
                 fence_after();
                 const uint32_t dcol = tmem + lane_base + kYAcc0 + d * 128 + sub * 32;
                 uint32_t v0[16], v1[16];
@@ -346,6 +379,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                     const double dd = __hiloint2double(0x43300000, (int)dv) - 4503599627370496.0;
                     acc[k & 3] = fma(dd, trow[off], acc[k & 3]);
                 }
+                ET(e_cmp);
             }
             const double acc0 = acc[0] + acc[1], acc1 = acc[2] + acc[3];
             // per-individual sum over its p rows and the 4 column quarters (fixed order)
@@ -358,6 +392,14 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 A.part[bbase + b2] = s;
             }
             epi_sync();
+            ET(e_red);
+        }
+        if (timed) {
+            atomicAdd(A.timing + 16, e_st);
+            atomicAdd(A.timing + 17, e_gen);
+            atomicAdd(A.timing + 18, e_wait);
+            atomicAdd(A.timing + 19, e_cmp);
+            atomicAdd(A.timing + 20, e_red);
         }
     }
     fence_before();
@@ -418,6 +460,7 @@ int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint
     A.acols = A.IT * 32;
     A.pss = y_pss(I.p);
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    A.timing = tc_timing_buffer();
     int g = grid;
     if (g > A.units) g = (int)A.units;
     CUtensorMap map = *static_cast<const CUtensorMap*>(wmap);
