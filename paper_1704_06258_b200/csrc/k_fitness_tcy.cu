@@ -156,12 +156,14 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
     unsigned char* ring = smem;                                          // W stages
     unsigned char* var = smem + kYStages * kYStageBytes;
     const size_t tb = y_T_bytes(ipt, p, A.pss), cb = y_C_bytes(ipt, A.npad);
-    double* sT[2] = {reinterpret_cast<double*>(var), reinterpret_cast<double*>(var + tb)};
+    // double buffers addressed arithmetically from the shared base (a pointer
+    // array indexed at run time would drop to local memory and generic loads)
+    unsigned char* sT0 = var;
     var += 2 * tb;
-    uint8_t* sC[2] = {var, var + cb};
+    unsigned char* sC0 = var;
     var += 2 * cb;
     const size_t ob = y_O_bytes(ipt, A.npad);
-    uint16_t* sO[2] = {reinterpret_cast<uint16_t*>(var), reinterpret_cast<uint16_t*>(var + ob)};
+    unsigned char* sO0 = var;
     var += 2 * ob;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
@@ -283,9 +285,9 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             const int buf = (int)((u - u0) & 1);
             const int64_t bbase = u * ipt;
             const int nind = (int)(A.B - bbase < ipt ? A.B - bbase : ipt);
-            double* Ts = sT[buf];
-            uint8_t* Cs = sC[buf];
-            uint16_t* Os = sO[buf];
+            double* Ts = reinterpret_cast<double*>(sT0 + buf * tb);
+            uint8_t* Cs = sC0 + buf * cb;
+            uint16_t* Os = reinterpret_cast<uint16_t*>(sO0 + buf * ob);
             // stage this unit's T tables (x 2^-7, zero tails) and cluster rows
             {
                 const int pss = A.pss, per = p * pss;
