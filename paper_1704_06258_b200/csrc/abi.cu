@@ -64,7 +64,8 @@ struct hg_pop {
 
 struct hg_inst {
     std::atomic<int> refs{1};  // the handle itself + every hg_pop / hg_ga built on it
-    alignas(64) unsigned char wmap[128];  // CUtensorMap of W8 (K3-TC)
+    alignas(64) unsigned char wmap[128];  // CUtensorMap of W8 (K3-TC), 128-row boxes
+    alignas(64) unsigned char wmapq[128]; // same, 128/kTcyCluster-row boxes (K3-TC/Y multicast)
     uint8_t* dW8 = nullptr;                // u8 copy of W, [npad_tc][npad_tc], when exact
     bool tc_ok = false;                    // flows are integers in [0, 255] and p fits
     bool tcy_ok = false;                   // ... and n <= 1024: one-hot resident in TMEM
@@ -163,7 +164,7 @@ int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* c
                     (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok);
     int tiles;
     if (tc && inst->tcy_ok) {
-        HG_TRY(launch_fitness_tcy(I, inst->wmap, B, cl, T, part, inst->sm_count, s));
+        HG_TRY(launch_fitness_tcy(I, inst->wmapq, B, cl, T, part, inst->sm_count, s));
         tiles = 1;
     } else if (tc) {
         HG_TRY(launch_fitness_tc(I, inst->wmap, B, cl, T, part, inst->sm_count, s));
@@ -417,7 +418,9 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             chk(cudaMalloc(&inst->dW8, w8.size()), "cudaMalloc(W8)");
             chk(cudaMemcpy(inst->dW8, w8.data(), w8.size(), cudaMemcpyHostToDevice), "H2D W8");
             if (rc) break;
-            rc = tc_make_wmap(inst->dW8, nt, inst->wmap);
+            rc = tc_make_wmap(inst->dW8, nt, 128, inst->wmap);
+            if (rc) break;
+            rc = tc_make_wmap(inst->dW8, nt, 128 / kTcyCluster, inst->wmapq);
             if (rc) break;
             rc = prepare_fitness_tc(p);
             if (rc) break;

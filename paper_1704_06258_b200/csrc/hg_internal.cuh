@@ -118,7 +118,9 @@ size_t tc_smem_bytes(int p);
 int prepare_fitness_tc(int p);
 int tc_timing_read(unsigned long long* out32);
 unsigned long long* tc_timing_buffer();  // HUBGPU_TC_TIMING=1, else nullptr
-int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out);  // map_out: CUtensorMap (128 B)
+// map_out: CUtensorMap (128 B) over the u8 W, boxes of 128 K bytes x box_rows rows
+int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out);
+constexpr int kTcyCluster = 4;  // k_fitness_tcy: W tiles multicast over 4-CTA clusters
 int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
                       const uint32_t* T, double* part, int grid, cudaStream_t s);
 // K3-TC/Y (k_fitness_tcy.cu): one-hot resident in TMEM, n <= 1024

@@ -503,7 +503,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out) {
+int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out) {
     auto enc = get_encode();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable");
@@ -512,7 +512,7 @@ int tc_make_wmap(const uint8_t* W8, int npad_tc, void* map_out) {
     CUtensorMap* m = static_cast<CUtensorMap*>(map_out);
     cuuint64_t dims[2] = {(cuuint64_t)npad_tc, (cuuint64_t)npad_tc};
     cuuint64_t strides[1] = {(cuuint64_t)npad_tc};
-    cuuint32_t box[2] = {128, 128};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)W8, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -19,6 +19,8 @@
 #include <cuda.h>
 #include <cuda_pipeline.h>
 
+#include <cstdlib>
+
 #include "hg_internal.cuh"
 
 namespace hg {
@@ -34,6 +36,7 @@ constexpr int kYStageBytes = 128 * 128;       // 128 W rows x 128 K (u8)
 constexpr int kYMaxIpt = 32;
 constexpr int kYTmemCols = 512;
 constexpr int kYAcc0 = 256;                   // first accumulator column
+constexpr int kYCluster = kTcyCluster;        // CTAs sharing each W tile by TMA multicast
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -64,6 +67,34 @@ __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int 
         "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
         "l"(map), "r"(x), "r"(y), "r"(bar)
         : "memory");
+}
+// one quarter of a W tile, multicast into the same smem offset of every CTA of
+// the cluster; each destination's mbarrier (same offset) gets the bytes
+__device__ __forceinline__ void tma2d_mc(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                         uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(bar), "h"(mask)
+        : "memory");
+}
+// arrive on the mbarrier at this offset in every CTA of the mask once the
+// issued MMAs have completed (frees a W stage cluster-wide)
+__device__ __forceinline__ void commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
 }
 __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
     uint64_t d = 0;
@@ -136,6 +167,7 @@ struct YArgs {
     int pss;          // staged T row stride (doubles)
     uint32_t idesc;   // kind::i8, M=128, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
+    int dbg;                     // ablation flags (tuning only): 1 = no epilogue math, 2 = no MMA
 };
 
 __host__ __device__ inline size_t y_T_bytes(int ipt, int p, int pss) {
@@ -177,7 +209,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
     if (tid == 0) {
         for (int s = 0; s < kYStages; ++s) {
             mb_init(b_full + 8 * s, 1);
-            mb_init(b_empty + 8 * s, 1);
+            mb_init(b_empty + 8 * s, kYCluster);  // every consumer CTA of the cluster
         }
         for (int d = 0; d < 2; ++d) {
             mb_init(b_accf + 8 * d, 1);
@@ -197,23 +229,32 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
     fence_before();
     __syncthreads();
     fence_after();
+    cluster_sync_all();  // peers' barriers are initialised before any multicast
     const uint32_t tmem = *tmem_slot;
 
-    const int64_t u0 = A.units * blockIdx.x / gridDim.x;
-    const int64_t u1 = A.units * (blockIdx.x + 1) / gridDim.x;
+    // units of this cluster, interleaved over its CTAs; every CTA runs the same
+    // number of slots (a slot past the end is a dummy unit) so the multicast W
+    // stream stays in lockstep
+    const uint32_t crank = cluster_rank();
+    const int64_t ncl = gridDim.x / kYCluster, cid = blockIdx.x / kYCluster;
+    const int64_t cs0 = A.units * cid / ncl, cs1 = A.units * (cid + 1) / ncl;
+    const int64_t nslots = (cs1 - cs0 + kYCluster - 1) / kYCluster;
+    const uint16_t all_mask = (uint16_t)((1u << kYCluster) - 1);
 
     if (warp == 1) {
         // ---------------- TMA producer: W tiles (it, kb), same order every unit
         if (lane == 0) {
             uint32_t g = 0;
-            for (int64_t u = u0; u < u1; ++u)
+            for (int64_t j = 0; j < nslots; ++j)
                 for (int it = 0; it < IT; ++it)
                     for (int kb = 0; kb < IT; ++kb, ++g) {
                         const int s = g % kYStages;
+                        // stage s is free in EVERY CTA of the cluster (kYCluster arrivals)
                         if (g >= kYStages) mb_wait(b_empty + 8 * s, ((g / kYStages) - 1) & 1);
                         mb_expect_tx(b_full + 8 * s, kYStageBytes);
-                        tma2d(su32(ring + s * kYStageBytes), &tmW, kb * 128, it * 128,
-                              b_full + 8 * s);
+                        const int q = (int)crank * (128 / kYCluster);
+                        tma2d_mc(su32(ring + s * kYStageBytes + q * 128), &tmW, kb * 128,
+                                 it * 128 + q, b_full + 8 * s, all_mask);
                     }
         }
     } else if (warp == 0) {
@@ -228,8 +269,8 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
         acc_ += (unsigned long long)(c1_ - c0);     \
         c0 = c1_;                                   \
     } while (0)
-            for (int64_t u = u0; u < u1; ++u) {
-                mb_wait(b_ard, (uint32_t)((u - u0) & 1));  // A of this unit is in TMEM
+            for (int64_t j = 0; j < nslots; ++j) {
+                mb_wait(b_ard, (uint32_t)(j & 1));  // A of this unit is in TMEM
                 YT(w_a);
                 fence_after();
                 for (int it = 0; it < IT; ++it, ++t) {
@@ -244,11 +285,13 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                         YT(w_f);
                         fence_after();
                         const uint64_t bd = sw128(su32(ring + s * kYStageBytes));
+                        if (!(A.dbg & 2)) {
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns of A
-                            mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
-                                   (kb | ks) != 0);
-                        commit(b_empty + 8 * s);
+                            for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns of A
+                                mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
+                                       (kb | ks) != 0);
+                        }
+                        commit_mc(b_empty + 8 * s, all_mask);
                         YT(w_i);
                     }
                     commit(b_accf + 8 * d);
@@ -271,7 +314,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         uint32_t t = 0;
         const bool timed = A.timing != nullptr && tid == kYEpiWarp0 * 32;
-        unsigned long long e_st = 0, e_gen = 0, e_wait = 0, e_cmp = 0, e_red = 0;
+        unsigned long long e_st = 0, e_gen = 0, e_wait = 0, e_cmp = 0, e_red = 0, e_ld = 0;
         long long c0 = timed ? clock64() : 0;
 #define ET(acc_)                                    \
     do {                                            \
@@ -281,10 +324,11 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             c0 = c1_;                               \
         }                                           \
     } while (0)
-        for (int64_t u = u0; u < u1; ++u) {
-            const int buf = (int)((u - u0) & 1);
+        for (int64_t j = 0; j < nslots; ++j) {
+            const int buf = (int)(j & 1);
+            const int64_t u = cs0 + j * kYCluster + crank;
             const int64_t bbase = u * ipt;
-            const int nind = (int)(A.B - bbase < ipt ? A.B - bbase : ipt);
+            const int nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
             double* Ts = reinterpret_cast<double*>(sT0 + buf * tb);
             uint8_t* Cs = sC0 + buf * cb;
             uint16_t* Os = reinterpret_cast<uint16_t*>(sO0 + buf * ob);
@@ -369,11 +413,16 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 const uint4* op = reinterpret_cast<const uint4*>(orow + it * 128 + sub * 32);
                 const uint4 o0 = op[0], o1 = op[1], o2 = op[2], o3 = op[3];
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                ET(e_ld);
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mb_arrive(b_acce + 8 * d);  // accumulator may be overwritten
                 const uint32_t ow[16] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w,
                                          o2.x, o2.y, o2.z, o2.w, o3.x, o3.y, o3.z, o3.w};
+                if (A.dbg & 1) {
+                    acc[0] += (double)(v0[0] + v1[15] + ow[3]);
+                    continue;
+                }
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
                     const uint32_t off = (k & 1) ? (ow[k >> 1] >> 16) : (ow[k >> 1] & 0xffffu);
@@ -402,10 +451,12 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             atomicAdd(A.timing + 18, e_wait);
             atomicAdd(A.timing + 19, e_cmp);
             atomicAdd(A.timing + 20, e_red);
+            atomicAdd(A.timing + 21, e_ld);
         }
     }
     fence_before();
     __syncthreads();
+    cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
     if (warp == 0) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -463,11 +514,29 @@ int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint
     A.pss = y_pss(I.p);
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     A.timing = tc_timing_buffer();
-    int g = grid;
-    if (g > A.units) g = (int)A.units;
+    {
+        const char* e = getenv("HUBGPU_TCY_DBG");
+        A.dbg = e ? atoi(e) : 0;
+    }
+    // whole clusters only; grid = SMs rounded down to the cluster size
+    int g = grid / kYCluster * kYCluster;
+    const int64_t need = round_up(A.units, kYCluster);
+    if (g > need) g = (int)need;
+    if (g < kYCluster) g = kYCluster;
     CUtensorMap map = *static_cast<const CUtensorMap*>(wmap);
-    k_fitness_tcy<<<g, kYThreads, tcy_smem_bytes(I.p, I.npad), s>>>(map, A);
-    HG_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(kYThreads);
+    cfg.dynamicSmemBytes = tcy_smem_bytes(I.p, I.npad);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kYCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HG_CUDA(cudaLaunchKernelEx(&cfg, k_fitness_tcy, map, A));
     return HG_OK;
 }
 

@@ -23,9 +23,9 @@ pop.evaluate(B)
 print("fitness ms", pop.last_fitness_ms())
 _lib.check(_lib.load().hg_debug_tc_timing(buf.ctypes.data_as(_lib._u64p)))
 m = buf[0:4].astype(float)
-e = buf[16:21].astype(float)
+e = buf[16:22].astype(float)
 print("MMA warp:", " ".join(f"{k}={100 * v / m.sum():.1f}%" for k, v in
                              zip(["waitA", "waitAccEmpty", "waitW", "issue"], m)))
 print("epi warp:", " ".join(f"{k}={100 * v / e.sum():.1f}%" for k, v in
-                             zip(["stage", "gen", "waitAcc", "compute", "reduce"], e)))
+                             zip(["stage", "gen", "waitAcc", "math", "reduce", "tmemld"], e)))
 print("cycles per CTA (MMA warp):", m.sum() / 148, " epi:", e.sum() / 148)
