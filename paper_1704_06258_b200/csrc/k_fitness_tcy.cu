@@ -489,9 +489,25 @@ bool tcy_supported(int n, int p, int npad) {
            tcy_smem_bytes(p, npad) <= 227 * 1024;
 }
 
+static int g_tcy_clusters = 0;  // co-resident clusters (cudaOccupancyMaxActiveClusters)
+
 int prepare_fitness_tcy(int p, int npad) {
     HG_CUDA(cudaFuncSetAttribute(k_fitness_tcy, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)tcy_smem_bytes(p, npad)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kYCluster);
+    cfg.blockDim = dim3(kYThreads);
+    cfg.dynamicSmemBytes = tcy_smem_bytes(p, npad);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kYCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    HG_CUDA(cudaOccupancyMaxActiveClusters(&nc, k_fitness_tcy, &cfg));
+    g_tcy_clusters = nc;
     return HG_OK;
 }
 
@@ -518,8 +534,9 @@ int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint
         const char* e = getenv("HUBGPU_TCY_DBG");
         A.dbg = e ? atoi(e) : 0;
     }
-    // whole clusters only; grid = SMs rounded down to the cluster size
-    int g = grid / kYCluster * kYCluster;
+    // whole clusters only, all co-resident (one wave): the GPCs need not hold a
+    // multiple of the cluster size, so ask the occupancy API
+    int g = (g_tcy_clusters > 0 ? g_tcy_clusters : grid / kYCluster) * kYCluster;
     const int64_t need = round_up(A.units, kYCluster);
     if (g > need) g = (int)need;
     if (g < kYCluster) g = kYCluster;
