@@ -324,79 +324,95 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             c0 = c1_;                               \
         }                                           \
     } while (0)
-        for (int64_t j = 0; j < nslots; ++j) {
-            const int buf = (int)(j & 1);
+        // per-slot unit geometry
+        auto slot_unit = [&](int64_t j, int64_t& bbase, int& nind) {
             const int64_t u = cs0 + j * kYCluster + crank;
-            const int64_t bbase = u * ipt;
-            const int nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
+            bbase = u * ipt;
+            nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
+        };
+        // stage a unit's T tables (x 2^-7, zero tails), cluster rows and the
+        // epilogue's T-row offsets into double buffer `buf`
+        auto stage = [&](int64_t j) {
+            int64_t bbase;
+            int nind;
+            slot_unit(j, bbase, nind);
+            const int buf = (int)(j & 1);
             double* Ts = reinterpret_cast<double*>(sT0 + buf * tb);
             uint8_t* Cs = sC0 + buf * cb;
             uint16_t* Os = reinterpret_cast<uint16_t*>(sO0 + buf * ob);
-            // stage this unit's T tables (x 2^-7, zero tails) and cluster rows
-            {
-                const int pss = A.pss, per = p * pss;
-                for (int x = et; x < ipt * per; x += kYEpiThreads) {
-                    const int b2 = x / per, y = x - b2 * per;
-                    const int c = y / pss, ll = y - c * pss;
-                    double v = 0.0;
-                    if (b2 < nind && ll < p) {
-                        const uint32_t* tbp = A.T + (bbase + b2) * 2 * p * (int64_t)A.ps;
-                        v = __hiloint2double((int)tbp[c * A.ps + ll], (int)tbp[(p + c) * A.ps + ll]) *
-                            0.0078125;
-                    }
-                    Ts[(b2 * p + c) * pss + ll] = v;
+            const int pss = A.pss, per = p * pss;
+            for (int x = et; x < ipt * per; x += kYEpiThreads) {
+                const int b2 = x / per, y = x - b2 * per;
+                const int c = y / pss, ll = y - c * pss;
+                double v = 0.0;
+                if (b2 < nind && ll < p) {
+                    const uint32_t* tbp = A.T + (bbase + b2) * 2 * p * (int64_t)A.ps;
+                    v = __hiloint2double((int)tbp[c * A.ps + ll], (int)tbp[(p + c) * A.ps + ll]) *
+                        0.0078125;
                 }
-                const int chunks = A.npad / 16;
-                for (int x = et; x < ipt * chunks; x += kYEpiThreads) {
-                    const int b2 = x / chunks, k = x - b2 * chunks;
-                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                    if (b2 < nind)
-                        v = __ldg(reinterpret_cast<const uint4*>(A.cl + (bbase + b2) * A.npad) + k);
-                    reinterpret_cast<uint4*>(Cs + (size_t)b2 * A.npad)[k] = v;
-                    // T-row offsets (in doubles) of these 16 columns for the epilogue
-                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-                    uint32_t o[8];
-#pragma unroll
-                    for (int h = 0; h < 8; ++h) {
-                        const uint32_t c0 = (w[h >> 1] >> ((h & 1) * 16)) & 0xffu;
-                        const uint32_t c1 = (w[h >> 1] >> ((h & 1) * 16 + 8)) & 0xffu;
-                        o[h] = (c0 * A.pss) | ((c1 * A.pss) << 16);
-                    }
-                    uint4* od = reinterpret_cast<uint4*>(Os + (size_t)b2 * A.npad + k * 16);
-                    od[0] = make_uint4(o[0], o[1], o[2], o[3]);
-                    od[1] = make_uint4(o[4], o[5], o[6], o[7]);
-                }
+                Ts[(b2 * p + c) * pss + ll] = v;
             }
+            const int chunks = A.npad / 16;
+            for (int x = et; x < ipt * chunks; x += kYEpiThreads) {
+                const int b2 = x / chunks, k = x - b2 * chunks;
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (b2 < nind)
+                    v = __ldg(reinterpret_cast<const uint4*>(A.cl + (bbase + b2) * A.npad) + k);
+                reinterpret_cast<uint4*>(Cs + (size_t)b2 * A.npad)[k] = v;
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                uint32_t o[8];
+#pragma unroll
+                for (int h = 0; h < 8; ++h) {
+                    const uint32_t ca = (w[h >> 1] >> ((h & 1) * 16)) & 0xffu;
+                    const uint32_t cz = (w[h >> 1] >> ((h & 1) * 16 + 8)) & 0xffu;
+                    o[h] = (ca * A.pss) | ((cz * A.pss) << 16);
+                }
+                uint4* od = reinterpret_cast<uint4*>(Os + (size_t)b2 * A.npad + k * 16);
+                od[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                od[1] = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+        };
+        // one-hot A of a unit into TMEM (row r = (bl, l), K = nodes); this warp
+        // writes columns [sub * acols/4, (sub+1) * acols/4) of its lane quadrant
+        auto gen = [&](int64_t j) {
+            int64_t bbase;
+            int nind;
+            slot_unit(j, bbase, nind);
+            const uint8_t* Cs = sC0 + (j & 1) * cb;
+            const bool live = r < ipt * p && bl < nind;
+            const uint32_t lrep = (uint32_t)l * 0x01010101u;
+            const int cq = A.acols / 4;
+            const uint4* crow = reinterpret_cast<const uint4*>(Cs + (size_t)(live ? bl : 0) * A.npad);
+            for (int c0 = sub * cq; c0 < (sub + 1) * cq; c0 += 8) {
+                uint32_t v[8];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint4 x = crow[(c0 >> 2) + h];  // 16 cluster ids = 4 columns
+                    v[4 * h + 0] = live ? oh4(x.x, lrep) : 0u;
+                    v[4 * h + 1] = live ? oh4(x.y, lrep) : 0u;
+                    v[4 * h + 2] = live ? oh4(x.z, lrep) : 0u;
+                    v[4 * h + 3] = live ? oh4(x.w, lrep) : 0u;
+                }
+                st8(tmem + lane_base + (uint32_t)c0, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(b_ard);
+        };
+
+        if (nslots > 0) {
+            stage(0);
             epi_sync();
-            ET(e_st);
-            // the previous unit's MMAs (which read A) are complete: its last
-            // accumulator was consumed below before we got here
-            // generate A: row r = (bl, l), K = nodes; this warp writes columns
-            // [sub * acols/4, (sub+1) * acols/4) of its quadrant's lanes
-            {
-                const bool live = r < ipt * p && bl < nind;
-                const uint32_t lrep = (uint32_t)l * 0x01010101u;
-                const int cq = A.acols / 4;
-                const uint4* crow = reinterpret_cast<const uint4*>(Cs + (size_t)(live ? bl : 0) * A.npad);
-                for (int c0 = sub * cq; c0 < (sub + 1) * cq; c0 += 8) {
-                    uint32_t v[8];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint4 x = crow[(c0 >> 2) + h];  // 16 cluster ids = 4 columns
-                        v[4 * h + 0] = live ? oh4(x.x, lrep) : 0u;
-                        v[4 * h + 1] = live ? oh4(x.y, lrep) : 0u;
-                        v[4 * h + 2] = live ? oh4(x.z, lrep) : 0u;
-                        v[4 * h + 3] = live ? oh4(x.w, lrep) : 0u;
-                    }
-                    st8(tmem + lane_base + (uint32_t)c0, v);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mb_arrive(b_ard);
-            }
-            ET(e_gen);
-            // epilogue over the 128-row W tiles
+            gen(0);
+        }
+        ET(e_st);
+        for (int64_t j = 0; j < nslots; ++j) {
+            int64_t bbase;
+            int nind;
+            slot_unit(j, bbase, nind);
+            const double* Ts = reinterpret_cast<const double*>(sT0 + (j & 1) * tb);
+            const uint16_t* Os = reinterpret_cast<const uint16_t*>(sO0 + (j & 1) * ob);
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             const double* trow = Ts + (size_t)(r < ipt * p ? bl * p : 0) * A.pss + l;
             const uint16_t* orow = Os + (size_t)(bl < ipt ? bl : 0) * A.npad;
@@ -417,6 +433,20 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mb_arrive(b_acce + 8 * d);  // accumulator may be overwritten
+                // next unit: staged early, its one-hot generated as soon as this
+                // unit's last MMAs are complete (this wait), so the tensor core
+                // starts on it while we finish this unit's epilogue
+                if (j + 1 < nslots) {
+                    if (it == 0) {
+                        stage(j + 1);
+                        ET(e_st);
+                    }
+                    if (it == IT - 1) {
+                        epi_sync();  // staging of j+1 complete
+                        gen(j + 1);
+                        ET(e_gen);
+                    }
+                }
                 const uint32_t ow[16] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w,
                                          o2.x, o2.y, o2.z, o2.w, o3.x, o3.y, o3.z, o3.w};
                 if (A.dbg & 1) {
