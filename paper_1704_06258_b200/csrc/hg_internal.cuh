@@ -120,7 +120,10 @@ int tc_timing_read(unsigned long long* out32);
 unsigned long long* tc_timing_buffer();  // HUBGPU_TC_TIMING=1, else nullptr
 // map_out: CUtensorMap (128 B) over the u8 W, boxes of 128 K bytes x box_rows rows
 int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out);
-constexpr int kTcyCluster = 1;  // k_fitness_tcy: CTAs per cluster sharing W tiles (TMA multicast)
+#ifndef HG_TCY_CLUSTER
+#define HG_TCY_CLUSTER 1
+#endif
+constexpr int kTcyCluster = HG_TCY_CLUSTER;  // k_fitness_tcy: CTAs per cluster sharing W tiles (TMA multicast)
 int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
                       const uint32_t* T, double* part, int grid, cudaStream_t s);
 // K3-TC/Y (k_fitness_tcy.cu): one-hot resident in TMEM, n <= 1024

@@ -31,7 +31,7 @@ constexpr int kYThreads = 640;
 constexpr int kYWarps = kYThreads / 32;
 constexpr int kYEpiWarp0 = 4;                 // first epilogue warp
 constexpr int kYEpiThreads = kYThreads - 128; // 512
-constexpr int kYStages = 6;                   // W ring depth
+constexpr int kYMaxStages = 16;               // W ring depth bound (runtime: YArgs::stages)
 constexpr int kYStageBytes = 128 * 128;       // 128 W rows x 128 K (u8)
 constexpr int kYMaxIpt = 32;
 constexpr int kYTmemCols = 512;
@@ -145,11 +145,11 @@ __device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
 __device__ __forceinline__ void epi_sync() {  // named barrier over the 16 epilogue warps
     asm volatile("bar.sync 1, %0;" ::"n"(kYEpiThreads) : "memory");
 }
-// byte-wise (x == l) -> 0x80 / 0x00 (see k_fitness_tc.cu)
+// byte-wise (x == l) -> 1 / 0
 __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
     const uint32_t y = x ^ lrep;
     const uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-    return ~(t | y) & 0x80808080u;
+    return (~(t | y) & 0x80808080u) >> 7;
 }
 
 }  // namespace
@@ -164,20 +164,15 @@ struct YArgs {
     int64_t units;
     int IT;           // 128-row W tiles (= K blocks)
     int acols;        // TMEM columns of A = IT * 32
-    int pss;          // staged T row stride (doubles)
+    int stages;       // W ring depth
+    int kbs;          // 128-byte K blocks per stage
     uint32_t idesc;   // kind::i8, M=128, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
     int dbg;                     // ablation flags (tuning only): 1 = no epilogue math, 2 = no MMA
 };
 
-__host__ __device__ inline size_t y_T_bytes(int ipt, int p, int pss) {
-    return ((size_t)ipt * p * pss * 8 + 15) & ~size_t(15);
-}
 __host__ __device__ inline size_t y_C_bytes(int ipt, int npad) {
     return ((size_t)ipt * npad + 15) & ~size_t(15);
-}
-__host__ __device__ inline size_t y_O_bytes(int ipt, int npad) {  // u16 T-row offsets
-    return ((size_t)ipt * npad * 2 + 15) & ~size_t(15);
 }
 
 __global__ void __launch_bounds__(kYThreads, 1)
@@ -186,28 +181,31 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int p = A.p, ipt = A.ipt, IT = A.IT;
     unsigned char* ring = smem;                                          // W stages
-    unsigned char* var = smem + kYStages * kYStageBytes;
-    const size_t tb = y_T_bytes(ipt, p, A.pss), cb = y_C_bytes(ipt, A.npad);
-    // double buffers addressed arithmetically from the shared base (a pointer
+    const int NS = A.stages, KBS = A.kbs;
+    unsigned char* var = smem + NS * KBS * kYStageBytes;
+    const size_t cb = y_C_bytes(ipt, A.npad);
+    // double buffer addressed arithmetically from the shared base (a pointer
     // array indexed at run time would drop to local memory and generic loads)
-    unsigned char* sT0 = var;
-    var += 2 * tb;
     unsigned char* sC0 = var;
     var += 2 * cb;
-    const size_t ob = y_O_bytes(ipt, A.npad);
-    unsigned char* sO0 = var;
-    var += 2 * ob;
+    uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [p][128] cluster-pair flow bins
+    var += (size_t)p * 512;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
-    // bars: full[6] empty[6] accfull[2] accempty[2] aready[1]
-    const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kYStages,
-                   b_accf = b_empty + 8 * kYStages, b_acce = b_accf + 16, b_ard = b_acce + 16;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kYStages + 5);
+    // bars: full[16] empty[16] accfull[2] accempty[2] kbfree[4] aready[4]
+    const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kYMaxStages,
+                   b_accf = b_empty + 8 * kYMaxStages, b_acce = b_accf + 16, b_kbf = b_acce + 16,
+                   b_ard = b_kbf + 32;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kYMaxStages + 12);
+    // A's K blocks are generated in 4 contiguous ranges, one per column-quarter
+    // warp group: quarter h owns K blocks [kq(h), kq(h+1))
+    auto kq = [&](int h) { return h * IT / 4; };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int x = tid; x < p * 128; x += kYThreads) bins[x] = 0u;
     if (tid == 0) {
-        for (int s = 0; s < kYStages; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mb_init(b_full + 8 * s, 1);
             mb_init(b_empty + 8 * s, kYCluster);  // every consumer CTA of the cluster
         }
@@ -215,7 +213,10 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             mb_init(b_accf + 8 * d, 1);
             mb_init(b_acce + 8 * d, kYWarps - kYEpiWarp0);
         }
-        mb_init(b_ard, kYWarps - kYEpiWarp0);
+        for (int h = 0; h < 4; ++h) {
+            mb_init(b_kbf + 8 * h, 1);
+            mb_init(b_ard + 8 * h, 4);  // the 4 lane-quadrant warps of quarter h
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
     }
@@ -242,69 +243,99 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
     const uint16_t all_mask = (uint16_t)((1u << kYCluster) - 1);
 
     if (warp == 1) {
-        // ---------------- TMA producer: W tiles (it, kb), same order every unit
+        // ---------------- TMA producer: W tiles (it, K-block group), same order
+        // every unit; a stage holds KBS consecutive 128-byte K blocks
         if (lane == 0) {
-            uint32_t g = 0;
+            uint32_t s = 0, ph = 0;
+            bool wrapped = false;
+            const int q = (int)crank * (128 / kYCluster);
             for (int64_t j = 0; j < nslots; ++j)
                 for (int it = 0; it < IT; ++it)
-                    for (int kb = 0; kb < IT; ++kb, ++g) {
-                        const int s = g % kYStages;
+                    for (int kb0 = 0; kb0 < IT; kb0 += KBS) {
+                        const int nk = IT - kb0 < KBS ? IT - kb0 : KBS;
                         // stage s is free in EVERY CTA of the cluster (kYCluster arrivals)
-                        if (g >= kYStages) mb_wait(b_empty + 8 * s, ((g / kYStages) - 1) & 1);
-                        mb_expect_tx(b_full + 8 * s, kYStageBytes);
-                        const int q = (int)crank * (128 / kYCluster);
-                        tma2d_mc(su32(ring + s * kYStageBytes + q * 128), &tmW, kb * 128,
-                                 it * 128 + q, b_full + 8 * s, all_mask);
+                        if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
+                        mb_expect_tx(b_full + 8 * s, (uint32_t)(nk * kYStageBytes));
+                        const uint32_t dst = su32(ring + s * (KBS * kYStageBytes) + q * 128);
+                        for (int kk = 0; kk < nk; ++kk)
+                            tma2d_mc(dst + kk * kYStageBytes, &tmW, (kb0 + kk) * 128,
+                                     it * 128 + q, b_full + 8 * s, all_mask);
+                        if (++s == (uint32_t)NS) {
+                            s = 0;
+                            ph ^= 1u;
+                            wrapped = true;
+                        }
                     }
         }
     } else if (warp == 0) {
         // ---------------- MMA issuer
         if (lane == 0) {
-            uint32_t g = 0, t = 0;
+            uint32_t s = 0, ph = 0, t = 0;
+            const bool timed = A.timing != nullptr;
             unsigned long long w_a = 0, w_e = 0, w_f = 0, w_i = 0;
-            long long c0 = clock64();
+            long long c0 = timed ? clock64() : 0;
 #define YT(acc_)                                    \
     do {                                            \
-        const long long c1_ = clock64();            \
-        acc_ += (unsigned long long)(c1_ - c0);     \
-        c0 = c1_;                                   \
+        if (timed) {                                \
+            const long long c1_ = clock64();        \
+            acc_ += (unsigned long long)(c1_ - c0); \
+            c0 = c1_;                               \
+        }                                           \
     } while (0)
             for (int64_t j = 0; j < nslots; ++j) {
-                mb_wait(b_ard, (uint32_t)(j & 1));  // A of this unit is in TMEM
-                YT(w_a);
-                fence_after();
                 for (int it = 0; it < IT; ++it, ++t) {
                     const int d = t & 1;
-                    if (t >= 2) mb_wait(b_acce + 8 * d, ((t >> 1) - 1) & 1);
+                    if (t >= 2 && !(A.dbg & 64)) mb_wait(b_acce + 8 * d, ((t >> 1) - 1) & 1);
                     YT(w_e);
                     fence_after();
                     const uint32_t dcol = tmem + kYAcc0 + d * 128;
-                    for (int kb = 0; kb < IT; ++kb, ++g) {
-                        const int s = g % kYStages;
-                        mb_wait(b_full + 8 * s, (g / kYStages) & 1);
+                    for (int kb0 = 0; kb0 < IT; kb0 += KBS) {
+                        const int nk = IT - kb0 < KBS ? IT - kb0 : KBS;
+                        if (it == 0 && !(A.dbg & 64)) {
+                            // first use of this unit's A: its quarters must be in TMEM
+                            for (int h = 0; h < 4; ++h)
+                                if (kq(h) >= kb0 && kq(h) < kb0 + nk && kq(h) < kq(h + 1))
+                                    mb_wait(b_ard + 8 * h, (uint32_t)(j & 1));
+                            fence_after();
+                            YT(w_a);
+                        }
+                        mb_wait(b_full + 8 * s, ph);
                         YT(w_f);
                         fence_after();
-                        const uint64_t bd = sw128(su32(ring + s * kYStageBytes));
+                        const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
                         if (!(A.dbg & 2)) {
+                            for (int kk = 0; kk < nk; ++kk) {
+                                const int kb = kb0 + kk;
+                                const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
 #pragma unroll
-                            for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns of A
-                                mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
-                                       (kb | ks) != 0);
+                                for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns of A
+                                    mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
+                                           (kb | ks) != 0);
+                            }
                         }
                         commit_mc(b_empty + 8 * s, all_mask);
+                        if (it == IT - 1)  // last use of this unit's A quarter: free it
+                            for (int h = 0; h < 4; ++h)
+                                if (kq(h + 1) - 1 >= kb0 && kq(h + 1) - 1 < kb0 + nk &&
+                                    kq(h) < kq(h + 1))
+                                    commit(b_kbf + 8 * h);
+                        if (++s == (uint32_t)NS) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
                         YT(w_i);
                     }
                     commit(b_accf + 8 * d);
                 }
             }
-            if (A.timing) {
+            if (timed) {
                 atomicAdd(A.timing + 0, w_a);
                 atomicAdd(A.timing + 1, w_e);
                 atomicAdd(A.timing + 2, w_f);
                 atomicAdd(A.timing + 3, w_i);
             }
         }
-    } else if (warp >= kYEpiWarp0) {
+    } else if (warp >= kYEpiWarp0 && !(A.dbg & 64)) {
         // ---------------- generators + epilogue (16 warps)
         const int et = tid - kYEpiWarp0 * 32;           // 0..511
         const int q = warp & 3;                         // TMEM lane quadrant
@@ -330,28 +361,12 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             bbase = u * ipt;
             nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
         };
-        // stage a unit's T tables (x 2^-7, zero tails), cluster rows and the
-        // epilogue's T-row offsets into double buffer `buf`
+        // stage a unit's cluster rows into double buffer j & 1
         auto stage = [&](int64_t j) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
-            const int buf = (int)(j & 1);
-            double* Ts = reinterpret_cast<double*>(sT0 + buf * tb);
-            uint8_t* Cs = sC0 + buf * cb;
-            uint16_t* Os = reinterpret_cast<uint16_t*>(sO0 + buf * ob);
-            const int pss = A.pss, per = p * pss;
-            for (int x = et; x < ipt * per; x += kYEpiThreads) {
-                const int b2 = x / per, y = x - b2 * per;
-                const int c = y / pss, ll = y - c * pss;
-                double v = 0.0;
-                if (b2 < nind && ll < p) {
-                    const uint32_t* tbp = A.T + (bbase + b2) * 2 * p * (int64_t)A.ps;
-                    v = __hiloint2double((int)tbp[c * A.ps + ll], (int)tbp[(p + c) * A.ps + ll]) *
-                        0.0078125;
-                }
-                Ts[(b2 * p + c) * pss + ll] = v;
-            }
+            uint8_t* Cs = sC0 + (j & 1) * cb;
             const int chunks = A.npad / 16;
             for (int x = et; x < ipt * chunks; x += kYEpiThreads) {
                 const int b2 = x / chunks, k = x - b2 * chunks;
@@ -359,21 +374,10 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 if (b2 < nind)
                     v = __ldg(reinterpret_cast<const uint4*>(A.cl + (bbase + b2) * A.npad) + k);
                 reinterpret_cast<uint4*>(Cs + (size_t)b2 * A.npad)[k] = v;
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-                uint32_t o[8];
-#pragma unroll
-                for (int h = 0; h < 8; ++h) {
-                    const uint32_t ca = (w[h >> 1] >> ((h & 1) * 16)) & 0xffu;
-                    const uint32_t cz = (w[h >> 1] >> ((h & 1) * 16 + 8)) & 0xffu;
-                    o[h] = (ca * A.pss) | ((cz * A.pss) << 16);
-                }
-                uint4* od = reinterpret_cast<uint4*>(Os + (size_t)b2 * A.npad + k * 16);
-                od[0] = make_uint4(o[0], o[1], o[2], o[3]);
-                od[1] = make_uint4(o[4], o[5], o[6], o[7]);
             }
         };
         // one-hot A of a unit into TMEM (row r = (bl, l), K = nodes); this warp
-        // writes columns [sub * acols/4, (sub+1) * acols/4) of its lane quadrant
+        // writes K blocks [kq(sub), kq(sub+1)) of its lane quadrant
         auto gen = [&](int64_t j) {
             int64_t bbase;
             int nind;
@@ -381,9 +385,8 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             const uint8_t* Cs = sC0 + (j & 1) * cb;
             const bool live = r < ipt * p && bl < nind;
             const uint32_t lrep = (uint32_t)l * 0x01010101u;
-            const int cq = A.acols / 4;
             const uint4* crow = reinterpret_cast<const uint4*>(Cs + (size_t)(live ? bl : 0) * A.npad);
-            for (int c0 = sub * cq; c0 < (sub + 1) * cq; c0 += 8) {
+            for (int c0 = kq(sub) * 32; c0 < kq(sub + 1) * 32; c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -398,7 +401,7 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             fence_before();
             __syncwarp();
-            if (lane == 0) mb_arrive(b_ard);
+            if (lane == 0) mb_arrive(b_ard + 8 * sub);
         };
 
         if (nslots > 0) {
@@ -407,17 +410,35 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
             gen(0);
         }
         ET(e_st);
+        // this thread's bin row: bins[k][r] at byte k * 512 + r * 4
+        const uint32_t bin_r = su32(bins) + (uint32_t)r * 4u;
         for (int64_t j = 0; j < nslots; ++j) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
-            const double* Ts = reinterpret_cast<const double*>(sT0 + (j & 1) * tb);
-            const uint16_t* Os = reinterpret_cast<const uint16_t*>(sO0 + (j & 1) * ob);
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            const double* trow = Ts + (size_t)(r < ipt * p ? bl * p : 0) * A.pss + l;
-            const uint16_t* orow = Os + (size_t)(bl < ipt ? bl : 0) * A.npad;
+            const bool live = r < ipt * p && bl < nind;
+            const uint8_t* crow = sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad;
+            if (j + 1 < nslots) {
+                stage(j + 1);  // the next unit's cluster rows, under this unit's MMAs
+                ET(e_st);
+            }
             for (int it = 0; it < IT; ++it, ++t) {
                 const int d = t & 1;
+                if (j + 1 < nslots && it == IT - 1) {
+                    // the next unit's one-hot, quarter by quarter as the last
+                    // tile's MMAs release this unit's A
+                    epi_sync();  // staging of j+1 complete
+                    if (kq(sub) < kq(sub + 1)) {
+                        mb_wait(b_kbf + 8 * sub, (uint32_t)(j & 1));
+                        fence_after();
+                    }
+                    if (A.dbg & 4) {  // ablation: wait for the whole last tile
+                        mb_wait(b_accf + 8 * d, (t >> 1) & 1);
+                        fence_after();
+                    }
+                    gen(j + 1);
+                    ET(e_gen);
+                }
                 mb_wait(b_accf + 8 * d, (t >> 1) & 1);
                 ET(e_wait);
                 fence_after();
@@ -425,54 +446,75 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
                 uint32_t v0[16], v1[16];
                 ld16(dcol, v0);
                 ld16(dcol + 16, v1);
-                // T-row offsets of the 32 columns i = it*128 + sub*32 + k
-                const uint4* op = reinterpret_cast<const uint4*>(orow + it * 128 + sub * 32);
-                const uint4 o0 = op[0], o1 = op[1], o2 = op[2], o3 = op[3];
+                // cluster ids of the 32 columns i = it*128 + sub*32 + k
+                const uint4* cp = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32);
+                const uint4 ca = cp[0], cz = cp[1];
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 ET(e_ld);
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mb_arrive(b_acce + 8 * d);  // accumulator may be overwritten
-                // next unit: staged early, its one-hot generated as soon as this
-                // unit's last MMAs are complete (this wait), so the tensor core
-                // starts on it while we finish this unit's epilogue
-                if (j + 1 < nslots) {
-                    if (it == 0) {
-                        stage(j + 1);
-                        ET(e_st);
-                    }
-                    if (it == IT - 1) {
-                        epi_sync();  // staging of j+1 complete
-                        gen(j + 1);
-                        ET(e_gen);
-                    }
-                }
-                const uint32_t ow[16] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w,
-                                         o2.x, o2.y, o2.z, o2.w, o3.x, o3.y, o3.z, o3.w};
-                if (A.dbg & 1) {
-                    acc[0] += (double)(v0[0] + v1[15] + ow[3]);
-                    continue;
-                }
+                if (live && !(A.dbg & 1)) {
+                    // G[c_i][r] += D[r][i]: exact integer bins, this row's own
+                    // (4 column-quarter warps share a row, hence the atomics)
+                    const uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cz.x, cz.y, cz.z, cz.w};
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const uint32_t off = (k & 1) ? (ow[k >> 1] >> 16) : (ow[k >> 1] & 0xffffu);
-                    const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
-                    const double dd = __hiloint2double(0x43300000, (int)dv) - 4503599627370496.0;
-                    acc[k & 3] = fma(dd, trow[off], acc[k & 3]);
+                    for (int k = 0; k < 32; ++k) {
+                        const uint32_t c = __byte_perm(cw[k >> 2], 0u, 0x4440u + (k & 3));
+                        const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
+                        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(bin_r + c * 512u),
+                                     "r"(dv)
+                                     : "memory");
+                    }
                 }
                 ET(e_cmp);
             }
-            const double acc0 = acc[0] + acc[1], acc1 = acc[2] + acc[3];
-            // per-individual sum over its p rows and the 4 column quarters (fixed order)
-            red[sub * 128 + r] = acc0 + acc1;
-            epi_sync();
-            for (int b2 = et; b2 < nind; b2 += kYEpiThreads) {
-                double s = 0.0;
-                for (int sq = 0; sq < 4; ++sq)
-                    for (int ll = 0; ll < p; ++ll) s += red[sq * 128 + b2 * p + ll];
-                A.part[bbase + b2] = s;
+            // S_T(b) = sum_l sum_k T_b[k][l] * G[k][(b,l)]; this thread takes
+            // k = sub, sub + 4, ... of row r (fixed order -> deterministic).
+            // The first 8 of its T values are fetched before the barrier.
+            const uint32_t* tbp = A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps + l;
+            uint32_t th[8], tl[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = sub + 4 * u;
+                const bool ok = live && k < p;
+                th[u] = ok ? __ldg(tbp + k * A.ps) : 0u;
+                tl[u] = ok ? __ldg(tbp + (p + k) * A.ps) : 0u;
             }
+            epi_sync();  // every bin of the unit is complete
+            double s = 0.0;
+            if (live) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = sub + 4 * u;
+                    if (k < p) {
+                        const uint32_t g = bins[k * 128 + r];
+                        bins[k * 128 + r] = 0u;
+                        s = fma((double)g, __hiloint2double((int)th[u], (int)tl[u]), s);
+                    }
+                }
+                for (int k = sub + 32; k < p; k += 4) {
+                    const uint32_t g = bins[k * 128 + r];
+                    bins[k * 128 + r] = 0u;
+                    s = fma((double)g,
+                            __hiloint2double((int)__ldg(tbp + k * A.ps), (int)__ldg(tbp + (p + k) * A.ps)),
+                            s);
+                }
+            }
+            red[sub * 128 + r] = s;
             epi_sync();
+            // one warp per individual: lanes stride its 4p partials, then a
+            // butterfly (fixed order -> deterministic)
+            for (int b2 = (warp - kYEpiWarp0); b2 < nind; b2 += kYEpiThreads / 32) {
+                double acc = 0.0;
+                for (int x = lane; x < 4 * p; x += 32) {
+                    const int sq = x / p, ll = x - sq * p;
+                    acc += red[sq * 128 + b2 * p + ll];
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                if (lane == 0) A.part[bbase + b2] = acc;
+            }
             ET(e_red);
         }
         if (timed) {
@@ -499,24 +541,41 @@ k_fitness_tcy(const __grid_constant__ CUtensorMap tmW, YArgs A) {
 // host side
 // ---------------------------------------------------------------------------
 
-static int y_pss(int p) { return ((p + 7) & ~7) + 2; }
-
 static int y_ipt(int p) {
     int ipt = 128 / p;
     return ipt > kYMaxIpt ? kYMaxIpt : ipt;
 }
 
-size_t tcy_smem_bytes(int p, int npad) {
+static size_t y_fixed_bytes(int p, int npad) {  // everything but the W ring
     const int ipt = y_ipt(p);
-    size_t b = 1024 + (size_t)kYStages * kYStageBytes;
-    b += 2 * y_T_bytes(ipt, p, y_pss(p)) + 2 * y_C_bytes(ipt, npad) + 2 * y_O_bytes(ipt, npad);
-    b += 4 * 128 * 8 + (2 * kYStages + 5) * 8 + 16;
-    return b;
+    return 1024 + 2 * y_C_bytes(ipt, npad) + (size_t)p * 512 + 4 * 128 * 8 +
+           (2 * kYMaxStages + 12) * 8 + 16;
+}
+
+// W ring depth: as deep as shared memory allows (TMA latency from L2 under load
+// is well above the few hundred cycles one stage's MMAs take)
+static int y_kbs() {
+    const char* e = getenv("HUBGPU_TCY_KBS");  // tuning override
+    const int k = e ? atoi(e) : 4;
+    return k >= 1 && k <= 8 ? k : 4;
+}
+
+static int y_stages(int p, int npad) {
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)y_fixed_bytes(p, npad);
+    int64_t s = room / ((int64_t)y_kbs() * kYStageBytes);
+    if (s > kYMaxStages) s = kYMaxStages;
+    const char* e = getenv("HUBGPU_TCY_STAGES");  // tuning override (shallower only)
+    if (e && atoi(e) >= 2 && atoi(e) < s) s = atoi(e);
+    return (int)s;
+}
+
+size_t tcy_smem_bytes(int p, int npad) {
+    return y_fixed_bytes(p, npad) + (size_t)y_stages(p, npad) * y_kbs() * kYStageBytes;
 }
 
 bool tcy_supported(int n, int p, int npad) {
     return p >= 1 && p <= 128 && round_up(n, 128) <= 1024 && npad <= 1024 &&
-           tcy_smem_bytes(p, npad) <= 227 * 1024;
+           y_stages(p, npad) >= 2;
 }
 
 static int g_tcy_clusters = 0;  // co-resident clusters (cudaOccupancyMaxActiveClusters)
@@ -557,7 +616,8 @@ int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint
     A.units = ceil_div(B, A.ipt);
     A.IT = (int)(round_up(I.n, 128) / 128);
     A.acols = A.IT * 32;
-    A.pss = y_pss(I.p);
+    A.stages = y_stages(I.p, I.npad);
+    A.kbs = y_kbs();
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     A.timing = tc_timing_buffer();
     {
