@@ -155,6 +155,12 @@ int scratch_pop(hg_inst* inst, int64_t B, hg_pop** out) {
     return HG_OK;
 }
 
+// the u16 column offsets K2 can emit are read only by the fp64 K3
+static bool fitness_is_tc(const hg_inst* inst) {
+    return inst->fit_kind == HG_FIT_TENSOR || (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok);
+}
+static uint16_t* co_for(const hg_inst* inst, uint16_t* co) { return fitness_is_tc(inst) ? nullptr : co; }
+
 // K3 (fp64 gather) or K3-TC (tensor cores) + finalise, by the instance's choice
 int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* co,
                   const uint32_t* T, double* part, const double* legs, double* out) {
@@ -184,9 +190,11 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
     if (alloc32)
-        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, P->co, P->T, P->legs, s));
+        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, co_for(inst, P->co), P->T,
+                                 P->legs, s));
     else
-        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, P->legs, nullptr, s));
+        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, co_for(inst, P->co), P->T, P->legs, nullptr,
+                               s));
     HG_CUDA(cudaEventRecord(P->ev0, s));
     HG_TRY(queue_fitness(inst, B, P->cl, P->co, P->T, P->part, P->legs, P->out));
     HG_CUDA(cudaEventRecord(P->ev1, s));
@@ -361,20 +369,6 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             rc = launch_transpose(inst->dC, inst->dCt, n, s);
             if (rc) break;
         }
-        {
-            // 16-bit monotone quantisation of Ct: exact pre-filter for allocation
-            double cmin = dist[0], cmax = dist[0];
-            for (size_t x = 1; x < nn; ++x) {
-                cmin = dist[x] < cmin ? dist[x] : cmin;
-                cmax = dist[x] > cmax ? dist[x] : cmax;
-            }
-            const double scale = cmax > cmin ? 65535.0 / (cmax - cmin) : 0.0;
-            // padded by 8*256 entries: K2 reads 8 strided nodes per hub row unguarded
-            chk(cudaMalloc(&inst->dCq, (nn + 2048) * sizeof(uint16_t)), "cudaMalloc(Cq)");
-            if (rc) break;
-            rc = launch_quantize(inst->dCt, inst->dCq, (int64_t)nn, cmin, scale, s);
-            if (rc) break;
-        }
         inst->flags = (sym ? HG_FLAG_SYMMETRIC : 0) | (exact ? HG_FLAG_WEIGHTS_EXACT : 0);
 
         DevInst& I = inst->I;
@@ -393,7 +387,6 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.D = inst->dD;
         I.wOD = inst->dwOD;
         I.rank = inst->drank;
-        I.Cq = inst->dCq;
         chk(cudaMalloc(&inst->derr, sizeof(int)), "cudaMalloc(err)");
         chk(cudaMemsetAsync(inst->derr, 0, sizeof(int), s), "memset(err)");
         I.err = inst->derr;
@@ -402,7 +395,32 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         int64_t q = inst->plan.tr > inst->plan.tc ? inst->plan.tr : inst->plan.tc;
         if (q < 128) q = 128;  // K3-TC reads 128-wide K blocks of cluster ids
         I.npad = (int)round_up(n, q);
+        {
+            // 16-bit monotone quantisation of Ct: exact pre-filter for allocation
+            double cmin = dist[0], cmax = dist[0];
+            for (size_t x = 1; x < nn; ++x) {
+                cmin = dist[x] < cmin ? dist[x] : cmin;
+                cmax = dist[x] > cmax ? dist[x] : cmax;
+            }
+            const double scale = cmax > cmin ? 65535.0 / (cmax - cmin) : 0.0;
+            // rows padded with 0xFFFF to nq = npad (K2 reads whole passes of
+            // nodes unguarded), plus slack for the tail of the last row
+            const int nq = I.npad;
+            chk(cudaMalloc(&inst->dCq, ((size_t)n * nq + 2048) * sizeof(uint16_t)),
+                "cudaMalloc(Cq)");
+            if (rc) break;
+            chk(cudaMemsetAsync(inst->dCq, 0xff, ((size_t)n * nq + 2048) * sizeof(uint16_t), s),
+                "memset(Cq)");
+            if (rc) break;
+            rc = launch_quantize(inst->dCt, inst->dCq, n, nq, cmin, scale, s);
+            if (rc) break;
+            I.Cq = inst->dCq;
+            I.nq = nq;
+            if (rc) break;
+        }
         rc = prepare_fitness(inst->plan);
+        if (rc) break;
+        rc = prepare_allocate(I);
         if (rc) break;
         // K3-TC eligibility: every flow an integer in [0, 255] -> exact u8 GEMM
         bool u8 = tc_supported(p);
@@ -790,8 +808,8 @@ int ga_queue_generation(hg_ga* ga) {
     HG_TRY(launch_mut_scan(G, s));
     HG_TRY(launch_mutate(G, s));
     HG_TRY(launch_correct(inst->I, ga->B, G.kids, 2 * G.p, G.khubs, s));
-    HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->co, ga->pop->T,
-                           ga->pop->legs, nullptr, s));
+    HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, co_for(inst, ga->pop->co),
+                           ga->pop->T, ga->pop->legs, nullptr, s));
     HG_TRY(queue_fitness(inst, ga->B, ga->pop->cl, ga->pop->co, ga->pop->T, ga->pop->part,
                          ga->pop->legs, ga->pop->out));
     HG_TRY(launch_select(G, s));

@@ -72,7 +72,9 @@ struct DevInst {
     const int32_t* rank;
     // Ct quantised monotonically to 16 bits: Cq = min(65535, floor((Ct - cmin) * s)).
     // q(a) < q(b) implies a < b, so it filters the allocation argmin exactly.
+    // Rows are nq = round_up(n, 8) entries (16-byte aligned, bulk-copyable).
     const uint16_t* Cq;
+    int nq;
     // input-validation flag of the current host call (0 = ok, else 0x7ffffffe - bad row)
     const int* err;
 };
@@ -100,8 +102,9 @@ int launch_idx_in(const int64_t* src, int32_t* dst, int64_t count, int n, int* e
 int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s);
 int launch_transpose(const double* src, double* dst, int n, cudaStream_t s);
 int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s);
-int launch_quantize(const double* Ct, uint16_t* Cq, int64_t count, double cmin, double scale,
+int launch_quantize(const double* Ct, uint16_t* Cq, int n, int nq, double cmin, double scale,
                     cudaStream_t s);
+int prepare_allocate(const DevInst& I);
 int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
                     uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s);
 int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,

@@ -131,19 +131,26 @@ __global__ void k_check_symmetric(const double* __restrict__ C, int n, int* flag
 
 // monotone 16-bit quantisation (x - cmin) * scale, floored and clamped: both
 // IEEE operations are monotone non-decreasing, so q(a) < q(b) => a < b
-__global__ void k_quantize(const double* __restrict__ Ct, uint16_t* __restrict__ Cq, int64_t m,
+__global__ void k_quantize(const double* __restrict__ Ct, uint16_t* __restrict__ Cq, int n, int nq,
                            double cmin, double scale) {
+    const int64_t m = (int64_t)n * nq;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
          x += (int64_t)gridDim.x * blockDim.x) {
-        double v = floor((Ct[x] - cmin) * scale);
+        const int64_t h = x / nq;
+        const int i = (int)(x - h * nq);
+        if (i >= n) {
+            Cq[x] = 0xFFFFu;  // row padding (never a minimum: masked by the readers)
+            continue;
+        }
+        double v = floor((Ct[h * n + i] - cmin) * scale);
         v = v < 0.0 ? 0.0 : (v > 65535.0 ? 65535.0 : v);
         Cq[x] = (uint16_t)v;
     }
 }
 
-int launch_quantize(const double* Ct, uint16_t* Cq, int64_t count, double cmin, double scale,
+int launch_quantize(const double* Ct, uint16_t* Cq, int n, int nq, double cmin, double scale,
                     cudaStream_t s) {
-    k_quantize<<<grid_for(count, 256), 256, 0, s>>>(Ct, Cq, count, cmin, scale);
+    k_quantize<<<grid_for((int64_t)n * nq, 256), 256, 0, s>>>(Ct, Cq, n, nq, cmin, scale);
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }
@@ -188,9 +195,9 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch
 
 // ----------------------------------------------------------------------------
 // K2 -- nearest-hub allocation (hm/model.py:202-207)
-//   one CTA per individual; thread owns nodes i = tid, tid+NT, ...;
-//   argmin over the p hubs reads Ct[h][i] (coalesced in i), strict '<' keeps
-//   the first (lowest-index) minimum, then a hub node is forced onto itself.
+//   one CTA per individual; the argmin over the p hubs reads the 16-bit
+//   quantised rows Cq[h][i] (coalesced in i), keeps the first (lowest-index)
+//   minimum, then a hub node is forced onto itself.
 //   Emits the cluster ids, the per-individual hub-cost table T and the two
 //   spoke-leg sums.
 // ----------------------------------------------------------------------------
@@ -212,85 +219,115 @@ __device__ __forceinline__ void write_T(const DevInst& I, const int32_t* hs, uin
     }
 }
 
+// Thread t owns the 4 consecutive nodes 4t..4t+3 of each 1024-node pass: one
+// 8-byte load of quantised costs per hub row.  Per node and hub the argmin is
+// 4 integer ops: key = (q << 8) | k by one byte permute, then the two
+// smallest keys (m1, m2) by min/max.  m1 is the first hub at the minimal
+// quantised cost; a second hub at that same q (m2's q equal) is a quantised
+// tie, resolved on the fp64 costs (first minimum, as the reference's argmin).
+// Quantised rows are padded to npad with 0xFFFF, so no node masks are needed.
+constexpr int kAllocNodes = 4 * kAllocThreads;  // nodes per pass
+
+__device__ __forceinline__ void min2(unsigned& m1, unsigned& m2, unsigned key) {
+    m2 = min(m2, max(m1, key));
+    m1 = min(m1, key);
+}
+
 __global__ void __launch_bounds__(kAllocThreads)
 k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
            uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
            int32_t* __restrict__ alloc) {
-    constexpr int NPT = 4;  // nodes per thread per pass (i, i+256, ...)
     __shared__ int32_t hs[kMaxP + 1];
     __shared__ double scratch[2 * (kAllocThreads / 32)];
-    const int n = I.n, p = I.p;
+    const int n = I.n, p = I.p, nq = I.nq;
     const int64_t b = blockIdx.x;
     const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
     for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = bad ? k : hubs[b * p + k];
     __syncthreads();
-
     double so = 0.0, sd = 0.0;
     uint8_t* clb = cl + b * I.npad;
-    uint16_t* cob = co + b * I.npad;
-    for (int base = 0; base < I.npad; base += kAllocThreads * NPT) {
-        const int i0 = base + threadIdx.x;
-        unsigned qmin[NPT];
-        int bk[NPT], ties[NPT];
+    for (int base = 0; base < I.npad; base += kAllocNodes) {
+        const int i0 = base + 4 * threadIdx.x;
+        if (i0 >= I.npad) break;
+        unsigned m1[4], m2[4];
 #pragma unroll
-        for (int t = 0; t < NPT; ++t) {
-            qmin[t] = 0xFFFFFFFFu;
-            bk[t] = 0;
-            ties[t] = 0;
-        }
-        // exact argmin through the monotone 16-bit pre-filter: the fp64
-        // minimum is among the hubs tied at the minimal quantised value
-        // Cq rows are padded (allocation + npad) so the NPT loads of a hub row are
-        // issued unconditionally and batched; out-of-range nodes are masked
-        for (int k = 0; k < p; ++k) {
-            const uint16_t* row = I.Cq + (size_t)hs[k] * n + i0;
-            unsigned q[NPT];
+        for (int t = 0; t < 4; ++t) m1[t] = m2[t] = 0xFFFFFFFFu;
+        const uint16_t* col = I.Cq + i0;
+        int k = 0;
+        for (; k + 4 <= p; k += 4) {
+            uint2 v[4];
 #pragma unroll
-            for (int t = 0; t < NPT; ++t) q[t] = row[t * kAllocThreads];
+            for (int u = 0; u < 4; ++u)
+                v[u] = __ldg(reinterpret_cast<const uint2*>(col + (size_t)hs[k + u] * nq));
 #pragma unroll
-            for (int t = 0; t < NPT; ++t) {
-                const unsigned qt = (i0 + t * kAllocThreads < n) ? q[t] : 0xFFFFFFFEu;
-                ties[t] = (qt == qmin[t]) ? 1 : (qt < qmin[t] ? 0 : ties[t]);
-                bk[t] = qt < qmin[t] ? k : bk[t];
-                qmin[t] = qt < qmin[t] ? qt : qmin[t];
+            for (int u = 0; u < 4; ++u) {
+                const unsigned kk = (unsigned)(k + u);
+                min2(m1[0], m2[0], __byte_perm(v[u].x, kk, 0x5104));
+                min2(m1[1], m2[1], __byte_perm(v[u].x, kk, 0x5324));
+                min2(m1[2], m2[2], __byte_perm(v[u].y, kk, 0x5104));
+                min2(m1[3], m2[3], __byte_perm(v[u].y, kk, 0x5324));
             }
         }
+        for (; k < p; ++k) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(col + (size_t)hs[k] * nq));
+            const unsigned kk = (unsigned)k;
+            min2(m1[0], m2[0], __byte_perm(v.x, kk, 0x5104));
+            min2(m1[1], m2[1], __byte_perm(v.x, kk, 0x5324));
+            min2(m1[2], m2[2], __byte_perm(v.y, kk, 0x5104));
+            min2(m1[3], m2[3], __byte_perm(v.y, kk, 0x5324));
+        }
+        // fp64 cost of each node's quantised argmin, and its weights (all loads first)
+        double best[4], ow[4], dw[4];
 #pragma unroll
-        for (int t = 0; t < NPT; ++t) {
-            const int i = i0 + t * kAllocThreads;
-            if (i >= I.npad) break;
-            int c = 0;
-            if (i < n) {
-                int kk = bk[t];
-                double best = I.Ct[(size_t)hs[kk] * n + i];
-                if (ties[t]) {  // resolve in fp64, first minimum among the tied hubs
-                    for (int k = kk + 1; k < p; ++k) {
-                        const int h = hs[k];
-                        if (I.Cq[(size_t)h * n + i] != qmin[t]) continue;
-                        const double d = I.Ct[(size_t)h * n + i];
-                        if (d < best) {
-                            best = d;
-                            kk = k;
-                        }
+        for (int t = 0; t < 4; ++t) {
+            const int i = i0 + t;
+            const bool in = i < n;
+            best[t] = in ? I.Ct[(size_t)hs[m1[t] & 0xffu] * n + i] : 0.0;
+            ow[t] = in ? I.O[i] : 0.0;
+            dw[t] = in ? I.D[i] : 0.0;
+        }
+        int c4[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = i0 + t;
+            int kk = (int)(m1[t] & 0xffu);
+            if (i < n && (m2[t] >> 8) == (m1[t] >> 8)) {
+                // quantised tie: first fp64 minimum among the hubs at q = qmin
+                const unsigned qmin = m1[t] >> 8;
+                for (int k2 = kk + 1; k2 < p; ++k2) {
+                    if (I.Cq[(size_t)hs[k2] * nq + i] != qmin) continue;
+                    const double d = I.Ct[(size_t)hs[k2] * n + i];
+                    if (d < best[t]) {
+                        best[t] = d;
+                        kk = k2;
                     }
                 }
-                // a hub's own row attains the minimum 0 (C[h][h] == 0), so its leg
-                // is 0 whichever hub the argmin picked; its cluster is fixed below
-                so += I.O[i] * best;
-                sd += I.D[i] * best;
-                c = kk;
-                if (alloc) alloc[b * n + i] = hs[kk];
             }
-            clb[i] = (uint8_t)c;
-            cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
+            // a hub's own row attains the minimum 0 (C[h][h] == 0), so its leg
+            // is 0 whichever hub the argmin picked; its cluster is fixed below
+            so = fma(ow[t], best[t], so);
+            sd = fma(dw[t], best[t], sd);
+            c4[t] = i < n ? kk : 0;
         }
+        // npad is a multiple of 16: the 4 cluster ids are one aligned word
+        *reinterpret_cast<uint32_t*>(clb + i0) =
+            (uint32_t)c4[0] | ((uint32_t)c4[1] << 8) | ((uint32_t)c4[2] << 16) |
+            ((uint32_t)c4[3] << 24);
+        if (co)  // byte offsets of the columns in a T plane row (fp64 K3 only)
+            *reinterpret_cast<uint2*>(co + b * I.npad + i0) =
+                make_uint2((uint32_t)(c4[0] * 4) | ((uint32_t)(c4[1] * 4) << 16),
+                           (uint32_t)(c4[2] * 4) | ((uint32_t)(c4[3] * 4) << 16));
+        if (alloc)
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (i0 + t < n) alloc[b * n + i0 + t] = hs[c4[t]];
     }
     __syncthreads();
     // hubs serve themselves (hm/model.py:206)
     for (int k = threadIdx.x; k < p; k += kAllocThreads) {
         const int h = hs[k];
         clb[h] = (uint8_t)k;
-        cob[h] = (uint16_t)(k * 4);
+        if (co) co[b * I.npad + h] = (uint16_t)(k * 4);
         if (alloc) alloc[b * n + h] = h;
     }
     write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
@@ -300,6 +337,8 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
         legs[2 * b + 1] = sd;
     }
 }
+
+int prepare_allocate(const DevInst&) { return HG_OK; }
 
 int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
                     uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s) {
@@ -340,7 +379,7 @@ k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restr
             sd += I.D[i] * leg;
         }
         clb[i] = (uint8_t)c;
-        cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
+        if (co) cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
     }
     write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
     block_sum2<kAllocThreads>(so, sd, scratch);

@@ -193,7 +193,7 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
             unsigned qmin = 0xFFFFFFFFu;
             for (int k = 0; k < h; ++k) {
                 const int hk = H[k];
-                const unsigned q = I.Cq[(size_t)hk * n + i];
+                const unsigned q = I.Cq[(size_t)hk * I.nq + i];
                 if (q < qmin) {
                     qmin = q;
                     bk = k;
@@ -206,7 +206,7 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
             if (ties) {
                 double best = I.Ct[(size_t)H[bk] * n + i];
                 for (int k = bk + 1; k < h; ++k) {
-                    if (I.Cq[(size_t)H[k] * n + i] != qmin) continue;
+                    if (I.Cq[(size_t)H[k] * I.nq + i] != qmin) continue;
                     const double d = I.Ct[(size_t)H[k] * n + i];
                     if (d < best) {
                         best = d;
