@@ -33,6 +33,12 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "fitness evals/sec at n=1000,p=20 (1-8 B200); GA time-to-best-cost vs CPU ref"
+KERNEL_NAMES = {
+    "tensor-pair": "k_fitness_tcp (K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs + integer bins)",
+    "tensor-tmem": "k_fitness_tcy (K3-TC/Y: u8 one-hot GEMM, one-hot in TMEM + integer bins)",
+    "tensor-smem": "k_fitness_tc (K3-TC/X: u8 one-hot GEMM, one-hot in smem + fp64 epilogue)",
+    "fp64": "k_fitness (K3: fp64 smem gather)",
+}
 N, P, SEED, FACTORS = 1000, 20, 1704, (1.0, 0.75, 1.0)
 POP = 8192
 HBM_FALLBACK = 6650.0
@@ -307,14 +313,20 @@ def run_gpu(args):
     # peak, taken as 2x the measured dense bf16 GEMM peak (nominal ratio)
     bf16 = peaks_bf16()
     tensor_ops = POP * 2.0 * N * N * P
-    # the fp64 gather kernel (K3) on the same population, for comparison
-    dinst.set_fitness(hg._lib.FIT_FP64)
-    with torch.cuda.stream(stream):
-        fp64_ms = []
-        for _ in range(3):
-            flush.zero_()
-            popd.evaluate(POP)
-            fp64_ms.append(popd.last_fitness_ms())
+    # every other K3 variant on the same population, for comparison
+    variant_ms = {}
+    for name in ("fp64", "tensor-smem", "tensor-tmem", "tensor-pair"):
+        try:
+            dinst.set_fitness(hg._lib.FIT_NAMES[name])
+        except ValueError:
+            continue
+        with torch.cuda.stream(stream):
+            ms = []
+            for _ in range(3):
+                flush.zero_()
+                popd.evaluate(POP)
+                ms.append(popd.last_fitness_ms())
+        variant_ms[name] = float(np.median(ms))
     dinst.set_fitness(hg._lib.FIT_AUTO)
 
     # e2e through the public API with pinned host buffers
@@ -378,8 +390,7 @@ def run_gpu(args):
                        "l2": "flushed between steps (256 MiB write, untimed)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
-                         "kernel": ("k_fitness_tc (K3-TC, tcgen05 u8)" if fit_kernel == "tensor"
-                                    else "k_fitness (K3, fp64 gather)"),
+                         "kernel": KERNEL_NAMES[fit_kernel],
                          "kernel_ms": fit_avg,
                          "alg_bytes_per_launch": alg_bytes, "peak_source": hbm_src,
                          "note": "SURVEY 8(d): 8n^2+4n bytes charged per eval; W is read "
@@ -390,8 +401,7 @@ def run_gpu(args):
                                     "frac": tensor_ops / (fit_avg * 1e-3) / 1e12 / (2.0 * bf16),
                                     "peak_source": "2x measured dense bf16 (nominal int8 ratio)"}},
             "kernels_ms": {"k3_selected": fit_kernel, "k3": fit_avg,
-                           "k3_fp64_gather": float(np.mean(fp64_ms)),
-                           "step_total": ms_per_step},
+                           "k3_variants": variant_ms, "step_total": ms_per_step},
             "e2e": {"value": e2e_value, "unit": "evals/s",
                     "h2d_bytes_per_step": int(pop_host.nbytes),
                     "d2h_bytes_per_step": int(res.nbytes),

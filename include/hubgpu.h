@@ -46,7 +46,10 @@ extern "C" {
 /* fitness kernel choice (hg_instance_set_fitness) */
 #define HG_FIT_AUTO 0      /* tensor cores when exact, else the fp64 gather   */
 #define HG_FIT_FP64 1      /* K3: fp64 smem-gather kernel (any flows)          */
-#define HG_FIT_TENSOR 2    /* K3-TC: u8 tcgen05 GEMM + fp64 epilogue           */
+#define HG_FIT_TENSOR 2    /* the fastest tensor-core variant this instance has */
+#define HG_FIT_TC_SMEM 3   /* K3-TC/X: one-hot B in smem, any n <= 32768       */
+#define HG_FIT_TC_TMEM 4   /* K3-TC/Y: one-hot A in TMEM, one CTA, n <= 1024  */
+#define HG_FIT_TC_PAIR 5   /* K3-TC/P: K3-TC/Y on CTA pairs (cta_group::2)   */
 
 typedef struct hg_inst hg_inst;
 typedef struct hg_pop hg_pop;
@@ -71,6 +74,7 @@ int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags);
  * GA objects created afterwards (both give the same values within fp64
  * summation-order rounding) */
 int hg_instance_set_fitness(hg_inst* inst, int kind);
+/* the kernel the next evaluation will run: HG_FIT_FP64 or one of HG_FIT_TC_* */
 int hg_instance_fitness(const hg_inst* inst, int* kind);
 /* the cudaStream_t all device work of this instance is queued on */
 int hg_instance_stream(const hg_inst* inst, void** stream);

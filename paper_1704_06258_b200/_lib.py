@@ -21,7 +21,9 @@ LIB_PATH = Path(__file__).resolve().parent / "libhubgpu.so"
 HG_OK, HG_EARG, HG_ECUDA, HG_ENODEV, HG_ESTATE = 0, 1, 2, 3, 4
 HG_HOST, HG_DEVICE = 0, 1
 FLAG_SYMMETRIC, FLAG_WEIGHTS_EXACT, FLAG_TENSOR_OK = 1, 2, 4
-FIT_AUTO, FIT_FP64, FIT_TENSOR = 0, 1, 2
+FIT_AUTO, FIT_FP64, FIT_TENSOR, FIT_TC_SMEM, FIT_TC_TMEM, FIT_TC_PAIR = 0, 1, 2, 3, 4, 5
+FIT_NAMES = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR,
+             "tensor-smem": FIT_TC_SMEM, "tensor-tmem": FIT_TC_TMEM, "tensor-pair": FIT_TC_PAIR}
 
 _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
@@ -124,16 +126,17 @@ def device_count() -> int:
 
 _device = int(os.environ.get("HUBGPU_DEVICE", os.environ.get("LOCAL_RANK", "0")))
 # transfer-term kernel for new device instances: auto (tensor cores when the
-# flows allow the exact u8 GEMM), fp64 (K3 gather) or tensor (K3-TC)
-_fit_default = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR}[
-    os.environ.get("HUBGPU_FITNESS", "auto")]
+# flows allow the exact u8 GEMM), fp64 (K3 gather), tensor (the fastest K3-TC
+# variant) or one variant by name (tensor-smem / tensor-tmem / tensor-pair)
+_fit_default = FIT_NAMES[os.environ.get("HUBGPU_FITNESS", "auto")]
 
 
 def set_fitness_default(kind: str) -> None:
-    """'auto' | 'fp64' | 'tensor' for device instances created from now on
-    ('tensor' falls back to fp64 where the flows are not u8 integers)."""
+    """A FIT_NAMES key for device instances created from now on (a tensor-core
+    choice the instance cannot run -- flows not u8 integers, or n too large for
+    the TMEM variants -- leaves it on 'auto')."""
     global _fit_default
-    _fit_default = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR}[kind]
+    _fit_default = FIT_NAMES[kind]
 
 
 def set_device(index: int) -> None:
@@ -178,8 +181,13 @@ class DeviceInstance:
         n_, p_, flags = C.c_int(), C.c_int(), C.c_int()
         check(lib.hg_instance_info(h, C.byref(n_), C.byref(p_), C.byref(flags)))
         self.flags = flags.value
-        if _fit_default == FIT_FP64 or (_fit_default == FIT_TENSOR and self.flags & FLAG_TENSOR_OK):
+        if _fit_default == FIT_FP64:
             self.set_fitness(_fit_default)
+        elif _fit_default != FIT_AUTO and self.flags & FLAG_TENSOR_OK:
+            try:
+                self.set_fitness(_fit_default)
+            except ValueError:
+                pass  # this variant does not fit the instance: keep auto
 
     def set_fitness(self, kind: int) -> None:
         check(load().hg_instance_set_fitness(self.handle, int(kind)))
@@ -188,7 +196,7 @@ class DeviceInstance:
     def fitness_kernel(self) -> str:
         k = C.c_int()
         check(load().hg_instance_fitness(self.handle, C.byref(k)))
-        return {FIT_FP64: "fp64", FIT_TENSOR: "tensor"}[k.value]
+        return {v: n for n, v in FIT_NAMES.items()}[k.value]
 
     @property
     def stream(self) -> int:

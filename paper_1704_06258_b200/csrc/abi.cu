@@ -66,9 +66,12 @@ struct hg_inst {
     std::atomic<int> refs{1};  // the handle itself + every hg_pop / hg_ga built on it
     alignas(64) unsigned char wmap[128];  // CUtensorMap of W8 (K3-TC), 128-row boxes
     alignas(64) unsigned char wmapq[128]; // same, 128/kTcyCluster-row boxes (K3-TC/Y multicast)
+    alignas(64) unsigned char wmapp[128]; // same, 64-row boxes (K3-TC/P: half a tile per CTA)
     uint8_t* dW8 = nullptr;                // u8 copy of W, [npad_tc][npad_tc], when exact
     bool tc_ok = false;                    // flows are integers in [0, 255] and p fits
+    bool tcx_ok = false;                   // ... and the smem one-hot kernel fits (p)
     bool tcy_ok = false;                   // ... and n <= 1024: one-hot resident in TMEM
+    bool tcp_ok = false;                   // ... and the CTA-pair (cta_group::2) kernel
     int fit_kind = HG_FIT_AUTO;
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -155,24 +158,33 @@ int scratch_pop(hg_inst* inst, int64_t B, hg_pop** out) {
     return HG_OK;
 }
 
-// the u16 column offsets K2 can emit are read only by the fp64 K3
-static bool fitness_is_tc(const hg_inst* inst) {
-    return inst->fit_kind == HG_FIT_TENSOR || (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok);
+// the concrete K3 kernel for the instance's choice: HG_FIT_FP64 or HG_FIT_TC_*
+static int fitness_kernel(const hg_inst* inst) {
+    int k = inst->fit_kind;
+    if (k == HG_FIT_AUTO) k = inst->tc_ok ? HG_FIT_TENSOR : HG_FIT_FP64;
+    if (k == HG_FIT_TENSOR)
+        k = inst->tcp_ok ? HG_FIT_TC_PAIR : inst->tcy_ok ? HG_FIT_TC_TMEM : HG_FIT_TC_SMEM;
+    return k;
 }
-static uint16_t* co_for(const hg_inst* inst, uint16_t* co) { return fitness_is_tc(inst) ? nullptr : co; }
+// the u16 column offsets K2 can emit are read only by the fp64 K3
+static uint16_t* co_for(const hg_inst* inst, uint16_t* co) {
+    return fitness_kernel(inst) == HG_FIT_FP64 ? co : nullptr;
+}
 
 // K3 (fp64 gather) or K3-TC (tensor cores) + finalise, by the instance's choice
 int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* co,
                   const uint32_t* T, double* part, const double* legs, double* out) {
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
-    const bool tc = inst->fit_kind == HG_FIT_TENSOR ||
-                    (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok);
+    const int kind = fitness_kernel(inst);
     int tiles;
-    if (tc && inst->tcy_ok) {
+    if (kind == HG_FIT_TC_PAIR) {
+        HG_TRY(launch_fitness_tcp(I, inst->wmapp, B, cl, T, part, inst->sm_count, s));
+        tiles = 1;
+    } else if (kind == HG_FIT_TC_TMEM) {
         HG_TRY(launch_fitness_tcy(I, inst->wmapq, B, cl, T, part, inst->sm_count, s));
         tiles = 1;
-    } else if (tc) {
+    } else if (kind == HG_FIT_TC_SMEM) {
         HG_TRY(launch_fitness_tc(I, inst->wmap, B, cl, T, part, inst->sm_count, s));
         tiles = tc_tiles(I.n);
     } else {
@@ -423,7 +435,7 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         rc = prepare_allocate(I);
         if (rc) break;
         // K3-TC eligibility: every flow an integer in [0, 255] -> exact u8 GEMM
-        bool u8 = tc_supported(p);
+        bool u8 = p >= 1 && p <= 128;
         for (size_t x = 0; u8 && x < nn; ++x) {
             const double v = flow[x];
             if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v))) u8 = false;
@@ -440,15 +452,25 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             if (rc) break;
             rc = tc_make_wmap(inst->dW8, nt, 128 / kTcyCluster, inst->wmapq);
             if (rc) break;
-            rc = prepare_fitness_tc(p);
-            if (rc) break;
-            inst->tc_ok = true;
-            const char* var = getenv("HUBGPU_TC_VARIANT");  // tuning override: "x" | "y"
+            if (tc_supported(p)) {
+                rc = prepare_fitness_tc(p);
+                if (rc) break;
+                inst->tcx_ok = true;
+            }
+            const char* var = getenv("HUBGPU_TC_VARIANT");  // tuning override: "x" | "y" | "p"
             if (tcy_supported(n, p, I.npad) && !(var && var[0] == 'x')) {
                 rc = prepare_fitness_tcy(p, I.npad);
                 if (rc) break;
                 inst->tcy_ok = true;
             }
+            if (tcp_supported(n, p, I.npad) && !(var && (var[0] == 'x' || var[0] == 'y'))) {
+                rc = tc_make_wmap(inst->dW8, nt, 64, inst->wmapp);
+                if (rc) break;
+                rc = prepare_fitness_tcp(p, I.npad);
+                if (rc) break;
+                inst->tcp_ok = true;
+            }
+            inst->tc_ok = inst->tcx_ok || inst->tcy_ok || inst->tcp_ok;
         }
         chk(cudaStreamSynchronize(s), "sync");
     } while (0);
@@ -501,19 +523,22 @@ int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags) {
 
 int hg_instance_set_fitness(hg_inst* inst, int kind) {
     HG_ARG(inst != nullptr, "instance is NULL");
-    HG_ARG(kind == HG_FIT_AUTO || kind == HG_FIT_FP64 || kind == HG_FIT_TENSOR,
-           "unknown fitness kernel %d", kind);
-    HG_ARG(kind != HG_FIT_TENSOR || inst->tc_ok,
+    HG_ARG(kind >= HG_FIT_AUTO && kind <= HG_FIT_TC_PAIR, "unknown fitness kernel %d", kind);
+    HG_ARG(kind < HG_FIT_TENSOR || inst->tc_ok,
            "tensor-core fitness needs integer flows in [0, 255] and p <= 128");
+    HG_ARG(kind != HG_FIT_TC_SMEM || inst->tcx_ok,
+           "the smem one-hot tensor-core kernel does not fit p = %d", inst->I.p);
+    HG_ARG(kind != HG_FIT_TC_TMEM || inst->tcy_ok,
+           "the TMEM-resident tensor-core kernel needs n <= 1024 (and was not disabled)");
+    HG_ARG(kind != HG_FIT_TC_PAIR || inst->tcp_ok,
+           "the CTA-pair tensor-core kernel needs n <= 1024 (and was not disabled)");
     inst->fit_kind = kind;
     return HG_OK;
 }
 
 int hg_instance_fitness(const hg_inst* inst, int* kind) {
     HG_ARG(inst && kind, "NULL argument");
-    *kind = (inst->fit_kind == HG_FIT_TENSOR || (inst->fit_kind == HG_FIT_AUTO && inst->tc_ok))
-                ? HG_FIT_TENSOR
-                : HG_FIT_FP64;
+    *kind = fitness_kernel(inst);
     return HG_OK;
 }
 

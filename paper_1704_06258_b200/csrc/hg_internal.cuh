@@ -135,6 +135,12 @@ size_t tcy_smem_bytes(int p, int npad);
 int prepare_fitness_tcy(int p, int npad);
 int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
                        const uint32_t* T, double* part, int grid, cudaStream_t s);
+// K3-TC/P (k_fitness_tcp.cu): the same on CTA pairs (cta_group::2, M = 256)
+bool tcp_supported(int n, int p, int npad);
+size_t tcp_smem_bytes(int p, int npad);
+int prepare_fitness_tcp(int p, int npad);
+int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
+                       const uint32_t* T, double* part, int grid, cudaStream_t s);
 
 // ---- launchers (k_ga.cu) ---------------------------------------------------
 int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n, int nw,

@@ -38,10 +38,11 @@ def _need_gpu():
         pytest.fail("no CUDA device: the gpu tests must run on a B200")
 
 
-@pytest.fixture(params=["fp64", "tensor"])
+@pytest.fixture(params=["fp64", "tensor-smem", "tensor-tmem", "tensor-pair"])
 def kernel(request):
-    """Run a test once with the fp64 gather kernel (K3) and once with the
-    tensor-core kernel (K3-TC, used wherever the flows are u8 integers)."""
+    """Run a test with the fp64 gather kernel (K3) and with each tensor-core
+    variant (K3-TC/X, /Y, /P -- used wherever the flows are u8 integers and,
+    for /Y and /P, n <= 1024; elsewhere the instance stays on auto)."""
     from paper_1704_06258_b200 import _lib
 
     _lib.set_fitness_default(request.param)
@@ -173,24 +174,33 @@ class TestKernels:
     def test_tensor_path_is_selected_for_u8_flows(self):
         inst = hg.generate_urand(300, 20, 3, (1.0, 0.75, 1.0))
         d = inst.device()
-        assert d.flags & 4 and d.fitness_kernel == "tensor"
+        assert d.flags & 4 and d.fitness_kernel == "tensor-pair"
+        big = hg.generate_urand(1100, 20, 3, (1.0, 0.75, 1.0))
+        assert big.device().fitness_kernel == "tensor-smem"  # n > 1024: one-hot in smem
+        with pytest.raises(ValueError, match="n <= 1024"):
+            big.device().set_fitness(5)
         frac = hg.Instance(inst.n, inst.p, inst.dist, inst.flow * 0.5, 1.0, 0.75, 1.0)
         assert frac.device().fitness_kernel == "fp64"
         with pytest.raises(ValueError, match="tensor-core"):
             frac.device().set_fitness(2)
 
     @pytest.mark.parametrize("n,p", [(1000, 20), (200, 10), (129, 50), (77, 3), (256, 1),
-                                     (300, 17)])
+                                     (300, 17), (1024, 128), (640, 7)])
     def test_tensor_equals_fp64(self, n, p):
         inst = hg.generate_urand(n, p, 21, (2.0, 0.6, 1.5))
-        pop = hg.random_population(n, p, 300, key=4)
+        pop = hg.random_population(n, p, 301, key=4)  # odd: a pair's dummy unit
         d = inst.device()
-        d.set_fitness(2)
-        tc = hg.evaluate_population(inst, pop)
         d.set_fitness(1)
         fp = hg.evaluate_population(inst, pop)
-        assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
-        assert close(tc, fp, rel=1e-13)
+        for kind in (3, 4, 5):  # smem one-hot, TMEM one-hot, CTA pair
+            try:
+                d.set_fitness(kind)
+            except ValueError as e:  # the smem one-hot kernel stops short of p = 128
+                assert kind == 3 and p > 64 and "does not fit" in str(e)
+                continue
+            tc = hg.evaluate_population(inst, pop)
+            assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
+            assert close(tc, fp, rel=1e-13), kind
 
 
 class TestOperators:
