@@ -166,6 +166,20 @@ int hg_ga_draw_counters(hg_ga* ga, uint64_t* counters);
 /* kernels launched per generation */
 int hg_ga_launches_per_generation(const hg_ga* ga);
 
+/* device generator.  generate_urand (hm/io.py:188-210)
+ * bit for bit on the GPU: the SplitMix64 stream derive_stream(seed, n, p)
+ * is counter-based, so every element computes its own draws.  Fills the host
+ * arrays dist and flow (n x n row-major fp64; either may be NULL). */
+int hg_generate_urand(int device, int n, int p, uint64_t seed, double* dist, double* flow);
+
+/* restricted_optimum (hm/oracle.py:42-54) on the GPU:
+ * every p-subset in itertools.combinations order through K2+K3, keeping the
+ * first strict minimum of raw (lexicographically smallest hub set on ties).
+ * Fails (HG_EARG) when C(n, p) > limit, as EnumerationLimitError.
+ * best_hubs: p int64 (host); *count_out = C(n, p) (saturated at 2^63). */
+int hg_restricted_optimum(hg_inst* inst, uint64_t limit, int64_t* best_hubs, double* best_raw,
+                          uint64_t* count_out);
+
 #ifdef __cplusplus
 }
 #endif

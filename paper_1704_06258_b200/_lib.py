@@ -76,6 +76,8 @@ SIGNATURES = {
     "hg_ga_last_children": (C.c_int, [_vp, _i64p, _f64p]),
     "hg_ga_draw_counters": (C.c_int, [_vp, _u64p]),
     "hg_ga_launches_per_generation": (C.c_int, [_vp]),
+    "hg_generate_urand": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, _f64p, _f64p]),
+    "hg_restricted_optimum": (C.c_int, [_vp, C.c_uint64, _i64p, _f64p, _u64p]),
 }
 
 _lib = None
@@ -365,3 +367,29 @@ def swap_masks(masks: np.ndarray, r_close: np.ndarray, r_open: np.ndarray,
     check(load().hg_swap(_device if device is None else device, n, B, ptr(masks, _u8p),
                          ptr(rc, _i64p), ptr(ro, _i64p), ptr(out, _u8p)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# device generator, GPU restricted optimum
+# ---------------------------------------------------------------------------
+
+
+def generate_urand_arrays(n: int, p: int, seed: int, device: int | None = None):
+    """(dist, flow) of generate_urand(n, p, seed, .) computed on the GPU
+    (hm/io.py:188-210 bit for bit)."""
+    dist = np.empty((n, n), dtype=np.float64)
+    flow = np.empty((n, n), dtype=np.float64)
+    check(load().hg_generate_urand(_device if device is None else int(device), int(n), int(p),
+                                   int(seed) & 0xFFFFFFFFFFFFFFFF, ptr(dist, _f64p),
+                                   ptr(flow, _f64p)))
+    return dist, flow
+
+
+def restricted_optimum(dinst: "DeviceInstance", limit: int):
+    """(best hubs int64[p], best raw, C(n, p)) over every p-subset."""
+    hubs = np.empty(dinst.p, dtype=np.int64)
+    raw = C.c_double()
+    count = C.c_uint64()
+    check(load().hg_restricted_optimum(dinst.handle, int(limit), ptr(hubs, _i64p), C.byref(raw),
+                                       C.byref(count)))
+    return hubs, raw.value, count.value

@@ -1045,4 +1045,125 @@ int hg_ga_launches_per_generation(const hg_ga* ga) {
     return kGaLaunches;
 }
 
+// ---------------------------------------------------------------------------
+// device generator, GPU restricted optimum
+// ---------------------------------------------------------------------------
+
+int hg_generate_urand(int device, int n, int p, uint64_t seed, double* dist, double* flow) {
+    HG_ARG(n >= 1, "node count must be positive, got %d", n);
+    HG_ARG(p >= 1 && p <= n, "hub count p=%d outside [1, %d]", p, n);
+    HG_TRY(set_device(device));
+    const uint64_t keys[2] = {(uint64_t)n, (uint64_t)p};
+    const uint64_t s = host_stream_key(seed, keys, 2);  // derive_stream(seed, n, p)
+    const size_t nn = (size_t)n * n;
+    DevBuf xy, C, W;
+    int rc = HG_OK;
+    do {
+        if ((rc = xy.ensure(2 * (size_t)n * sizeof(double)))) break;
+        if (dist && (rc = C.ensure(nn * sizeof(double)))) break;
+        if (flow && (rc = W.ensure(nn * sizeof(double)))) break;
+        if ((rc = launch_gen_urand(s, n, xy.as<double>(), dist ? C.as<double>() : nullptr,
+                                   flow ? W.as<double>() : nullptr, 0)))
+            break;
+        cudaError_t e = cudaSuccess;
+        if (dist) e = cudaMemcpy(dist, C.ptr, nn * sizeof(double), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && flow)
+            e = cudaMemcpy(flow, W.ptr, nn * sizeof(double), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            set_error("generate_urand copy-out failed: %s", cudaGetErrorString(e));
+            rc = HG_ECUDA;
+        }
+    } while (0);
+    xy.release();
+    C.release();
+    W.release();
+    return rc;
+}
+
+// C(n, p) saturated at 2^63
+static uint64_t binom_sat(int n, int p) {
+    const uint64_t cap = 1ull << 63;
+    uint64_t c = 1;
+    for (int i = 1; i <= p; ++i) {
+        // c * (n - p + i) / i stays an integer at every step
+        const unsigned __int128 t = (unsigned __int128)c * (uint64_t)(n - p + i) / (uint64_t)i;
+        if (t >= cap) return cap;
+        c = (uint64_t)t;
+    }
+    return c;
+}
+
+int hg_restricted_optimum(hg_inst* inst, uint64_t limit, int64_t* best_hubs, double* best_raw,
+                          uint64_t* count_out) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    HG_ARG(best_hubs && best_raw, "NULL buffer");
+    HG_TRY(set_device(inst->device));
+    const DevInst& I = inst->I;
+    const int n = I.n, p = I.p;
+    const uint64_t count = binom_sat(n, p);
+    if (count_out) *count_out = count;
+    HG_ARG(count <= limit,
+           "enumeration needs %llu candidates, over the limit of %llu; raise `limit` "
+           "explicitly to allow it",
+           (unsigned long long)count, (unsigned long long)limit);
+    cudaStream_t s = inst->stream;
+    // binomial table C(a, b), a <= n, b <= p
+    std::vector<uint64_t> bt((size_t)(n + 1) * (p + 1), 0);
+    for (int x = 0; x <= n; ++x)
+        for (int y = 0; y <= p; ++y) bt[(size_t)x * (p + 1) + y] = y <= x ? binom_sat(x, y) : 0;
+    const int64_t Bb = count < (uint64_t)65536 ? (int64_t)count : 65536;
+    hg_pop* P;
+    HG_TRY(scratch_pop(inst, Bb, &P));
+    DevBuf dbt, dbest;
+    int rc = HG_OK;
+    do {
+        if ((rc = dbt.ensure(bt.size() * sizeof(uint64_t)))) break;
+        if ((rc = dbest.ensure(2 * sizeof(uint64_t)))) break;
+        cudaError_t e = cudaMemcpyAsync(dbt.ptr, bt.data(), bt.size() * sizeof(uint64_t),
+                                        cudaMemcpyHostToDevice, s);
+        const unsigned long long none[2] = {0ull, ~0ull};  // raw (unused until set), rank
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(dbest.ptr, none, sizeof(none), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(inst->derr, 0, sizeof(int), s);
+        if (e != cudaSuccess) {
+            set_error("restricted_optimum setup failed: %s", cudaGetErrorString(e));
+            rc = HG_ECUDA;
+            break;
+        }
+        double* d_raw = dbest.as<double>();
+        unsigned long long* d_rank = reinterpret_cast<unsigned long long*>(d_raw + 1);
+        for (uint64_t r0 = 0; r0 < count && rc == HG_OK; r0 += (uint64_t)Bb) {
+            rc = launch_unrank_combos(dbt.as<uint64_t>(), n, p, r0, Bb, count, P->hubs, s);
+            if (!rc) rc = pop_eval_queue(P, Bb, nullptr);
+            if (!rc) rc = launch_batch_best(P->out, Bb, r0, count, d_raw, d_rank, s);
+        }
+        if (rc) break;
+        unsigned long long hb[2];
+        e = cudaMemcpyAsync(hb, dbest.ptr, sizeof(hb), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            set_error("restricted_optimum failed: %s", cudaGetErrorString(e));
+            rc = HG_ECUDA;
+            break;
+        }
+        double raw;
+        std::memcpy(&raw, &hb[0], sizeof(raw));
+        *best_raw = raw;
+        // unrank the winner on the host (same lexicographic order)
+        uint64_t r = hb[1];
+        int x = 0;
+        for (int i = 0; i < p; ++i) {
+            for (;; ++x) {
+                const uint64_t c = (n - 1 - x >= 0) ? bt[(size_t)(n - 1 - x) * (p + 1) + (p - 1 - i)] : 0;
+                if (r < c) break;
+                r -= c;
+            }
+            best_hubs[i] = x++;
+        }
+    } while (0);
+    dbt.release();
+    dbest.release();
+    return rc;
+}
+
 }  // extern "C"

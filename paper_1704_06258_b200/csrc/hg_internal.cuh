@@ -142,6 +142,15 @@ int prepare_fitness_tcp(int p, int npad);
 int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
                        const uint32_t* T, double* part, int grid, cudaStream_t s);
 
+// ---- k_gen.cu: device generator and hub-set enumeration ---------------------
+// xy: 2n scratch; C / W: n x n (either may be null)
+int launch_gen_urand(uint64_t s, int n, double* xy, double* C, double* W, cudaStream_t st);
+// binom[a * (p+1) + b] = C(a, b), a <= n, b <= p
+int launch_unrank_combos(const uint64_t* binom, int n, int p, uint64_t rank0, int64_t B,
+                         uint64_t count, int32_t* hubs, cudaStream_t st);
+int launch_batch_best(const double* out, int64_t B, uint64_t rank0, uint64_t count,
+                      double* best_raw, unsigned long long* best_rank, cudaStream_t st);
+
 // ---- launchers (k_ga.cu) ---------------------------------------------------
 int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n, int nw,
                          cudaStream_t s);

@@ -29,19 +29,27 @@ def urand_coordinates(n: int, p: int, seed: int) -> np.ndarray:
     return derive_stream(seed, n, p).random_block(2 * n).reshape(n, 2) * COORD_RANGE
 
 
-def generate_urand(n: int, p: int, seed: int, factors) -> Instance:
+def generate_urand(n: int, p: int, seed: int, factors, device: bool = False) -> Instance:
     """Random Euclidean instance reproducible from (n, p, seed, factors):
     2n uniforms for x0 y0 x1 y1 ..., then n*n flows in [0, 100] row-major,
-    diagonal zeroed (hm/io.py:188-210)."""
+    diagonal zeroed (hm/io.py:188-210).  device=True draws and builds both
+    matrices on the GPU (k_gen.cu, the same bits; n=6000 in milliseconds
+    instead of seconds); the default keeps the host numpy path."""
     if n < 1:
         raise ValueError(f"node count must be positive, got {n}")
     if not 1 <= p <= n:
         raise ValueError(f"hub count p={p} outside [1, {n}]")
+    chi, alpha, delta = factors
+    if device:
+        from ._lib import generate_urand_arrays
+
+        dist, flow = generate_urand_arrays(n, p, seed)
+        return Instance(n=n, p=p, dist=dist, flow=flow, chi=chi, alpha=alpha, delta=delta,
+                        name=f"urand-n{n}-p{p}-s{seed}")
     st = derive_stream(seed, n, p)
     coords = st.random_block(2 * n).reshape(n, 2) * COORD_RANGE
     flow = st.randint_block(n * n, FLOW_RANGE + 1).astype(np.float64).reshape(n, n)
     np.fill_diagonal(flow, 0.0)
-    chi, alpha, delta = factors
     return Instance(n=n, p=p, dist=euclidean_distances(coords), flow=flow,
                     chi=chi, alpha=alpha, delta=delta, name=f"urand-n{n}-p{p}-s{seed}")
 

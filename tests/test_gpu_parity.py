@@ -339,3 +339,63 @@ class TestGa:
             assert rep.raw_objective == ref.raw_objective
             assert rep.trace == ref.trace
             assert rep.best_solution == ref.best_solution
+
+
+class TestNext:
+    """device generator and GPU restricted optimum."""
+
+    @pytest.mark.parametrize("idx", range(4))
+    def test_device_generator_small_bit_exact(self, idx):
+        g = golden("instances")
+        n, p, seed, *f = g[f"urand{idx}_args"]
+        inst = hg.generate_urand(int(n), int(p), int(seed), tuple(f), device=True)
+        assert np.array_equal(inst.dist, g[f"urand{idx}_dist"])
+        assert np.array_equal(inst.flow, g[f"urand{idx}_flow"])
+        assert np.array_equal(inst.middle_rank, g[f"urand{idx}_rank"])
+
+    @pytest.mark.parametrize("idx", range(2))
+    def test_device_generator_big_digest(self, idx):
+        import hashlib
+
+        g = golden("instances")
+        n, p, seed, *f = g[f"big{idx}_args"]
+        inst = hg.generate_urand(int(n), int(p), int(seed), tuple(f), device=True)
+        sha = [hashlib.sha256(inst.dist.tobytes()).hexdigest(),
+               hashlib.sha256(inst.flow.tobytes()).hexdigest()]
+        assert sha == g[f"big{idx}_sha"].tolist()
+        assert inst.total_flow == float(g[f"big{idx}_total"][0])
+
+    def test_device_generator_matches_host_at_bench_size(self):
+        a = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0), device=True)
+        b = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
+        assert np.array_equal(a.dist, b.dist) and np.array_equal(a.flow, b.flow)
+
+    @pytest.mark.parametrize("idx", range(12))
+    def test_restricted_optimum_vs_reference(self, idx, kernel):
+        g = golden("restricted")
+        inst = inst_from(g, f"r{idx}")
+        sol, raw = hg.restricted_optimum(inst)
+        assert np.array_equal(sol.hubs, g[f"r{idx}_hubs"])
+        assert close(raw, float(g[f"r{idx}_raw"][0]), rel=1e-12)
+
+    def test_restricted_optimum_multi_batch(self):
+        """C(40, 4) = 91,390 sets: two device batches; the winner and its raw
+        equal a host sweep over the same scores (itertools order, first
+        strict minimum)."""
+        import itertools
+
+        inst = hg.generate_urand(40, 4, 11, (1.0, 0.75, 1.0))
+        combos = np.array(list(itertools.combinations(range(40), 4)), dtype=np.int64)
+        raw = hg.evaluate_population(inst, combos)[:, 3]
+        sol, best = hg.restricted_optimum(inst)
+        k = int(np.argmin(raw))  # numpy argmin = first minimum
+        assert np.array_equal(sol.hubs, combos[k]) and best == raw[k]
+
+    def test_restricted_optimum_limit(self):
+        inst = hg.generate_urand(30, 5, 2, (1.0, 0.75, 1.0))
+        with pytest.raises(hg.EnumerationLimitError, match="142506 candidates"):
+            hg.restricted_optimum(inst, limit=100_000)
+        from paper_1704_06258_b200 import _lib
+
+        with pytest.raises(ValueError, match="over the limit of 10"):
+            _lib.restricted_optimum(inst.device(), 10)

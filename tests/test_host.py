@@ -160,3 +160,15 @@ class TestValidate:
         with pytest.raises(hg.InfeasibleSolutionError):
             hg.objective(inst, hg.Solution(hub=np.array([True, False, False]),
                                            alloc=np.array([0, 0, 0])))
+
+
+def test_enumeration_limit_raised_on_host():
+    """restricted_optimum checks C(n, p) against the limit before any device
+    work, with the reference's exception and message (hm/oracle.py:32-40)."""
+    inst = hg.generate_urand(30, 5, 2, (1.0, 0.75, 1.0))
+    with pytest.raises(hg.EnumerationLimitError) as e:
+        hg.restricted_optimum(inst, limit=1000)
+    assert e.value.required == 142506 and e.value.limit == 1000
+    assert str(e.value) == ("enumeration needs 142506 candidates, over the limit of 1000; "
+                            "raise `limit` explicitly to allow it")
+    assert isinstance(e.value, ValueError)
