@@ -195,9 +195,9 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch
 
 // ----------------------------------------------------------------------------
 // K2 -- nearest-hub allocation (hm/model.py:202-207)
-//   one CTA per individual; the argmin over the p hubs reads the 16-bit
+//   one WARP per individual; the argmin over the p hubs reads the 16-bit
 //   quantised rows Cq[h][i] (coalesced in i), keeps the first (lowest-index)
-//   minimum, then a hub node is forced onto itself.
+//   minimum, and a hub node is its own hub.
 //   Emits the cluster ids, the per-individual hub-cost table T and the two
 //   spoke-leg sums.
 // ----------------------------------------------------------------------------
@@ -219,14 +219,17 @@ __device__ __forceinline__ void write_T(const DevInst& I, const int32_t* hs, uin
     }
 }
 
-// Thread t owns the 4 consecutive nodes 4t..4t+3 of each 1024-node pass: one
-// 8-byte load of quantised costs per hub row.  Per node and hub the argmin is
-// 4 integer ops: key = (q << 8) | k by one byte permute, then the two
+// WARP per individual, no block barriers: the warp sweeps its individual's
+// nodes in chunks of 128 -- lane owns the 4 consecutive nodes c0+4*lane..+3,
+// one 8-byte load of quantised costs per hub row.  Per node and hub the argmin
+// is 4 integer ops: key = (q << 8) | k by one byte permute, then the two
 // smallest keys (m1, m2) by min/max.  m1 is the first hub at the minimal
-// quantised cost; a second hub at that same q (m2's q equal) is a quantised
-// tie, resolved on the fp64 costs (first minimum, as the reference's argmin).
-// Quantised rows are padded to npad with 0xFFFF, so no node masks are needed.
-constexpr int kAllocNodes = 4 * kAllocThreads;  // nodes per pass
+// quantised cost; a second hub at that same q is a quantised tie, resolved on
+// the fp64 costs (first minimum, hm/model.py:205).  A hub node's own q is 0
+// (C[h][h] = 0 = cmin), so any competing hub at q = 0 sends it down the tie
+// path, which also applies the self-allocation (hm/model.py:206).  Quantised
+// rows are padded to npad with 0xFFFF, so no node masks are needed.
+constexpr int kAllocWarps = kAllocThreads / 32;
 
 __device__ __forceinline__ void min2(unsigned& m1, unsigned& m2, unsigned key) {
     m2 = min(m2, max(m1, key));
@@ -234,38 +237,52 @@ __device__ __forceinline__ void min2(unsigned& m1, unsigned& m2, unsigned key) {
 }
 
 __global__ void __launch_bounds__(kAllocThreads)
-k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
+k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
            uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
            int32_t* __restrict__ alloc) {
-    __shared__ int32_t hs[kMaxP + 1];
-    __shared__ double scratch[2 * (kAllocThreads / 32)];
+    __shared__ int32_t hs_all[kAllocWarps][kMaxP + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * kAllocWarps + warp;
+    if (b >= B) return;
     const int n = I.n, p = I.p, nq = I.nq;
-    const int64_t b = blockIdx.x;
+    int32_t* hs = hs_all[warp];
     const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
-    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = bad ? k : hubs[b * p + k];
-    __syncthreads();
+    for (int k = lane; k < p; k += 32) hs[k] = bad ? k : hubs[b * p + k];
+    __syncwarp();
+
     double so = 0.0, sd = 0.0;
     uint8_t* clb = cl + b * I.npad;
-    for (int base = 0; base < I.npad; base += kAllocNodes) {
-        const int i0 = base + 4 * threadIdx.x;
-        if (i0 >= I.npad) break;
+    for (int c0 = 0; c0 < I.npad; c0 += 128) {
+        const int i0 = c0 + 4 * lane;
         unsigned m1[4], m2[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) m1[t] = m2[t] = 0xFFFFFFFFu;
         const uint16_t* col = I.Cq + i0;
+        const int p4 = p & ~3;
         int k = 0;
-        for (; k + 4 <= p; k += 4) {
+        if (p4) {
+            // software pipelined: the next 4 hub rows are in flight while the
+            // current 4 are reduced
             uint2 v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                v[u] = __ldg(reinterpret_cast<const uint2*>(col + (size_t)hs[k + u] * nq));
+                v[u] = __ldg(reinterpret_cast<const uint2*>(col + (size_t)hs[u] * nq));
+            for (; k < p4; k += 4) {
+                uint2 w[4];
+                const int kn = k + 4 < p4 ? k + 4 : k;  // last round: harmless reload
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const unsigned kk = (unsigned)(k + u);
-                min2(m1[0], m2[0], __byte_perm(v[u].x, kk, 0x5104));
-                min2(m1[1], m2[1], __byte_perm(v[u].x, kk, 0x5324));
-                min2(m1[2], m2[2], __byte_perm(v[u].y, kk, 0x5104));
-                min2(m1[3], m2[3], __byte_perm(v[u].y, kk, 0x5324));
+                for (int u = 0; u < 4; ++u)
+                    w[u] = __ldg(reinterpret_cast<const uint2*>(col + (size_t)hs[kn + u] * nq));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const unsigned kk = (unsigned)(k + u);
+                    min2(m1[0], m2[0], __byte_perm(v[u].x, kk, 0x5104));
+                    min2(m1[1], m2[1], __byte_perm(v[u].x, kk, 0x5324));
+                    min2(m1[2], m2[2], __byte_perm(v[u].y, kk, 0x5104));
+                    min2(m1[3], m2[3], __byte_perm(v[u].y, kk, 0x5324));
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = w[u];
             }
         }
         for (; k < p; ++k) {
@@ -291,20 +308,25 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
         for (int t = 0; t < 4; ++t) {
             const int i = i0 + t;
             int kk = (int)(m1[t] & 0xffu);
-            if (i < n && (m2[t] >> 8) == (m1[t] >> 8)) {
-                // quantised tie: first fp64 minimum among the hubs at q = qmin
+            if (i < n && (m2[t] >> 8) == (m1[t] >> 8) && hs[kk] != i) {
+                // quantised tie: first fp64 minimum among the hubs at q = qmin,
+                // except that a hub node is always its own hub
                 const unsigned qmin = m1[t] >> 8;
                 for (int k2 = kk + 1; k2 < p; ++k2) {
-                    if (I.Cq[(size_t)hs[k2] * nq + i] != qmin) continue;
-                    const double d = I.Ct[(size_t)hs[k2] * n + i];
+                    const int h = hs[k2];
+                    if (I.Cq[(size_t)h * nq + i] != qmin) continue;
+                    if (h == i) {
+                        best[t] = 0.0;
+                        kk = k2;
+                        break;
+                    }
+                    const double d = I.Ct[(size_t)h * n + i];
                     if (d < best[t]) {
                         best[t] = d;
                         kk = k2;
                     }
                 }
             }
-            // a hub's own row attains the minimum 0 (C[h][h] == 0), so its leg
-            // is 0 whichever hub the argmin picked; its cluster is fixed below
             so = fma(ow[t], best[t], so);
             sd = fma(dw[t], best[t], sd);
             c4[t] = i < n ? kk : 0;
@@ -322,17 +344,19 @@ k_allocate(DevInst I, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl
             for (int t = 0; t < 4; ++t)
                 if (i0 + t < n) alloc[b * n + i0 + t] = hs[c4[t]];
     }
-    __syncthreads();
-    // hubs serve themselves (hm/model.py:206)
-    for (int k = threadIdx.x; k < p; k += kAllocThreads) {
-        const int h = hs[k];
-        clb[h] = (uint8_t)k;
-        if (co) co[b * I.npad + h] = (uint16_t)(k * 4);
-        if (alloc) alloc[b * n + h] = h;
+    // hub-to-hub cost table T_b (warp-wide, row by row)
+    uint32_t* Tb = T + b * 2 * (int64_t)p * I.ps;
+    for (int k = 0; k < p; ++k) {
+        const double* crow = I.C + (size_t)hs[k] * n;
+        for (int l = lane; l < p; l += 32) {
+            const double v = crow[hs[l]];
+            Tb[k * I.ps + l] = (uint32_t)__double2hiint(v);
+            Tb[(p + k) * I.ps + l] = (uint32_t)__double2loint(v);
+        }
     }
-    write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
-    block_sum2<kAllocThreads>(so, sd, scratch);
-    if (threadIdx.x == 0) {
+    so = warp_sum(so);  // fixed butterfly order: deterministic
+    sd = warp_sum(sd);
+    if (lane == 0) {
         legs[2 * b] = so;
         legs[2 * b + 1] = sd;
     }
@@ -343,7 +367,8 @@ int prepare_allocate(const DevInst&) { return HG_OK; }
 int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
                     uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s) {
     if (B <= 0) return HG_OK;
-    k_allocate<<<(unsigned)B, kAllocThreads, 0, s>>>(I, hubs, cl, co, T, legs, alloc);
+    k_allocate<<<(unsigned)ceil_div(B, kAllocWarps), kAllocThreads, 0, s>>>(I, B, hubs, cl, co, T,
+                                                                         legs, alloc);
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }
