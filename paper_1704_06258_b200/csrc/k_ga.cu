@@ -141,6 +141,35 @@ __device__ int block_extract(const uint32_t* mask, int nw, int32_t* H,
     return base;
 }
 
+// position in H[0..h) of node i's hub under allocate_to_nearest
+// (hm/model.py:202-207): first fp64 minimum through the exact 16-bit
+// pre-filter (keys (q << 16) | k, two smallest kept; a second hub at the same
+// q is a tie resolved in fp64), and a hub node is its own hub (its q is 0,
+// so a competing hub at q = 0 takes the tie path, which checks for it)
+__device__ __forceinline__ int corr_nearest(const DevInst& I, const int32_t* H, int h, int i) {
+    unsigned m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+    for (int k = 0; k < h; ++k) {
+        const unsigned key = ((unsigned)I.Cq[(size_t)H[k] * I.nq + i] << 16) | (unsigned)k;
+        m2 = min(m2, max(m1, key));
+        m1 = min(m1, key);
+    }
+    int kk = (int)(m1 & 0xFFFFu);
+    if ((m2 >> 16) == (m1 >> 16) && H[kk] != i) {
+        const unsigned qmin = m1 >> 16;
+        double best = I.Ct[(size_t)H[kk] * I.n + i];
+        for (int k = kk + 1; k < h; ++k) {
+            if (I.Cq[(size_t)H[k] * I.nq + i] != qmin) continue;
+            if (H[k] == i) return k;
+            const double d = I.Ct[(size_t)H[k] * I.n + i];
+            if (d < best) {
+                best = d;
+                kk = k;
+            }
+        }
+    }
+    return kk;
+}
+
 __global__ void __launch_bounds__(kCorrThreads)
 k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __restrict__ hubs_out) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -151,7 +180,7 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
     double* carried = reinterpret_cast<double*>(sm);                 // [hmax]
     uint32_t* mask = reinterpret_cast<uint32_t*>(carried + hmax);     // [nw]
     int32_t* H = reinterpret_cast<int32_t*>(mask + nw);               // [hmax]
-    int16_t* cls = reinterpret_cast<int16_t*>(H + hmax);              // [n] (inexact weights only)
+    int16_t* cls = reinterpret_cast<int16_t*>(H + hmax);              // [n] hub position per node
 
     int cnt = 0;
     for (int w = threadIdx.x; w < nw; w += kCorrThreads) {
@@ -184,53 +213,80 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
     __syncthreads();
 
     // excess: close the least-loaded hub, one at a time (hm/operators.py:94-100)
-    while (h > p) {
-        for (int k = threadIdx.x; k < h; k += kCorrThreads) carried[k] = 0.0;
+    if (h > p && I.weights_exact) {
+        // carried loads are integer-valued: exact in any order, so the nearest
+        // allocation is computed once and afterwards only the nodes of the
+        // closed hub move (closing a hub that is not a node's first minimum
+        // leaves that node's first minimum unchanged)
+        long long* carr = reinterpret_cast<long long*>(carried);
+        for (int k = threadIdx.x; k < h; k += kCorrThreads) carr[k] = 0;
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += kCorrThreads) {
-            // first fp64 minimum over H via the exact 16-bit pre-filter (see k_allocate)
-            int bk = 0, self = -1, ties = 0;
-            unsigned qmin = 0xFFFFFFFFu;
-            for (int k = 0; k < h; ++k) {
-                const int hk = H[k];
-                const unsigned q = I.Cq[(size_t)hk * I.nq + i];
-                if (q < qmin) {
-                    qmin = q;
-                    bk = k;
-                    ties = 0;
-                } else if (q == qmin) {
-                    ++ties;
+            const int c = corr_nearest(I, H, h, i);
+            cls[i] = (int16_t)c;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&carr[c]),
+                      (unsigned long long)(long long)I.wOD[i]);
+        }
+        __syncthreads();
+        while (h > p) {
+            if (threadIdx.x < 32) {
+                // first minimum of carr[0..h)
+                long long bv = 0;
+                int bi = -1;
+                for (int k = threadIdx.x; k < h; k += 32) {
+                    const long long v = carr[k];
+                    if (bi < 0 || v < bv) {
+                        bv = v;
+                        bi = k;
+                    }
                 }
-                if (hk == i) self = k;
-            }
-            if (ties) {
-                double best = I.Ct[(size_t)H[bk] * n + i];
-                for (int k = bk + 1; k < h; ++k) {
-                    if (I.Cq[(size_t)H[k] * I.nq + i] != qmin) continue;
-                    const double d = I.Ct[(size_t)H[k] * n + i];
-                    if (d < best) {
-                        best = d;
-                        bk = k;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const long long ov = __shfl_xor_sync(kFull, bv, o);
+                    const int oi = __shfl_xor_sync(kFull, bi, o);
+                    if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) {
+                        bv = ov;
+                        bi = oi;
+                    }
+                }
+                if (threadIdx.x == 0) {
+                    s_kill = bi;
+                    // delete position bi of H and carr (np.delete keeps the order)
+                    for (int k = bi; k < h - 1; ++k) {
+                        H[k] = H[k + 1];
+                        carr[k] = carr[k + 1];
                     }
                 }
             }
-            if (self >= 0) bk = self;
-            if (I.weights_exact)
-                atomicAdd(&carried[bk], I.wOD[i]);  // integer-valued: order-free, exact
-            else
-                cls[i] = (int16_t)bk;
-        }
-        __syncthreads();
-        if (!I.weights_exact) {
-            // index-ordered accumulation per hub, as np.bincount does
-            for (int k = threadIdx.x; k < h; k += kCorrThreads) {
-                double acc = 0.0;
-                for (int i = 0; i < n; ++i)
-                    if (cls[i] == k) acc += I.wOD[i];
-                carried[k] = acc;
+            __syncthreads();
+            const int kill = s_kill;
+            --h;
+            for (int i = threadIdx.x; i < n; i += kCorrThreads) {
+                int c = cls[i];
+                if (c == kill) {
+                    c = corr_nearest(I, H, h, i);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&carr[c]),
+                              (unsigned long long)(long long)I.wOD[i]);
+                } else if (c > kill) {
+                    --c;
+                }
+                cls[i] = (int16_t)c;
             }
             __syncthreads();
         }
+    }
+    // fractional weights: a fresh allocation and index-ordered per-hub sums
+    // each round, exactly np.bincount's order
+    while (h > p) {
+        for (int i = threadIdx.x; i < n; i += kCorrThreads) cls[i] = (int16_t)corr_nearest(I, H, h, i);
+        __syncthreads();
+        for (int k = threadIdx.x; k < h; k += kCorrThreads) {
+            double acc = 0.0;
+            for (int i = 0; i < n; ++i)
+                if (cls[i] == k) acc += I.wOD[i];
+            carried[k] = acc;
+        }
+        __syncthreads();
         if (threadIdx.x < 32) {
             // first minimum of carried[0..h)
             double bv = 0.0;
@@ -251,12 +307,9 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
                     bi = oi;
                 }
             }
-            if (threadIdx.x == 0) s_kill = bi;
+            if (threadIdx.x == 0)
+                for (int k = bi; k < h - 1; ++k) H[k] = H[k + 1];
         }
-        __syncthreads();
-        // delete H[kill] (np.delete keeps the order); h is small, shift serially
-        if (threadIdx.x == 0)
-            for (int k = s_kill; k < h - 1; ++k) H[k] = H[k + 1];
         __syncthreads();
         --h;
     }
@@ -269,7 +322,7 @@ int launch_correct(const DevInst& I, int64_t B, const uint32_t* bits, int hmax, 
     if (hmax < I.p) hmax = I.p;
     size_t smem = (size_t)hmax * 8 + (size_t)I.nw * 4 + (size_t)hmax * 4;
     smem = (smem + 7) & ~size_t(7);
-    if (!I.weights_exact) smem += (size_t)I.n * 2;
+    smem += (size_t)I.n * 2;
     if (smem > 48 * 1024)
         HG_CUDA(cudaFuncSetAttribute(k_correct, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
