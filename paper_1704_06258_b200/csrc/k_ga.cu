@@ -182,14 +182,43 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
     int32_t* H = reinterpret_cast<int32_t*>(mask + nw);               // [hmax]
     int16_t* cls = reinterpret_cast<int16_t*>(H + hmax);              // [n] hub position per node
 
-    int cnt = 0;
-    for (int w = threadIdx.x; w < nw; w += kCorrThreads) {
-        const uint32_t v = bits[b * nw + w];
-        mask[w] = v;
-        cnt += __popc(v);
-    }
     int h;
-    {
+    if (nw <= 32) {
+        // one warp counts the hubs; a child that already has p of them (the
+        // common case) is extracted by that warp alone and the CTA is done
+        __shared__ int s_h;
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            const uint32_t v = lane < nw ? bits[b * nw + lane] : 0u;
+            if (lane < nw) mask[lane] = v;
+            const int c = __popc(v);
+            int pre = c;  // inclusive warp scan of the popcounts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(kFull, pre, o);
+                if (lane >= o) pre += x;
+            }
+            const int tot = __shfl_sync(kFull, pre, 31);
+            if (tot == p) {
+                uint32_t w = v;
+                int k = pre - c;
+                while (w) {
+                    hubs_out[b * p + k++] = lane * 32 + (__ffs(w) - 1);
+                    w &= w - 1u;
+                }
+            }
+            if (lane == 0) s_h = tot;
+        }
+        __syncthreads();
+        h = s_h;
+        if (h == p) return;
+    } else {
+        int cnt = 0;
+        for (int w = threadIdx.x; w < nw; w += kCorrThreads) {
+            const uint32_t v = bits[b * nw + w];
+            mask[w] = v;
+            cnt += __popc(v);
+        }
         int dummy;
         CorrScan(tmp).ExclusiveSum(cnt, dummy, h);
         __syncthreads();
