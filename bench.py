@@ -102,10 +102,11 @@ class CpuBaseline:
 
         self.cores = cores or os.cpu_count() or 1
         self.pool = mp.get_context("fork").Pool(self.cores, initializer=_cpu_init)
-        # calibrate: evals per second per core
+        # calibrate: evals per second per process with every process busy
         self.pool.map(_cpu_work, [(0, 2)] * self.cores)
-        dt, _ = self.pool.apply(_cpu_work, ((0, 16),))
-        self.per_core = 16 / dt
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_work, [(0, 8)] * self.cores)
+        self.per_core = 8 / (time.perf_counter() - t0)
 
     def step(self, seconds: float):
         m = max(2, int(self.per_core * seconds))
@@ -432,12 +433,14 @@ def run_reference(args):
     if rank != 0:
         return
     cb = CpuBaseline()
+    # each step is a bounded sample: the whole K + W run stays within ~2.5 min
+    per_step = max(0.03, min(args.ref_seconds, 100.0 / (args.steps + args.warmup / 4.0)))
     for _ in range(args.warmup):
-        cb.step(args.ref_seconds / 4)
+        cb.step(per_step / 4)
     evals, walls = 0, 0.0
     m = 0
     for _ in range(args.steps):
-        e, w, m = cb.step(args.ref_seconds)
+        e, w, m = cb.step(per_step)
         evals += e
         walls += w
     cb.close()
