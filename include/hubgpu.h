@@ -97,6 +97,14 @@ int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc);
 int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* alloc,
                 double* out);
 
+/* duplicate-aware hg_evaluate (nearest allocation): the B
+ * hub sets are grouped on the device (hash, sort, equality against the sorted
+ * predecessor), each distinct set is scored once and its scores are copied to
+ * every member -- what the reference's memo does for repeated sets
+ * (_Evaluator, hm/engine.py:102-129).  *groups = number of distinct sets. */
+int hg_evaluate_unique(hg_inst* inst, int64_t B, const int64_t* hubs, double* out,
+                       int64_t* groups);
+
 /* Device-resident population (the bench's `value` path and the GA's own
  * children buffer).  hg_pop_load_hubs takes int32 hub sets (host or device);
  * hg_pop_evaluate queues K2+K3+finalise on the instance stream and returns

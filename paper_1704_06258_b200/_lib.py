@@ -57,6 +57,7 @@ SIGNATURES = {
     "hg_synchronize": (C.c_int, [_vp]),
     "hg_allocate": (C.c_int, [_vp, C.c_int64, _i64p, _i64p]),
     "hg_evaluate": (C.c_int, [_vp, C.c_int64, _i64p, _i64p, _f64p]),
+    "hg_evaluate_unique": (C.c_int, [_vp, C.c_int64, _i64p, _f64p, _i64p]),
     "hg_pop_create": (C.c_int, [_vp, C.c_int64, C.POINTER(_vp)]),
     "hg_pop_free": (None, [_vp]),
     "hg_pop_load_hubs": (C.c_int, [_vp, C.c_int64, _vp, C.c_int]),
@@ -215,10 +216,17 @@ class DeviceInstance:
         check(load().hg_allocate(self.handle, hubs.shape[0], ptr(hubs, _i64p), ptr(out, _i64p)))
         return out
 
-    def evaluate(self, hubs: np.ndarray, alloc: np.ndarray | None = None) -> np.ndarray:
+    def evaluate(self, hubs: np.ndarray, alloc: np.ndarray | None = None,
+                 unique: bool = False) -> np.ndarray:
         hubs = np.ascontiguousarray(hubs, dtype=np.int64).reshape(-1, self.p)
         B = hubs.shape[0]
         out = np.empty((B, 4), dtype=np.float64)
+        if unique and alloc is None:
+            groups = C.c_int64()
+            check(load().hg_evaluate_unique(self.handle, B, ptr(hubs, _i64p), ptr(out, _f64p),
+                                            C.byref(groups)))
+            self.last_groups = groups.value
+            return out
         ap = None
         if alloc is not None:
             alloc = np.ascontiguousarray(alloc, dtype=np.int64).reshape(B, self.n)

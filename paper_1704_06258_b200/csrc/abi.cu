@@ -601,6 +601,44 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
     return check_input_flag(inst, flag, alloc ? "solution" : "hub set");
 }
 
+int hg_evaluate_unique(hg_inst* inst, int64_t B, const int64_t* hubs, double* out,
+                       int64_t* groups) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    HG_ARG(B >= 0, "negative batch");
+    if (groups) *groups = 0;
+    if (B == 0) return HG_OK;
+    HG_ARG(hubs && out, "NULL buffer");
+    HG_TRY(set_device(inst->device));
+    hg_pop* P;
+    HG_TRY(scratch_pop(inst, B, &P));
+    const DevInst& I = inst->I;
+    cudaStream_t s = inst->stream;
+    // all hub sets (validated) -> t3; grouping scratch, map, count, full results -> t4
+    HG_TRY(inst->t3.ensure((size_t)B * I.p * sizeof(int32_t)));
+    int32_t* all = inst->t3.as<int32_t>();
+    HG_TRY(h2d_hubs_checked(inst, inst->t1, hubs, B, all));
+    const size_t gbytes = (unique_scratch_bytes(B) + 255) & ~size_t(255);
+    HG_TRY(inst->t4.ensure(gbytes + (size_t)B * 4 + 16 + (size_t)B * 32 + 256));
+    unsigned char* w = inst->t4.as<unsigned char>();
+    int32_t* map = reinterpret_cast<int32_t*>(w + gbytes);
+    int32_t* dcount = map + B + (B & 1);  // 8-byte aligned
+    double* full = reinterpret_cast<double*>(
+        w + ((gbytes + (size_t)B * 4 + 16 + 255) & ~size_t(255)));
+    HG_TRY(launch_unique_groups(all, B, I.p, w, gbytes, P->hubs, map, dcount, s));
+    int hc[3] = {0, 0, 0};
+    HG_CUDA(cudaMemcpyAsync(hc, dcount, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaMemcpyAsync(hc + 2, inst->derr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    HG_TRY(check_input_flag(inst, hc[2], "hub set"));
+    const int64_t U = (int64_t)hc[0] + hc[1];
+    HG_TRY(pop_eval_queue(P, U, nullptr));
+    HG_TRY(launch_scatter_out(P->out, map, B, full, s));
+    HG_CUDA(cudaMemcpyAsync(out, full, (size_t)B * 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    if (groups) *groups = U;
+    return HG_OK;
+}
+
 int hg_pop_create(hg_inst* inst, int64_t capacity, hg_pop** out) {
     HG_ARG(inst && out, "NULL argument");
     HG_ARG(capacity >= 1, "capacity must be >= 1");

@@ -151,6 +151,16 @@ int launch_unrank_combos(const uint64_t* binom, int n, int p, uint64_t rank0, in
 int launch_batch_best(const double* out, int64_t B, uint64_t rank0, uint64_t count,
                       double* best_raw, unsigned long long* best_rank, cudaStream_t st);
 
+// ---- k_unique.cu: duplicate-aware evaluation ---------------------------------
+size_t unique_scratch_bytes(int64_t B);
+// groups the B hub sets (int32 [B][p]); writes one representative per group to
+// uhubs (dense, in sorted-hash order), map[b] = group of set b, and
+// d_count[0] + d_count[1] = number of groups
+int launch_unique_groups(const int32_t* hubs, int64_t B, int p, void* scratch, size_t bytes,
+                         int32_t* uhubs, int32_t* map, int32_t* d_count, cudaStream_t s);
+int launch_scatter_out(const double* uout, const int32_t* map, int64_t B, double* out,
+                       cudaStream_t s);
+
 // ---- launchers (k_ga.cu) ---------------------------------------------------
 int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n, int nw,
                          cudaStream_t s);

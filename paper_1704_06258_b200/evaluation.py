@@ -83,19 +83,22 @@ def fitness(inst: Instance, sol: Solution, mode: FitnessMode) -> float:
     return objective(inst, sol, mode).scaled_fitness
 
 
-def evaluate_population(inst: Instance, hubs: np.ndarray, alloc: np.ndarray | None = None
-                        ) -> np.ndarray:
+def evaluate_population(inst: Instance, hubs: np.ndarray, alloc: np.ndarray | None = None,
+                        unique: bool = False) -> np.ndarray:
     """Batched objective: B sorted hub sets (B x p) -> B x 4 array of
     (collection, transfer, distribution, raw).  ``alloc=None`` scores the
     nearest allocation of each hub set (what the GA and _Evaluator.evaluate,
     hm/engine.py:116-129, score); otherwise ``alloc`` (B x n) must be a
-    feasible allocation onto the given hubs (not re-validated here)."""
+    feasible allocation onto the given hubs (not re-validated here).
+    ``unique=True`` (nearest allocation only) scores each distinct hub set
+    once on the device and copies its row to every repeat -- the reference's
+    memo (_Evaluator) for batches with many repeated sets."""
     hubs = np.asarray(hubs, dtype=np.int64)
     if hubs.ndim != 2 or hubs.shape[1] != inst.p:
         raise ValueError(f"hubs must be B x p={inst.p}, got {hubs.shape}")
     # range / order of every hub set (and alloc range) is validated on the
     # device by the C-ABI; a bad batch raises ValueError naming the first row
-    return inst.device().evaluate(hubs, alloc)
+    return inst.device().evaluate(hubs, alloc, unique=unique)
 
 
 def avg_interhub_distance(inst: Instance, sol: Solution) -> float:

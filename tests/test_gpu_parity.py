@@ -399,3 +399,26 @@ class TestNext:
 
         with pytest.raises(ValueError, match="over the limit of 10"):
             _lib.restricted_optimum(inst.device(), 10)
+
+    def test_unique_evaluation_matches(self, kernel):
+        """Duplicate-aware scoring: every repeat gets its group's row, bit for
+        bit, and each distinct set is scored once."""
+        inst = hg.generate_urand(300, 12, 9, (1.0, 0.75, 1.0))
+        base = hg.random_population(300, 12, 500, key=3)
+        rng = np.random.default_rng(5)
+        pop = base[rng.integers(0, 500, size=3000)]
+        plain = hg.evaluate_population(inst, pop)
+        uniq = hg.evaluate_population(inst, pop, unique=True)
+        assert np.array_equal(plain, uniq)
+        assert inst.device().last_groups == len(np.unique(pop, axis=0))
+        allu = hg.evaluate_population(inst, base, unique=True)
+        assert np.array_equal(allu, hg.evaluate_population(inst, base))
+        assert inst.device().last_groups == 500
+
+    def test_unique_evaluation_validates(self):
+        inst = hg.generate_urand(50, 4, 9, (1.0, 0.75, 1.0))
+        pop = hg.random_population(50, 4, 20, key=3)
+        pop[7] = [3, 3, 4, 5]
+        with pytest.raises(ValueError, match="hub set 7"):
+            hg.evaluate_population(inst, pop, unique=True)
+        assert hg.evaluate_population(inst, pop[:7], unique=True).shape == (7, 4)
