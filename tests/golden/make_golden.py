@@ -270,7 +270,76 @@ def gen_restricted():
     save("restricted", **out)
 
 
+def gen_cli():
+    """Reference command-line outputs (hm/cli.py, hm/bench.py): instance files
+    written by `gen`, CSV schema v1 rows of `solve` and `bench` (wall time
+    dropped), `oracle` text, `eval` text, and parameter fingerprints."""
+    import contextlib
+    import io as _io
+    import tempfile
+
+    from hubmedian import bench as hm_bench
+    from hubmedian import cli as hm_cli
+
+    def run(args):
+        buf = _io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = hm_cli.main(args)
+        return rc, buf.getvalue()
+
+    out = {}
+    fps = []
+    for prm, mode in [((64, 64, 50, 10, 0, None, False), "raw"), ((8, 8, 5, 3, 42, None, False), "milli"),
+                      ((2, 100, 20, 2, 1, 2, True), "cab")]:
+        params = hm.GaParams(islands=prm[0], pop_size=prm[1], inner_iters=prm[2],
+                             outer_iters=prm[3], seed=prm[4], perturb_strength=prm[5],
+                             strict_paper=prm[6])
+        fps.append([json.dumps(prm), mode,
+                    hm_bench.params_fingerprint(params, hm.FitnessMode.from_string(mode))])
+    out["fingerprints"] = np.array(fps)
+    with tempfile.TemporaryDirectory() as td:
+        td = Path(td)
+        texts = []
+        for idx, (n, p, seed, alpha) in enumerate([(12, 3, 606, 0.75), (25, 3, 1704, 0.2)]):
+            f = td / f"g{idx}.usaphmp"
+            rc, text = run(["gen", "-n", str(n), "-p", str(p), "--seed", str(seed), "--alpha",
+                            str(alpha), "-o", str(f)])
+            out[f"gen{idx}_args"] = np.array([n, p, seed, alpha])
+            out[f"gen{idx}_bytes"] = np.frombuffer(f.read_bytes(), dtype=np.uint8)
+            solve_args = ["--fitness-mode", "milli", "--islands", "8", "--pop", "8", "--inner",
+                          "5", "--outer", "3", "--seed", "42"]
+            rc, text = run(["solve", str(f), "--csv", "-"] + solve_args)
+            cells = text.strip().splitlines()
+            rows = [",".join(c for k, c in enumerate(line.split(",")) if k != 9) for line in cells]
+            out[f"solve{idx}_rows"] = np.array(rows)
+            out[f"solve{idx}_args"] = np.array(solve_args)
+            rc, text = run(["oracle", str(f), "--which", "restricted"])
+            out[f"oracle{idx}_text"] = np.array(text)
+        # eval of a solution file against instance 0
+        from hubmedian import io as hm_io
+
+        inst = hm_io.load_instance(td / "g0.usaphmp")
+        sol = hm.nearest_allocation([1, 5, 9], inst)
+        sf = td / "s0.sol"
+        sf.write_bytes(hm_io.write_solution(sol))
+        out["eval0_solution"] = np.frombuffer(sf.read_bytes(), dtype=np.uint8)
+        rc, text = run(["eval", str(td / "g0.usaphmp"), str(sf), "--fitness-mode", "cab"])
+        out["eval0_text"] = np.array(text)
+        # a two-row manifest
+        (td / "m.csv").write_text("label,path,format,p,mode,known_best\n"
+                                  "a,g0.usaphmp,,,milli,\n"
+                                  "b,g1.usaphmp,canonical,2,raw,1e6\n")
+        rc, text = run(["bench", str(td / "m.csv"), "--seeds", "0,1", "--islands", "4",
+                        "--pop", "8", "--inner", "3", "--outer", "2", "--csv", "-"])
+        lines = [ln for ln in text.strip().splitlines() if "," in ln]
+        out["bench_rows"] = np.array([",".join(c for k, c in enumerate(ln.split(",")) if k != 9)
+                                      for ln in lines])
+        out["bench_rc"] = np.array([rc])
+    save("cli", **out)
+
+
 if __name__ == "__main__":
+    gen_cli()
     gen_rng()
     gen_instances()
     gen_eval()

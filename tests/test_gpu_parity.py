@@ -422,3 +422,75 @@ class TestNext:
         with pytest.raises(ValueError, match="hub set 7"):
             hg.evaluate_population(inst, pop, unique=True)
         assert hg.evaluate_population(inst, pop[:7], unique=True).shape == (7, 4)
+
+
+class TestCli:
+    """the command line runs the reference's manifests and
+    emits its CSV schema v1 rows -- equal, field by field but the wall time,
+    to the reference's own output (tests/golden/cli.npz)."""
+
+    @staticmethod
+    def _run(args, capsys):
+        from paper_1704_06258_b200 import cli
+
+        rc = cli.main(args)
+        return rc, capsys.readouterr().out
+
+    @staticmethod
+    def _write(tmp_path, idx):
+        f = tmp_path / f"g{idx}.usaphmp"
+        f.write_bytes(golden("cli")[f"gen{idx}_bytes"].tobytes())
+        return f
+
+    @pytest.mark.parametrize("idx", range(2))
+    def test_solve_rows(self, idx, tmp_path, capsys):
+        g = golden("cli")
+        f = self._write(tmp_path, idx)
+        rc, text = self._run(["solve", str(f), "--csv", "-"] + g[f"solve{idx}_args"].tolist(),
+                             capsys)
+        assert rc == 0
+        rows = [",".join(c for k, c in enumerate(ln.split(",")) if k != 9)
+                for ln in text.strip().splitlines()]
+        assert rows == g[f"solve{idx}_rows"].tolist()
+
+    @pytest.mark.parametrize("idx", range(2))
+    def test_oracle_text(self, idx, tmp_path, capsys):
+        f = self._write(tmp_path, idx)
+        rc, text = self._run(["oracle", str(f), "--which", "restricted"], capsys)
+        assert rc == 0 and text == str(golden("cli")[f"oracle{idx}_text"])
+
+    def test_eval_text(self, tmp_path, capsys):
+        g = golden("cli")
+        f = self._write(tmp_path, 0)
+        sf = tmp_path / "s0.sol"
+        sf.write_bytes(g["eval0_solution"].tobytes())
+        rc, text = self._run(["eval", str(f), str(sf), "--fitness-mode", "cab"], capsys)
+        assert rc == 0
+        ref = str(g["eval0_text"]).splitlines()
+        got = text.splitlines()
+        assert [ln.split()[0] for ln in got] == [ln.split()[0] for ln in ref]
+        assert close([float(ln.split()[-1]) for ln in got],
+                     [float(ln.split()[-1]) for ln in ref], rel=1e-12)
+
+    def test_bench_rows(self, tmp_path, capsys):
+        g = golden("cli")
+        self._write(tmp_path, 0)
+        self._write(tmp_path, 1)
+        (tmp_path / "m.csv").write_text("label,path,format,p,mode,known_best\n"
+                                        "a,g0.usaphmp,,,milli,\n"
+                                        "b,g1.usaphmp,canonical,2,raw,1e6\n")
+        rc, text = self._run(["bench", str(tmp_path / "m.csv"), "--seeds", "0,1", "--islands",
+                              "4", "--pop", "8", "--inner", "3", "--outer", "2", "--csv", "-"],
+                             capsys)
+        assert rc == int(g["bench_rc"][0])
+        lines = [ln for ln in text.strip().splitlines() if "," in ln]
+        rows = [",".join(c for k, c in enumerate(ln.split(",")) if k != 9) for ln in lines]
+        assert rows == g["bench_rows"].tolist()
+
+    def test_gen_on_device(self, tmp_path, capsys):
+        g = golden("cli")
+        n, p, seed, alpha = g["gen1_args"]
+        out = tmp_path / "d.usaphmp"
+        rc, _ = self._run(["gen", "-n", str(int(n)), "-p", str(int(p)), "--seed", str(int(seed)),
+                           "--alpha", repr(float(alpha)), "-o", str(out), "--device"], capsys)
+        assert rc == 0 and out.read_bytes() == g["gen1_bytes"].tobytes()
