@@ -141,6 +141,15 @@ __device__ int block_extract(const uint32_t* mask, int nw, int32_t* H,
     return base;
 }
 
+// exact integer load += w (w integer-valued, totals < 2^53) on (hi, lo) words
+__device__ __forceinline__ void carried_add(uint32_t* lo, uint32_t* hi, int c, double wd) {
+    const uint64_t w = (uint64_t)(long long)wd;
+    const uint32_t wl = (uint32_t)w, wh = (uint32_t)(w >> 32);
+    const uint32_t old = atomicAdd(&lo[c], wl);
+    const uint32_t up = wh + ((uint32_t)(old + wl) < old ? 1u : 0u);
+    if (up) atomicAdd(&hi[c], up);
+}
+
 // position in H[0..h) of node i's hub under allocate_to_nearest
 // (hm/model.py:202-207): first fp64 minimum through the exact 16-bit
 // pre-filter (keys (q << 16) | k, two smallest kept; a second hub at the same
@@ -247,23 +256,49 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
         // allocation is computed once and afterwards only the nodes of the
         // closed hub move (closing a hub that is not a node's first minimum
         // leaves that node's first minimum unchanged)
-        long long* carr = reinterpret_cast<long long*>(carried);
-        for (int k = threadIdx.x; k < h; k += kCorrThreads) carr[k] = 0;
+        // loads as (hi, lo) 32-bit words: native shared atomics (a 64-bit
+        // shared add is a compare-and-swap loop), the carry moved by hand
+        uint32_t* clo = reinterpret_cast<uint32_t*>(carried);
+        uint32_t* chi = clo + hmax;
+        for (int k = threadIdx.x; k < h; k += kCorrThreads) clo[k] = chi[k] = 0u;
         __syncthreads();
-        for (int i = threadIdx.x; i < n; i += kCorrThreads) {
-            const int c = corr_nearest(I, H, h, i);
-            cls[i] = (int16_t)c;
-            atomicAdd(reinterpret_cast<unsigned long long*>(&carr[c]),
-                      (unsigned long long)(long long)I.wOD[i]);
+        // 4 consecutive nodes per thread, one 8-byte load per hub row (rows are
+        // padded to npad with 0xFFFF, a multiple of 16)
+        for (int i0 = 4 * threadIdx.x; i0 < n; i0 += 4 * kCorrThreads) {
+            unsigned m1[4], m2[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) m1[t] = m2[t] = 0xFFFFFFFFu;
+            const uint16_t* col = I.Cq + i0;
+#pragma unroll 4
+            for (int k = 0; k < h; ++k) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(col + (size_t)H[k] * I.nq));
+                const unsigned q[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const unsigned key = (q[t] << 16) | (unsigned)k;
+                    m2[t] = min(m2[t], max(m1[t], key));
+                    m1[t] = min(m1[t], key);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int i = i0 + t;
+                if (i >= n) break;
+                int c = (int)(m1[t] & 0xFFFFu);
+                if ((m2[t] >> 16) == (m1[t] >> 16) && H[c] != i)
+                    c = corr_nearest(I, H, h, i);  // quantised tie (or a hub node): exact path
+                cls[i] = (int16_t)c;
+                carried_add(clo, chi, c, I.wOD[i]);
+            }
         }
         __syncthreads();
         while (h > p) {
             if (threadIdx.x < 32) {
-                // first minimum of carr[0..h)
+                // first minimum of the loads[0..h)
                 long long bv = 0;
                 int bi = -1;
                 for (int k = threadIdx.x; k < h; k += 32) {
-                    const long long v = carr[k];
+                    const long long v = (long long)(((uint64_t)chi[k] << 32) | clo[k]);
                     if (bi < 0 || v < bv) {
                         bv = v;
                         bi = k;
@@ -280,10 +315,11 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
                 }
                 if (threadIdx.x == 0) {
                     s_kill = bi;
-                    // delete position bi of H and carr (np.delete keeps the order)
+                    // delete position bi of H and the loads (np.delete keeps the order)
                     for (int k = bi; k < h - 1; ++k) {
                         H[k] = H[k + 1];
-                        carr[k] = carr[k + 1];
+                        clo[k] = clo[k + 1];
+                        chi[k] = chi[k + 1];
                     }
                 }
             }
@@ -294,8 +330,7 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
                 int c = cls[i];
                 if (c == kill) {
                     c = corr_nearest(I, H, h, i);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&carr[c]),
-                              (unsigned long long)(long long)I.wOD[i]);
+                    carried_add(clo, chi, c, I.wOD[i]);
                 } else if (c > kill) {
                     --c;
                 }
