@@ -172,3 +172,21 @@ def test_enumeration_limit_raised_on_host():
     assert str(e.value) == ("enumeration needs 142506 candidates, over the limit of 1000; "
                             "raise `limit` explicitly to allow it")
     assert isinstance(e.value, ValueError)
+
+
+def test_bench_reference_arm_line():
+    """bench.py --impl reference prints the contract's JSON line on the host
+    cores (no GPU needed)."""
+    import json
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "3", "--ref-seconds", "0.05"],
+                         capture_output=True, text=True, timeout=300, check=True).stdout
+    line = json.loads(out.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["steps"] == 2 and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
