@@ -531,7 +531,7 @@ int hg_instance_set_fitness(hg_inst* inst, int kind) {
     HG_ARG(kind != HG_FIT_TC_TMEM || inst->tcy_ok,
            "the TMEM-resident tensor-core kernel needs n <= 1024 (and was not disabled)");
     HG_ARG(kind != HG_FIT_TC_PAIR || inst->tcp_ok,
-           "the CTA-pair tensor-core kernel needs n <= 1024 (and was not disabled)");
+           "the CTA-pair tensor-core kernel needs n <= 16384 (and was not disabled)");
     inst->fit_kind = kind;
     return HG_OK;
 }

@@ -13,6 +13,12 @@
 //   accf[d]   each CTA's (multicast commit); acce[d] leader's, 2 x 16 epilogue warps arrive
 //   kbf[h]    each CTA's (multicast commit); ard[h] leader's, 2 x 4 generator warps arrive
 //
+// Any n: the K dimension is cut into chunks of 1024 nodes (the 256 TMEM
+// columns of a resident one-hot).  Integer bins are linear in D, so every
+// (chunk, output tile) accumulator drains into them independently, and a
+// chunk's bins are folded into S_T (p fp64 FMAs per row) before the next
+// chunk -- no accumulator ever spans chunks.
+//
 #include <cuda.h>
 #include <cuda_pipeline.h>
 
@@ -156,6 +162,10 @@ __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
 
 }  // namespace
 
+__host__ __device__ inline size_t p_C_bytes(int ipt, int npad) {
+    return ((size_t)ipt * npad + 15) & ~size_t(15);
+}
+
 struct PArgs {
     const uint8_t* cl;
     const uint32_t* T;
@@ -164,30 +174,34 @@ struct PArgs {
     int n, p, ps, npad;
     int ipt;          // individuals per unit (ipt * p <= 128)
     int64_t units;
-    int IT;           // 128-row W tiles (= K blocks)
-    int acols;        // TMEM columns of A = IT * 32
+    int ITO;          // 128-row W tiles (output columns i)
+    int KBT;          // 128-node K blocks in all
+    int NC;           // K chunks of <= 8 blocks (1024 nodes): one resident one-hot each
     int stages;       // W ring depth
     int kbs;          // 128-byte K blocks per stage
+    int csm;          // 1: a unit's cluster rows are staged in shared memory (they fit)
     uint32_t idesc;   // kind::i8, M=256, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
     int dbg;                     // ablation flags (tuning only): 1 = no epilogue math, 2 = no MMA
 };
 
-__host__ __device__ inline size_t p_C_bytes(int ipt, int npad) {
-    return ((size_t)ipt * npad + 15) & ~size_t(15);
-}
+constexpr int kYChunkKB = 8;  // K blocks per chunk: 8 x 128 nodes = 256 TMEM columns of A
 
+// CSM: a unit's cluster rows staged in shared memory (known address space ->
+// LDS) rather than read from global memory
+template <bool CSM>
 __global__ void __launch_bounds__(kYThreads, 1)
 k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-    const int p = A.p, ipt = A.ipt, IT = A.IT;
+    const int p = A.p, ipt = A.ipt, ITO = A.ITO, KBT = A.KBT, NC = A.NC;
     unsigned char* ring = smem;                                          // W stages
     const int NS = A.stages, KBS = A.kbs;
     unsigned char* var = smem + NS * KBS * kYStageBytes;
-    const size_t cb = p_C_bytes(ipt, A.npad);
-    // double buffer addressed arithmetically from the shared base (a pointer
-    // array indexed at run time would drop to local memory and generic loads)
+    // cluster rows of the current / next unit, when they fit (CSM); a double
+    // buffer addressed arithmetically (a runtime-indexed pointer array would
+    // drop to local memory)
+    const size_t cb = CSM ? p_C_bytes(ipt, A.npad) : 0;
     unsigned char* sC0 = var;
     var += 2 * cb;
     uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [p][128] cluster-pair flow bins
@@ -200,9 +214,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                    b_accf = b_empty + 8 * kYMaxStages, b_acce = b_accf + 16, b_kbf = b_acce + 16,
                    b_ard = b_kbf + 32;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kYMaxStages + 12);
-    // A's K blocks are generated in 4 contiguous ranges, one per column-quarter
-    // warp group: quarter h owns K blocks [kq(h), kq(h+1))
-    auto kq = [&](int h) { return h * IT / 4; };
+    // chunk c of the K dimension: K blocks [c*8, c*8 + nkb(c)); its one-hot is
+    // generated in 4 contiguous ranges of K blocks, one per column-quarter warp
+    // group: quarter h owns chunk-local blocks [kq(c,h), kq(c,h+1))
+    auto nkb = [&](int c) { return KBT - c * kYChunkKB < kYChunkKB ? KBT - c * kYChunkKB : kYChunkKB; };
+    auto kq = [&](int c, int h) { return h * nkb(c) / 4; };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int x = tid; x < p * 128; x += kYThreads) bins[x] = 0u;
@@ -236,7 +252,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     const uint32_t tmem = *tmem_slot;
 
     // units of this pair, interleaved over its 2 CTAs; both run the same number
-    // of slots (a slot past the end is a dummy unit): one MMA stream serves both
+    // of slots (a slot past the end is a dummy unit): one MMA stream serves both.
+    // A phase is (slot, chunk): one resident one-hot, ITO output tiles.
     const uint32_t crank = cluster_rank();
     const int64_t ncl = gridDim.x / kYCluster, cid = blockIdx.x / kYCluster;
     const int64_t cs0 = A.units * cid / ncl, cs1 = A.units * (cid + 1) / ncl;
@@ -247,34 +264,36 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
 
     if (warp == 1) {
         // ---------------- TMA producer: W tiles (it, K-block group), same order
-        // every unit; a stage holds KBS consecutive 128-byte K blocks
+        // every phase; a stage holds up to KBS consecutive 128-byte K blocks
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
             bool wrapped = false;
             const int q = (int)crank * 64;  // this CTA's W rows within a tile
             for (int64_t j = 0; j < nslots; ++j)
-                for (int it = 0; it < IT; ++it)
-                    for (int kb0 = 0; kb0 < IT; kb0 += KBS) {
-                        const int nk = IT - kb0 < KBS ? IT - kb0 : KBS;
-                        // stage s is free: the leader's MMAs reading it completed
-                        if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
-                        if (leader)  // both halves land on the leader's barrier
-                            mb_expect_tx(b_full + 8 * s, (uint32_t)(2 * nk * kYStageBytes));
-                        const uint32_t dst = su32(ring + s * (KBS * kYStageBytes));
-                        for (int kk = 0; kk < nk; ++kk)
-                            tma2d_pair(dst + kk * kYStageBytes, &tmW, (kb0 + kk) * 128,
-                                       it * 128 + q, L_full + 8 * s);
-                        if (++s == (uint32_t)NS) {
-                            s = 0;
-                            ph ^= 1u;
-                            wrapped = true;
+                for (int c = 0; c < NC; ++c)
+                    for (int it = 0; it < ITO; ++it)
+                        for (int kb0 = 0; kb0 < nkb(c); kb0 += KBS) {
+                            const int nk = nkb(c) - kb0 < KBS ? nkb(c) - kb0 : KBS;
+                            // stage s is free: the leader's MMAs reading it completed
+                            if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
+                            if (leader)  // both halves land on the leader's barrier
+                                mb_expect_tx(b_full + 8 * s, (uint32_t)(2 * nk * kYStageBytes));
+                            const uint32_t dst = su32(ring + s * (KBS * kYStageBytes));
+                            for (int kk = 0; kk < nk; ++kk)
+                                tma2d_pair(dst + kk * kYStageBytes, &tmW,
+                                           (c * kYChunkKB + kb0 + kk) * 128, it * 128 + q,
+                                           L_full + 8 * s);
+                            if (++s == (uint32_t)NS) {
+                                s = 0;
+                                ph ^= 1u;
+                                wrapped = true;
+                            }
                         }
-                    }
         }
     } else if (warp == 0) {
         // ---------------- MMA issuer (leader CTA only)
         if (lane == 0 && leader) {
-            uint32_t s = 0, ph = 0, t = 0;
+            uint32_t s = 0, ph = 0, t = 0, phase = 0;
             const bool timed = A.timing != nullptr;
             unsigned long long w_a = 0, w_e = 0, w_f = 0, w_i = 0;
             long long c0 = timed ? clock64() : 0;
@@ -287,49 +306,54 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         }                                           \
     } while (0)
             for (int64_t j = 0; j < nslots; ++j) {
-                for (int it = 0; it < IT; ++it, ++t) {
-                    const int d = t & 1;
-                    if (t >= 2 && !(A.dbg & 64)) mb_wait_cl(b_acce + 8 * d, ((t >> 1) - 1) & 1);
-                    YT(w_e);
-                    fence_after();
-                    const uint32_t dcol = tmem + kYAcc0 + d * 128;
-                    for (int kb0 = 0; kb0 < IT; kb0 += KBS) {
-                        const int nk = IT - kb0 < KBS ? IT - kb0 : KBS;
-                        if (it == 0 && !(A.dbg & 64)) {
-                            // first use of this unit's A: its quarters must be in TMEM
-                            for (int h = 0; h < 4; ++h)
-                                if (kq(h) >= kb0 && kq(h) < kb0 + nk && kq(h) < kq(h + 1))
-                                    mb_wait_cl(b_ard + 8 * h, (uint32_t)(j & 1));
-                            fence_after();
-                            YT(w_a);
-                        }
-                        mb_wait(b_full + 8 * s, ph);
-                        YT(w_f);
+                for (int c = 0; c < NC; ++c, ++phase) {
+                    const int nb = nkb(c);
+                    for (int it = 0; it < ITO; ++it, ++t) {
+                        const int d = t & 1;
+                        if (t >= 2 && !(A.dbg & 64))
+                            mb_wait_cl(b_acce + 8 * d, ((t >> 1) - 1) & 1);
+                        YT(w_e);
                         fence_after();
-                        const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
-                        if (!(A.dbg & 2)) {
-                            for (int kk = 0; kk < nk; ++kk) {
-                                const int kb = kb0 + kk;
-                                const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
-#pragma unroll
-                                for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns of A
-                                    mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
-                                           (kb | ks) != 0);
+                        const uint32_t dcol = tmem + kYAcc0 + d * 128;
+                        for (int kb0 = 0; kb0 < nb; kb0 += KBS) {
+                            const int nk = nb - kb0 < KBS ? nb - kb0 : KBS;
+                            if (it == 0 && !(A.dbg & 64)) {
+                                // first use of this phase's A: its quarters must be in TMEM
+                                for (int h = 0; h < 4; ++h)
+                                    if (kq(c, h) >= kb0 && kq(c, h) < kb0 + nk &&
+                                        kq(c, h) < kq(c, h + 1))
+                                        mb_wait_cl(b_ard + 8 * h, phase & 1u);
+                                fence_after();
+                                YT(w_a);
                             }
+                            mb_wait(b_full + 8 * s, ph);
+                            YT(w_f);
+                            fence_after();
+                            const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
+                            if (!(A.dbg & 2)) {
+                                for (int kk = 0; kk < nk; ++kk) {
+                                    const int kb = kb0 + kk;
+                                    const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
+#pragma unroll
+                                    for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns
+                                        mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks,
+                                               A.idesc, (kb | ks) != 0);
+                                }
+                            }
+                            commit_pair(b_empty + 8 * s);
+                            if (it == ITO - 1)  // last use of this phase's A quarter: free it
+                                for (int h = 0; h < 4; ++h)
+                                    if (kq(c, h + 1) - 1 >= kb0 && kq(c, h + 1) - 1 < kb0 + nk &&
+                                        kq(c, h) < kq(c, h + 1))
+                                        commit_pair(b_kbf + 8 * h);
+                            if (++s == (uint32_t)NS) {
+                                s = 0;
+                                ph ^= 1u;
+                            }
+                            YT(w_i);
                         }
-                        commit_pair(b_empty + 8 * s);
-                        if (it == IT - 1)  // last use of this unit's A quarter: free it
-                            for (int h = 0; h < 4; ++h)
-                                if (kq(h + 1) - 1 >= kb0 && kq(h + 1) - 1 < kb0 + nk &&
-                                    kq(h) < kq(h + 1))
-                                    commit_pair(b_kbf + 8 * h);
-                        if (++s == (uint32_t)NS) {
-                            s = 0;
-                            ph ^= 1u;
-                        }
-                        YT(w_i);
+                        commit_pair(b_accf + 8 * d);
                     }
-                    commit_pair(b_accf + 8 * d);
                 }
             }
             if (timed) {
@@ -341,7 +365,6 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         }
     } else if (warp >= kYEpiWarp0 && !(A.dbg & 64)) {
         // ---------------- generators + epilogue (16 warps)
-        const int et = tid - kYEpiWarp0 * 32;           // 0..511
         const int q = warp & 3;                         // TMEM lane quadrant
         const int sub = (warp - kYEpiWarp0) >> 2;       // 0..3: column quarter
         const int r = q * 32 + lane;                    // A row / accumulator lane
@@ -365,36 +388,25 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             bbase = u * ipt;
             nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
         };
-        // stage a unit's cluster rows into double buffer j & 1
-        auto stage = [&](int64_t j) {
+        // one-hot A of phase (j, c) into TMEM (row r = (bl, l), K = the chunk's
+        // nodes); this warp writes chunk blocks [kq(c,sub), kq(c,sub+1)) of its
+        // lane quadrant, reading the cluster rows straight from global memory
+        // (lanes of one individual read the same bytes: L1 broadcasts)
+        auto gen = [&](int64_t j, int c) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
-            uint8_t* Cs = sC0 + (j & 1) * cb;
-            const int chunks = A.npad / 16;
-            for (int x = et; x < ipt * chunks; x += kYEpiThreads) {
-                const int b2 = x / chunks, k = x - b2 * chunks;
-                uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                if (b2 < nind)
-                    v = __ldg(reinterpret_cast<const uint4*>(A.cl + (bbase + b2) * A.npad) + k);
-                reinterpret_cast<uint4*>(Cs + (size_t)b2 * A.npad)[k] = v;
-            }
-        };
-        // one-hot A of a unit into TMEM (row r = (bl, l), K = nodes); this warp
-        // writes K blocks [kq(sub), kq(sub+1)) of its lane quadrant
-        auto gen = [&](int64_t j) {
-            int64_t bbase;
-            int nind;
-            slot_unit(j, bbase, nind);
-            const uint8_t* Cs = sC0 + (j & 1) * cb;
             const bool live = r < ipt * p && bl < nind;
             const uint32_t lrep = (uint32_t)l * 0x01010101u;
-            const uint4* crow = reinterpret_cast<const uint4*>(Cs + (size_t)(live ? bl : 0) * A.npad);
-            for (int c0 = kq(sub) * 32; c0 < kq(sub + 1) * 32; c0 += 8) {
+            const uint8_t* rowp = CSM ? sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad
+                                        : A.cl + (bbase + (live ? bl : 0)) * A.npad;
+            const uint4* crow =
+                reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
+            for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32; c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const uint4 x = crow[(c0 >> 2) + h];  // 16 cluster ids = 4 columns
+                    const uint4 x = live ? crow[(c0 >> 2) + h] : make_uint4(0, 0, 0, 0);
                     v[4 * h + 0] = live ? oh4(x.x, lrep) : 0u;
                     v[4 * h + 1] = live ? oh4(x.y, lrep) : 0u;
                     v[4 * h + 2] = live ? oh4(x.z, lrep) : 0u;
@@ -408,105 +420,134 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             if (lane == 0) arrive_remote(L_ard + 8 * sub);
         };
 
+        // stage a unit's cluster rows into double buffer j & 1 (CSM)
+        auto stage = [&](int64_t j) {
+            int64_t bbase;
+            int nind;
+            slot_unit(j, bbase, nind);
+            uint8_t* Cs = sC0 + (j & 1) * cb;
+            const int chunks = A.npad / 16;
+            for (int x = tid - kYEpiWarp0 * 32; x < ipt * chunks; x += kYEpiThreads) {
+                const int b2 = x / chunks, k = x - b2 * chunks;
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (b2 < nind)
+                    v = __ldg(reinterpret_cast<const uint4*>(A.cl + (bbase + b2) * A.npad) + k);
+                reinterpret_cast<uint4*>(Cs + (size_t)b2 * A.npad)[k] = v;
+            }
+        };
         if (nslots > 0) {
-            stage(0);
-            epi_sync();
-            gen(0);
+            if (CSM) {
+                stage(0);
+                epi_sync();
+            }
+            gen(0, 0);
         }
-        ET(e_st);
+        ET(e_gen);
         // this thread's bin row: bins[k][r] at byte k * 512 + r * 4
         const uint32_t bin_r = su32(bins) + (uint32_t)r * 4u;
+        uint32_t phase = 0;
         for (int64_t j = 0; j < nslots; ++j) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
             const bool live = r < ipt * p && bl < nind;
-            const uint8_t* crow = sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad;
-            if (j + 1 < nslots) {
+            const uint8_t* crow = CSM ? sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad
+                                        : A.cl + (bbase + (live ? bl : 0)) * A.npad;
+            if (CSM && j + 1 < nslots) {
                 stage(j + 1);  // the next unit's cluster rows, under this unit's MMAs
                 ET(e_st);
             }
-            for (int it = 0; it < IT; ++it, ++t) {
-                const int d = t & 1;
-                if (j + 1 < nslots && it == IT - 1) {
-                    // the next unit's one-hot, quarter by quarter as the last
-                    // tile's MMAs release this unit's A
-                    epi_sync();  // staging of j+1 complete
-                    if (kq(sub) < kq(sub + 1)) {
-                        mb_wait(b_kbf + 8 * sub, (uint32_t)(j & 1));
-                        fence_after();
-                    }
-                    if (A.dbg & 4) {  // ablation: wait for the whole last tile
-                        mb_wait(b_accf + 8 * d, (t >> 1) & 1);
-                        fence_after();
-                    }
-                    gen(j + 1);
-                    ET(e_gen);
-                }
-                mb_wait(b_accf + 8 * d, (t >> 1) & 1);
-                ET(e_wait);
-                fence_after();
-                const uint32_t dcol = tmem + lane_base + kYAcc0 + d * 128 + sub * 32;
-                uint32_t v0[16], v1[16];
-                ld16(dcol, v0);
-                ld16(dcol + 16, v1);
-                // cluster ids of the 32 columns i = it*128 + sub*32 + k
-                const uint4* cp = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32);
-                const uint4 ca = cp[0], cz = cp[1];
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                ET(e_ld);
-                fence_before();
-                __syncwarp();
-                if (lane == 0) arrive_remote(L_acce + 8 * d);  // accumulator may be overwritten
-                if (live && !(A.dbg & 1)) {
-                    // G[c_i][r] += D[r][i]: exact integer bins, this row's own
-                    // (4 column-quarter warps share a row, hence the atomics)
-                    const uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cz.x, cz.y, cz.z, cz.w};
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const uint32_t c = __byte_perm(cw[k >> 2], 0u, 0x4440u + (k & 3));
-                        const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
-                        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(bin_r + c * 512u),
-                                     "r"(dv)
-                                     : "memory");
-                    }
-                }
-                ET(e_cmp);
-            }
-            // S_T(b) = sum_l sum_k T_b[k][l] * G[k][(b,l)]; this thread takes
-            // k = sub, sub + 4, ... of row r (fixed order -> deterministic).
-            // The first 8 of its T values are fetched before the barrier.
             const uint32_t* tbp = A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps + l;
-            uint32_t th[8], tl[8];
+            double s_acc = 0.0;  // this thread's share of S_T over the chunks
+            for (int c = 0; c < NC; ++c, ++phase) {
+                const bool last_phase = j + 1 == nslots && c + 1 == NC;
+                for (int it = 0; it < ITO; ++it, ++t) {
+                    const int d = t & 1;
+                    if (!last_phase && it == ITO - 1) {
+                        // the next phase's one-hot, quarter by quarter as this
+                        // tile's MMAs release the current A
+                        if (kq(c, sub) < kq(c, sub + 1)) {
+                            mb_wait(b_kbf + 8 * sub, phase & 1u);
+                            fence_after();
+                        }
+                        if (c + 1 < NC) {
+                            gen(j, c + 1);
+                        } else {
+                            if (CSM) epi_sync();  // staging of j+1 complete
+                            gen(j + 1, 0);
+                        }
+                        ET(e_gen);
+                    }
+                    // cluster ids of the 32 columns i = it*128 + sub*32 + k
+                    uint4 ca = make_uint4(0, 0, 0, 0), cz = ca;
+                    if (live) {
+                        const uint4* cp = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32);
+                        ca = cp[0];
+                        cz = cp[1];
+                    }
+                    mb_wait(b_accf + 8 * d, (t >> 1) & 1);
+                    ET(e_wait);
+                    fence_after();
+                    const uint32_t dcol = tmem + lane_base + kYAcc0 + d * 128 + sub * 32;
+                    uint32_t v0[16], v1[16];
+                    ld16(dcol, v0);
+                    ld16(dcol + 16, v1);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    ET(e_ld);
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) arrive_remote(L_acce + 8 * d);  // accumulator may be overwritten
+                    if (live && !(A.dbg & 1)) {
+                        // G[c_i][r] += D[r][i]: exact integer bins, this row's own
+                        // (4 column-quarter warps share a row, hence the atomics)
+                        const uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cz.x, cz.y, cz.z, cz.w};
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = sub + 4 * u;
-                const bool ok = live && k < p;
-                th[u] = ok ? __ldg(tbp + k * A.ps) : 0u;
-                tl[u] = ok ? __ldg(tbp + (p + k) * A.ps) : 0u;
-            }
-            epi_sync();  // every bin of the unit is complete
-            double s = 0.0;
-            if (live) {
+                        for (int k = 0; k < 32; ++k) {
+                            const uint32_t cc = __byte_perm(cw[k >> 2], 0u, 0x4440u + (k & 3));
+                            const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
+                            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(bin_r + cc * 512u),
+                                         "r"(dv)
+                                         : "memory");
+                        }
+                    }
+                    ET(e_cmp);
+                }
+                // this chunk's bins into S_T: sum_k T_b[k][l] * G_c[k][(b,l)] over
+                // k = sub, sub + 4, ... (fixed order -> deterministic); one chunk's
+                // bins stay below 2^32 (<= 255 * 1024 * n, n <= 16384).  The first
+                // 8 T values are fetched before the barrier.
+                uint32_t th[8], tl[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int k = sub + 4 * u;
-                    if (k < p) {
+                    const bool ok = live && k < p;
+                    th[u] = ok ? __ldg(tbp + k * A.ps) : 0u;
+                    tl[u] = ok ? __ldg(tbp + (p + k) * A.ps) : 0u;
+                }
+                epi_sync();  // every bin of the chunk is complete
+                if (live) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int k = sub + 4 * u;
+                        if (k < p) {
+                            const uint32_t g = bins[k * 128 + r];
+                            bins[k * 128 + r] = 0u;
+                            s_acc = fma((double)g, __hiloint2double((int)th[u], (int)tl[u]), s_acc);
+                        }
+                    }
+                    for (int k = sub + 32; k < p; k += 4) {
                         const uint32_t g = bins[k * 128 + r];
                         bins[k * 128 + r] = 0u;
-                        s = fma((double)g, __hiloint2double((int)th[u], (int)tl[u]), s);
+                        s_acc = fma((double)g,
+                                    __hiloint2double((int)__ldg(tbp + k * A.ps),
+                                                     (int)__ldg(tbp + (p + k) * A.ps)),
+                                    s_acc);
                     }
                 }
-                for (int k = sub + 32; k < p; k += 4) {
-                    const uint32_t g = bins[k * 128 + r];
-                    bins[k * 128 + r] = 0u;
-                    s = fma((double)g,
-                            __hiloint2double((int)__ldg(tbp + k * A.ps), (int)__ldg(tbp + (p + k) * A.ps)),
-                            s);
-                }
+                if (c + 1 == NC) red[sub * 128 + r] = s_acc;
+                epi_sync();  // bins zeroed before the next chunk's atomics (and red written)
+                ET(e_st);
             }
-            red[sub * 128 + r] = s;
-            epi_sync();
             // one warp per individual: lanes stride its 4p partials, then a
             // butterfly (fixed order -> deterministic)
             for (int b2 = (warp - kYEpiWarp0); b2 < nind; b2 += kYEpiThreads / 32) {
@@ -532,7 +573,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     }
     fence_before();
     __syncthreads();
-    cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
+    cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
     if (warp == 0) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -550,14 +591,19 @@ static int p_ipt(int p) {
     return ipt > kYMaxIpt ? kYMaxIpt : ipt;
 }
 
-static size_t p_fixed_bytes(int p, int npad) {  // everything but the W ring
-    const int ipt = p_ipt(p);
-    return 1024 + 2 * p_C_bytes(ipt, npad) + (size_t)p * 512 + 4 * 128 * 8 +
-           (2 * kYMaxStages + 12) * 8 + 16;
+// stage a unit's cluster rows in shared memory when the double buffer is small
+static bool p_csm(int p, int npad) {
+    const char* e = getenv("HUBGPU_TCP_CSM");  // tuning override: 0 disables
+    if (e && atoi(e) == 0) return false;
+    return 2 * p_C_bytes(p_ipt(p), npad) <= 48 * 1024;
 }
 
-// W ring depth: as deep as shared memory allows (TMA latency from L2 under load
-// is well above the few hundred cycles one stage's MMAs take)
+static size_t p_fixed_bytes(int p, int npad) {  // everything but the W ring
+    return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) + (size_t)p * 512 +
+           4 * 128 * 8 + (2 * kYMaxStages + 12) * 8 + 16;
+}
+
+// W ring depth: as deep as shared memory allows
 static int p_kbs() {
     const char* e = getenv("HUBGPU_TCP_KBS");  // tuning override
     const int k = e ? atoi(e) : 8;
@@ -578,14 +624,17 @@ size_t tcp_smem_bytes(int p, int npad) {
 }
 
 bool tcp_supported(int n, int p, int npad) {
-    return p >= 1 && p <= 128 && round_up(n, 128) <= 1024 && npad <= 1024 &&
+    // p <= 128: a unit's one-hot rows fit the 128 TMEM lanes; n <= 16384: a
+    // chunk's u32 bins cannot overflow
+    return p >= 1 && p <= 128 && n >= 1 && n <= 16384 && npad % 128 == 0 &&
            p_stages(p, npad) >= 2;
 }
 
 static int g_tcp_pairs = 0;  // co-resident clusters (cudaOccupancyMaxActiveClusters)
 
 int prepare_fitness_tcp(int p, int npad) {
-    HG_CUDA(cudaFuncSetAttribute(k_fitness_tcp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = p_csm(p, npad) ? k_fitness_tcp<true> : k_fitness_tcp<false>;
+    HG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)tcp_smem_bytes(p, npad)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kYCluster);
@@ -599,7 +648,7 @@ int prepare_fitness_tcp(int p, int npad) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nc = 0;
-    HG_CUDA(cudaOccupancyMaxActiveClusters(&nc, k_fitness_tcp, &cfg));
+    HG_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
     g_tcp_pairs = nc;
     return HG_OK;
 }
@@ -618,10 +667,12 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     A.npad = I.npad;
     A.ipt = p_ipt(I.p);
     A.units = ceil_div(B, A.ipt);
-    A.IT = (int)(round_up(I.n, 128) / 128);
-    A.acols = A.IT * 32;
+    A.ITO = (int)(round_up(I.n, 128) / 128);
+    A.KBT = A.ITO;
+    A.NC = (A.KBT + kYChunkKB - 1) / kYChunkKB;
     A.stages = p_stages(I.p, I.npad);
     A.kbs = p_kbs();
+    A.csm = p_csm(I.p, I.npad) ? 1 : 0;
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
     A.timing = tc_timing_buffer();
     {
@@ -647,7 +698,10 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    HG_CUDA(cudaLaunchKernelEx(&cfg, k_fitness_tcp, map, A));
+    if (A.csm)
+        HG_CUDA(cudaLaunchKernelEx(&cfg, k_fitness_tcp<true>, map, A));
+    else
+        HG_CUDA(cudaLaunchKernelEx(&cfg, k_fitness_tcp<false>, map, A));
     return HG_OK;
 }
 

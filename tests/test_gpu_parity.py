@@ -176,16 +176,17 @@ class TestKernels:
         d = inst.device()
         assert d.flags & 4 and d.fitness_kernel == "tensor-pair"
         big = hg.generate_urand(1100, 20, 3, (1.0, 0.75, 1.0))
-        assert big.device().fitness_kernel == "tensor-smem"  # n > 1024: one-hot in smem
+        assert big.device().fitness_kernel == "tensor-pair"  # K chunks of 1024 nodes
         with pytest.raises(ValueError, match="n <= 1024"):
-            big.device().set_fitness(5)
+            big.device().set_fitness(4)  # the one-CTA TMEM kernel keeps n <= 1024
         frac = hg.Instance(inst.n, inst.p, inst.dist, inst.flow * 0.5, 1.0, 0.75, 1.0)
         assert frac.device().fitness_kernel == "fp64"
         with pytest.raises(ValueError, match="tensor-core"):
             frac.device().set_fitness(2)
 
     @pytest.mark.parametrize("n,p", [(1000, 20), (200, 10), (129, 50), (77, 3), (256, 1),
-                                     (300, 17), (1024, 128), (640, 7)])
+                                     (300, 17), (1024, 128), (640, 7), (1025, 20), (2100, 9),
+                                     (3000, 60)])
     def test_tensor_equals_fp64(self, n, p):
         inst = hg.generate_urand(n, p, 21, (2.0, 0.6, 1.5))
         pop = hg.random_population(n, p, 301, key=4)  # odd: a pair's dummy unit
@@ -195,8 +196,9 @@ class TestKernels:
         for kind in (3, 4, 5):  # smem one-hot, TMEM one-hot, CTA pair
             try:
                 d.set_fitness(kind)
-            except ValueError as e:  # the smem one-hot kernel stops short of p = 128
-                assert kind == 3 and p > 64 and "does not fit" in str(e)
+            except ValueError as e:  # smem one-hot: p <= ~100; TMEM one-CTA: n <= 1024
+                assert (kind == 3 and p > 64 and "does not fit" in str(e)) or (
+                    kind == 4 and n > 1024 and "n <= 1024" in str(e)), (kind, str(e))
                 continue
             tc = hg.evaluate_population(inst, pop)
             assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
