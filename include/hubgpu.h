@@ -154,8 +154,20 @@ typedef struct {
     int32_t pop_size;       /* even, >= 2                               */
     int32_t strength;       /* perturbation swaps, 1..p                 */
     int32_t strict_paper;   /* 0 elitist (default), 1 strict            */
+    int32_t rng;            /* HG_RNG_REPLAY (default) or HG_RNG_PHILOX */
     uint64_t seed;          /* GaParams.seed reduced mod 2^64           */
 } hg_ga_params;
+
+/* draw generator of the island GA.  REPLAY: the reference's SplitMix64
+ * streams, draw k = mix64(s + k*gamma) -- trajectories equal the reference's.
+ * PHILOX: Philox4x32-10 keyed by the same per-(island, role) stream key, with
+ * the draw index as counter -- the same draw accounting and operators, a
+ * different (and independent) stream of numbers. */
+#define HG_RNG_REPLAY 0
+#define HG_RNG_PHILOX 1
+/* Philox4x32-10 block (Salmon et al., SC'11), the GA's PHILOX generator;
+ * host-side entry for known-answer tests */
+void hg_philox4x32_10(const uint32_t key[2], const uint32_t ctr[4], uint32_t out[4]);
 
 int hg_ga_create(hg_inst* inst, const hg_ga_params* params, hg_ga** out);
 void hg_ga_free(hg_ga* ga);

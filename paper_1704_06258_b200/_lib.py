@@ -22,6 +22,7 @@ HG_OK, HG_EARG, HG_ECUDA, HG_ENODEV, HG_ESTATE = 0, 1, 2, 3, 4
 HG_HOST, HG_DEVICE = 0, 1
 FLAG_SYMMETRIC, FLAG_WEIGHTS_EXACT, FLAG_TENSOR_OK = 1, 2, 4
 FIT_AUTO, FIT_FP64, FIT_TENSOR, FIT_TC_SMEM, FIT_TC_TMEM, FIT_TC_PAIR = 0, 1, 2, 3, 4, 5
+RNG_MODES = {"replay": 0, "philox": 1}  # hg_ga_params.rng
 FIT_NAMES = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR,
              "tensor-smem": FIT_TC_SMEM, "tensor-tmem": FIT_TC_TMEM, "tensor-pair": FIT_TC_PAIR}
 
@@ -36,7 +37,7 @@ _vp = C.c_void_p
 class GaParamsC(C.Structure):
     _fields_ = [("islands_total", C.c_int32), ("island_lo", C.c_int32),
                 ("island_hi", C.c_int32), ("pop_size", C.c_int32),
-                ("strength", C.c_int32), ("strict_paper", C.c_int32),
+                ("strength", C.c_int32), ("strict_paper", C.c_int32), ("rng", C.c_int32),
                 ("seed", C.c_uint64)]
 
 
@@ -79,6 +80,8 @@ SIGNATURES = {
     "hg_ga_launches_per_generation": (C.c_int, [_vp]),
     "hg_generate_urand": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, _f64p, _f64p]),
     "hg_restricted_optimum": (C.c_int, [_vp, C.c_uint64, _i64p, _f64p, _u64p]),
+    "hg_philox4x32_10": (None, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                C.POINTER(C.c_uint32)]),
 }
 
 _lib = None
@@ -307,13 +310,13 @@ class DeviceGa:
     """Islands [lo, hi) of an island-GA run on one device (hg_ga)."""
 
     def __init__(self, dinst: DeviceInstance, islands_total: int, lo: int, hi: int,
-                 pop_size: int, strength: int, strict: bool, seed: int):
+                 pop_size: int, strength: int, strict: bool, seed: int, rng: str = "replay"):
         lib = load()
         self.dinst = dinst
         self.lo, self.hi = lo, hi
         self.pop = pop_size
         prm = GaParamsC(islands_total, lo, hi, pop_size, strength, 1 if strict else 0,
-                        seed & ((1 << 64) - 1))
+                        RNG_MODES[rng], seed & ((1 << 64) - 1))
         h = _vp()
         check(lib.hg_ga_create(dinst.handle, C.byref(prm), C.byref(h)))
         self.handle = h
@@ -401,3 +404,12 @@ def restricted_optimum(dinst: "DeviceInstance", limit: int):
     check(load().hg_restricted_optimum(dinst.handle, int(limit), ptr(hubs, _i64p), C.byref(raw),
                                        C.byref(count)))
     return hubs, raw.value, count.value
+
+
+def philox4x32_10(key, ctr) -> list[int]:
+    """One Philox4x32-10 block (the GA's rng='philox' generator), host side."""
+    k = (C.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    c = (C.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    out = (C.c_uint32 * 4)()
+    load().hg_philox4x32_10(k, c, out)
+    return list(out)

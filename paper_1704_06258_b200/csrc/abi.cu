@@ -909,6 +909,8 @@ int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
            "pop_size must be even for pairwise crossover, got %d", prm->pop_size);
     HG_ARG(prm->strength >= 1 && prm->strength <= I.p, "perturb_strength %d exceeds p=%d",
            prm->strength, I.p);
+    HG_ARG(prm->rng == HG_RNG_REPLAY || prm->rng == HG_RNG_PHILOX, "unknown rng mode %d",
+           prm->rng);
     HG_TRY(set_device(inst->device));
     hg_ga* ga = new (std::nothrow) hg_ga();
     if (!ga) {
@@ -936,6 +938,7 @@ int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
         G.pop = prm->pop_size;
         G.strength = prm->strength;
         G.strict_mode = prm->strict_paper ? 1 : 0;
+        G.rng = prm->rng == HG_RNG_PHILOX ? HG_RNG_PHILOX : HG_RNG_REPLAY;
         G.island_lo = prm->island_lo;
         const size_t B = (size_t)ga->B, nw = (size_t)I.nw, p = (size_t)I.p;
         if ((rc = ga_alloc(ga, &G.anc, nloc * nw))) break;
@@ -1076,6 +1079,12 @@ int hg_ga_draw_counters(hg_ga* ga, uint64_t* counters) {
                             cudaMemcpyDeviceToHost, ga->inst->stream));
     HG_CUDA(cudaStreamSynchronize(ga->inst->stream));
     return HG_OK;
+}
+
+void hg_philox4x32_10(const uint32_t key[2], const uint32_t ctr[4], uint32_t out[4]) {
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    philox4x32_10(key[0], key[1], c);
+    for (int i = 0; i < 4; ++i) out[i] = c[i];
 }
 
 int hg_ga_launches_per_generation(const hg_ga* ga) {

@@ -176,6 +176,7 @@ int launch_swap_given(int64_t B, int n, int nw, uint32_t* bits, const int64_t* r
 struct GaDev {
     int n, p, nw;
     int nloc, pop, strength, strict_mode;
+    int rng;              // HG_RNG_REPLAY / HG_RNG_PHILOX
     int island_lo;
     uint32_t* anc;        // [nloc][nw]
     uint32_t* popbits;    // [B][nw]
@@ -213,6 +214,35 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // k-th output (1-based) of the stream whose state is s
 __host__ __device__ __forceinline__ uint64_t sm_draw(uint64_t s, uint64_t k) {
     return mix64(s + k * kGolden);
+}
+
+// Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11): 10 rounds of two
+// 32x32->64 multiplies with the key bumped by the Weyl constants between rounds
+__host__ __device__ __forceinline__ void philox4x32_10(uint32_t k0, uint32_t k1, uint32_t c[4]) {
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+    }
+}
+
+// the GA's k-th draw of the stream with key s: SplitMix64 replay (mode 0) or
+// Philox4x32-10 keyed by s with counter (k, 0) (mode 1)
+__host__ __device__ __forceinline__ uint64_t ga_draw(int mode, uint64_t s, uint64_t k) {
+    if (mode == 0) return sm_draw(s, k);
+    uint32_t c[4] = {(uint32_t)k, (uint32_t)(k >> 32), 0u, 0u};
+    philox4x32_10((uint32_t)s, (uint32_t)(s >> 32), c);
+    return (uint64_t)c[0] | ((uint64_t)c[1] << 32);
 }
 
 // int(random() * bound) with random() = (x >> 11) * 2^-53 (hm/rng.py:74-82)

@@ -499,8 +499,8 @@ __global__ void k_build_pop(GaDev G) {
         const uint64_t s = G.st[li * 3 + 0];
         const uint64_t base = G.ctr[li * 3 + 0] + (uint64_t)(m - e) * G.strength * 2;
         for (int k = 0; k < G.strength; ++k) {
-            const int r1 = below(sm_draw(s, base + 2 * k + 1), p);
-            const int r2 = below(sm_draw(s, base + 2 * k + 2), n - p);
+            const int r1 = below(ga_draw(G.rng, s, base + 2 * k + 1), p);
+            const int r2 = below(ga_draw(G.rng, s, base + 2 * k + 2), n - p);
             const int pc = warp_select(mk, nw, n, r1, true, lane);
             const int po = warp_select(mk, nw, n, r2, false, lane);
             if (lane == 0) {
@@ -533,7 +533,8 @@ __global__ void k_crossover(GaDev G) {
     const int li = (int)(gid / half), j = (int)(gid - (int64_t)li * half);
     const int n = G.n, nw = G.nw;
     int cut = n;  // n == 1: both children are copies, no draw
-    if (n > 1) cut = 1 + below(sm_draw(G.st[li * 3 + 1], G.ctr[li * 3 + 1] + j + 1), n - 1);
+    if (n > 1)
+        cut = 1 + below(ga_draw(G.rng, G.st[li * 3 + 1], G.ctr[li * 3 + 1] + j + 1), n - 1);
     const int64_t ia = (int64_t)li * G.pop + 2 * j;
     const uint32_t* a = G.popbits + ia * nw;
     const uint32_t* bb = a + nw;
@@ -619,8 +620,8 @@ __global__ void k_mutate(GaDev G) {
     __syncwarp();
     const uint64_t s = G.st[li * 3 + 2];
     const uint64_t base = G.ctr[li * 3 + 2] + 2ull * (uint64_t)G.moff[gid];
-    const int r1 = below(sm_draw(s, base + 1), cnt);
-    const int r2 = below(sm_draw(s, base + 2), n - cnt);
+    const int r1 = below(ga_draw(G.rng, s, base + 1), cnt);
+    const int r2 = below(ga_draw(G.rng, s, base + 2), n - cnt);
     const int pc = warp_select(mk, nw, n, r1, true, lane);
     const int po = warp_select(mk, nw, n, r2, false, lane);  // closed list before closing
     if (lane == 0) {

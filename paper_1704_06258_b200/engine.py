@@ -53,6 +53,10 @@ class GaParams:
     seed: int = 0
     perturb_strength: int | None = None
     strict_paper: bool = False
+    # draw generator: "replay" = the reference's SplitMix64 streams (identical
+    # trajectories); "philox" = Philox4x32-10 on the same stream keys and draw
+    # accounting (an independent stream; not part of the reference API)
+    rng: str = "replay"
 
     def __post_init__(self):
         for label in ("islands", "pop_size", "inner_iters", "outer_iters"):
@@ -61,6 +65,8 @@ class GaParams:
                 raise ValueError(f"{label} must be >= 1, got {v}")
         if self.pop_size % 2:
             raise ValueError(f"pop_size must be even for pairwise crossover, got {self.pop_size}")
+        if self.rng not in ("replay", "philox"):
+            raise ValueError(f"rng must be 'replay' or 'philox', got {self.rng!r}")
         if self.perturb_strength is not None and self.perturb_strength < 1:
             raise ValueError(f"perturb_strength must be >= 1, got {self.perturb_strength}")
 
@@ -95,7 +101,7 @@ class DeviceIslands:
         self.params = params
         self.lo, self.hi = lo, hi
         self.ga = _lib.DeviceGa(inst.device(), params.islands, lo, hi, params.pop_size,
-                                strength, params.strict_paper, params.seed)
+                                strength, params.strict_paper, params.seed, params.rng)
 
     def run_round(self, ancestor_hubs: np.ndarray, audit=None):
         """One outer round: N1 generations from the ancestor.  Returns the

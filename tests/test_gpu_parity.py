@@ -496,3 +496,33 @@ class TestCli:
         rc, _ = self._run(["gen", "-n", str(int(n)), "-p", str(int(p)), "--seed", str(int(seed)),
                            "--alpha", repr(float(alpha)), "-o", str(out), "--device"], capsys)
         assert rc == 0 and out.read_bytes() == g["gen1_bytes"].tobytes()
+
+
+class TestPhilox:
+    """rng='philox': the same operators and draw accounting on Philox4x32-10
+    streams -- deterministic, shard-invariant, feasible, elitist-monotone."""
+
+    def test_philox_ga(self):
+        from paper_1704_06258_b200 import engine
+
+        inst = hg.generate_urand(200, 10, 1704, (3.0, 0.75, 2.0))
+        params = hg.GaParams(islands=12, pop_size=16, inner_iters=4, outer_iters=3, seed=3,
+                             rng="philox")
+        a = hg.solve(inst, params, hg.FitnessMode.STANDARD_MILLI)
+        b = hg.solve(inst, params, hg.FitnessMode.STANDARD_MILLI)
+        assert a.trace == b.trace and np.array_equal(a.best_solution.hubs, b.best_solution.hubs)
+        assert hg.validate(a.best_solution, inst).ok
+        assert all(y <= x for x, y in zip(a.trace, a.trace[1:]))
+        rep = hg.solve(inst, hg.GaParams(islands=12, pop_size=16, inner_iters=4, outer_iters=3,
+                                         seed=3), hg.FitnessMode.STANDARD_MILLI)
+        assert rep.evaluations == a.evaluations
+        # sharding the islands does not change the philox run either
+        for world in (2, 3):
+            shards = [engine.DeviceIslands(inst, params, params.resolved_strength(inst.p),
+                                           *hg.island_shard(12, r, world)) for r in range(world)]
+            anc = np.sort(inst.middle_rank[:inst.p])
+            full = engine.DeviceIslands(inst, params, params.resolved_strength(inst.p), 0, 12)
+            ref_raw, ref_hubs = full.run_round(anc)
+            parts = [s.run_round(anc) for s in shards]
+            assert np.array_equal(np.concatenate([r for r, _ in parts]), ref_raw)
+            assert np.array_equal(np.concatenate([h for _, h in parts]), ref_hubs)

@@ -190,3 +190,21 @@ def test_bench_reference_arm_line():
         assert key in line, key
     assert line["impl"] == "reference" and line["steps"] == 2 and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_philox_known_answers():
+    """The GA's optional Philox4x32-10 generator (rng='philox') against the
+    Random123 known-answer vectors (host entry of the same inline function the
+    kernels use)."""
+    kat = [([0, 0], [0, 0, 0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+           ([0xFFFFFFFF] * 2, [0xFFFFFFFF] * 4, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+           ([0xA4093822, 0x299F31D0], [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+            [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1])]
+    for key, ctr, want in kat:
+        assert _lib.philox4x32_10(key, ctr) == want
+
+
+def test_rng_mode_validated():
+    with pytest.raises(ValueError, match="rng must be"):
+        hg.GaParams(rng="mt19937")
+    assert hg.GaParams().rng == "replay"
