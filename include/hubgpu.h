@@ -186,6 +186,11 @@ int hg_ga_draw_counters(hg_ga* ga, uint64_t* counters);
 /* kernels launched per generation */
 int hg_ga_launches_per_generation(const hg_ga* ga);
 
+/* page-locked host memory (cudaHostAlloc / cudaFreeHost): result buffers the
+ * device can write by DMA directly (the Python layer pools them) */
+int hg_host_alloc(size_t bytes, void** out);
+void hg_host_free(void* p);
+
 /* device generator.  generate_urand (hm/io.py:188-210)
  * bit for bit on the GPU: the SplitMix64 stream derive_stream(seed, n, p)
  * is counter-based, so every element computes its own draws.  Fills the host

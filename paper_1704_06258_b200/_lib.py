@@ -82,6 +82,8 @@ SIGNATURES = {
     "hg_restricted_optimum": (C.c_int, [_vp, C.c_uint64, _i64p, _f64p, _u64p]),
     "hg_philox4x32_10": (None, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                 C.POINTER(C.c_uint32)]),
+    "hg_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
+    "hg_host_free": (None, [_vp]),
 }
 
 _lib = None
@@ -223,7 +225,9 @@ class DeviceInstance:
                  unique: bool = False) -> np.ndarray:
         hubs = np.ascontiguousarray(hubs, dtype=np.int64).reshape(-1, self.p)
         B = hubs.shape[0]
-        out = np.empty((B, 4), dtype=np.float64)
+        # results land by DMA in a pooled page-locked buffer (a pageable
+        # destination costs the driver a staging copy)
+        out = pinned_array((B, 4), np.float64)
         if unique and alloc is None:
             groups = C.c_int64()
             check(load().hg_evaluate_unique(self.handle, B, ptr(hubs, _i64p), ptr(out, _f64p),
@@ -413,3 +417,51 @@ def philox4x32_10(key, ctr) -> list[int]:
     out = (C.c_uint32 * 4)()
     load().hg_philox4x32_10(k, c, out)
     return list(out)
+
+
+# ---------------------------------------------------------------------------
+# pooled page-locked result buffers
+# ---------------------------------------------------------------------------
+
+
+class _PinnedPool:
+    """Page-locked blocks by size; a block returns to the pool when the numpy
+    array built on it (and every view of it) is garbage-collected."""
+
+    KEEP = 8  # cached free blocks per size
+
+    def __init__(self):
+        self._free: dict[int, list[int]] = {}
+        self._lock = threading.Lock()
+
+    def array(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        if nbytes == 0:
+            return np.empty(shape, dtype=dtype)
+        with self._lock:
+            blocks = self._free.get(nbytes)
+            addr = blocks.pop() if blocks else None
+        if addr is None:
+            p = _vp()
+            check(load().hg_host_alloc(nbytes, C.byref(p)))
+            addr = p.value
+        raw = (C.c_char * nbytes).from_address(addr)
+        arr = np.frombuffer(raw, dtype=dtype).reshape(shape)
+        weakref.finalize(arr, self._give_back, nbytes, addr)
+        return arr
+
+    def _give_back(self, nbytes: int, addr: int) -> None:
+        with self._lock:
+            blocks = self._free.setdefault(nbytes, [])
+            if len(blocks) < self.KEEP:
+                blocks.append(addr)
+                return
+        load().hg_host_free(addr)
+
+
+_pinned = _PinnedPool()
+
+
+def pinned_array(shape, dtype) -> np.ndarray:
+    return _pinned.array(shape, dtype)

@@ -1081,6 +1081,17 @@ int hg_ga_draw_counters(hg_ga* ga, uint64_t* counters) {
     return HG_OK;
 }
 
+int hg_host_alloc(size_t bytes, void** out) {
+    HG_ARG(out != nullptr, "NULL argument");
+    *out = nullptr;
+    HG_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+    return HG_OK;
+}
+
+void hg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 void hg_philox4x32_10(const uint32_t key[2], const uint32_t ctr[4], uint32_t out[4]) {
     uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
     philox4x32_10(key[0], key[1], c);

@@ -19,7 +19,7 @@ for _ in range(5):
     hg.evaluate_population(inst, pin)
 
 
-def t(f, reps=50):
+def t(f, reps=100):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(reps):
@@ -27,14 +27,20 @@ def t(f, reps=50):
     return (time.perf_counter() - t0) / reps * 1e6
 
 
-print("evaluate_population pinned  us", t(lambda: hg.evaluate_population(inst, pin)))
-print("evaluate_population pageable us", t(lambda: hg.evaluate_population(inst, pop)))
 out = np.empty((B, 4))
-print("hg_evaluate direct          us", t(lambda: _lib.check(_lib.load().hg_evaluate(
-    d.handle, B, _lib.ptr(pin, _lib._i64p), None, _lib.ptr(out, _lib._f64p)))))
 outp = torch.empty((B, 4), dtype=torch.float64).pin_memory().numpy()
-print("hg_evaluate pinned out      us", t(lambda: _lib.check(_lib.load().hg_evaluate(
-    d.handle, B, _lib.ptr(pin, _lib._i64p), None, _lib.ptr(outp, _lib._f64p)))))
 popd = _lib.DevicePopulation(d, B)
 popd.load_hubs(pop.astype(np.int32))
-print("device evaluate+sync        us", t(lambda: (popd.evaluate(B), d.synchronize())))
+cases = {
+    "evaluate_population (pinned hubs)": lambda: hg.evaluate_population(inst, pin),
+    "evaluate_population (pageable hubs)": lambda: hg.evaluate_population(inst, pop),
+    "hg_evaluate, pageable out": lambda: _lib.check(_lib.load().hg_evaluate(
+        d.handle, B, _lib.ptr(pin, _lib._i64p), None, _lib.ptr(out, _lib._f64p))),
+    "hg_evaluate, pinned out": lambda: _lib.check(_lib.load().hg_evaluate(
+        d.handle, B, _lib.ptr(pin, _lib._i64p), None, _lib.ptr(outp, _lib._f64p))),
+    "device evaluate + sync": lambda: (popd.evaluate(B), d.synchronize()),
+}
+for rep in range(2):
+    for name, f in cases.items():
+        print(f"{name:40s} {t(f):8.1f} us")
+print("pool:", {k: len(v) for k, v in _lib._pinned._free.items()})
