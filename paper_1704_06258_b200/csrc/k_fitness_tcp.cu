@@ -465,9 +465,23 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     const int d = t & 1;
                     if (!last_phase && it == ITO - 1) {
                         // the next phase's one-hot, quarter by quarter as this
-                        // tile's MMAs release the current A
-                        if (kq(c, sub) < kq(c, sub + 1)) {
-                            mb_wait(b_kbf + 8 * sub, phase & 1u);
+                        // tile's MMAs release the current A.  The next quarter
+                        // covers blocks [kq(cn,sub), X); every current-phase MMA
+                        // on blocks < X must be done: wait on the current quarter
+                        // holding block X-1 (in-order MMAs, so every earlier
+                        // quarter is free too) -- chunks of different sizes
+                        // (the last one) have different quarter boundaries
+                        const int cn = c + 1 < NC ? c + 1 : 0;
+                        const int X = kq(cn, sub + 1);
+                        if (kq(cn, sub) < X) {
+                            const int need = X - 1 < nkb(c) ? X - 1 : nkb(c) - 1;
+                            int hq = 3;
+                            for (int h = 0; h < 4; ++h)
+                                if (kq(c, h) <= need && need < kq(c, h + 1)) {
+                                    hq = h;
+                                    break;
+                                }
+                            mb_wait(b_kbf + 8 * hq, phase & 1u);
                             fence_after();
                         }
                         if (c + 1 < NC) {
