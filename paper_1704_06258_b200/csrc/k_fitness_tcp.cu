@@ -342,10 +342,15 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             }
                             commit_pair(b_empty + 8 * s);
                             if (it == ITO - 1)  // last use of this phase's A quarter: free it
-                                for (int h = 0; h < 4; ++h)
-                                    if (kq(c, h + 1) - 1 >= kb0 && kq(c, h + 1) - 1 < kb0 + nk &&
-                                        kq(c, h) < kq(c, h + 1))
-                                        commit_pair(b_kbf + 8 * h);
+                                for (int h = 0; h < 4; ++h) {
+                                    // every kbf[h] completes exactly once per phase
+                                    // (its parity is the phase's), an empty quarter
+                                    // together with the block before it
+                                    const int rb = kq(c, h) < kq(c, h + 1)
+                                                       ? kq(c, h + 1) - 1
+                                                       : (kq(c, h) > 0 ? kq(c, h) - 1 : 0);
+                                    if (rb >= kb0 && rb < kb0 + nk) commit_pair(b_kbf + 8 * h);
+                                }
                             if (++s == (uint32_t)NS) {
                                 s = 0;
                                 ph ^= 1u;

@@ -526,3 +526,23 @@ class TestPhilox:
             parts = [s.run_round(anc) for s in shards]
             assert np.array_equal(np.concatenate([r for r, _ in parts]), ref_raw)
             assert np.array_equal(np.concatenate([h for _, h in parts]), ref_hubs)
+
+
+class TestPairChunks:
+    """K3-TC/P with n > 1024: K chunks of 1024 nodes and a partial last chunk,
+    whose one-hot quarters have different boundaries from a full chunk's.
+    Large batches (many phases per CTA pair) against the fp64 kernel."""
+
+    @pytest.mark.parametrize("n,p,B", [(1030, 5, 4096), (1100, 20, 2048), (2100, 9, 2048),
+                                       (3000, 40, 512)])
+    def test_partial_chunks_many_phases(self, n, p, B):
+        inst = hg.generate_urand(n, p, 77, (1.0, 0.75, 1.0))
+        pop = hg.random_population(n, p, B, key=6)
+        d = inst.device()
+        d.set_fitness(1)
+        fp = hg.evaluate_population(inst, pop)
+        d.set_fitness(5)
+        for _ in range(3):  # repeated launches: a timing race would show up as a mismatch
+            tc = hg.evaluate_population(inst, pop)
+            assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
+            assert close(tc, fp, rel=1e-13)
