@@ -153,11 +153,13 @@ __device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
 __device__ __forceinline__ void epi_sync() {  // named barrier over the 16 epilogue warps
     asm volatile("bar.sync 1, %0;" ::"n"(kYEpiThreads) : "memory");
 }
-// byte-wise (x == l) -> 1 / 0
+// byte-wise (x == l) -> 1 / 0.  Cluster ids and l are < 128, so every byte of
+// y = x ^ l has its top bit clear and y + 0x7F per byte cannot carry: bit 7 of
+// a byte of t is set exactly when that byte of y is nonzero (4 integer ops)
 __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
     const uint32_t y = x ^ lrep;
-    const uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-    return (~(t | y) & 0x80808080u) >> 7;
+    const uint32_t t = y + 0x7F7F7F7Fu;
+    return (~t & 0x80808080u) >> 7;
 }
 
 }  // namespace
