@@ -41,7 +41,8 @@ extern "C" {
 /* instance flags reported by hg_instance_info */
 #define HG_FLAG_SYMMETRIC 1    /* dist == dist^T exactly: one matrix serves both */
 #define HG_FLAG_WEIGHTS_EXACT 2 /* out+in flow integer-valued, total < 2^53      */
-#define HG_FLAG_TENSOR_OK 4     /* flows integers in [0,255]: exact u8 tensor path */
+#define HG_FLAG_TENSOR_OK 4     /* flows non-negative integers < 2^32 (p <= 128):
+                                   exact u8 tensor path on 1..4 byte planes of W  */
 
 /* fitness kernel choice (hg_instance_set_fitness) */
 #define HG_FIT_AUTO 0      /* tensor cores when exact, else the fp64 gather   */

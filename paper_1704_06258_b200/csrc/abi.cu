@@ -434,39 +434,52 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         if (rc) break;
         rc = prepare_allocate(I);
         if (rc) break;
-        // K3-TC eligibility: every flow an integer in [0, 255] -> exact u8 GEMM
-        bool u8 = p >= 1 && p <= 128;
-        for (size_t x = 0; u8 && x < nn; ++x) {
+        // K3-TC eligibility: every flow a non-negative integer below 2^32 ->
+        // exact u8 GEMMs on P byte planes of W (P = 1 when every flow < 256;
+        // the smem and one-CTA TMEM kernels take P = 1 only)
+        bool intw = p >= 1 && p <= 128;
+        double wmax = 0.0;
+        for (size_t x = 0; intw && x < nn; ++x) {
             const double v = flow[x];
-            if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v))) u8 = false;
+            if (!(v >= 0.0 && v < 4294967296.0 && v == std::floor(v))) intw = false;
+            wmax = v > wmax ? v : wmax;
         }
-        if (u8) {
+        int P = 1;
+        while (P < 4 && wmax >= std::ldexp(1.0, 8 * P)) ++P;
+        I.wplanes = P;
+        if (intw) {
             const int nt = (int)round_up(n, 128);
-            std::vector<uint8_t> w8((size_t)nt * nt, 0);
-            for (int i = 0; i < n; ++i)
-                for (int j = 0; j < n; ++j) w8[(size_t)i * nt + j] = (uint8_t)flow[(size_t)i * n + j];
+            // planes stacked by rows: plane d holds byte d of every flow
+            std::vector<uint8_t> w8((size_t)P * nt * nt, 0);
+            for (int d = 0; d < P; ++d)
+                for (int i = 0; i < n; ++i)
+                    for (int j = 0; j < n; ++j)
+                        w8[((size_t)d * nt + i) * nt + j] =
+                            (uint8_t)((uint64_t)flow[(size_t)i * n + j] >> (8 * d));
             chk(cudaMalloc(&inst->dW8, w8.size()), "cudaMalloc(W8)");
             chk(cudaMemcpy(inst->dW8, w8.data(), w8.size(), cudaMemcpyHostToDevice), "H2D W8");
             if (rc) break;
-            rc = tc_make_wmap(inst->dW8, nt, 128, inst->wmap);
-            if (rc) break;
-            rc = tc_make_wmap(inst->dW8, nt, 128 / kTcyCluster, inst->wmapq);
-            if (rc) break;
-            if (tc_supported(p)) {
-                rc = prepare_fitness_tc(p);
-                if (rc) break;
-                inst->tcx_ok = true;
-            }
             const char* var = getenv("HUBGPU_TC_VARIANT");  // tuning override: "x" | "y" | "p"
-            if (tcy_supported(n, p, I.npad) && !(var && var[0] == 'x')) {
-                rc = prepare_fitness_tcy(p, I.npad);
+            if (P == 1) {
+                rc = tc_make_wmap(inst->dW8, nt, 128, inst->wmap);
                 if (rc) break;
-                inst->tcy_ok = true;
+                rc = tc_make_wmap(inst->dW8, nt, 128 / kTcyCluster, inst->wmapq);
+                if (rc) break;
+                if (tc_supported(p)) {
+                    rc = prepare_fitness_tc(p);
+                    if (rc) break;
+                    inst->tcx_ok = true;
+                }
+                if (tcy_supported(n, p, I.npad) && !(var && var[0] == 'x')) {
+                    rc = prepare_fitness_tcy(p, I.npad);
+                    if (rc) break;
+                    inst->tcy_ok = true;
+                }
             }
-            if (tcp_supported(n, p, I.npad) && !(var && (var[0] == 'x' || var[0] == 'y'))) {
-                rc = tc_make_wmap(inst->dW8, nt, 64, inst->wmapp);
+            if (tcp_supported(n, p, I.npad, P) && !(var && (var[0] == 'x' || var[0] == 'y'))) {
+                rc = tc_make_wmap(inst->dW8, nt, 64, inst->wmapp, P * nt);
                 if (rc) break;
-                rc = prepare_fitness_tcp(p, I.npad);
+                rc = prepare_fitness_tcp(p, I.npad, P);
                 if (rc) break;
                 inst->tcp_ok = true;
             }
@@ -525,11 +538,13 @@ int hg_instance_set_fitness(hg_inst* inst, int kind) {
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_ARG(kind >= HG_FIT_AUTO && kind <= HG_FIT_TC_PAIR, "unknown fitness kernel %d", kind);
     HG_ARG(kind < HG_FIT_TENSOR || inst->tc_ok,
-           "tensor-core fitness needs integer flows in [0, 255] and p <= 128");
+           "tensor-core fitness needs non-negative integer flows below 2^32 and p <= 128");
     HG_ARG(kind != HG_FIT_TC_SMEM || inst->tcx_ok,
-           "the smem one-hot tensor-core kernel does not fit p = %d", inst->I.p);
+           "the smem one-hot tensor-core kernel does not fit p = %d (or flows >= 256)",
+           inst->I.p);
     HG_ARG(kind != HG_FIT_TC_TMEM || inst->tcy_ok,
-           "the TMEM-resident tensor-core kernel needs n <= 1024 (and was not disabled)");
+           "the TMEM-resident tensor-core kernel needs n <= 1024 and flows < 256 (and was not "
+           "disabled)");
     HG_ARG(kind != HG_FIT_TC_PAIR || inst->tcp_ok,
            "the CTA-pair tensor-core kernel needs n <= 16384 (and was not disabled)");
     inst->fit_kind = kind;

@@ -62,6 +62,7 @@ struct DevInst {
     int ps;        // row stride (uint32 words) of the T hi/lo planes: p rounded up to 4
     int npad;      // row stride (bytes) of cluster-id rows
     int weights_exact;
+    int wplanes;   // byte planes of the u8 flow tensor W8 (1 when every flow < 256)
     double chi, alpha, delta;
     const double* C;
     const double* Ct;
@@ -122,7 +123,8 @@ int prepare_fitness_tc(int p);
 int tc_timing_read(unsigned long long* out32);
 unsigned long long* tc_timing_buffer();  // HUBGPU_TC_TIMING=1, else nullptr
 // map_out: CUtensorMap (128 B) over the u8 W, boxes of 128 K bytes x box_rows rows
-int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out);
+// rows: total rows of the (plane-stacked) tensor, default npad_tc
+int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out, int rows = 0);
 #ifndef HG_TCY_CLUSTER
 #define HG_TCY_CLUSTER 1
 #endif
@@ -136,9 +138,10 @@ int prepare_fitness_tcy(int p, int npad);
 int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
                        const uint32_t* T, double* part, int grid, cudaStream_t s);
 // K3-TC/P (k_fitness_tcp.cu): the same on CTA pairs (cta_group::2, M = 256)
-bool tcp_supported(int n, int p, int npad);
-size_t tcp_smem_bytes(int p, int npad);
-int prepare_fitness_tcp(int p, int npad);
+// P: byte planes of W (integer flows < 256^P), stacked in the u8 tensor
+bool tcp_supported(int n, int p, int npad, int P);
+size_t tcp_smem_bytes(int p, int npad, int P);
+int prepare_fitness_tcp(int p, int npad, int P);
 int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
                        const uint32_t* T, double* part, int grid, cudaStream_t s);
 

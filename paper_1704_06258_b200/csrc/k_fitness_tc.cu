@@ -503,14 +503,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out) {
+int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out, int rows) {
     auto enc = get_encode();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable");
         return HG_ECUDA;
     }
     CUtensorMap* m = static_cast<CUtensorMap*>(map_out);
-    cuuint64_t dims[2] = {(cuuint64_t)npad_tc, (cuuint64_t)npad_tc};
+    cuuint64_t dims[2] = {(cuuint64_t)npad_tc, (cuuint64_t)(rows > 0 ? rows : npad_tc)};
     cuuint64_t strides[1] = {(cuuint64_t)npad_tc};
     cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};

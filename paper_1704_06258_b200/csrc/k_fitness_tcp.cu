@@ -177,6 +177,8 @@ struct PArgs {
     int ipt;          // individuals per unit (ipt * p <= 128)
     int64_t units;
     int ITO;          // 128-row W tiles (output columns i)
+    int P;            // byte planes of W (flows < 256^P): tiles per phase = P * ITO
+    int nt;           // W rows per plane in the stacked u8 tensor
     int KBT;          // 128-node K blocks in all
     int NC;           // K chunks of <= 8 blocks (1024 nodes): one resident one-hot each
     int stages;       // W ring depth
@@ -197,6 +199,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int p = A.p, ipt = A.ipt, ITO = A.ITO, KBT = A.KBT, NC = A.NC;
+    const int NT = A.P * ITO;  // tiles per phase: every (plane, W row block)
     unsigned char* ring = smem;                                          // W stages
     const int NS = A.stages, KBS = A.kbs;
     unsigned char* var = smem + NS * KBS * kYStageBytes;
@@ -206,8 +209,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     const size_t cb = CSM ? p_C_bytes(ipt, A.npad) : 0;
     unsigned char* sC0 = var;
     var += 2 * cb;
-    uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [p][128] cluster-pair flow bins
-    var += (size_t)p * 512;
+    uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [P][p][128] cluster-pair flow bins
+    var += (size_t)A.P * p * 512;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
@@ -223,7 +226,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     auto kq = [&](int c, int h) { return h * nkb(c) / 4; };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int x = tid; x < p * 128; x += kYThreads) bins[x] = 0u;
+    for (int x = tid; x < A.P * p * 128; x += kYThreads) bins[x] = 0u;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mb_init(b_full + 8 * s, 1);
@@ -273,8 +276,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             const int q = (int)crank * 64;  // this CTA's W rows within a tile
             for (int64_t j = 0; j < nslots; ++j)
                 for (int c = 0; c < NC; ++c)
-                    for (int it = 0; it < ITO; ++it)
+                    for (int tt = 0; tt < NT; ++tt)
                         for (int kb0 = 0; kb0 < nkb(c); kb0 += KBS) {
+                            const int pl = tt / ITO, it = tt - pl * ITO;
                             const int nk = nkb(c) - kb0 < KBS ? nkb(c) - kb0 : KBS;
                             // stage s is free: the leader's MMAs reading it completed
                             if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
@@ -283,8 +287,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             const uint32_t dst = su32(ring + s * (KBS * kYStageBytes));
                             for (int kk = 0; kk < nk; ++kk)
                                 tma2d_pair(dst + kk * kYStageBytes, &tmW,
-                                           (c * kYChunkKB + kb0 + kk) * 128, it * 128 + q,
-                                           L_full + 8 * s);
+                                           (c * kYChunkKB + kb0 + kk) * 128,
+                                           pl * A.nt + it * 128 + q, L_full + 8 * s);
                             if (++s == (uint32_t)NS) {
                                 s = 0;
                                 ph ^= 1u;
@@ -310,7 +314,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             for (int64_t j = 0; j < nslots; ++j) {
                 for (int c = 0; c < NC; ++c, ++phase) {
                     const int nb = nkb(c);
-                    for (int it = 0; it < ITO; ++it, ++t) {
+                    for (int tt = 0; tt < NT; ++tt, ++t) {
                         const int d = t & 1;
                         if (t >= 2 && !(A.dbg & 64))
                             mb_wait_cl(b_acce + 8 * d, ((t >> 1) - 1) & 1);
@@ -319,7 +323,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         const uint32_t dcol = tmem + kYAcc0 + d * 128;
                         for (int kb0 = 0; kb0 < nb; kb0 += KBS) {
                             const int nk = nb - kb0 < KBS ? nb - kb0 : KBS;
-                            if (it == 0 && !(A.dbg & 64)) {
+                            if (tt == 0 && !(A.dbg & 64)) {
                                 // first use of this phase's A: its quarters must be in TMEM
                                 for (int h = 0; h < 4; ++h)
                                     if (kq(c, h) >= kb0 && kq(c, h) < kb0 + nk &&
@@ -343,7 +347,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                 }
                             }
                             commit_pair(b_empty + 8 * s);
-                            if (it == ITO - 1)  // last use of this phase's A quarter: free it
+                            if (tt == NT - 1)  // last use of this phase's A quarter: free it
                                 for (int h = 0; h < 4; ++h) {
                                     // every kbf[h] completes exactly once per phase
                                     // (its parity is the phase's), an empty quarter
@@ -468,9 +472,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             double s_acc = 0.0;  // this thread's share of S_T over the chunks
             for (int c = 0; c < NC; ++c, ++phase) {
                 const bool last_phase = j + 1 == nslots && c + 1 == NC;
-                for (int it = 0; it < ITO; ++it, ++t) {
+                for (int tt = 0; tt < NT; ++tt, ++t) {
                     const int d = t & 1;
-                    if (!last_phase && it == ITO - 1) {
+                    const int pl = tt / ITO, it = tt - pl * ITO;
+                    if (!last_phase && tt == NT - 1) {
                         // the next phase's one-hot, quarter by quarter as this
                         // tile's MMAs release the current A.  The next quarter
                         // covers blocks [kq(cn,sub), X); every current-phase MMA
@@ -526,7 +531,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         for (int k = 0; k < 32; ++k) {
                             const uint32_t cc = __byte_perm(cw[k >> 2], 0u, 0x4440u + (k & 3));
                             const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
-                            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(bin_r + cc * 512u),
+                            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(
+                                             bin_r + (uint32_t)pl * (uint32_t)p * 512u + cc * 512u),
                                          "r"(dv)
                                          : "memory");
                         }
@@ -547,22 +553,29 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 }
                 epi_sync();  // every bin of the chunk is complete
                 if (live) {
+                    // plane pl of W carries weight 256^pl: an exact power-of-2
+                    // scaling of T, so each product is the one-plane product
+                    for (int pl = 0; pl < A.P; ++pl) {
+                        uint32_t* bp = bins + (size_t)pl * p * 128;
+                        const double sc = ldexp(1.0, 8 * pl);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int k = sub + 4 * u;
-                        if (k < p) {
-                            const uint32_t g = bins[k * 128 + r];
-                            bins[k * 128 + r] = 0u;
-                            s_acc = fma((double)g, __hiloint2double((int)th[u], (int)tl[u]), s_acc);
+                        for (int u = 0; u < 8; ++u) {
+                            const int k = sub + 4 * u;
+                            if (k < p) {
+                                const uint32_t g = bp[k * 128 + r];
+                                bp[k * 128 + r] = 0u;
+                                s_acc = fma((double)g,
+                                            __hiloint2double((int)th[u], (int)tl[u]) * sc, s_acc);
+                            }
                         }
-                    }
-                    for (int k = sub + 32; k < p; k += 4) {
-                        const uint32_t g = bins[k * 128 + r];
-                        bins[k * 128 + r] = 0u;
-                        s_acc = fma((double)g,
-                                    __hiloint2double((int)__ldg(tbp + k * A.ps),
-                                                     (int)__ldg(tbp + (p + k) * A.ps)),
-                                    s_acc);
+                        for (int k = sub + 32; k < p; k += 4) {
+                            const uint32_t g = bp[k * 128 + r];
+                            bp[k * 128 + r] = 0u;
+                            s_acc = fma((double)g,
+                                        __hiloint2double((int)__ldg(tbp + k * A.ps),
+                                                         (int)__ldg(tbp + (p + k) * A.ps)) * sc,
+                                        s_acc);
+                        }
                     }
                 }
                 if (c + 1 == NC) red[sub * 128 + r] = s_acc;
@@ -619,8 +632,8 @@ static bool p_csm(int p, int npad) {
     return 2 * p_C_bytes(p_ipt(p), npad) <= 48 * 1024;
 }
 
-static size_t p_fixed_bytes(int p, int npad) {  // everything but the W ring
-    return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) + (size_t)p * 512 +
+static size_t p_fixed_bytes(int p, int npad, int P) {  // everything but the W ring
+    return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) + (size_t)P * p * 512 +
            4 * 128 * 8 + (2 * kYMaxStages + 12) * 8 + 16;
 }
 
@@ -631,8 +644,8 @@ static int p_kbs() {
     return k >= 1 && k <= 8 ? k : 8;
 }
 
-static int p_stages(int p, int npad) {
-    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad);
+static int p_stages(int p, int npad, int P) {
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P);
     int64_t s = room / ((int64_t)p_kbs() * kYStageBytes);
     if (s > kYMaxStages) s = kYMaxStages;
     const char* e = getenv("HUBGPU_TCP_STAGES");  // tuning override (shallower only)
@@ -640,27 +653,27 @@ static int p_stages(int p, int npad) {
     return (int)s;
 }
 
-size_t tcp_smem_bytes(int p, int npad) {
-    return p_fixed_bytes(p, npad) + (size_t)p_stages(p, npad) * p_kbs() * kYStageBytes;
+size_t tcp_smem_bytes(int p, int npad, int P) {
+    return p_fixed_bytes(p, npad, P) + (size_t)p_stages(p, npad, P) * p_kbs() * kYStageBytes;
 }
 
-bool tcp_supported(int n, int p, int npad) {
+bool tcp_supported(int n, int p, int npad, int P) {
     // p <= 128: a unit's one-hot rows fit the 128 TMEM lanes; n <= 16384: a
     // chunk's u32 bins cannot overflow
     return p >= 1 && p <= 128 && n >= 1 && n <= 16384 && npad % 128 == 0 &&
-           p_stages(p, npad) >= 2;
+           P >= 1 && P <= 4 && p_stages(p, npad, P) >= 2;
 }
 
 static int g_tcp_pairs = 0;  // co-resident clusters (cudaOccupancyMaxActiveClusters)
 
-int prepare_fitness_tcp(int p, int npad) {
+int prepare_fitness_tcp(int p, int npad, int P) {
     auto kern = p_csm(p, npad) ? k_fitness_tcp<true> : k_fitness_tcp<false>;
     HG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tcp_smem_bytes(p, npad)));
+                                 (int)tcp_smem_bytes(p, npad, P)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kYCluster);
     cfg.blockDim = dim3(kYThreads);
-    cfg.dynamicSmemBytes = tcp_smem_bytes(p, npad);
+    cfg.dynamicSmemBytes = tcp_smem_bytes(p, npad, P);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kYCluster;
@@ -691,7 +704,9 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     A.ITO = (int)(round_up(I.n, 128) / 128);
     A.KBT = A.ITO;
     A.NC = (A.KBT + kYChunkKB - 1) / kYChunkKB;
-    A.stages = p_stages(I.p, I.npad);
+    A.P = I.wplanes;
+    A.nt = (int)round_up(I.n, 128);
+    A.stages = p_stages(I.p, I.npad, A.P);
     A.kbs = p_kbs();
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -710,7 +725,7 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3(kYThreads);
-    cfg.dynamicSmemBytes = tcp_smem_bytes(I.p, I.npad);
+    cfg.dynamicSmemBytes = tcp_smem_bytes(I.p, I.npad, A.P);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -546,3 +546,34 @@ class TestPairChunks:
             tc = hg.evaluate_population(inst, pop)
             assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
             assert close(tc, fp, rel=1e-13)
+
+
+class TestWidePlanes:
+    """Integer flows above 255: K3-TC/P on 2..4 byte planes of W (exact), the
+    one-plane kernels unavailable, results equal to the fp64 kernel."""
+
+    @pytest.mark.parametrize("wmax,planes", [(300, 2), (70000, 3), (2**24 + 5, 4)])
+    def test_planes_match_fp64(self, wmax, planes):
+        base = hg.generate_urand(700, 12, 5, (1.0, 0.75, 1.0))
+        rng = np.random.default_rng(planes)
+        flow = rng.integers(0, wmax + 1, size=(700, 700)).astype(np.float64)
+        np.fill_diagonal(flow, 0.0)
+        flow[3, 4] = float(wmax)
+        inst = hg.Instance(700, 12, base.dist, flow, 1.0, 0.75, 1.0)
+        d = inst.device()
+        assert d.flags & 4 and d.fitness_kernel == "tensor-pair"
+        with pytest.raises(ValueError, match="flows"):
+            d.set_fitness(4)  # the one-CTA TMEM kernel takes one plane only
+        pop = hg.random_population(700, 12, 999, key=2)
+        tc = hg.evaluate_population(inst, pop)
+        d.set_fitness(1)
+        fp = hg.evaluate_population(inst, pop)
+        assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
+        assert close(tc, fp, rel=1e-13)
+
+    def test_flows_from_2_32_use_fp64(self):
+        base = hg.generate_urand(50, 4, 5, (1.0, 0.75, 1.0))
+        flow = base.flow.copy()
+        flow[1, 2] = 2.0**32
+        inst = hg.Instance(50, 4, base.dist, flow, 1.0, 0.75, 1.0)
+        assert inst.device().fitness_kernel == "fp64"
