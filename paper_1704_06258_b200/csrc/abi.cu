@@ -213,14 +213,6 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
     return HG_OK;
 }
 
-int h2d_i64_as_i32(hg_inst* inst, DevBuf& tmp, const int64_t* host, int64_t count, int32_t* dst) {
-    if (count <= 0) return HG_OK;
-    HG_TRY(tmp.ensure((size_t)count * sizeof(int64_t)));
-    HG_CUDA(cudaMemcpyAsync(tmp.ptr, host, (size_t)count * sizeof(int64_t), cudaMemcpyHostToDevice,
-                            inst->stream));
-    return launch_i64_to_i32(tmp.as<int64_t>(), dst, count, inst->stream);
-}
-
 // host hub sets / allocations in, validated on the device (see k_hubs_in)
 int h2d_hubs_checked(hg_inst* inst, DevBuf& tmp, const int64_t* host, int64_t B, int32_t* dst) {
     const int64_t count = B * inst->I.p;

@@ -95,7 +95,6 @@ FitPlan fitness_plan(const DevInst& I, int sm_count);
 int prepare_fitness(const FitPlan& P);
 
 // ---- launchers (k_eval.cu) -------------------------------------------------
-int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStream_t s);
 int launch_hubs_in(const int64_t* src, int32_t* dst, int64_t B, int p, int n, int* err,
                    cudaStream_t s);
 int launch_idx_in(const int64_t* src, int32_t* dst, int64_t count, int n, int* err,

@@ -20,12 +20,6 @@ namespace hg {
 // small utilities
 // ----------------------------------------------------------------------------
 
-__global__ void k_i64_to_i32(const int64_t* __restrict__ s, int32_t* __restrict__ d, int64_t m) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x)
-        d[i] = (int32_t)s[i];
-}
-
 __global__ void k_i32_to_i64(const int32_t* __restrict__ s, int64_t* __restrict__ d, int64_t m) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -80,13 +74,6 @@ int launch_idx_in(const int64_t* src, int32_t* dst, int64_t count, int n, int* e
                   cudaStream_t s) {
     if (count <= 0) return HG_OK;
     k_idx_in<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count, n, err);
-    HG_CUDA(cudaGetLastError());
-    return HG_OK;
-}
-
-int launch_i64_to_i32(const int64_t* src, int32_t* dst, int64_t count, cudaStream_t s) {
-    if (count <= 0) return HG_OK;
-    k_i64_to_i32<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count);
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }

@@ -60,14 +60,6 @@ __device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int x, int y,
-                                      uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(map), "r"(x), "r"(y), "r"(bar)
-        : "memory");
-}
 // one quarter of a W tile, multicast into the same smem offset of every CTA of
 // the cluster; each destination's mbarrier (same offset) gets the bytes
 __device__ __forceinline__ void tma2d_mc(uint32_t dst, const CUtensorMap* map, int x, int y,
