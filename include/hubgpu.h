@@ -172,6 +172,10 @@ void hg_philox4x32_10(const uint32_t key[2], const uint32_t ctr[4], uint32_t out
 
 int hg_ga_create(hg_inst* inst, const hg_ga_params* params, hg_ga** out);
 void hg_ga_free(hg_ga* ga);
+/* restart the run with another seed: stream states derive_stream(seed, island,
+ * role) and draw counters reset, buffers and the captured graph reused (a
+ * solve() on the same instance and shape needs no new allocation) */
+int hg_ga_reseed(hg_ga* ga, uint64_t seed);
 /* start an outer round: every local island's ancestor := hubs (p sorted int64) */
 int hg_ga_begin_round(hg_ga* ga, const int64_t* ancestor_hubs);
 /* queue `count` generations (one CUDA graph launch each); asynchronous */

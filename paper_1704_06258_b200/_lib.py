@@ -72,6 +72,7 @@ SIGNATURES = {
     "hg_swap": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _i64p, _i64p, _u8p]),
     "hg_ga_create": (C.c_int, [_vp, C.POINTER(GaParamsC), C.POINTER(_vp)]),
     "hg_ga_free": (None, [_vp]),
+    "hg_ga_reseed": (C.c_int, [_vp, C.c_uint64]),
     "hg_ga_begin_round": (C.c_int, [_vp, _i64p]),
     "hg_ga_generations": (C.c_int, [_vp, C.c_int]),
     "hg_ga_round_results": (C.c_int, [_vp, _f64p, _i64p]),
@@ -329,6 +330,9 @@ class DeviceGa:
     @property
     def n_local(self) -> int:
         return self.hi - self.lo
+
+    def reseed(self, seed: int) -> None:
+        check(load().hg_ga_reseed(self.handle, seed & ((1 << 64) - 1)))
 
     def begin_round(self, hubs: np.ndarray) -> None:
         hubs = np.ascontiguousarray(hubs, dtype=np.int64)

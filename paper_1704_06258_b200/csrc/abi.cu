@@ -1023,6 +1023,25 @@ void hg_ga_free(hg_ga* ga) {
     inst_release(inst);
 }
 
+int hg_ga_reseed(hg_ga* ga, uint64_t seed) {
+    HG_ARG(ga != nullptr, "GA is NULL");
+    hg_inst* inst = ga->inst;
+    HG_TRY(set_device(inst->device));
+    const int nloc = ga->prm.island_hi - ga->prm.island_lo;
+    std::vector<uint64_t> st((size_t)nloc * 3), zero((size_t)nloc * 3, 0);
+    for (int li = 0; li < nloc; ++li)
+        for (int role = 0; role < 3; ++role) {
+            uint64_t keys[2] = {(uint64_t)(ga->prm.island_lo + li), (uint64_t)role};
+            st[(size_t)li * 3 + role] = host_stream_key(seed, keys, 2);
+        }
+    cudaStream_t s = inst->stream;
+    HG_CUDA(cudaMemcpyAsync(ga->G.st, st.data(), st.size() * 8, cudaMemcpyHostToDevice, s));
+    HG_CUDA(cudaMemcpyAsync(ga->G.ctr, zero.data(), zero.size() * 8, cudaMemcpyHostToDevice, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    ga->prm.seed = seed;
+    return HG_OK;
+}
+
 int hg_ga_begin_round(hg_ga* ga, const int64_t* ancestor_hubs) {
     HG_ARG(ga && ancestor_hubs, "NULL argument");
     HG_TRY(set_device(ga->inst->device));

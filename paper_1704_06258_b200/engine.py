@@ -100,8 +100,20 @@ class DeviceIslands:
         self.inst = inst
         self.params = params
         self.lo, self.hi = lo, hi
-        self.ga = _lib.DeviceGa(inst.device(), params.islands, lo, hi, params.pop_size,
-                                strength, params.strict_paper, params.seed, params.rng)
+        # one hg_ga per (instance, islands, shard, shape): a later solve() with
+        # the same shape reseeds it instead of allocating and capturing anew
+        dinst = inst.device()
+        cache = dinst.__dict__.setdefault("_ga_cache", {})
+        key = (params.islands, lo, hi, params.pop_size, strength, params.strict_paper,
+               params.rng)
+        ga = cache.get(key)
+        if ga is None:
+            ga = _lib.DeviceGa(dinst, params.islands, lo, hi, params.pop_size, strength,
+                               params.strict_paper, params.seed, params.rng)
+            cache[key] = ga
+        else:
+            ga.reseed(params.seed)
+        self.ga = ga
 
     def run_round(self, ancestor_hubs: np.ndarray, audit=None):
         """One outer round: N1 generations from the ancestor.  Returns the
