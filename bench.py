@@ -34,7 +34,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "fitness evals/sec at n=1000,p=20 (1-8 B200); GA time-to-best-cost vs CPU ref"
 KERNEL_NAMES = {
-    "tensor-pair": "k_fitness_tcp (K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs + integer bins)",
+    "tensor-pair": "k_fitness_tcp (K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs + integer bins + fused finalise)",
     "tensor-tmem": "k_fitness_tcy (K3-TC/Y: u8 one-hot GEMM, one-hot in TMEM + integer bins)",
     "tensor-smem": "k_fitness_tc (K3-TC/X: u8 one-hot GEMM, one-hot in smem + fp64 epilogue)",
     "fp64": "k_fitness (K3: fp64 smem gather)",
@@ -430,7 +430,7 @@ def run_gpu(args):
                     "h2d_bytes_per_step": int(pop_host.nbytes),
                     "d2h_bytes_per_step": int(res.nbytes),
                     "api": "paper_1704_06258_b200.evaluate_population (hg_evaluate)"},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": (2 if fit_kernel == "tensor-pair" else 3) * args.steps,
             "clocks": clk,
             "ga": {"child_evals_per_s": world * 128 * 64 / (ga_ms * 1e-3),
                    "ms_per_generation": ga_ms, "config": "R=128 x pop 64 per GPU, strength 3",

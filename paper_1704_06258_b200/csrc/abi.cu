@@ -178,10 +178,9 @@ int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* c
     cudaStream_t s = inst->stream;
     const int kind = fitness_kernel(inst);
     int tiles;
-    if (kind == HG_FIT_TC_PAIR) {
-        HG_TRY(launch_fitness_tcp(I, inst->wmapp, B, cl, T, part, inst->sm_count, s));
-        tiles = 1;
-    } else if (kind == HG_FIT_TC_TMEM) {
+    if (kind == HG_FIT_TC_PAIR)  // finaliser fused into the kernel
+        return launch_fitness_tcp(I, inst->wmapp, B, cl, T, part, inst->sm_count, s, legs, out);
+    if (kind == HG_FIT_TC_TMEM) {
         HG_TRY(launch_fitness_tcy(I, inst->wmapq, B, cl, T, part, inst->sm_count, s));
         tiles = 1;
     } else if (kind == HG_FIT_TC_SMEM) {
@@ -886,7 +885,8 @@ int ga_queue_generation(hg_ga* ga) {
     return HG_OK;
 }
 
-constexpr int kGaLaunches = 9;
+// build_pop, crossover, mut_scan, mutate, correct, allocate, fitness, [finalise,] select
+int ga_launches(const hg_ga* ga) { return fitness_kernel(ga->inst) == HG_FIT_TC_PAIR ? 8 : 9; }
 
 void ga_release(hg_ga* ga) {
     if (ga->exec) cudaGraphExecDestroy(ga->exec);
@@ -1125,8 +1125,7 @@ void hg_philox4x32_10(const uint32_t key[2], const uint32_t ctr[4], uint32_t out
 }
 
 int hg_ga_launches_per_generation(const hg_ga* ga) {
-    (void)ga;
-    return kGaLaunches;
+    return ga_launches(ga);
 }
 
 // ---------------------------------------------------------------------------

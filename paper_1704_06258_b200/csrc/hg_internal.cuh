@@ -141,8 +141,10 @@ int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint
 bool tcp_supported(int n, int p, int npad, int P);
 size_t tcp_smem_bytes(int p, int npad, int P);
 int prepare_fitness_tcp(int p, int npad, int P);
+// legs / out set: the finaliser is fused (out gets the 4 cost terms, part unused)
 int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
-                       const uint32_t* T, double* part, int grid, cudaStream_t s);
+                       const uint32_t* T, double* part, int grid, cudaStream_t s,
+                       const double* legs = nullptr, double* out = nullptr);
 
 // ---- k_gen.cu: device generator and hub-set enumeration ---------------------
 // xy: 2n scratch; C / W: n x n (either may be null)

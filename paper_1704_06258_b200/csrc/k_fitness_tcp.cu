@@ -168,7 +168,10 @@ __host__ __device__ inline size_t p_C_bytes(int ipt, int npad) {
 struct PArgs {
     const uint8_t* cl;
     const uint32_t* T;
-    double* part;     // [B][1]: S_T complete per individual
+    double* part;     // [B][1]: S_T complete per individual (when out is null)
+    const double* legs;  // [B][2] spoke-leg sums from K2 (finalise fused when out is set)
+    double* out;         // [B][4] collection, transfer, distribution, raw
+    double chi, alpha, delta;
     int64_t B;
     int n, p, ps, npad;
     int ipt;          // individuals per unit (ipt * p <= 128)
@@ -589,7 +592,21 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 }
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                if (lane == 0) A.part[bbase + b2] = acc;
+                if (lane == 0) {
+                    if (A.out) {
+                        // the finaliser (k_finalize), fused: same operations
+                        const int64_t b = bbase + b2;
+                        const double coll = A.chi * A.legs[2 * b];
+                        const double dist = A.delta * A.legs[2 * b + 1];
+                        const double tran = A.alpha * acc;
+                        A.out[4 * b + 0] = coll;
+                        A.out[4 * b + 1] = tran;
+                        A.out[4 * b + 2] = dist;
+                        A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
+                    } else {
+                        A.part[bbase + b2] = acc;
+                    }
+                }
             }
             ET(e_red);
         }
@@ -685,12 +702,18 @@ int prepare_fitness_tcp(int p, int npad, int P) {
 }
 
 int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
-                       const uint32_t* T, double* part, int grid, cudaStream_t s) {
+                       const uint32_t* T, double* part, int grid, cudaStream_t s,
+                       const double* legs, double* out) {
     if (B <= 0) return HG_OK;
     PArgs A;
     A.cl = cl;
     A.T = T;
     A.part = part;
+    A.legs = legs;
+    A.out = out;
+    A.chi = I.chi;
+    A.alpha = I.alpha;
+    A.delta = I.delta;
     A.B = B;
     A.n = I.n;
     A.p = I.p;
