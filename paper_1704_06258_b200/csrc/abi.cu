@@ -89,6 +89,7 @@ struct hg_inst {
     int32_t* drank = nullptr;
     uint16_t* dCq = nullptr;
     int* derr = nullptr;  // input-validation flag (DevInst::err)
+    int* hflag = nullptr;  // page-locked landing slots for small device->host reads
     hg_pop* scratch = nullptr;
     DevBuf t1, t2, t3, t4;
 };
@@ -391,6 +392,8 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.wOD = inst->dwOD;
         I.rank = inst->drank;
         chk(cudaMalloc(&inst->derr, sizeof(int)), "cudaMalloc(err)");
+        chk(cudaHostAlloc(reinterpret_cast<void**>(&inst->hflag), 4 * sizeof(int),
+                          cudaHostAllocDefault), "cudaHostAlloc(flag)");
         chk(cudaMemsetAsync(inst->derr, 0, sizeof(int), s), "memset(err)");
         I.err = inst->derr;
         I.npad = 16;  // provisional for the plan
@@ -502,6 +505,7 @@ static void inst_destroy(hg_inst* inst) {
     cudaFree(inst->drank);
     cudaFree(inst->dCq);
     cudaFree(inst->derr);
+    if (inst->hflag) cudaFreeHost(inst->hflag);
     cudaFree(inst->dW8);
     inst->t1.release();
     inst->t2.release();
@@ -575,9 +579,10 @@ int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc) {
     HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, P->legs, P->alloc.as<int32_t>(),
                            inst->stream));
     HG_TRY(d2h_i32_as_i64(inst, inst->t2, P->alloc.as<int32_t>(), B * I.n, alloc));
-    int flag = 0;
-    HG_CUDA(cudaMemcpyAsync(&flag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost, inst->stream));
+    HG_CUDA(cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,
+                            inst->stream));
     HG_CUDA(cudaStreamSynchronize(inst->stream));
+    const int flag = inst->hflag[0];
     return check_input_flag(inst, flag, "hub set");
 }
 
@@ -601,9 +606,10 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
     HG_TRY(pop_eval_queue(P, B, a32));
     HG_CUDA(cudaMemcpyAsync(out, P->out, (size_t)B * 4 * sizeof(double), cudaMemcpyDeviceToHost,
                             inst->stream));
-    int flag = 0;
-    HG_CUDA(cudaMemcpyAsync(&flag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost, inst->stream));
+    HG_CUDA(cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,
+                            inst->stream));
     HG_CUDA(cudaStreamSynchronize(inst->stream));
+    const int flag = inst->hflag[0];
     return check_input_flag(inst, flag, alloc ? "solution" : "hub set");
 }
 
@@ -631,7 +637,7 @@ int hg_evaluate_unique(hg_inst* inst, int64_t B, const int64_t* hubs, double* ou
     double* full = reinterpret_cast<double*>(
         w + ((gbytes + (size_t)B * 4 + 16 + 255) & ~size_t(255)));
     HG_TRY(launch_unique_groups(all, B, I.p, w, gbytes, P->hubs, map, dcount, s));
-    int hc[3] = {0, 0, 0};
+    int* hc = inst->hflag;
     HG_CUDA(cudaMemcpyAsync(hc, dcount, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     HG_CUDA(cudaMemcpyAsync(hc + 2, inst->derr, sizeof(int), cudaMemcpyDeviceToHost, s));
     HG_CUDA(cudaStreamSynchronize(s));
@@ -712,8 +718,7 @@ int hg_debug_tc_timing(unsigned long long* out32) {
 }
 
 int hg_pop_launches_per_evaluate(const hg_pop* pop) {
-    (void)pop;
-    return 3;
+    return fitness_kernel(pop->inst) == HG_FIT_TC_PAIR ? 2 : 3;
 }
 
 int hg_pop_last_fitness_ms(hg_pop* pop, float* ms) {

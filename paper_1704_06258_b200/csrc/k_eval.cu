@@ -331,14 +331,22 @@ k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __re
             for (int t = 0; t < 4; ++t)
                 if (i0 + t < n) alloc[b * n + i0 + t] = hs[c4[t]];
     }
-    // hub-to-hub cost table T_b (warp-wide, row by row)
+    // hub-to-hub cost table T_b (lane = column, 8 rows per round: the 8
+    // scattered L2 gathers are in flight together, not 8 round trips)
     uint32_t* Tb = T + b * 2 * (int64_t)p * I.ps;
-    for (int k = 0; k < p; ++k) {
-        const double* crow = I.C + (size_t)hs[k] * n;
+    for (int k0 = 0; k0 < p; k0 += 8) {
         for (int l = lane; l < p; l += 32) {
-            const double v = crow[hs[l]];
-            Tb[k * I.ps + l] = (uint32_t)__double2hiint(v);
-            Tb[(p + k) * I.ps + l] = (uint32_t)__double2loint(v);
+            const int hl = hs[l];
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = k0 + u < p ? __ldg(I.C + (size_t)hs[k0 + u] * n + hl) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k0 + u < p) {
+                    Tb[(k0 + u) * I.ps + l] = (uint32_t)__double2hiint(v[u]);
+                    Tb[(p + k0 + u) * I.ps + l] = (uint32_t)__double2loint(v[u]);
+                }
         }
     }
     so = warp_sum(so);  // fixed butterfly order: deterministic
