@@ -329,8 +329,13 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         };
         chk(cudaMalloc(&inst->dC, nn * 8), "cudaMalloc(dist)");
         chk(cudaMalloc(&inst->dW, nn * 8), "cudaMalloc(flow)");
-        chk(cudaMalloc(&inst->dO, (size_t)n * 8), "cudaMalloc");
-        chk(cudaMalloc(&inst->dD, (size_t)n * 8), "cudaMalloc");
+        // O and D zero-padded to a multiple of 4 nodes (K2 reads them 4 at a time)
+        const size_t n4 = ((size_t)n + 3) & ~size_t(3);
+        chk(cudaMalloc(&inst->dO, n4 * 8), "cudaMalloc");
+        chk(cudaMalloc(&inst->dD, n4 * 8), "cudaMalloc");
+        if (rc) break;
+        chk(cudaMemsetAsync(inst->dO, 0, n4 * 8, s), "memset");
+        chk(cudaMemsetAsync(inst->dD, 0, n4 * 8, s), "memset");
         chk(cudaMalloc(&inst->dwOD, (size_t)n * 8), "cudaMalloc");
         chk(cudaMalloc(&inst->drank, (size_t)n * 4), "cudaMalloc");
         if (rc) break;
@@ -410,13 +415,13 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             }
             const double scale = cmax > cmin ? 65535.0 / (cmax - cmin) : 0.0;
             // rows padded with 0xFFFF to nq = npad (K2 reads whole passes of
-            // nodes unguarded), plus slack for the tail of the last row
+            // nodes unguarded), one all-0xFFFF row n (the register K2's
+            // stand-in for hub slots >= p), plus slack for the tail
             const int nq = I.npad;
-            chk(cudaMalloc(&inst->dCq, ((size_t)n * nq + 2048) * sizeof(uint16_t)),
-                "cudaMalloc(Cq)");
+            const size_t cq_elems = (size_t)(n + 1) * nq + 2048;
+            chk(cudaMalloc(&inst->dCq, cq_elems * sizeof(uint16_t)), "cudaMalloc(Cq)");
             if (rc) break;
-            chk(cudaMemsetAsync(inst->dCq, 0xff, ((size_t)n * nq + 2048) * sizeof(uint16_t), s),
-                "memset(Cq)");
+            chk(cudaMemsetAsync(inst->dCq, 0xff, cq_elems * sizeof(uint16_t), s), "memset(Cq)");
             if (rc) break;
             rc = launch_quantize(inst->dCt, inst->dCq, n, nq, cmin, scale, s);
             if (rc) break;

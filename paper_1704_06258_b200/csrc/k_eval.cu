@@ -223,6 +223,37 @@ __device__ __forceinline__ void min2(unsigned& m1, unsigned& m2, unsigned key) {
     m1 = min(m1, key);
 }
 
+// the end of one individual in K2 (warp-wide): hub-to-hub cost table T_b
+// (lane = column, 8 rows per round: the 8 scattered L2 gathers are in flight
+// together, not 8 round trips) and the two leg sums in a fixed order
+__device__ __forceinline__ void alloc_finish(const DevInst& I, const int32_t* hs, int64_t b,
+                                             int lane, double so, double sd,
+                                             uint32_t* __restrict__ T, double* __restrict__ legs) {
+    const int p = I.p, n = I.n;
+    uint32_t* Tb = T + b * 2 * (int64_t)p * I.ps;
+    for (int k0 = 0; k0 < p; k0 += 8) {
+        for (int l = lane; l < p; l += 32) {
+            const int hl = hs[l];
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = k0 + u < p ? __ldg(I.C + (size_t)hs[k0 + u] * n + hl) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k0 + u < p) {
+                    Tb[(k0 + u) * I.ps + l] = (uint32_t)__double2hiint(v[u]);
+                    Tb[(p + k0 + u) * I.ps + l] = (uint32_t)__double2loint(v[u]);
+                }
+        }
+    }
+    so = warp_sum(so);  // fixed butterfly order: deterministic
+    sd = warp_sum(sd);
+    if (lane == 0) {
+        legs[2 * b] = so;
+        legs[2 * b + 1] = sd;
+    }
+}
+
 __global__ void __launch_bounds__(kAllocThreads)
 k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
            uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
@@ -331,30 +362,146 @@ k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __re
             for (int t = 0; t < 4; ++t)
                 if (i0 + t < n) alloc[b * n + i0 + t] = hs[c4[t]];
     }
-    // hub-to-hub cost table T_b (lane = column, 8 rows per round: the 8
-    // scattered L2 gathers are in flight together, not 8 round trips)
-    uint32_t* Tb = T + b * 2 * (int64_t)p * I.ps;
-    for (int k0 = 0; k0 < p; k0 += 8) {
-        for (int l = lane; l < p; l += 32) {
-            const int hl = hs[l];
-            double v[8];
+    alloc_finish(I, hs, b, lane, so, sd, T, legs);
+}
+
+// K2/R -- the same allocation for p <= 32 with the hub rows of a pass in
+// registers.  Lane = 2 consecutive nodes of a 64-node pass, one u32 load of
+// quantised costs per hub row (slots p..PM-1 read the all-0xFFFF row n).
+// qmin of both nodes by 16x2 SIMD min (VIMNMX3.U16x2); then per hub
+// t = min_u16x2(v - qmin, 1) -- 0 exactly where the hub is at qmin, and
+// v >= qmin so the 32-bit subtraction never borrows across halves -- and
+// acc += t * (256 + k).  With S = sum_k (256 + k) (< 2^16 for PM <= 32),
+// S - acc per half = sum over the hubs at qmin of (256 + k): the count in the
+// high byte, the hub slot in the low byte when the count is 1.  Two passes'
+// results are moved by 4 shuffles into k_allocate's 4-nodes-per-lane layout,
+// so the fp64 leg sums accumulate in k_allocate's order: bit-identical
+// outputs.  A count above 1 is a quantised tie, resolved on the fp64 costs as
+// in k_allocate (first minimum, a hub node is its own hub).
+template <int PM>
+__global__ void __launch_bounds__(kAllocThreads, 4)
+k_allocate_r(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
+             uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
+             int32_t* __restrict__ alloc) {
+    static_assert(PM % 4 == 0 && PM <= 32, "hub slots");
+    __shared__ int32_t hs_all[kAllocWarps][32];
+    __shared__ uint32_t ro_all[kAllocWarps][32];  // element offset of hub slot k's row in Cq
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * kAllocWarps + warp;
+    if (b >= B) return;
+    const int n = I.n, p = I.p, nq = I.nq;
+    int32_t* hs = hs_all[warp];
+    uint32_t* ro = ro_all[warp];
+    const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
+    if (lane < p) hs[lane] = bad ? lane : hubs[b * p + lane];
+    __syncwarp();
+    if (lane < PM) ro[lane] = (uint32_t)(lane < p ? hs[lane] : n) * (uint32_t)nq;
+    __syncwarp();
+    constexpr unsigned S = 256u * PM + PM * (PM - 1) / 2;
+
+    double so = 0.0, sd = 0.0;
+    uint8_t* clb = cl + b * I.npad;
+    const int sl = (2 * lane) & 31;
+    for (int c0 = 0; c0 < I.npad; c0 += 128) {
+        unsigned wv[2];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                v[u] = k0 + u < p ? __ldg(I.C + (size_t)hs[k0 + u] * n + hl) : 0.0;
+        for (int h = 0; h < 2; ++h) {
+            const uint16_t* col = I.Cq + c0 + 64 * h + 2 * lane;
+            unsigned r[PM];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k0 + u < p) {
-                    Tb[(k0 + u) * I.ps + l] = (uint32_t)__double2hiint(v[u]);
-                    Tb[(p + k0 + u) * I.ps + l] = (uint32_t)__double2loint(v[u]);
-                }
+            for (int k = 0; k < PM; ++k)
+                r[k] = __ldg(reinterpret_cast<const unsigned*>(col + ro[k]));
+            unsigned m = r[0];
+#pragma unroll
+            for (int k = 1; k < PM; ++k) m = __vminu2(m, r[k]);
+            unsigned acc = 0;
+#pragma unroll
+            for (int k = 0; k < PM; ++k) acc += __vminu2(r[k] - m, 0x00010001u) * (256u + k);
+            wv[h] = S * 0x00010001u - acc;
         }
+        // lane L takes nodes c0+4L..+3: pass 0 for L < 16, pass 1 above
+        const unsigned a0 = __shfl_sync(0xffffffffu, wv[0], sl);
+        const unsigned a1 = __shfl_sync(0xffffffffu, wv[0], sl + 1);
+        const unsigned b0 = __shfl_sync(0xffffffffu, wv[1], sl);
+        const unsigned b1 = __shfl_sync(0xffffffffu, wv[1], sl + 1);
+        const unsigned w01 = lane < 16 ? a0 : b0, w23 = lane < 16 ? a1 : b1;
+        const unsigned val[4] = {w01 & 0xffffu, w01 >> 16, w23 & 0xffffu, w23 >> 16};
+        const int i0 = c0 + 4 * lane;
+        // fp64 cost of each node's quantised argmin, and its weights (all
+        // loads first; O and D are zero-padded to 4 nodes: two 16-byte loads)
+        double best[4], ow[4] = {0.0, 0.0, 0.0, 0.0}, dw[4] = {0.0, 0.0, 0.0, 0.0};
+        int c4[4];
+        if (i0 < n) {
+            const double2* o2 = reinterpret_cast<const double2*>(I.O + i0);
+            const double2* d2 = reinterpret_cast<const double2*>(I.D + i0);
+            const double2 oa = __ldg(o2), ob = __ldg(o2 + 1), da = __ldg(d2), db = __ldg(d2 + 1);
+            ow[0] = oa.x, ow[1] = oa.y, ow[2] = ob.x, ow[3] = ob.y;
+            dw[0] = da.x, dw[1] = da.y, dw[2] = db.x, dw[3] = db.y;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = i0 + t;
+            c4[t] = (val[t] >> 8) == 1 ? (int)(val[t] & 0xffu) : 0;
+            best[t] = i < n ? I.Ct[(size_t)hs[c4[t]] * n + i] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = i0 + t;
+            if (i < n && (val[t] >> 8) != 1) {
+                // quantised tie: first fp64 minimum among the hubs at qmin,
+                // except that a hub node is always its own hub
+                unsigned qmin = 0xFFFFu;
+                for (int k2 = 0; k2 < p; ++k2)
+                    qmin = min(qmin, (unsigned)I.Cq[(size_t)hs[k2] * nq + i]);
+                int kf = -1;
+                for (int k2 = 0; k2 < p; ++k2) {
+                    const int h = hs[k2];
+                    if (I.Cq[(size_t)h * nq + i] != qmin) continue;
+                    if (kf < 0) {  // k_allocate's m1: the first hub at qmin
+                        kf = k2;
+                        best[t] = I.Ct[(size_t)h * n + i];
+                        if (h == i) break;
+                        continue;
+                    }
+                    if (h == i) {
+                        best[t] = 0.0;
+                        kf = k2;
+                        break;
+                    }
+                    const double d = I.Ct[(size_t)h * n + i];
+                    if (d < best[t]) {
+                        best[t] = d;
+                        kf = k2;
+                    }
+                }
+                c4[t] = kf;
+            }
+            so = fma(ow[t], best[t], so);
+            sd = fma(dw[t], best[t], sd);
+            if (i >= n) c4[t] = 0;
+        }
+        *reinterpret_cast<uint32_t*>(clb + i0) =
+            (uint32_t)c4[0] | ((uint32_t)c4[1] << 8) | ((uint32_t)c4[2] << 16) |
+            ((uint32_t)c4[3] << 24);
+        if (co)
+            *reinterpret_cast<uint2*>(co + b * I.npad + i0) =
+                make_uint2((uint32_t)(c4[0] * 4) | ((uint32_t)(c4[1] * 4) << 16),
+                           (uint32_t)(c4[2] * 4) | ((uint32_t)(c4[3] * 4) << 16));
+        if (alloc)
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (i0 + t < n) alloc[b * n + i0 + t] = hs[c4[t]];
     }
-    so = warp_sum(so);  // fixed butterfly order: deterministic
-    sd = warp_sum(sd);
-    if (lane == 0) {
-        legs[2 * b] = so;
-        legs[2 * b + 1] = sd;
-    }
+    alloc_finish(I, hs, b, lane, so, sd, T, legs);
+}
+
+// tuning / A-B override: HUBGPU_K2_SCALAR=1 keeps k_allocate for every p
+static bool k2_scalar() {
+    static const bool v = [] {
+        const char* e = getenv("HUBGPU_K2_SCALAR");
+        return e != nullptr && atoi(e) != 0;
+    }();
+    return v;
 }
 
 int prepare_allocate(const DevInst&) { return HG_OK; }
@@ -362,8 +509,19 @@ int prepare_allocate(const DevInst&) { return HG_OK; }
 int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
                     uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s) {
     if (B <= 0) return HG_OK;
-    k_allocate<<<(unsigned)ceil_div(B, kAllocWarps), kAllocThreads, 0, s>>>(I, B, hubs, cl, co, T,
-                                                                         legs, alloc);
+    const unsigned grid = (unsigned)ceil_div(B, kAllocWarps);
+    if (I.p <= 32 && (int64_t)(I.n + 1) * I.nq < (int64_t(1) << 31) && !k2_scalar()) {
+        switch ((I.p + 3) & ~3) {
+#define HG_K2R(PM)                                                                            \
+    case PM:                                                                                  \
+        k_allocate_r<PM><<<grid, kAllocThreads, 0, s>>>(I, B, hubs, cl, co, T, legs, alloc); \
+        break;
+            HG_K2R(4) HG_K2R(8) HG_K2R(12) HG_K2R(16) HG_K2R(20) HG_K2R(24) HG_K2R(28) HG_K2R(32)
+#undef HG_K2R
+        }
+    } else {
+        k_allocate<<<grid, kAllocThreads, 0, s>>>(I, B, hubs, cl, co, T, legs, alloc);
+    }
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }
