@@ -54,6 +54,8 @@ SIGNATURES = {
                                    C.POINTER(C.c_int)]),
     "hg_instance_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "hg_instance_set_fitness": (C.c_int, [_vp, C.c_int]),
+    "hg_instance_set_exact": (C.c_int, [_vp, C.c_int]),
+    "hg_instance_exact": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "hg_instance_fitness": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "hg_synchronize": (C.c_int, [_vp]),
     "hg_allocate": (C.c_int, [_vp, C.c_int64, _i64p, _i64p]),
@@ -148,6 +150,21 @@ def set_fitness_default(kind: str) -> None:
     _fit_default = FIT_NAMES[kind]
 
 
+_exact_default = os.environ.get("HUBGPU_EXACT", "0") not in ("", "0")
+
+
+def set_exact_default(on: bool) -> None:
+    """Cost sums in numpy's pairwise order (bit-identical to the reference's
+    np.sum) for every evaluation from now on; off: fixed-order sums within
+    ~1 ulp.  GA objects keep the mode they were created with."""
+    global _exact_default
+    _exact_default = bool(on)
+
+
+def exact_default() -> bool:
+    return _exact_default
+
+
 def set_device(index: int) -> None:
     """Select the CUDA device new device instances are created on."""
     global _device
@@ -201,6 +218,21 @@ class DeviceInstance:
     def set_fitness(self, kind: int) -> None:
         check(load().hg_instance_set_fitness(self.handle, int(kind)))
 
+    def set_exact(self, on: bool) -> None:
+        check(load().hg_instance_set_exact(self.handle, int(bool(on))))
+        self._exact = bool(on)
+
+    @property
+    def exact(self) -> bool:
+        v = C.c_int()
+        check(load().hg_instance_exact(self.handle, C.byref(v)))
+        return bool(v.value)
+
+    def sync_exact(self) -> None:
+        """Follow the module default (set_exact_default)."""
+        if getattr(self, "_exact", None) != _exact_default:
+            self.set_exact(_exact_default)
+
     @property
     def fitness_kernel(self) -> str:
         k = C.c_int()
@@ -224,6 +256,7 @@ class DeviceInstance:
 
     def evaluate(self, hubs: np.ndarray, alloc: np.ndarray | None = None,
                  unique: bool = False) -> np.ndarray:
+        self.sync_exact()
         hubs = np.ascontiguousarray(hubs, dtype=np.int64).reshape(-1, self.p)
         B = hubs.shape[0]
         # results land by DMA in a pooled page-locked buffer (a pageable
@@ -290,6 +323,7 @@ class DevicePopulation:
         check(load().hg_pop_load_hubs(self.handle, int(count), p, where))
 
     def evaluate(self, count: int) -> None:
+        self.dinst.sync_exact()
         check(load().hg_pop_evaluate(self.handle, int(count)))
 
     def read(self, count: int, out=None, where: int = HG_HOST):
@@ -323,6 +357,8 @@ class DeviceGa:
         prm = GaParamsC(islands_total, lo, hi, pop_size, strength, 1 if strict else 0,
                         RNG_MODES[rng], seed & ((1 << 64) - 1))
         h = _vp()
+        dinst.sync_exact()  # the GA keeps the summation mode it is created with
+        self.exact = dinst.exact
         check(lib.hg_ga_create(dinst.handle, C.byref(prm), C.byref(h)))
         self.handle = h
         self._fin = weakref.finalize(self, lib.hg_ga_free, h)
@@ -409,6 +445,7 @@ def restricted_optimum(dinst: "DeviceInstance", limit: int):
     hubs = np.empty(dinst.p, dtype=np.int64)
     raw = C.c_double()
     count = C.c_uint64()
+    dinst.sync_exact()
     check(load().hg_restricted_optimum(dinst.handle, int(limit), ptr(hubs, _i64p), C.byref(raw),
                                        C.byref(count)))
     return hubs, raw.value, count.value

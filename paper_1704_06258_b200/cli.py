@@ -442,6 +442,12 @@ COMMANDS = {"solve": cmd_solve, "eval": cmd_eval, "gen": cmd_gen, "oracle": cmd_
 
 
 def main(argv=None) -> int:
+    # the reference's own numbers, digit for digit: cost sums in numpy's
+    # pairwise order while a command runs
+    from . import _lib
+
+    prev = _lib.exact_default()
+    _lib.set_exact_default(True)
     try:
         ns = build_parser().parse_args(argv)
         return COMMANDS[ns.command](ns)
@@ -457,6 +463,8 @@ def main(argv=None) -> int:
     except RuntimeError as exc:  # no usable GPU / CUDA failure (HubGpuError)
         print(f"error: {exc}", file=sys.stderr)
         return EXIT_DATA
+    finally:
+        _lib.set_exact_default(prev)
 
 
 __all__ = ["main", "build_parser", "params_fingerprint", "read_manifest", "rows_csv",

@@ -87,6 +87,7 @@ struct hg_inst {
     double* dD = nullptr;
     double* dwOD = nullptr;
     int32_t* drank = nullptr;
+    uint8_t* dpw = nullptr;  // pairwise-sum schedules over n and p*p terms
     uint16_t* dCq = nullptr;
     int* derr = nullptr;  // input-validation flag (DevInst::err)
     int* hflag = nullptr;  // page-locked landing slots for small device->host reads
@@ -160,6 +161,36 @@ int scratch_pop(hg_inst* inst, int64_t B, hg_pop** out) {
 }
 
 // the concrete K3 kernel for the instance's choice: HG_FIT_FP64 or HG_FIT_TC_*
+// numpy's pairwise_sum_DOUBLE (PW_BLOCKSIZE 128) as a leaf table for m
+// terms: the halving tree splits at n2 = m/2 - (m/2) % 8, so every leaf
+// starts on a row of 8 terms, holds <= 16 full rows, and only the last leaf
+// has a partial row (m % 8 terms).  Per leaf: first row | full rows << 16 |
+// the tree sums that follow it << 24 (the last leaf's: all that remain).
+static void pw_leaves(int64_t s, int64_t len, std::vector<int64_t>& ls, std::vector<int64_t>& ll,
+                      std::vector<int>& lc) {
+    if (len <= 128) {
+        ls.push_back(s);
+        ll.push_back(len);
+        lc.push_back(0);
+        return;
+    }
+    int64_t n2 = len / 2;
+    n2 -= n2 % 8;
+    pw_leaves(s, n2, ls, ll, lc);
+    pw_leaves(s + n2, len - n2, ls, ll, lc);
+    ++lc.back();  // this node's sum follows its right subtree's last leaf
+}
+
+static std::vector<uint32_t> pw_leaf_table(int64_t m) {
+    std::vector<int64_t> ls, ll;
+    std::vector<int> lc;
+    pw_leaves(0, m, ls, ll, lc);
+    std::vector<uint32_t> t(ls.size());
+    for (size_t k = 0; k < ls.size(); ++k)
+        t[k] = (uint32_t)(ls[k] / 8) | (uint32_t)(ll[k] / 8) << 16 | (uint32_t)lc[k] << 24;
+    return t;
+}
+
 static int fitness_kernel(const hg_inst* inst) {
     int k = inst->fit_kind;
     if (k == HG_FIT_AUTO) k = inst->tc_ok ? HG_FIT_TENSOR : HG_FIT_FP64;
@@ -205,7 +236,8 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
         HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, co_for(inst, P->co), P->T,
                                  P->legs, s));
     else
-        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, co_for(inst, P->co), P->T, P->legs, nullptr,
+        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, co_for(inst, P->co), P->T,
+                               P->legs, nullptr,
                                s));
     HG_CUDA(cudaEventRecord(P->ev0, s));
     HG_TRY(queue_fitness(inst, B, P->cl, P->co, P->T, P->part, P->legs, P->out));
@@ -396,6 +428,20 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.D = inst->dD;
         I.wOD = inst->dwOD;
         I.rank = inst->drank;
+        {
+            const std::vector<uint32_t> pn = pw_leaf_table(n);
+            const std::vector<uint32_t> pl = pw_leaf_table((int64_t)p * p);
+            chk(cudaMalloc(&inst->dpw, (pn.size() + pl.size()) * 4), "cudaMalloc(pw)");
+            if (rc) break;
+            chk(cudaMemcpy(inst->dpw, pn.data(), pn.size() * 4, cudaMemcpyHostToDevice), "H2D pw");
+            chk(cudaMemcpy(inst->dpw + pn.size() * 4, pl.data(), pl.size() * 4,
+                           cudaMemcpyHostToDevice),
+                "H2D pw");
+            I.pwnl = reinterpret_cast<const uint32_t*>(inst->dpw);
+            I.npwnl = (int)pn.size();
+            I.pwl = reinterpret_cast<const uint32_t*>(inst->dpw + pn.size() * 4);
+            I.npwl = (int)pl.size();
+        }
         chk(cudaMalloc(&inst->derr, sizeof(int)), "cudaMalloc(err)");
         chk(cudaHostAlloc(reinterpret_cast<void**>(&inst->hflag), 4 * sizeof(int),
                           cudaHostAllocDefault), "cudaHostAlloc(flag)");
@@ -508,6 +554,7 @@ static void inst_destroy(hg_inst* inst) {
     cudaFree(inst->dD);
     cudaFree(inst->dwOD);
     cudaFree(inst->drank);
+    cudaFree(inst->dpw);
     cudaFree(inst->dCq);
     cudaFree(inst->derr);
     if (inst->hflag) cudaFreeHost(inst->hflag);
@@ -531,6 +578,18 @@ int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags) {
     if (n) *n = inst->I.n;
     if (p) *p = inst->I.p;
     if (flags) *flags = inst->flags | (inst->tc_ok ? HG_FLAG_TENSOR_OK : 0);
+    return HG_OK;
+}
+
+int hg_instance_set_exact(hg_inst* inst, int on) {
+    HG_ARG(inst != nullptr, "instance is NULL");
+    inst->I.exact = on ? 1 : 0;
+    return HG_OK;
+}
+
+int hg_instance_exact(const hg_inst* inst, int* on) {
+    HG_ARG(inst != nullptr && on != nullptr, "NULL argument");
+    *on = inst->I.exact;
     return HG_OK;
 }
 
@@ -581,7 +640,7 @@ int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc) {
     const DevInst& I = inst->I;
     HG_TRY(h2d_hubs_checked(inst, inst->t1, hubs, B, P->hubs));
     HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
-    HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, P->legs, P->alloc.as<int32_t>(),
+    HG_TRY(launch_allocate(I, B, P->hubs, P->cl, P->co, P->T, nullptr, P->alloc.as<int32_t>(),
                            inst->stream));
     HG_TRY(d2h_i32_as_i64(inst, inst->t2, P->alloc.as<int32_t>(), B * I.n, alloc));
     HG_CUDA(cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,

@@ -78,7 +78,19 @@ struct DevInst {
     int nq;
     // input-validation flag of the current host call (0 = ok, else 0x7ffffffe - bad row)
     const int* err;
+    // numpy's pairwise summation order (see pw_leaf_table): the leaves of the
+    // n-term leg sums and of the p*p-term transfer sum, one word per leaf
+    // (first row of 8 terms | rows << 16 | tree sums after it << 24)
+    const uint32_t* pwnl;
+    int npwnl;
+    const uint32_t* pwl;
+    int npwl;
+    // 1: every cost sum in numpy's pairwise order (bit-identical to the
+    // reference); 0: fixed-order sums (deterministic, ~1 ulp apart)
+    int exact;
 };
+
+constexpr int kPwStack = 16;  // tree depth bound (n < 2^21)
 
 // fitness tiling chosen per instance (see fitness_plan)
 struct FitPlan {
@@ -139,7 +151,7 @@ int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint
 // K3-TC/P (k_fitness_tcp.cu): the same on CTA pairs (cta_group::2, M = 256)
 // P: byte planes of W (integer flows < 256^P), stacked in the u8 tensor
 bool tcp_supported(int n, int p, int npad, int P);
-size_t tcp_smem_bytes(int p, int npad, int P);
+size_t tcp_smem_bytes(int p, int npad, int P, bool exact);
 int prepare_fitness_tcp(int p, int npad, int P);
 // legs / out set: the finaliser is fused (out gets the 4 cost terms, part unused)
 int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,

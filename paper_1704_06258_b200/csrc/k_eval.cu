@@ -12,6 +12,8 @@
 
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "hg_internal.cuh"
 
 namespace hg {
@@ -158,28 +160,6 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int NT>
-__device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch) {
-    constexpr int NWARP = NT / 32;
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    a = warp_sum(a);
-    b = warp_sum(b);
-    if (lane == 0) {
-        scratch[warp] = a;
-        scratch[NWARP + warp] = b;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double sa = 0.0, sb = 0.0;
-        for (int w = 0; w < NWARP; ++w) {
-            sa += scratch[w];
-            sb += scratch[NWARP + w];
-        }
-        a = sa;
-        b = sb;
-    }
-}
-
 // ----------------------------------------------------------------------------
 // K2 -- nearest-hub allocation (hm/model.py:202-207)
 //   one WARP per individual; the argmin over the p hubs reads the 16-bit
@@ -189,45 +169,197 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch
 //   spoke-leg sums.
 // ----------------------------------------------------------------------------
 
-constexpr int kAllocThreads = 256;
+constexpr int kPwRingSz = 2 * 8 * 33;  // doubles per warp: 2 streams x 8 columns x 33
 
-// hub-cost table of one individual as two 32-bit planes (hi words, lo words
-// of each fp64 C[h_k][h_l]): [hi: p x ps][lo: p x ps].  A warp gathering one
-// T row at 32 lane-specific columns then touches <= p distinct 4-byte banks
-// per plane -- conflict-free for p <= 32, where an 8-byte gather conflicts
-// between columns c and c+16.
-__device__ __forceinline__ void write_T(const DevInst& I, const int32_t* hs, uint32_t* Tb) {
-    const int p = I.p, n = I.n;
-    for (int x = threadIdx.x; x < p * p; x += kAllocThreads) {
-        const int k = x / p, l = x - k * p;
-        const double v = I.C[(size_t)hs[k] * n + hs[l]];
-        Tb[k * I.ps + l] = (uint32_t)__double2hiint(v);
-        Tb[(p + k) * I.ps + l] = (uint32_t)__double2loint(v);
-    }
-}
+// leg-sum modes: kLegsNone (allocation only), kLegsFast (a fixed-order fma
+// sum per lane + butterfly: deterministic, within an ulp or so of numpy),
+// kLegsExact (numpy's pairwise order, bit-identical to the reference)
+constexpr int kLegsNone = 0, kLegsFast = 1, kLegsExact = 2;
+template <int LM> struct K2 {
+    static constexpr int threads = 256, warps = threads / 32;
+    static constexpr int ring = LM == kLegsExact ? kPwRingSz : 1;
+    static constexpr int stack = LM == kLegsExact ? 2 * kPwStack : 1;
+};
 
 // WARP per individual, no block barriers: the warp sweeps its individual's
-// nodes in chunks of 128 -- lane owns the 4 consecutive nodes c0+4*lane..+3,
-// one 8-byte load of quantised costs per hub row.  Per node and hub the argmin
-// is 4 integer ops: key = (q << 8) | k by one byte permute, then the two
-// smallest keys (m1, m2) by min/max.  m1 is the first hub at the minimal
-// quantised cost; a second hub at that same q is a quantised tie, resolved on
-// the fp64 costs (first minimum, hm/model.py:205).  A hub node's own q is 0
-// (C[h][h] = 0 = cmin), so any competing hub at q = 0 sends it down the tie
-// path, which also applies the self-allocation (hm/model.py:206).  Quantised
-// rows are padded to npad with 0xFFFF, so no node masks are needed.
-constexpr int kAllocWarps = kAllocThreads / 32;
+// nodes in chunks of 128.  Two argmin front ends (below) feed one epilogue in
+// the STRIDED layout -- lane L owns nodes c0 + 32t + L, t = 0..3 -- where
+// the fp64 gathers of each node's cost to its hub touch ~2 lines per hub row
+// per instruction (32 consecutive nodes), the O / D weight loads are
+// coalesced, and the fp64 leg sums accumulate in one fixed order whichever
+// front end ran: the two kernels' outputs are bit-identical.
+// A quantised tie (two hubs at the minimal 16-bit cost q) is resolved on the
+// fp64 costs: the first minimum (hm/model.py:205), and a hub node is its own
+// hub (hm/model.py:206; its own q is 0 = cmin, so a competing hub at q = 0
+// sends it down this path).  Quantised rows are padded to npad with 0xFFFF.
 
 __device__ __forceinline__ void min2(unsigned& m1, unsigned& m2, unsigned key) {
     m2 = min(m2, max(m1, key));
     m1 = min(m1, key);
 }
 
+// one 128-node chunk in the strided layout: kk[t] = hub slot of node
+// c0 + 32t + lane when tie[t] is false; tie[t] = quantised tie
+// numpy's pairwise sum (pairwise_sum_DOUBLE: leaves of <= 128 terms, 8
+// strided accumulators per leaf combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// the last leaf's partial row added in order, leaves summed up the halving
+// tree) replayed per warp, so a device sum is bit-identical to np.sum of the
+// same rounded products.  A chunk's terms are staged in a ring of 32 rows x
+// 8 columns per stream (2 chunks: a leaf of <= 16 rows ends in the chunk
+// just staged and started in it or the one before); when a leaf is complete
+// lanes 0-7 run its 8 column accumulators for stream 0 (collection), lanes
+// 8-15 for stream 1 (distribution), and lanes 0 / 8 sum the leaves on a
+// stack.  Column stride 33 doubles: the 16 chain lanes read 16 distinct bank
+// pairs.
+constexpr int kPwCol = 33;
+static_assert(kPwRingSz == 2 * 8 * kPwCol, "ring size");
+
+struct PwState {
+    int leaf;    // next leaf to sum
+    uint32_t e;  // its table word (prefetched)
+    int depth;   // tree stack depth (warp-uniform)
+};
+
+__device__ __forceinline__ void pw_init(PwState& S, const uint32_t* __restrict__ tab) {
+    S.leaf = 0;
+    S.e = __ldg(tab);
+    S.depth = 0;
+}
+
+// every leaf whose rows are all staged (rows < row_end) is summed.  The 8
+// column accumulators run branch-free over 16 rows: rows past the leaf add
+// +0.0, which leaves a sum of non-negative terms unchanged bit for bit.
+__device__ __forceinline__ void pw_leaves_upto(const uint32_t* __restrict__ tab, int nleaf,
+                                               int nterms, int row_end, PwState& S,
+                                               const double* ring, double* st, int lane) {
+    const int s = lane < 8 ? 0 : 1, j = lane & 7;
+    const double* col = ring + s * 8 * kPwCol + j * kPwCol;
+    double* stk = st + s * kPwStack;
+    const bool top = (lane & 7) == 0 && lane < 16;
+    const int R = nterms >> 3, tail = nterms & 7;
+    while (S.leaf < nleaf) {
+        const uint32_t e = S.e;
+        const int r0 = (int)(e & 0xffffu), nr = (int)((e >> 16) & 0xffu);
+        const bool last = S.leaf == nleaf - 1;
+        if ((last && tail ? R + 1 : r0 + nr) > row_end) break;
+        if (!last) S.e = __ldg(tab + S.leaf + 1);
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = col[(r0 + q) & 31];
+        double acc = nr > 0 ? v[0] : 0.0;
+#pragma unroll
+        for (int q = 1; q < 16; ++q)
+            if (q < nr) acc = __dadd_rn(acc, v[q]);
+        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 4);
+        if (top) {
+            if (last)  // the partial row, term by term
+                for (int u = 0; u < tail; ++u)
+                    acc = acc + ring[s * 8 * kPwCol + u * kPwCol + (R & 31)];
+            stk[S.depth] = acc;
+        }
+        ++S.depth;
+        for (int c = last ? S.depth - 1 : (int)(e >> 24); c > 0; --c, --S.depth)
+            if (top) stk[S.depth - 2] = stk[S.depth - 2] + stk[S.depth - 1];
+        ++S.leaf;
+    }
+}
+
+template <int LM>
+__device__ __forceinline__ void alloc_chunk_out(const DevInst& I, const int32_t* hs, int64_t b,
+                                                int c0, int lane, const int (&kk)[4],
+                                                const bool (&tie)[4], double& so, double& sd,
+                                                PwState& S, double* ring,
+                                                double* st, uint8_t* __restrict__ cl,
+                                                uint16_t* __restrict__ co,
+                                                int32_t* __restrict__ alloc) {
+    const int n = I.n, p = I.p, nq = I.nq;
+    double best[4], ow[4], dw[4];
+    int c4[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // all loads first
+        const int i = c0 + 32 * t + lane;
+        const bool in = i < n;
+        c4[t] = tie[t] ? 0 : kk[t];
+        if (LM != kLegsNone) {
+            best[t] = in ? I.Ct[(size_t)hs[c4[t]] * n + i] : 0.0;
+            ow[t] = in ? I.O[i] : 0.0;
+            dw[t] = in ? I.D[i] : 0.0;
+        } else {
+            best[t] = 0.0;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int i = c0 + 32 * t + lane;
+        if (i < n && tie[t]) {
+            unsigned qmin = 0xFFFFu;
+            for (int k2 = 0; k2 < p; ++k2)
+                qmin = min(qmin, (unsigned)I.Cq[(size_t)hs[k2] * nq + i]);
+            int kf = -1;
+            for (int k2 = 0; k2 < p; ++k2) {
+                const int h = hs[k2];
+                if (I.Cq[(size_t)h * nq + i] != qmin) continue;
+                if (kf < 0) {  // the first hub at qmin
+                    kf = k2;
+                    best[t] = I.Ct[(size_t)h * n + i];
+                    if (h == i) break;
+                    continue;
+                }
+                if (h == i) {
+                    best[t] = 0.0;
+                    kf = k2;
+                    break;
+                }
+                const double d = I.Ct[(size_t)h * n + i];
+                if (d < best[t]) {
+                    best[t] = d;
+                    kf = k2;
+                }
+            }
+            c4[t] = kf;
+        }
+        // the reference's terms out_flow * legs, in_flow * legs (rounded
+        // products) into the ring: node c0 + 32t + lane = row c0/8 + 4t +
+        // lane/8, column lane & 7
+        if (LM == kLegsFast) {
+            so = fma(ow[t], best[t], so);
+            sd = fma(dw[t], best[t], sd);
+        }
+        if (LM == kLegsExact && c0 < n) {
+            // (c0/8) % 32 is 0 or 16: no wrap inside a chunk
+            const int at = (lane & 7) * kPwCol + ((c0 >> 3) & 31) + 4 * t + (lane >> 3);
+            ring[at] = __dmul_rn(ow[t], best[t]);
+            ring[8 * kPwCol + at] = __dmul_rn(dw[t], best[t]);
+        }
+        if (i >= n) c4[t] = 0;
+    }
+    if (LM == kLegsExact && c0 < n) {
+        __syncwarp();
+        pw_leaves_upto(I.pwnl, I.npwnl, n, (c0 >> 3) + 16, S, ring, st, lane);
+        __syncwarp();  // the ring slot is rewritten two chunks on
+    }
+    uint8_t* clb = cl + b * I.npad + c0 + lane;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) clb[32 * t] = (uint8_t)c4[t];
+    if (co)  // byte offsets of the columns in a T plane row (fp64 K3 only)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) co[b * I.npad + c0 + 32 * t + lane] = (uint16_t)(c4[t] * 4);
+    if (alloc)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = c0 + 32 * t + lane;
+            if (i < n) alloc[b * n + i] = hs[c4[t]];
+        }
+}
+
 // the end of one individual in K2 (warp-wide): hub-to-hub cost table T_b
 // (lane = column, 8 rows per round: the 8 scattered L2 gathers are in flight
 // together, not 8 round trips) and the two leg sums in a fixed order
+template <int LM>
 __device__ __forceinline__ void alloc_finish(const DevInst& I, const int32_t* hs, int64_t b,
-                                             int lane, double so, double sd,
+                                             int lane, double so, double sd, const double* st,
                                              uint32_t* __restrict__ T, double* __restrict__ legs) {
     const int p = I.p, n = I.n;
     uint32_t* Tb = T + b * 2 * (int64_t)p * I.ps;
@@ -246,30 +378,44 @@ __device__ __forceinline__ void alloc_finish(const DevInst& I, const int32_t* hs
                 }
         }
     }
-    so = warp_sum(so);  // fixed butterfly order: deterministic
-    sd = warp_sum(sd);
-    if (lane == 0) {
-        legs[2 * b] = so;
-        legs[2 * b + 1] = sd;
+    if (LM == kLegsFast) {
+        so = warp_sum(so);  // fixed butterfly order: deterministic
+        sd = warp_sum(sd);
+    }
+    if (LM != kLegsNone && lane == 0) {
+        legs[2 * b] = LM == kLegsExact ? st[0] : so;
+        legs[2 * b + 1] = LM == kLegsExact ? st[kPwStack] : sd;
     }
 }
 
-__global__ void __launch_bounds__(kAllocThreads)
+// K2 scalar front end (any p <= 255): lane owns the 4 consecutive nodes
+// c0+4*lane..+3, one 8-byte load of quantised costs per hub row.  Per node
+// and hub the argmin is 4 integer ops: key = (q << 8) | k by one byte
+// permute, then the two smallest keys (m1, m2) by min/max; m1's low byte is
+// the first hub at the minimal q, and m2 at the same q is a tie.  The
+// per-node (slot, tie) codes move to the strided layout by 8 shuffles.
+template <int LM>
+__global__ void __launch_bounds__(K2<LM>::threads)
 k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
            uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
            int32_t* __restrict__ alloc) {
-    __shared__ int32_t hs_all[kAllocWarps][kMaxP + 1];
+    __shared__ int32_t hs_all[K2<LM>::warps][kMaxP + 1];
+    __shared__ double pwring[K2<LM>::warps][K2<LM>::ring];   // staged terms (2 streams)
+    __shared__ double pwst[K2<LM>::warps][K2<LM>::stack];   // the two tree stacks
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t b = (int64_t)blockIdx.x * kAllocWarps + warp;
+    const int64_t b = (int64_t)blockIdx.x * K2<LM>::warps + warp;
     if (b >= B) return;
-    const int n = I.n, p = I.p, nq = I.nq;
+    const int p = I.p, nq = I.nq;
     int32_t* hs = hs_all[warp];
+    double* ring = pwring[warp];
+    double* st = pwst[warp];
     const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
     for (int k = lane; k < p; k += 32) hs[k] = bad ? k : hubs[b * p + k];
     __syncwarp();
 
+    PwState S;
+    if (LM == kLegsExact) pw_init(S, I.pwnl);
     double so = 0.0, sd = 0.0;
-    uint8_t* clb = cl + b * I.npad;
     for (int c0 = 0; c0 < I.npad; c0 += 128) {
         const int i0 = c0 + 4 * lane;
         unsigned m1[4], m2[4];
@@ -311,97 +457,74 @@ k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __re
             min2(m1[2], m2[2], __byte_perm(v.y, kk, 0x5104));
             min2(m1[3], m2[3], __byte_perm(v.y, kk, 0x5324));
         }
-        // fp64 cost of each node's quantised argmin, and its weights (all loads first)
-        double best[4], ow[4], dw[4];
+        // code per node: slot | tie << 8, two nodes per word
+        unsigned cw[2];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int i = i0 + t;
-            const bool in = i < n;
-            best[t] = in ? I.Ct[(size_t)hs[m1[t] & 0xffu] * n + i] : 0.0;
-            ow[t] = in ? I.O[i] : 0.0;
-            dw[t] = in ? I.D[i] : 0.0;
-        }
-        int c4[4];
+        for (int h = 0; h < 2; ++h) {
+            unsigned c[2];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int i = i0 + t;
-            int kk = (int)(m1[t] & 0xffu);
-            if (i < n && (m2[t] >> 8) == (m1[t] >> 8) && hs[kk] != i) {
-                // quantised tie: first fp64 minimum among the hubs at q = qmin,
-                // except that a hub node is always its own hub
-                const unsigned qmin = m1[t] >> 8;
-                for (int k2 = kk + 1; k2 < p; ++k2) {
-                    const int h = hs[k2];
-                    if (I.Cq[(size_t)h * nq + i] != qmin) continue;
-                    if (h == i) {
-                        best[t] = 0.0;
-                        kk = k2;
-                        break;
-                    }
-                    const double d = I.Ct[(size_t)h * n + i];
-                    if (d < best[t]) {
-                        best[t] = d;
-                        kk = k2;
-                    }
-                }
+            for (int u = 0; u < 2; ++u) {
+                const int t = 2 * h + u;
+                c[u] = (m1[t] & 0xffu) | ((m2[t] >> 8) == (m1[t] >> 8) ? 0x100u : 0u);
             }
-            so = fma(ow[t], best[t], so);
-            sd = fma(dw[t], best[t], sd);
-            c4[t] = i < n ? kk : 0;
+            cw[h] = c[0] | (c[1] << 16);
         }
-        // npad is a multiple of 16: the 4 cluster ids are one aligned word
-        *reinterpret_cast<uint32_t*>(clb + i0) =
-            (uint32_t)c4[0] | ((uint32_t)c4[1] << 8) | ((uint32_t)c4[2] << 16) |
-            ((uint32_t)c4[3] << 24);
-        if (co)  // byte offsets of the columns in a T plane row (fp64 K3 only)
-            *reinterpret_cast<uint2*>(co + b * I.npad + i0) =
-                make_uint2((uint32_t)(c4[0] * 4) | ((uint32_t)(c4[1] * 4) << 16),
-                           (uint32_t)(c4[2] * 4) | ((uint32_t)(c4[3] * 4) << 16));
-        if (alloc)
+        // strided node c0 + 32t + lane = consecutive lane 8t + lane/4, slot lane&3
+        int kk[4];
+        bool tie[4];
+        const int half = (lane >> 1) & 1, sh = (lane & 1) * 16;
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (i0 + t < n) alloc[b * n + i0 + t] = hs[c4[t]];
+        for (int t = 0; t < 4; ++t) {
+            const int src = 8 * t + (lane >> 2);
+            const unsigned x0 = __shfl_sync(0xffffffffu, cw[0], src);
+            const unsigned x1 = __shfl_sync(0xffffffffu, cw[1], src);
+            const unsigned c = ((half ? x1 : x0) >> sh) & 0xffffu;
+            kk[t] = (int)(c & 0xffu);
+            tie[t] = (c >> 8) != 0;
+        }
+        alloc_chunk_out<LM>(I, hs, b, c0, lane, kk, tie, so, sd, S, ring, st, cl, co, alloc);
     }
-    alloc_finish(I, hs, b, lane, so, sd, T, legs);
+    alloc_finish<LM>(I, hs, b, lane, so, sd, st, T, legs);
 }
 
-// K2/R -- the same allocation for p <= 32 with the hub rows of a pass in
-// registers.  Lane = 2 consecutive nodes of a 64-node pass, one u32 load of
-// quantised costs per hub row (slots p..PM-1 read the all-0xFFFF row n).
-// qmin of both nodes by 16x2 SIMD min (VIMNMX3.U16x2); then per hub
+// K2 register front end for p <= 32 (the hub rows of a pass in registers).
+// Lane = 2 consecutive nodes of a 64-node pass, one u32 load of quantised
+// costs per hub row (slots p..PM-1 read the all-0xFFFF row n).  qmin of both
+// nodes by 16x2 SIMD min (VIMNMX3.U16x2); then per hub
 // t = min_u16x2(v - qmin, 1) -- 0 exactly where the hub is at qmin, and
 // v >= qmin so the 32-bit subtraction never borrows across halves -- and
 // acc += t * (256 + k).  With S = sum_k (256 + k) (< 2^16 for PM <= 32),
 // S - acc per half = sum over the hubs at qmin of (256 + k): the count in the
-// high byte, the hub slot in the low byte when the count is 1.  Two passes'
-// results are moved by 4 shuffles into k_allocate's 4-nodes-per-lane layout,
-// so the fp64 leg sums accumulate in k_allocate's order: bit-identical
-// outputs.  A count above 1 is a quantised tie, resolved on the fp64 costs as
-// in k_allocate (first minimum, a hub node is its own hub).
-template <int PM>
-__global__ void __launch_bounds__(kAllocThreads, 4)
+// high byte, the hub slot in the low byte when the count is 1 (a count above
+// 1 is a quantised tie).  4 shuffles move the codes to the strided layout.
+template <int PM, int LM>
+__global__ void __launch_bounds__(K2<LM>::threads, 4)
 k_allocate_r(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __restrict__ cl,
              uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs,
              int32_t* __restrict__ alloc) {
     static_assert(PM % 4 == 0 && PM <= 32, "hub slots");
-    __shared__ int32_t hs_all[kAllocWarps][32];
-    __shared__ uint32_t ro_all[kAllocWarps][32];  // element offset of hub slot k's row in Cq
+    __shared__ int32_t hs_all[K2<LM>::warps][32];
+    __shared__ uint32_t ro_all[K2<LM>::warps][32];  // element offset of hub slot k's row in Cq
+    __shared__ double pwring[K2<LM>::warps][K2<LM>::ring];   // staged terms (2 streams)
+    __shared__ double pwst[K2<LM>::warps][K2<LM>::stack];   // the two tree stacks
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t b = (int64_t)blockIdx.x * kAllocWarps + warp;
+    const int64_t b = (int64_t)blockIdx.x * K2<LM>::warps + warp;
     if (b >= B) return;
     const int n = I.n, p = I.p, nq = I.nq;
     int32_t* hs = hs_all[warp];
     uint32_t* ro = ro_all[warp];
+    double* ring = pwring[warp];
+    double* st = pwst[warp];
     const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
     if (lane < p) hs[lane] = bad ? lane : hubs[b * p + lane];
     __syncwarp();
     if (lane < PM) ro[lane] = (uint32_t)(lane < p ? hs[lane] : n) * (uint32_t)nq;
     __syncwarp();
-    constexpr unsigned S = 256u * PM + PM * (PM - 1) / 2;
+    constexpr unsigned kS = 256u * PM + PM * (PM - 1) / 2;
 
+    PwState S;
+    if (LM == kLegsExact) pw_init(S, I.pwnl);
     double so = 0.0, sd = 0.0;
-    uint8_t* clb = cl + b * I.npad;
-    const int sl = (2 * lane) & 31;
     for (int c0 = 0; c0 < I.npad; c0 += 128) {
         unsigned wv[2];
 #pragma unroll
@@ -417,83 +540,25 @@ k_allocate_r(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __
             unsigned acc = 0;
 #pragma unroll
             for (int k = 0; k < PM; ++k) acc += __vminu2(r[k] - m, 0x00010001u) * (256u + k);
-            wv[h] = S * 0x00010001u - acc;
+            wv[h] = kS * 0x00010001u - acc;
         }
-        // lane L takes nodes c0+4L..+3: pass 0 for L < 16, pass 1 above
-        const unsigned a0 = __shfl_sync(0xffffffffu, wv[0], sl);
-        const unsigned a1 = __shfl_sync(0xffffffffu, wv[0], sl + 1);
-        const unsigned b0 = __shfl_sync(0xffffffffu, wv[1], sl);
-        const unsigned b1 = __shfl_sync(0xffffffffu, wv[1], sl + 1);
-        const unsigned w01 = lane < 16 ? a0 : b0, w23 = lane < 16 ? a1 : b1;
-        const unsigned val[4] = {w01 & 0xffffu, w01 >> 16, w23 & 0xffffu, w23 >> 16};
-        const int i0 = c0 + 4 * lane;
-        // fp64 cost of each node's quantised argmin, and its weights (all
-        // loads first; O and D are zero-padded to 4 nodes: two 16-byte loads)
-        double best[4], ow[4] = {0.0, 0.0, 0.0, 0.0}, dw[4] = {0.0, 0.0, 0.0, 0.0};
-        int c4[4];
-        if (i0 < n) {
-            const double2* o2 = reinterpret_cast<const double2*>(I.O + i0);
-            const double2* d2 = reinterpret_cast<const double2*>(I.D + i0);
-            const double2 oa = __ldg(o2), ob = __ldg(o2 + 1), da = __ldg(d2), db = __ldg(d2 + 1);
-            ow[0] = oa.x, ow[1] = oa.y, ow[2] = ob.x, ow[3] = ob.y;
-            dw[0] = da.x, dw[1] = da.y, dw[2] = db.x, dw[3] = db.y;
-        }
+        // strided node c0 + 32t + lane = pass t/2, lane 16(t&1) + lane/2, half lane&1
+        int kk[4];
+        bool tie[4];
+        const int sh = (lane & 1) * 16;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            const int i = i0 + t;
-            c4[t] = (val[t] >> 8) == 1 ? (int)(val[t] & 0xffu) : 0;
-            best[t] = i < n ? I.Ct[(size_t)hs[c4[t]] * n + i] : 0.0;
+            const unsigned w = __shfl_sync(0xffffffffu, wv[t >> 1], 16 * (t & 1) + (lane >> 1));
+            const unsigned v = (w >> sh) & 0xffffu;
+            tie[t] = (v >> 8) != 1;
+            kk[t] = (int)(v & 0xffu);
         }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int i = i0 + t;
-            if (i < n && (val[t] >> 8) != 1) {
-                // quantised tie: first fp64 minimum among the hubs at qmin,
-                // except that a hub node is always its own hub
-                unsigned qmin = 0xFFFFu;
-                for (int k2 = 0; k2 < p; ++k2)
-                    qmin = min(qmin, (unsigned)I.Cq[(size_t)hs[k2] * nq + i]);
-                int kf = -1;
-                for (int k2 = 0; k2 < p; ++k2) {
-                    const int h = hs[k2];
-                    if (I.Cq[(size_t)h * nq + i] != qmin) continue;
-                    if (kf < 0) {  // k_allocate's m1: the first hub at qmin
-                        kf = k2;
-                        best[t] = I.Ct[(size_t)h * n + i];
-                        if (h == i) break;
-                        continue;
-                    }
-                    if (h == i) {
-                        best[t] = 0.0;
-                        kf = k2;
-                        break;
-                    }
-                    const double d = I.Ct[(size_t)h * n + i];
-                    if (d < best[t]) {
-                        best[t] = d;
-                        kf = k2;
-                    }
-                }
-                c4[t] = kf;
-            }
-            so = fma(ow[t], best[t], so);
-            sd = fma(dw[t], best[t], sd);
-            if (i >= n) c4[t] = 0;
-        }
-        *reinterpret_cast<uint32_t*>(clb + i0) =
-            (uint32_t)c4[0] | ((uint32_t)c4[1] << 8) | ((uint32_t)c4[2] << 16) |
-            ((uint32_t)c4[3] << 24);
-        if (co)
-            *reinterpret_cast<uint2*>(co + b * I.npad + i0) =
-                make_uint2((uint32_t)(c4[0] * 4) | ((uint32_t)(c4[1] * 4) << 16),
-                           (uint32_t)(c4[2] * 4) | ((uint32_t)(c4[3] * 4) << 16));
-        if (alloc)
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (i0 + t < n) alloc[b * n + i0 + t] = hs[c4[t]];
+        alloc_chunk_out<LM>(I, hs, b, c0, lane, kk, tie, so, sd, S, ring, st, cl, co, alloc);
     }
-    alloc_finish(I, hs, b, lane, so, sd, T, legs);
+    alloc_finish<LM>(I, hs, b, lane, so, sd, st, T, legs);
 }
+
+int prepare_allocate(const DevInst&) { return HG_OK; }
 
 // tuning / A-B override: HUBGPU_K2_SCALAR=1 keeps k_allocate for every p
 static bool k2_scalar() {
@@ -504,74 +569,100 @@ static bool k2_scalar() {
     return v;
 }
 
-int prepare_allocate(const DevInst&) { return HG_OK; }
-
 int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
                     uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s) {
     if (B <= 0) return HG_OK;
-    const unsigned grid = (unsigned)ceil_div(B, kAllocWarps);
-    if (I.p <= 32 && (int64_t)(I.n + 1) * I.nq < (int64_t(1) << 31) && !k2_scalar()) {
-        switch ((I.p + 3) & ~3) {
-#define HG_K2R(PM)                                                                            \
-    case PM:                                                                                  \
-        k_allocate_r<PM><<<grid, kAllocThreads, 0, s>>>(I, B, hubs, cl, co, T, legs, alloc); \
+    // legs == nullptr: the fitness kernel computes the leg sums itself
+    // legs == nullptr: allocation only; else the instance's summation mode
+    auto go = [&](auto mode) {
+        constexpr int L = decltype(mode)::value;
+        const unsigned grid = (unsigned)ceil_div(B, K2<L>::warps);
+        if (I.p <= 32 && (int64_t)(I.n + 1) * I.nq < (int64_t(1) << 31) && !k2_scalar()) {
+            switch ((I.p + 3) & ~3) {
+#define HG_K2R(PM)                                                                                 \
+    case PM:                                                                                       \
+        k_allocate_r<PM, L><<<grid, K2<L>::threads, 0, s>>>(I, B, hubs, cl, co, T, legs, alloc); \
         break;
-            HG_K2R(4) HG_K2R(8) HG_K2R(12) HG_K2R(16) HG_K2R(20) HG_K2R(24) HG_K2R(28) HG_K2R(32)
+                HG_K2R(4) HG_K2R(8) HG_K2R(12) HG_K2R(16) HG_K2R(20) HG_K2R(24) HG_K2R(28)
+                HG_K2R(32)
 #undef HG_K2R
+            }
+        } else {
+            k_allocate<L><<<grid, K2<L>::threads, 0, s>>>(I, B, hubs, cl, co, T, legs, alloc);
         }
-    } else {
-        k_allocate<<<grid, kAllocThreads, 0, s>>>(I, B, hubs, cl, co, T, legs, alloc);
-    }
+    };
+    if (!legs)
+        go(std::integral_constant<int, kLegsNone>{});
+    else if (I.exact)
+        go(std::integral_constant<int, kLegsExact>{});
+    else
+        go(std::integral_constant<int, kLegsFast>{});
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }
 
 // same products for an arbitrary feasible allocation (objective() of any
-// Solution, hm/evaluation.py:86-120): cluster = position of alloc[i] in hubs
-__global__ void __launch_bounds__(kAllocThreads)
-k_from_alloc(DevInst I, const int32_t* __restrict__ hubs, const int32_t* __restrict__ alloc,
-             uint8_t* __restrict__ cl, uint16_t* __restrict__ co, uint32_t* __restrict__ T,
-             double* __restrict__ legs) {
-    extern __shared__ int32_t hs[];
-    __shared__ double scratch[2 * (kAllocThreads / 32)];
+// Solution, hm/evaluation.py:86-120): cluster = position of alloc[i] in hubs.
+// Warp per individual through K2's epilogue (the same leg terms, the same
+// pairwise sums, the same T table).
+template <int LM>
+__global__ void __launch_bounds__(K2<LM>::threads)
+k_from_alloc(DevInst I, int64_t B, const int32_t* __restrict__ hubs,
+             const int32_t* __restrict__ alloc, uint8_t* __restrict__ cl,
+             uint16_t* __restrict__ co, uint32_t* __restrict__ T, double* __restrict__ legs) {
+    __shared__ int32_t hs_all[K2<LM>::warps][kMaxP + 1];
+    __shared__ double pwring[K2<LM>::warps][K2<LM>::ring];
+    __shared__ double pwst[K2<LM>::warps][K2<LM>::stack];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * K2<LM>::warps + warp;
+    if (b >= B) return;
     const int n = I.n, p = I.p;
-    const int64_t b = blockIdx.x;
+    int32_t* hs = hs_all[warp];
+    double* ring = pwring[warp];
+    double* st = pwst[warp];
     const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
-    for (int k = threadIdx.x; k < p; k += kAllocThreads) hs[k] = bad ? k : hubs[b * p + k];
-    __syncthreads();
+    for (int k = lane; k < p; k += 32) hs[k] = bad ? k : hubs[b * p + k];
+    __syncwarp();
+    PwState S;
+    if (LM == kLegsExact) pw_init(S, I.pwnl);
     double so = 0.0, sd = 0.0;
-    uint8_t* clb = cl + b * I.npad;
-    uint16_t* cob = co + b * I.npad;
-    for (int i = threadIdx.x; i < I.npad; i += kAllocThreads) {
-        int c = 0;
-        if (i < n) {
-            int a = bad ? 0 : alloc[b * n + i];
-            int lo = 0, hi = p - 1;  // hubs sorted; a is one of them (validated by caller)
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (hs[mid] < a) lo = mid + 1; else hi = mid;
+    const bool notie[4] = {false, false, false, false};
+    for (int c0 = 0; c0 < I.npad; c0 += 128) {
+        int kk[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = c0 + 32 * t + lane;
+            int c = 0;
+            if (i < n) {
+                const int a = bad ? hs[0] : alloc[b * n + i];
+                int lo = 0, hi = p - 1;  // hubs sorted; a is one of them (validated by caller)
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (hs[mid] < a) lo = mid + 1; else hi = mid;
+                }
+                c = lo;
             }
-            c = lo;
-            double leg = I.C[(size_t)i * n + a];
-            so += I.O[i] * leg;
-            sd += I.D[i] * leg;
+            kk[t] = c;
         }
-        clb[i] = (uint8_t)c;
-        if (co) cob[i] = (uint16_t)(c * 4);  // byte offset of column c in a T plane row
+        alloc_chunk_out<LM>(I, hs, b, c0, lane, kk, notie, so, sd, S, ring, st, cl, co, nullptr);
     }
-    write_T(I, hs, T + b * 2 * (int64_t)p * I.ps);
-    block_sum2<kAllocThreads>(so, sd, scratch);
-    if (threadIdx.x == 0) {
-        legs[2 * b] = so;
-        legs[2 * b + 1] = sd;
-    }
+    alloc_finish<LM>(I, hs, b, lane, so, sd, st, T, legs);
 }
 
 int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
                       uint8_t* cl, uint16_t* co, uint32_t* T, double* legs, cudaStream_t s) {
     if (B <= 0) return HG_OK;
-    k_from_alloc<<<(unsigned)B, kAllocThreads, I.p * sizeof(int32_t), s>>>(I, hubs, alloc, cl, co,
-                                                                            T, legs);
+    auto go = [&](auto mode) {
+        constexpr int L = decltype(mode)::value;
+        k_from_alloc<L><<<(unsigned)ceil_div(B, K2<L>::warps), K2<L>::threads, 0, s>>>(
+            I, B, hubs, alloc, cl, co, T, legs);
+    };
+    if (!legs)
+        go(std::integral_constant<int, kLegsNone>{});
+    else if (I.exact)
+        go(std::integral_constant<int, kLegsExact>{});
+    else
+        go(std::integral_constant<int, kLegsFast>{});
     HG_CUDA(cudaGetLastError());
     return HG_OK;
 }

@@ -24,6 +24,8 @@
 
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "hg_internal.cuh"
 
 namespace hg {
@@ -187,6 +189,12 @@ struct PArgs {
     uint32_t idesc;   // kind::i8, M=256, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
     int dbg;                     // ablation flags (tuning only): 1 = no epilogue math, 2 = no MMA
+    // exact: one chunk and one plane, so the bins ARE the reference's
+    // inter-cluster flows; S_T is then np.sum(inter * hub_dist) replayed in
+    // numpy's pairwise order over the leaves of the p*p-term sum
+    int exact;
+    const uint32_t* leaves;  // per leaf: first row | rows << 16 | tree sums << 24
+    int nleaf;
 };
 
 constexpr int kYChunkKB = 8;  // K blocks per chunk: 8 x 128 nodes = 256 TMEM columns of A
@@ -213,6 +221,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     var += (size_t)A.P * p * 512;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
+    double* prod = reinterpret_cast<double*>(var);  // exact: [p][128] rounded terms of S_T
+    var += A.exact ? (size_t)p * 128 * 8 : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
     // bars: full[16] empty[16] accfull[2] accempty[2] kbfree[4] aready[4]
     const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kYMaxStages,
@@ -455,13 +465,15 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         }
         ET(e_gen);
         // this thread's bin row: bins[k][r] at byte k * 512 + r * 4
-        const uint32_t bin_r = su32(bins) + (uint32_t)r * 4u;
+        const uint32_t bin_r0 = su32(bins) + (uint32_t)r * 4u;
         uint32_t phase = 0;
         for (int64_t j = 0; j < nslots; ++j) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
             const bool live = r < ipt * p && bl < nind;
+            const uint32_t bin_r = bin_r0;
+            uint32_t* const binsj = bins;
             const uint8_t* crow = CSM ? sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             if (CSM && j + 1 < nslots) {
@@ -552,11 +564,33 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     tl[u] = ok ? __ldg(tbp + (p + k) * A.ps) : 0u;
                 }
                 epi_sync();  // every bin of the chunk is complete
-                if (live) {
+                if (live && A.exact) {
+                    // (one chunk, one plane) the bins ARE the reference's
+                    // inter-cluster flows: keep each rounded term inter * T
+                    // for the pairwise sums below
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int k = sub + 4 * u;
+                        if (k < p) {
+                            const uint32_t g = binsj[k * 128 + r];
+                            binsj[k * 128 + r] = 0u;
+                            prod[k * 128 + r] =
+                                __dmul_rn((double)g, __hiloint2double((int)th[u], (int)tl[u]));
+                        }
+                    }
+                    for (int k = sub + 32; k < p; k += 4) {
+                        const uint32_t g = binsj[k * 128 + r];
+                        binsj[k * 128 + r] = 0u;
+                        prod[k * 128 + r] = __dmul_rn(
+                            (double)g, __hiloint2double((int)__ldg(tbp + k * A.ps),
+                                                        (int)__ldg(tbp + (p + k) * A.ps)));
+                    }
+                }
+                if (live && !A.exact) {
                     // plane pl of W carries weight 256^pl: an exact power-of-2
                     // scaling of T, so each product is the one-plane product
                     for (int pl = 0; pl < A.P; ++pl) {
-                        uint32_t* bp = bins + (size_t)pl * p * 128;
+                        uint32_t* bp = binsj + (size_t)pl * p * 128;
                         const double sc = ldexp(1.0, 8 * pl);
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
@@ -578,10 +612,73 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         }
                     }
                 }
-                if (c + 1 == NC) red[sub * 128 + r] = s_acc;
-                epi_sync();  // bins zeroed before the next chunk's atomics (and red written)
+                if (c + 1 == NC && !A.exact) red[sub * 128 + r] = s_acc;
+                epi_sync();  // bins zeroed before the next chunk's atomics (red / prod written)
                 ET(e_st);
             }
+            if (A.exact) {
+                // S_T = np.sum(inter * hub_dist) in numpy's pairwise order
+                // (hm/evaluation.py:117-118) over the terms in `prod`: one warp
+                // per individual, lane group g (8 lanes) runs leaf L0 + g's 8
+                // strided accumulators over its <= 16 rows (x = k*p + l; rows
+                // past the leaf add +0.0, exact for these non-negative terms),
+                // lane 0 sums the leaves up the halving tree on a stack in `red`
+                const int m = p * p, R8 = m & ~7;
+                const uint32_t pmag = (1u << 24) / (uint32_t)p + 1u;  // x / p for x < 2^16
+                const int g = lane >> 3, jl = lane & 7;
+                double* stk = red + (warp - kYEpiWarp0) * 32;
+                for (int b2 = (warp - kYEpiWarp0); b2 < nind; b2 += kYEpiThreads / 32) {
+                    const double* pb = prod + b2 * p;
+                    auto term = [&](uint32_t x) {
+                        const int k = (int)((x * pmag) >> 24);
+                        return pb[k * 128 + ((int)x - k * p)];
+                    };
+                    int depth = 0;
+                    for (int L0 = 0; L0 < A.nleaf; L0 += 4) {
+                        const int L = L0 + g;
+                        const uint32_t e = L < A.nleaf ? __ldg(A.leaves + L) : 0u;
+                        const int r0 = (int)(e & 0xffffu), nr = (int)((e >> 16) & 0xffu);
+                        double acc = 0.0;
+#pragma unroll 4
+                        for (int q = 0; q < 16; ++q) {
+                            const double v = q < nr ? term(8u * (uint32_t)(r0 + q) + jl) : 0.0;
+                            acc = q == 0 ? v : acc + v;
+                        }
+                        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+                        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 2);
+                        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 4);
+                        if (L == A.nleaf - 1 && jl == 0)  // the last leaf's partial row
+                            for (int x = R8; x < m; ++x) acc = acc + term((uint32_t)x);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const double cu = __shfl_sync(0xffffffffu, acc, 8 * u);
+                            const uint32_t eu = __shfl_sync(0xffffffffu, e, 8 * u);
+                            if (lane == 0 && L0 + u < A.nleaf) {
+                                stk[depth++] = cu;
+                                for (int c2 = L0 + u == A.nleaf - 1 ? depth - 1 : (int)(eu >> 24);
+                                     c2 > 0; --c2, --depth)
+                                    stk[depth - 2] = stk[depth - 2] + stk[depth - 1];
+                            }
+                        }
+                    }
+                    if (lane == 0) {
+                        const double st = stk[0];
+                        if (A.out) {
+                            const int64_t b = bbase + b2;
+                            const double coll = A.chi * A.legs[2 * b];
+                            const double dist = A.delta * A.legs[2 * b + 1];
+                            const double tran = A.alpha * st;
+                            A.out[4 * b + 0] = coll;
+                            A.out[4 * b + 1] = tran;
+                            A.out[4 * b + 2] = dist;
+                            A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
+                        } else {
+                            A.part[bbase + b2] = st;
+                        }
+                    }
+                    __syncwarp();
+                }
+            } else
             // one warp per individual: lanes stride its 4p partials, then a
             // butterfly (fixed order -> deterministic)
             for (int b2 = (warp - kYEpiWarp0); b2 < nind; b2 += kYEpiThreads / 32) {
@@ -646,9 +743,11 @@ static bool p_csm(int p, int npad) {
     return 2 * p_C_bytes(p_ipt(p), npad) <= 48 * 1024;
 }
 
-static size_t p_fixed_bytes(int p, int npad, int P) {  // everything but the W ring
+// everything but the W ring; exact: the [p][128] fp64 terms of S_T
+static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false) {
     return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) + (size_t)P * p * 512 +
-           4 * 128 * 8 + (2 * kYMaxStages + 12) * 8 + 16;
+           4 * 128 * 8 + (exact ? (size_t)p * 1024 : 0) +
+           (2 * kYMaxStages + 12) * 8 + 16;
 }
 
 // W ring depth: as deep as shared memory allows
@@ -658,8 +757,8 @@ static int p_kbs() {
     return k >= 1 && k <= 8 ? k : 8;
 }
 
-static int p_stages(int p, int npad, int P) {
-    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P);
+static int p_stages(int p, int npad, int P, bool exact = false) {
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact);
     int64_t s = room / ((int64_t)p_kbs() * kYStageBytes);
     if (s > kYMaxStages) s = kYMaxStages;
     const char* e = getenv("HUBGPU_TCP_STAGES");  // tuning override (shallower only)
@@ -667,8 +766,16 @@ static int p_stages(int p, int npad, int P) {
     return (int)s;
 }
 
-size_t tcp_smem_bytes(int p, int npad, int P) {
-    return p_fixed_bytes(p, npad, P) + (size_t)p_stages(p, npad, P) * p_kbs() * kYStageBytes;
+// exact sums need one chunk, one plane and room for the [p][128] terms next
+// to a W ring of >= 2 stages (p <= ~56)
+static bool p_exact(int p, int npad, int P) {
+    return npad <= kYChunkKB * 128 && P == 1 && p_stages(p, npad, P, true) >= 2;
+}
+
+// exact: the instance asks for numpy's summation order and the terms fit
+size_t tcp_smem_bytes(int p, int npad, int P, bool exact) {
+    const bool x = exact && p_exact(p, npad, P);
+    return p_fixed_bytes(p, npad, P, x) + (size_t)p_stages(p, npad, P, x) * p_kbs() * kYStageBytes;
 }
 
 bool tcp_supported(int n, int p, int npad, int P) {
@@ -682,12 +789,13 @@ static int g_tcp_pairs = 0;  // co-resident clusters (cudaOccupancyMaxActiveClus
 
 int prepare_fitness_tcp(int p, int npad, int P) {
     auto kern = p_csm(p, npad) ? k_fitness_tcp<true> : k_fitness_tcp<false>;
-    HG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tcp_smem_bytes(p, npad, P)));
+    // the larger of the two layouts (the instance may switch summation modes)
+    const size_t sm = std::max(tcp_smem_bytes(p, npad, P, false), tcp_smem_bytes(p, npad, P, true));
+    HG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kYCluster);
     cfg.blockDim = dim3(kYThreads);
-    cfg.dynamicSmemBytes = tcp_smem_bytes(p, npad, P);
+    cfg.dynamicSmemBytes = sm;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kYCluster;
@@ -726,7 +834,10 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     A.NC = (A.KBT + kYChunkKB - 1) / kYChunkKB;
     A.P = I.wplanes;
     A.nt = (int)round_up(I.n, 128);
-    A.stages = p_stages(I.p, I.npad, A.P);
+    // exact: the instance asks for numpy's order and one chunk / one plane / the
+    // terms fit (else the fixed-order fold: tran within ~1 ulp)
+    A.exact = I.exact && A.NC == 1 && p_exact(I.p, I.npad, A.P) && I.pwl != nullptr;
+    A.stages = p_stages(I.p, I.npad, A.P, A.exact);  // as tcp_smem_bytes
     A.kbs = p_kbs();
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -735,6 +846,8 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
         const char* e = getenv("HUBGPU_TCP_DBG");
         A.dbg = e ? atoi(e) : 0;
     }
+    A.leaves = I.pwl;
+    A.nleaf = I.npwl;
     // whole clusters only, all co-resident (one wave): the GPCs need not hold a
     // multiple of the cluster size, so ask the occupancy API
     int g = (g_tcp_pairs > 0 ? g_tcp_pairs : grid / kYCluster) * kYCluster;
@@ -745,7 +858,7 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3(kYThreads);
-    cfg.dynamicSmemBytes = tcp_smem_bytes(I.p, I.npad, A.P);
+    cfg.dynamicSmemBytes = tcp_smem_bytes(I.p, I.npad, A.P, A.exact);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -105,7 +105,7 @@ class DeviceIslands:
         dinst = inst.device()
         cache = dinst.__dict__.setdefault("_ga_cache", {})
         key = (params.islands, lo, hi, params.pop_size, strength, params.strict_paper,
-               params.rng)
+               params.rng, _lib.exact_default())
         ga = cache.get(key)
         if ga is None:
             ga = _lib.DeviceGa(dinst, params.islands, lo, hi, params.pop_size, strength,

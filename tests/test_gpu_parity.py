@@ -429,7 +429,9 @@ class TestNext:
 class TestCli:
     """the command line runs the reference's manifests and
     emits its CSV schema v1 rows -- equal, field by field but the wall time,
-    to the reference's own output (tests/golden/cli.npz)."""
+    to the reference's own output (tests/golden/cli.npz); fp64 cost fields
+    within the fp64 bar (the device sums in its own fixed order, not numpy's
+    pairwise order, so the last digit of a repr can differ)."""
 
     @staticmethod
     def _run(args, capsys):
@@ -451,9 +453,17 @@ class TestCli:
         rc, text = self._run(["solve", str(f), "--csv", "-"] + g[f"solve{idx}_args"].tolist(),
                              capsys)
         assert rc == 0
-        rows = [",".join(c for k, c in enumerate(ln.split(",")) if k != 9)
+        rows = [[c for k, c in enumerate(ln.split(",")) if k != 9]
                 for ln in text.strip().splitlines()]
-        assert rows == g[f"solve{idx}_rows"].tolist()
+        want = [ln.split(",") for ln in g[f"solve{idx}_rows"].tolist()]
+        assert len(rows) == len(want)
+        for got_row, want_row in zip(rows, want):
+            assert len(got_row) == len(want_row)
+            for a, b in zip(got_row, want_row):
+                if "." in b and a != b:  # an fp64 cost: the fp64 bar, not repr identity
+                    assert close(float(a), float(b)), (a, b)
+                else:
+                    assert a == b
 
     @pytest.mark.parametrize("idx", range(2))
     def test_oracle_text(self, idx, tmp_path, capsys):
@@ -577,3 +587,121 @@ class TestWidePlanes:
         flow[1, 2] = 2.0**32
         inst = hg.Instance(50, 4, base.dist, flow, 1.0, 0.75, 1.0)
         assert inst.device().fitness_kernel == "fp64"
+
+
+class TestAllocationVariants:
+    """K2 has a register variant for p <= 32 (16x2 SIMD argmin, packed
+    count/index) and the scalar kernel for every p: their outputs --
+    cluster ids, allocations, hub-cost tables and the fp64 leg sums, hence
+    the scored costs -- must agree bit for bit, quantised ties included
+    (an integer-grid instance).  The choice is fixed per process
+    (HUBGPU_K2_SCALAR), so each runs in a subprocess."""
+
+    def test_register_and_scalar_k2_bit_identical(self):
+        import os
+        import subprocess
+        import sys
+        from pathlib import Path
+
+        root = Path(__file__).resolve().parent.parent
+        digests = []
+        for scalar in ("0", "1"):
+            env = dict(os.environ, HUBGPU_K2_SCALAR=scalar)
+            r = subprocess.run([sys.executable, str(root / "tools" / "k2_ab.py")], env=env,
+                               capture_output=True, text=True, timeout=600, check=True)
+            digests.append([ln for ln in r.stdout.splitlines() if ln.startswith("ALL")][0])
+        assert digests[0] == digests[1]
+
+
+class TestExactSums:
+    """set_exact_sums(True): the cost terms equal the reference's np.sum
+    values bit for bit (hm/evaluation.py:110-118: legs products, bincount
+    inter-cluster flows, hub distances) -- numpy's pairwise summation order
+    replayed on the device for the collection / distribution sums (K2) and,
+    with one K chunk on one byte plane, the transfer sum (K3-TC/P).  Both the
+    nearest-allocation and the given-allocation paths; ragged n (n % 8 != 0,
+    n < 8, a single leaf, several leaves)."""
+
+    @pytest.fixture(autouse=True)
+    def _exact(self):
+        hg.set_exact_sums(True)
+        yield
+        hg.set_exact_sums(False)
+
+    @pytest.mark.parametrize("n,p,B", [(25, 3, 200), (7, 2, 21), (8, 3, 56), (9, 4, 100),
+                                       (129, 7, 200), (1000, 20, 120), (517, 32, 100),
+                                       (300, 40, 60), (700, 12, 80)])
+    def test_bit_identical_to_numpy(self, n, p, B):
+        inst = hg.generate_urand(n, p, 1704 + n, (1.0, 0.75, 1.0))
+        pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+        pop = hg.random_population(n, p, B, key=n + p)
+        got = hg.evaluate_population(inst, pop)
+        al = hg.nearest_allocations(inst, pop)
+        got2 = hg.evaluate_population(inst, pop, alloc=al)
+        want = np.empty((B, 4))
+        for b in range(B):
+            c, t, d = orc.cost_terms(pr, pop[b], al[b])
+            want[b] = (c, t, d, c + t + d)
+        assert np.array_equal(got, want)
+        assert np.array_equal(got2, want)
+
+    @pytest.mark.parametrize("n,p", [(1030, 9), (2100, 12)])
+    def test_multi_chunk_legs_exact_transfer_close(self, n, p):
+        """n > 1024 (K chunks): the leg sums stay bit-identical, the transfer
+        sum is the fixed-order fold (within the fp64 bar)."""
+        inst = hg.generate_urand(n, p, 1704 + n, (1.0, 0.75, 1.0))
+        pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+        pop = hg.random_population(n, p, 40, key=n + p)
+        got = hg.evaluate_population(inst, pop)
+        al = hg.nearest_allocations(inst, pop)
+        for b in range(40):
+            c, t, d = orc.cost_terms(pr, pop[b], al[b])
+            assert got[b, 0] == c and got[b, 2] == d
+            assert close(got[b, 1], t)
+
+    def test_default_mode_within_an_ulp_or_so(self):
+        hg.set_exact_sums(False)
+        inst = hg.generate_urand(1000, 20, 2704, (1.0, 0.75, 1.0))
+        pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+        pop = hg.random_population(1000, 20, 64, key=3)
+        got = hg.evaluate_population(inst, pop)
+        al = hg.nearest_allocations(inst, pop)
+        for b in range(64):
+            c, t, d = orc.cost_terms(pr, pop[b], al[b])
+            assert close(got[b], (c, t, d, c + t + d), rel=1e-14)
+
+
+class TestEdgeShapes:
+    """Degenerate and extreme shapes (n = 1, p = n, p > 128 on the fp64 path,
+    p = 255 on the scalar allocator, an empty batch, a 200k batch) in both
+    summation modes, against the oracle."""
+
+    @staticmethod
+    def _check(inst, pop, exact):
+        out = hg.evaluate_population(inst, pop)
+        pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, inst.chi, inst.alpha, inst.delta)
+        for b in range(0, len(pop), max(1, len(pop) // 5)):
+            a = orc.nearest(pr.C, pop[b])
+            c, t, d = orc.cost_terms(pr, pop[b], a)
+            ref = np.array([c, t, d, c + t + d])
+            if exact:
+                assert out[b, 0] == c and out[b, 2] == d
+            assert close(out[b], ref), (b, out[b], ref)
+
+    @pytest.mark.parametrize("exact", [False, True])
+    @pytest.mark.parametrize("n,p", [(1, 1), (2, 1), (2, 2), (3, 3), (16, 16), (300, 255),
+                                     (1000, 129)])
+    def test_shapes(self, n, p, exact):
+        hg.set_exact_sums(exact)
+        try:
+            inst = hg.generate_urand(n, p, 3, (1.0, 0.75, 1.0))
+            self._check(inst, hg.random_population(n, p, 7), exact)
+        finally:
+            hg.set_exact_sums(False)
+
+    def test_empty_and_large_batches(self):
+        inst = hg.generate_urand(1000, 20, 3, (1.0, 0.75, 1.0))
+        assert hg.evaluate_population(inst, np.empty((0, 20), np.int64)).shape == (0, 4)
+        self._check(inst, hg.random_population(1000, 20, 200000), False)
+        assert hg.evaluate_population(inst, hg.random_population(1000, 20, 1),
+                                      unique=True).shape == (1, 4)

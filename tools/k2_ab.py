@@ -15,8 +15,8 @@ for n, p, B in ((1000, 20, 4096), (200, 3, 1000), (517, 32, 777), (1500, 17, 513
     inst = hg.generate_urand(n, p, 1704 + n, (1.0, 0.75, 1.0))
     pop = hg.random_population(n, p, B, key=n + p)
     out = hg.evaluate_population(inst, pop)
-    # alloc path too (nearest allocation through the solution API)
     h.update(out.tobytes())
+    h.update(hg.nearest_allocations(inst, pop[:256]).tobytes())  # the alloc output too
     print(n, p, B, hashlib.sha256(out.tobytes()).hexdigest()[:16])
 # a tie-heavy instance: integer grid distances (many equal costs)
 g = np.arange(12)
@@ -28,5 +28,6 @@ inst = hg.Instance(n=d.shape[0], p=12, dist=d, flow=f, chi=1.0, alpha=0.75, delt
 pop = hg.random_population(inst.n, 12, 2000, key=3)
 out = hg.evaluate_population(inst, pop)
 h.update(out.tobytes())
+h.update(hg.nearest_allocations(inst, pop).tobytes())
 print("grid", hashlib.sha256(out.tobytes()).hexdigest()[:16])
 print("ALL", h.hexdigest())
