@@ -44,6 +44,27 @@ POP = 8192
 HBM_FALLBACK = 6650.0
 
 
+NCU_TRAFFIC_FILE = "profiles/ncu_traffic_r1j.json"
+
+
+def ncu_traffic(fit_kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the K3 launch from one
+    committed `ncu --set full` capture of this bench (None when absent)."""
+    try:
+        with open(Path(__file__).resolve().parent / NCU_TRAFFIC_FILE) as f:
+            ks = json.load(f)["kernels"]
+    except (OSError, ValueError, KeyError):
+        return None
+    import re
+
+    pat = {"tensor-pair": r"k_fitness_tcp\b", "tensor-tmem": r"k_fitness_tcy\b",
+           "tensor-smem": r"k_fitness_tc\b", "fp64": r"k_fitness<"}[fit_kernel]
+    for name, v in ks.items():
+        if re.search(pat, name):
+            return v["dram_bytes"]
+    return None
+
+
 def peaks():
     try:
         d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -413,7 +434,8 @@ def run_gpu(args):
                        "parallelism": f"population sharded, {world} rank(s)",
                        "l2": "flushed between steps (256 MiB write, untimed)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
+                         "frac": achieved / hbm, "traffic": ncu_traffic(fit_kernel),
+                         "traffic_source": NCU_TRAFFIC_FILE,
                          "kernel": KERNEL_NAMES[fit_kernel],
                          "kernel_ms": fit_avg,
                          "alg_bytes_per_launch": alg_bytes, "peak_source": hbm_src,

@@ -201,7 +201,7 @@ constexpr int kYChunkKB = 8;  // K blocks per chunk: 8 x 128 nodes = 256 TMEM co
 
 // CSM: a unit's cluster rows staged in shared memory (known address space ->
 // LDS) rather than read from global memory
-template <bool CSM>
+template <bool CSM, bool EX>
 __global__ void __launch_bounds__(kYThreads, 1)
 k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -222,7 +222,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
     double* prod = reinterpret_cast<double*>(var);  // exact: [p][128] rounded terms of S_T
-    var += A.exact ? (size_t)p * 128 * 8 : 0;
+    var += EX ? (size_t)p * 128 * 8 : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
     // bars: full[16] empty[16] accfull[2] accempty[2] kbfree[4] aready[4]
     const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kYMaxStages,
@@ -564,7 +564,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     tl[u] = ok ? __ldg(tbp + (p + k) * A.ps) : 0u;
                 }
                 epi_sync();  // every bin of the chunk is complete
-                if (live && A.exact) {
+                if (live && EX) {
                     // (one chunk, one plane) the bins ARE the reference's
                     // inter-cluster flows: keep each rounded term inter * T
                     // for the pairwise sums below
@@ -586,7 +586,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                                         (int)__ldg(tbp + (p + k) * A.ps)));
                     }
                 }
-                if (live && !A.exact) {
+                if (live && !EX) {
                     // plane pl of W carries weight 256^pl: an exact power-of-2
                     // scaling of T, so each product is the one-plane product
                     for (int pl = 0; pl < A.P; ++pl) {
@@ -612,11 +612,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         }
                     }
                 }
-                if (c + 1 == NC && !A.exact) red[sub * 128 + r] = s_acc;
+                if (c + 1 == NC && !EX) red[sub * 128 + r] = s_acc;
                 epi_sync();  // bins zeroed before the next chunk's atomics (red / prod written)
                 ET(e_st);
             }
-            if (A.exact) {
+            if (EX) {
                 // S_T = np.sum(inter * hub_dist) in numpy's pairwise order
                 // (hm/evaluation.py:117-118) over the terms in `prod`: one warp
                 // per individual, lane group g (8 lanes) runs leaf L0 + g's 8
@@ -788,9 +788,14 @@ bool tcp_supported(int n, int p, int npad, int P) {
 static int g_tcp_pairs = 0;  // co-resident clusters (cudaOccupancyMaxActiveClusters)
 
 int prepare_fitness_tcp(int p, int npad, int P) {
-    auto kern = p_csm(p, npad) ? k_fitness_tcp<true> : k_fitness_tcp<false>;
-    // the larger of the two layouts (the instance may switch summation modes)
-    const size_t sm = std::max(tcp_smem_bytes(p, npad, P, false), tcp_smem_bytes(p, npad, P, true));
+    // both summation modes (the instance may switch), each at its layout
+    const bool c = p_csm(p, npad);
+    using KernFn = void (*)(const CUtensorMap, PArgs);
+    const KernFn fx = c ? k_fitness_tcp<true, true> : k_fitness_tcp<false, true>;
+    HG_CUDA(cudaFuncSetAttribute(fx, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tcp_smem_bytes(p, npad, P, true)));
+    const KernFn kern = c ? k_fitness_tcp<true, false> : k_fitness_tcp<false, false>;
+    const size_t sm = tcp_smem_bytes(p, npad, P, false);
     HG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kYCluster);
@@ -868,9 +873,11 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (A.csm)
-        HG_CUDA(cudaLaunchKernelEx(&cfg, k_fitness_tcp<true>, map, A));
+        HG_CUDA(cudaLaunchKernelEx(&cfg, A.exact ? k_fitness_tcp<true, true>
+                                             : k_fitness_tcp<true, false>, map, A));
     else
-        HG_CUDA(cudaLaunchKernelEx(&cfg, k_fitness_tcp<false>, map, A));
+        HG_CUDA(cudaLaunchKernelEx(&cfg, A.exact ? k_fitness_tcp<false, true>
+                                             : k_fitness_tcp<false, false>, map, A));
     return HG_OK;
 }
 
