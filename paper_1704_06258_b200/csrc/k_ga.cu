@@ -157,6 +157,7 @@ __device__ __forceinline__ void carried_add(uint32_t* lo, uint32_t* hi, int c, d
 // so a competing hub at q = 0 takes the tie path, which checks for it)
 __device__ __forceinline__ int corr_nearest(const DevInst& I, const int32_t* H, int h, int i) {
     unsigned m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+#pragma unroll 8
     for (int k = 0; k < h; ++k) {
         const unsigned key = ((unsigned)I.Cq[(size_t)H[k] * I.nq + i] << 16) | (unsigned)k;
         m2 = min(m2, max(m1, key));
@@ -313,14 +314,25 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
                         bi = oi;
                     }
                 }
-                if (threadIdx.x == 0) {
-                    s_kill = bi;
-                    // delete position bi of H and the loads (np.delete keeps the order)
-                    for (int k = bi; k < h - 1; ++k) {
-                        H[k] = H[k + 1];
-                        clo[k] = clo[k + 1];
-                        chi[k] = chi[k + 1];
+                if (threadIdx.x == 0) s_kill = bi;
+                // delete position bi of H and the loads (np.delete keeps the
+                // order): the warp shifts 32 entries per step
+                for (int k0 = bi; k0 < h - 1; k0 += 32) {
+                    const int k = k0 + (int)threadIdx.x;
+                    int hv = 0;
+                    uint32_t lo = 0, hi = 0;
+                    if (k < h - 1) {
+                        hv = H[k + 1];
+                        lo = clo[k + 1];
+                        hi = chi[k + 1];
                     }
+                    __syncwarp();
+                    if (k < h - 1) {
+                        H[k] = hv;
+                        clo[k] = lo;
+                        chi[k] = hi;
+                    }
+                    __syncwarp();
                 }
             }
             __syncthreads();
@@ -371,8 +383,13 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
                     bi = oi;
                 }
             }
-            if (threadIdx.x == 0)
-                for (int k = bi; k < h - 1; ++k) H[k] = H[k + 1];
+            for (int k0 = bi; k0 < h - 1; k0 += 32) {  // delete position bi, 32 at a time
+                const int k = k0 + (int)threadIdx.x;
+                const int hv = k < h - 1 ? H[k + 1] : 0;
+                __syncwarp();
+                if (k < h - 1) H[k] = hv;
+                __syncwarp();
+            }
         }
         __syncthreads();
         --h;
