@@ -191,6 +191,7 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
     uint32_t* mask = reinterpret_cast<uint32_t*>(carried + hmax);     // [nw]
     int32_t* H = reinterpret_cast<int32_t*>(mask + nw);               // [hmax]
     int16_t* cls = reinterpret_cast<int16_t*>(H + hmax);              // [n] hub position per node
+    uint16_t* nxt = reinterpret_cast<uint16_t*>(cls + n);             // [n] see below
 
     int h;
     if (nw <= 32) {
@@ -265,10 +266,13 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
         __syncthreads();
         // 4 consecutive nodes per thread, one 8-byte load per hub row (rows are
         // padded to npad with 0xFFFF, a multiple of 16)
+        // nxt[i]: node i's second-nearest hub (node id) when its three smallest
+        // quantised costs are strictly ordered -- then, once its hub closes,
+        // that hub (if still open) is its exact nearest, no rescan; else 0xFFFF
         for (int i0 = 4 * threadIdx.x; i0 < n; i0 += 4 * kCorrThreads) {
-            unsigned m1[4], m2[4];
+            unsigned m1[4], m2[4], m3[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) m1[t] = m2[t] = 0xFFFFFFFFu;
+            for (int t = 0; t < 4; ++t) m1[t] = m2[t] = m3[t] = 0xFFFFFFFFu;
             const uint16_t* col = I.Cq + i0;
 #pragma unroll 4
             for (int k = 0; k < h; ++k) {
@@ -277,6 +281,7 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const unsigned key = (q[t] << 16) | (unsigned)k;
+                    m3[t] = min(m3[t], max(m2[t], key));
                     m2[t] = min(m2[t], max(m1[t], key));
                     m1[t] = min(m1[t], key);
                 }
@@ -289,6 +294,9 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
                 if ((m2[t] >> 16) == (m1[t] >> 16) && H[c] != i)
                     c = corr_nearest(I, H, h, i);  // quantised tie (or a hub node): exact path
                 cls[i] = (int16_t)c;
+                const unsigned q1 = m1[t] >> 16, q2 = m2[t] >> 16, q3 = m3[t] >> 16;
+                nxt[i] = q1 < q2 && q2 < q3 && m2[t] != 0xFFFFFFFFu
+                             ? (uint16_t)H[m2[t] & 0xFFFFu] : (uint16_t)0xFFFFu;
                 carried_add(clo, chi, c, I.wOD[i]);
             }
         }
@@ -341,7 +349,18 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
             for (int i = threadIdx.x; i < n; i += kCorrThreads) {
                 int c = cls[i];
                 if (c == kill) {
-                    c = corr_nearest(I, H, h, i);
+                    const int h2 = nxt[i];
+                    nxt[i] = 0xFFFFu;
+                    int pos = -1;
+                    if (h2 != 0xFFFF) {  // still open?  H is ascending: binary search
+                        int lo = 0, hi = h - 1;
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (H[mid] < h2) lo = mid + 1; else hi = mid;
+                        }
+                        if (H[lo] == h2) pos = lo;
+                    }
+                    c = pos >= 0 ? pos : corr_nearest(I, H, h, i);
                     carried_add(clo, chi, c, I.wOD[i]);
                 } else if (c > kill) {
                     --c;
@@ -403,7 +422,7 @@ int launch_correct(const DevInst& I, int64_t B, const uint32_t* bits, int hmax, 
     if (hmax < I.p) hmax = I.p;
     size_t smem = (size_t)hmax * 8 + (size_t)I.nw * 4 + (size_t)hmax * 4;
     smem = (smem + 7) & ~size_t(7);
-    smem += (size_t)I.n * 2;
+    smem += (size_t)I.n * 4;  // cls, nxt
     if (smem > 48 * 1024)
         HG_CUDA(cudaFuncSetAttribute(k_correct, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
