@@ -11,7 +11,7 @@ import paper_1704_06258_b200 as hg  # noqa: E402
 
 h = hashlib.sha256()
 for n, p, B in ((1000, 20, 4096), (200, 3, 1000), (517, 32, 777), (1500, 17, 513), (64, 5, 300),
-                (300, 29, 200)):
+                (300, 29, 200), (400, 50, 300), (300, 64, 200), (1000, 40, 500), (200, 33, 100)):
     inst = hg.generate_urand(n, p, 1704 + n, (1.0, 0.75, 1.0))
     pop = hg.random_population(n, p, B, key=n + p)
     out = hg.evaluate_population(inst, pop)
