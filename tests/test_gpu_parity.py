@@ -645,6 +645,22 @@ class TestExactSums:
         assert np.array_equal(got, want)
         assert np.array_equal(got2, want)
 
+    def test_full_batch_many_units(self):
+        """8192 hub sets: every CTA pair runs ~9 units back to back, so the
+        shared-memory terms, stacks and bins are reused across units; sampled
+        rows bit-identical to numpy, the whole batch identical run to run."""
+        inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
+        pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+        pop = hg.random_population(1000, 20, 8192, key=11)
+        got = hg.evaluate_population(inst, pop)
+        again = hg.evaluate_population(inst, pop)
+        assert np.array_equal(got, again)
+        rows = np.arange(0, 8192, 129)
+        al = hg.nearest_allocations(inst, pop[rows])
+        for j, b in enumerate(rows):
+            c, t, d = orc.cost_terms(pr, pop[b], al[j])
+            assert np.array_equal(got[b], [c, t, d, c + t + d]), b
+
     @pytest.mark.parametrize("n,p", [(1030, 9), (2100, 12)])
     def test_multi_chunk_legs_exact_transfer_close(self, n, p):
         """n > 1024 (K chunks): the leg sums stay bit-identical, the transfer
