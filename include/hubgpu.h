@@ -178,6 +178,11 @@ typedef struct {
 /* Philox4x32-10 block (Salmon et al., SC'11), the GA's PHILOX generator;
  * host-side entry for known-answer tests */
 void hg_philox4x32_10(const uint32_t key[2], const uint32_t ctr[4], uint32_t out[4]);
+/* numpy's pairwise summation (pairwise_sum_DOUBLE, the order of every np.sum
+ * in hm/evaluation.py:110-118) as the leaf table the exact mode replays: per
+ * leaf first row of 8 terms | full rows << 16 | tree sums after it << 24;
+ * host-only, for tests */
+int hg_pairwise_leaves(int64_t m, uint32_t* out, int cap, int* count);
 
 int hg_ga_create(hg_inst* inst, const hg_ga_params* params, hg_ga** out);
 void hg_ga_free(hg_ga* ga);

@@ -55,6 +55,8 @@ SIGNATURES = {
     "hg_instance_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "hg_instance_set_fitness": (C.c_int, [_vp, C.c_int]),
     "hg_instance_set_exact": (C.c_int, [_vp, C.c_int]),
+    "hg_pairwise_leaves": (C.c_int, [C.c_int64, C.POINTER(C.c_uint32), C.c_int,
+                                     C.POINTER(C.c_int)]),
     "hg_instance_exact": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "hg_instance_fitness": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "hg_synchronize": (C.c_int, [_vp]),
@@ -506,3 +508,13 @@ _pinned = _PinnedPool()
 
 def pinned_array(shape, dtype) -> np.ndarray:
     return _pinned.array(shape, dtype)
+
+
+def pairwise_leaves(m: int) -> np.ndarray:
+    """The exact mode's leaf table for an m-term np.sum (hg_pairwise_leaves)."""
+    cnt = C.c_int()
+    check(load().hg_pairwise_leaves(int(m), None, 0, C.byref(cnt)))
+    out = np.zeros(max(cnt.value, 1), dtype=np.uint32)
+    check(load().hg_pairwise_leaves(int(m), out.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                    out.size, C.byref(cnt)))
+    return out[:cnt.value]

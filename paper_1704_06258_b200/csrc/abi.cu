@@ -1197,6 +1197,14 @@ int hg_ga_launches_per_generation(const hg_ga* ga) {
     return ga_launches(ga);
 }
 
+int hg_pairwise_leaves(int64_t m, uint32_t* out, int cap, int* count) {
+    HG_ARG(m >= 0 && count != nullptr, "bad arguments");
+    const std::vector<uint32_t> t = pw_leaf_table(m);
+    *count = (int)t.size();
+    for (int k = 0; k < cap && k < (int)t.size(); ++k) out[k] = t[k];
+    return HG_OK;
+}
+
 // ---------------------------------------------------------------------------
 // device generator, GPU restricted optimum
 // ---------------------------------------------------------------------------

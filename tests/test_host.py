@@ -208,3 +208,47 @@ def test_rng_mode_validated():
     with pytest.raises(ValueError, match="rng must be"):
         hg.GaParams(rng="mt19937")
     assert hg.GaParams().rng == "replay"
+
+
+def _replay_pairwise(a: np.ndarray) -> float:
+    """The exact mode's device algorithm, step for step, in Python: per leaf
+    the 8 strided accumulators (rows of 8 terms), their fixed combine, the
+    last leaf's partial row term by term, then the tree sums on a stack."""
+    m = a.size
+    table = _lib.pairwise_leaves(m)
+    rows, tail = m // 8, m % 8
+    stack = []
+    for k, e in enumerate(table):
+        r0, nr, nsum = int(e & 0xFFFF), int((e >> 16) & 0xFF), int(e >> 24)
+        last = k == len(table) - 1
+        if nr == 0:
+            acc = [0.0] * 8
+        else:
+            acc = [float(a[8 * r0 + j]) for j in range(8)]
+            for q in range(1, nr):
+                for j in range(8):
+                    acc[j] = acc[j] + float(a[8 * (r0 + q) + j])
+        c = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]))
+        if last:
+            for u in range(tail):
+                c = c + float(a[8 * rows + u])
+        stack.append(c)
+        for _ in range(len(stack) - 1 if last else nsum):
+            right = stack.pop()
+            stack[-1] = stack[-1] + right
+    return stack[0]
+
+
+@pytest.mark.parametrize("m", [0, 1, 5, 7, 8, 9, 15, 16, 100, 127, 128, 129, 136, 257, 400,
+                               1000, 1024, 1030, 2100, 4096, 6000, 16384])
+def test_pairwise_leaf_table_replays_numpy_sum(m):
+    """hg_pairwise_leaves (the table exact mode replays on the device) gives
+    np.sum's value bit for bit (hm/evaluation.py:110-118 sum products this
+    way); leaves hold <= 16 rows and start on rows of 8."""
+    rng = np.random.default_rng(m)
+    a = rng.random(m) * rng.random(m) * 1e6
+    table = _lib.pairwise_leaves(m)
+    assert all(((e >> 16) & 0xFF) <= 16 for e in table)
+    if m == 0:
+        return
+    assert _replay_pairwise(a) == float(np.sum(a))
