@@ -482,6 +482,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             }
             const uint32_t* tbp = A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps + l;
             double s_acc = 0.0;  // this thread's share of S_T over the chunks
+            double lg0 = 0.0, lg1 = 0.0;  // leg sums of this warp's first individual
             for (int c = 0; c < NC; ++c, ++phase) {
                 const bool last_phase = j + 1 == nslots && c + 1 == NC;
                 for (int tt = 0; tt < NT; ++tt, ++t) {
@@ -562,6 +563,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     const bool ok = live && k < p;
                     th[u] = ok ? __ldg(tbp + k * A.ps) : 0u;
                     tl[u] = ok ? __ldg(tbp + (p + k) * A.ps) : 0u;
+                }
+                if (c + 1 == NC && A.out && lane == 0 && warp - kYEpiWarp0 < nind) {
+                    // the finaliser's leg sums, fetched now: their L2 latency
+                    // hides under the barrier instead of the reduce
+                    const int64_t b = bbase + (warp - kYEpiWarp0);
+                    lg0 = __ldg(A.legs + 2 * b);
+                    lg1 = __ldg(A.legs + 2 * b + 1);
                 }
                 epi_sync();  // every bin of the chunk is complete
                 if (live && EX) {
@@ -665,8 +673,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         const double st = stk[0];
                         if (A.out) {
                             const int64_t b = bbase + b2;
-                            const double coll = A.chi * A.legs[2 * b];
-                            const double dist = A.delta * A.legs[2 * b + 1];
+                            const bool pre = b2 == warp - kYEpiWarp0;
+                            const double coll = A.chi * (pre ? lg0 : A.legs[2 * b]);
+                            const double dist = A.delta * (pre ? lg1 : A.legs[2 * b + 1]);
                             const double tran = A.alpha * st;
                             A.out[4 * b + 0] = coll;
                             A.out[4 * b + 1] = tran;
@@ -682,10 +691,12 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             // one warp per individual: lanes stride its 4p partials, then a
             // butterfly (fixed order -> deterministic)
             for (int b2 = (warp - kYEpiWarp0); b2 < nind; b2 += kYEpiThreads / 32) {
+                // lane l sums column l's 4 quarter partials ((q0+q1)+(q2+q3)),
+                // columns l >= 32 folded in after (fixed order)
                 double acc = 0.0;
-                for (int x = lane; x < 4 * p; x += 32) {
-                    const int sq = x / p, ll = x - sq * p;
-                    acc += red[sq * 128 + b2 * p + ll];
+                for (int ll = lane; ll < p; ll += 32) {
+                    const double* rp = red + b2 * p + ll;
+                    acc += (rp[0] + rp[128]) + (rp[256] + rp[384]);
                 }
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
@@ -693,8 +704,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     if (A.out) {
                         // the finaliser (k_finalize), fused: same operations
                         const int64_t b = bbase + b2;
-                        const double coll = A.chi * A.legs[2 * b];
-                        const double dist = A.delta * A.legs[2 * b + 1];
+                        const bool pre = b2 == warp - kYEpiWarp0;
+                        const double coll = A.chi * (pre ? lg0 : A.legs[2 * b]);
+                        const double dist = A.delta * (pre ? lg1 : A.legs[2 * b + 1]);
                         const double tran = A.alpha * acc;
                         A.out[4 * b + 0] = coll;
                         A.out[4 * b + 1] = tran;
