@@ -661,6 +661,25 @@ class TestExactSums:
             c, t, d = orc.cost_terms(pr, pop[b], al[j])
             assert np.array_equal(got[b], [c, t, d, c + t + d]), b
 
+    @pytest.mark.parametrize("n,p,full", [(1024, 56, True), (1024, 8, True), (1000, 64, False),
+                                          (1000, 100, False)])
+    def test_large_p(self, n, p, full):
+        """p up to ~56 keeps the [p][128] fp64 terms beside two W stages: all
+        four terms bit-identical; beyond that the transfer sum is the
+        fixed-order fold (within the fp64 bar), the leg sums stay exact."""
+        inst = hg.generate_urand(n, p, 7 + p, (1.0, 0.75, 1.0))
+        pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
+        pop = hg.random_population(n, p, 60, key=p)
+        got = hg.evaluate_population(inst, pop)
+        al = hg.nearest_allocations(inst, pop)
+        for b in range(60):
+            c, t, d = orc.cost_terms(pr, pop[b], al[b])
+            assert got[b, 0] == c and got[b, 2] == d
+            if full:
+                assert got[b, 1] == t and got[b, 3] == c + t + d
+            else:
+                assert close(got[b, 1], t) and close(got[b, 3], c + t + d)
+
     @pytest.mark.parametrize("n,p", [(1030, 9), (2100, 12)])
     def test_multi_chunk_legs_exact_transfer_close(self, n, p):
         """n > 1024 (K chunks): the leg sums stay bit-identical, the transfer
