@@ -74,8 +74,8 @@ int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags);
 /* cost sums in numpy's pairwise order (on = 1): the collection, distribution
  * and transfer sums np.sum(out_flow * legs), np.sum(in_flow * legs),
  * np.sum(inter * hub_dist) of hm/evaluation.py:110-118 reproduced bit for bit
- * (the transfer sum when the CTA-pair kernel runs one K chunk on one byte
- * plane: n <= 1024, flows < 256, p <= ~56).  on = 0 (default): fixed-order
+ * (the transfer sum when the CTA-pair kernel runs and p <= ~56, with a
+ * total flow below 2^32 when n > 1024 or flows >= 256).  on = 0 (default): fixed-order
  * sums, deterministic, within ~1 ulp of the reference.  Read at each launch;
  * GA objects keep the mode they were created with. */
 int hg_instance_set_exact(hg_inst* inst, int on);

@@ -483,12 +483,16 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         // exact u8 GEMMs on P byte planes of W (P = 1 when every flow < 256;
         // the smem and one-CTA TMEM kernels take P = 1 only)
         bool intw = p >= 1 && p <= 128;
-        double wmax = 0.0;
+        double wmax = 0.0, wsum = 0.0;
         for (size_t x = 0; intw && x < nn; ++x) {
             const double v = flow[x];
             if (!(v >= 0.0 && v < 4294967296.0 && v == std::floor(v))) intw = false;
             wmax = v > wmax ? v : wmax;
+            wsum += v;
         }
+        // every byte plane's total below 2^32: u32 bins may accumulate over
+        // all K chunks (the exact transfer sum for n > 1024)
+        I.bins_total_ok = intw && wsum < 4294967296.0 ? 1 : 0;
         int P = 1;
         while (P < 4 && wmax >= std::ldexp(1.0, 8 * P)) ++P;
         I.wplanes = P;

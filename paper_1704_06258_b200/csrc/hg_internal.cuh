@@ -88,6 +88,7 @@ struct DevInst {
     // 1: every cost sum in numpy's pairwise order (bit-identical to the
     // reference); 0: fixed-order sums (deterministic, ~1 ulp apart)
     int exact;
+    int bins_total_ok;  // total flow < 2^32: integer bins can span every K chunk
 };
 
 constexpr int kPwStack = 16;  // tree depth bound (n < 2^21)

@@ -572,27 +572,37 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     lg1 = __ldg(A.legs + 2 * b + 1);
                 }
                 epi_sync();  // every bin of the chunk is complete
-                if (live && EX) {
-                    // (one chunk, one plane) the bins ARE the reference's
-                    // inter-cluster flows: keep each rounded term inter * T
-                    // for the pairwise sums below
+                if (live && EX && c + 1 == NC) {
+                    // the bins (every K chunk accumulated, planes weighted
+                    // 256^pl) ARE the reference's inter-cluster flows, exact
+                    // integers: keep each rounded term inter * T for the
+                    // pairwise sums below
+                    const bool one_plane = A.P == 1;
+                    auto inter = [&](int k) {
+                        uint32_t* bp = binsj + k * 128 + r;
+                        if (one_plane) {
+                            const uint32_t g = *bp;
+                            *bp = 0u;
+                            return (double)g;
+                        }
+                        uint64_t g = 0;
+                        for (int pl = 0; pl < A.P; ++pl, bp += p * 128) {
+                            g += (uint64_t)*bp << (8 * pl);
+                            *bp = 0u;
+                        }
+                        return (double)g;
+                    };
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int k = sub + 4 * u;
-                        if (k < p) {
-                            const uint32_t g = binsj[k * 128 + r];
-                            binsj[k * 128 + r] = 0u;
+                        if (k < p)
                             prod[k * 128 + r] =
-                                __dmul_rn((double)g, __hiloint2double((int)th[u], (int)tl[u]));
-                        }
+                                __dmul_rn(inter(k), __hiloint2double((int)th[u], (int)tl[u]));
                     }
-                    for (int k = sub + 32; k < p; k += 4) {
-                        const uint32_t g = binsj[k * 128 + r];
-                        binsj[k * 128 + r] = 0u;
+                    for (int k = sub + 32; k < p; k += 4)
                         prod[k * 128 + r] = __dmul_rn(
-                            (double)g, __hiloint2double((int)__ldg(tbp + k * A.ps),
-                                                        (int)__ldg(tbp + (p + k) * A.ps)));
-                    }
+                            inter(k), __hiloint2double((int)__ldg(tbp + k * A.ps),
+                                                       (int)__ldg(tbp + (p + k) * A.ps)));
                 }
                 if (live && !EX) {
                     // plane pl of W carries weight 256^pl: an exact power-of-2
@@ -781,7 +791,7 @@ static int p_stages(int p, int npad, int P, bool exact = false) {
 // exact sums need one chunk, one plane and room for the [p][128] terms next
 // to a W ring of >= 2 stages (p <= ~56)
 static bool p_exact(int p, int npad, int P) {
-    return npad <= kYChunkKB * 128 && P == 1 && p_stages(p, npad, P, true) >= 2;
+    return p_stages(p, npad, P, true) >= 2;
 }
 
 // exact: the instance asks for numpy's summation order and the terms fit
@@ -851,9 +861,12 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     A.NC = (A.KBT + kYChunkKB - 1) / kYChunkKB;
     A.P = I.wplanes;
     A.nt = (int)round_up(I.n, 128);
-    // exact: the instance asks for numpy's order and one chunk / one plane / the
-    // terms fit (else the fixed-order fold: tran within ~1 ulp)
-    A.exact = I.exact && A.NC == 1 && p_exact(I.p, I.npad, A.P) && I.pwl != nullptr;
+    // exact: the instance asks for numpy's order and the [p][128] terms fit
+    // beside two W stages (else the fixed-order fold: tran within ~1 ulp)
+    // (several K chunks or planes: the bins accumulate over all of them, exact
+    // while the total flow stays below 2^32)
+    A.exact = I.exact && (A.NC == 1 && A.P == 1 || I.bins_total_ok) && p_exact(I.p, I.npad, A.P) &&
+              I.pwl != nullptr;
     A.stages = p_stages(I.p, I.npad, A.P, A.exact);  // as tcp_smem_bytes
     A.kbs = p_kbs();
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;

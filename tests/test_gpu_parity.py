@@ -680,19 +680,25 @@ class TestExactSums:
             else:
                 assert close(got[b, 1], t) and close(got[b, 3], c + t + d)
 
-    @pytest.mark.parametrize("n,p", [(1030, 9), (2100, 12)])
-    def test_multi_chunk_legs_exact_transfer_close(self, n, p):
-        """n > 1024 (K chunks): the leg sums stay bit-identical, the transfer
-        sum is the fixed-order fold (within the fp64 bar)."""
+    @pytest.mark.parametrize("n,p,wmax", [(1030, 9, None), (2100, 12, None), (3000, 20, None),
+                                          (300, 7, 1000), (200, 12, 70000)])
+    def test_multi_chunk_and_planes(self, n, p, wmax):
+        """n > 1024 (K chunks) and flows >= 256 (byte planes): the integer
+        bins accumulate over every chunk and plane (total flow < 2^32 here),
+        so all four terms stay bit-identical."""
         inst = hg.generate_urand(n, p, 1704 + n, (1.0, 0.75, 1.0))
+        if wmax is not None:
+            rng = np.random.default_rng(n)
+            flow = rng.integers(0, wmax + 1, size=(n, n)).astype(np.float64)
+            np.fill_diagonal(flow, 0.0)
+            inst = hg.Instance(n, p, inst.dist, flow, 1.0, 0.75, 1.0)
         pr = orc.Problem(inst.n, inst.p, inst.dist, inst.flow, 1.0, 0.75, 1.0)
         pop = hg.random_population(n, p, 40, key=n + p)
         got = hg.evaluate_population(inst, pop)
         al = hg.nearest_allocations(inst, pop)
         for b in range(40):
             c, t, d = orc.cost_terms(pr, pop[b], al[b])
-            assert got[b, 0] == c and got[b, 2] == d
-            assert close(got[b, 1], t)
+            assert np.array_equal(got[b], [c, t, d, c + t + d]), b
 
     def test_default_mode_within_an_ulp_or_so(self):
         hg.set_exact_sums(False)
