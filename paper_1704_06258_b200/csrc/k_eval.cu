@@ -220,10 +220,13 @@ struct PwState {
     int depth;   // tree stack depth (warp-uniform)
 };
 
-__device__ __forceinline__ void pw_init(PwState& S, const uint32_t* __restrict__ tab) {
+__device__ __forceinline__ void pw_init(PwState& S, const uint32_t* __restrict__ tab,
+                                        double* ring, int lane) {
     S.leaf = 0;
     S.e = __ldg(tab);
     S.depth = 0;
+    if (lane < 16) ring[(lane >> 3) * 8 * kPwCol + (lane & 7) * kPwCol + 32] = 0.0;  // zero slots
+    __syncwarp();
 }
 
 // every leaf whose rows are all staged (rows < row_end) is summed.  The 8
@@ -243,13 +246,15 @@ __device__ __forceinline__ void pw_leaves_upto(const uint32_t* __restrict__ tab,
         const bool last = S.leaf == nleaf - 1;
         if ((last && tail ? R + 1 : r0 + nr) > row_end) break;
         if (!last) S.e = __ldg(tab + S.leaf + 1);
+        // rows past the leaf read slot 32 of the column, kept at +0.0 (adding
+        // it leaves a sum of non-negative terms unchanged bit for bit)
+        const int s0 = r0 & 31;
         double v[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = col[(r0 + q) & 31];
-        double acc = nr > 0 ? v[0] : 0.0;
+        for (int q = 0; q < 16; ++q) v[q] = col[q < nr ? (s0 + q) & 31 : 32];
+        double acc = v[0];
 #pragma unroll
-        for (int q = 1; q < 16; ++q)
-            if (q < nr) acc = __dadd_rn(acc, v[q]);
+        for (int q = 1; q < 16; ++q) acc = acc + v[q];
         acc = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
         acc = acc + __shfl_xor_sync(0xffffffffu, acc, 2);
         acc = acc + __shfl_xor_sync(0xffffffffu, acc, 4);
@@ -414,7 +419,7 @@ k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __re
     __syncwarp();
 
     PwState S;
-    if (LM == kLegsExact) pw_init(S, I.pwnl);
+    if (LM == kLegsExact) pw_init(S, I.pwnl, ring, lane);
     double so = 0.0, sd = 0.0;
     for (int c0 = 0; c0 < I.npad; c0 += 128) {
         const int i0 = c0 + 4 * lane;
@@ -523,7 +528,7 @@ k_allocate_r(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __
     constexpr unsigned kS = 256u * PM + PM * (PM - 1) / 2;
 
     PwState S;
-    if (LM == kLegsExact) pw_init(S, I.pwnl);
+    if (LM == kLegsExact) pw_init(S, I.pwnl, ring, lane);
     double so = 0.0, sd = 0.0;
     for (int c0 = 0; c0 < I.npad; c0 += 128) {
         unsigned wv[2];
@@ -624,7 +629,7 @@ k_from_alloc(DevInst I, int64_t B, const int32_t* __restrict__ hubs,
     for (int k = lane; k < p; k += 32) hs[k] = bad ? k : hubs[b * p + k];
     __syncwarp();
     PwState S;
-    if (LM == kLegsExact) pw_init(S, I.pwnl);
+    if (LM == kLegsExact) pw_init(S, I.pwnl, ring, lane);
     double so = 0.0, sd = 0.0;
     const bool notie[4] = {false, false, false, false};
     for (int c0 = 0; c0 < I.npad; c0 += 128) {
