@@ -466,6 +466,108 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         ET(e_gen);
         // this thread's bin row: bins[k][r] at byte k * 512 + r * 4
         const uint32_t bin_r0 = su32(bins) + (uint32_t)r * 4u;
+        // a unit's S_T reduce and finaliser, run during the next unit's first
+        // tile (the MMA keeps its two accumulators busy meanwhile; red and prod
+        // are rewritten only after the next chunk-pass barrier)
+        auto reduce_unit = [&](const int64_t bbase_u, const int nind_u, const double lg0_u,
+                               const double lg1_u) {
+                if (EX) {
+                    // S_T = np.sum(inter * hub_dist) in numpy's pairwise order
+                    // (hm/evaluation.py:117-118) over the terms in `prod`: one warp
+                    // per individual, lane group g (8 lanes) runs leaf L0 + g's 8
+                    // strided accumulators over its <= 16 rows (x = k*p + l; rows
+                    // past the leaf add +0.0, exact for these non-negative terms),
+                    // lane 0 sums the leaves up the halving tree on a stack in `red`
+                    const int m = p * p, R8 = m & ~7;
+                    const uint32_t pmag = (1u << 24) / (uint32_t)p + 1u;  // x / p for x < 2^16
+                    const int g = lane >> 3, jl = lane & 7;
+                    double* stk = red + (warp - kYEpiWarp0) * 32;
+                    for (int b2 = (warp - kYEpiWarp0); b2 < nind_u; b2 += kYEpiThreads / 32) {
+                        const double* pb = prod + b2 * p;
+                        auto term = [&](uint32_t x) {
+                            const int k = (int)((x * pmag) >> 24);
+                            return pb[k * 128 + ((int)x - k * p)];
+                        };
+                        int depth = 0;
+                        for (int L0 = 0; L0 < A.nleaf; L0 += 4) {
+                            const int L = L0 + g;
+                            const uint32_t e = L < A.nleaf ? __ldg(A.leaves + L) : 0u;
+                            const int r0 = (int)(e & 0xffffu), nr = (int)((e >> 16) & 0xffu);
+                            double acc = 0.0;
+    #pragma unroll 4
+                            for (int q = 0; q < 16; ++q) {
+                                const double v = q < nr ? term(8u * (uint32_t)(r0 + q) + jl) : 0.0;
+                                acc = q == 0 ? v : acc + v;
+                            }
+                            acc = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+                            acc = acc + __shfl_xor_sync(0xffffffffu, acc, 2);
+                            acc = acc + __shfl_xor_sync(0xffffffffu, acc, 4);
+                            if (L == A.nleaf - 1 && jl == 0)  // the last leaf's partial row
+                                for (int x = R8; x < m; ++x) acc = acc + term((uint32_t)x);
+    #pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const double cu = __shfl_sync(0xffffffffu, acc, 8 * u);
+                                const uint32_t eu = __shfl_sync(0xffffffffu, e, 8 * u);
+                                if (lane == 0 && L0 + u < A.nleaf) {
+                                    stk[depth++] = cu;
+                                    for (int c2 = L0 + u == A.nleaf - 1 ? depth - 1 : (int)(eu >> 24);
+                                         c2 > 0; --c2, --depth)
+                                        stk[depth - 2] = stk[depth - 2] + stk[depth - 1];
+                                }
+                            }
+                        }
+                        if (lane == 0) {
+                            const double st = stk[0];
+                            if (A.out) {
+                                const int64_t b = bbase_u + b2;
+                                const bool pre = b2 == warp - kYEpiWarp0;
+                                const double coll = A.chi * (pre ? lg0_u : A.legs[2 * b]);
+                                const double dist = A.delta * (pre ? lg1_u : A.legs[2 * b + 1]);
+                                const double tran = A.alpha * st;
+                                A.out[4 * b + 0] = coll;
+                                A.out[4 * b + 1] = tran;
+                                A.out[4 * b + 2] = dist;
+                                A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
+                            } else {
+                                A.part[bbase_u + b2] = st;
+                            }
+                        }
+                        __syncwarp();
+                    }
+                } else
+                // one warp per individual: lanes stride its 4p partials, then a
+                // butterfly (fixed order -> deterministic)
+                for (int b2 = (warp - kYEpiWarp0); b2 < nind_u; b2 += kYEpiThreads / 32) {
+                    // lane l sums column l's 4 quarter partials ((q0+q1)+(q2+q3)),
+                    // columns l >= 32 folded in after (fixed order)
+                    double acc = 0.0;
+                    for (int ll = lane; ll < p; ll += 32) {
+                        const double* rp = red + b2 * p + ll;
+                        acc += (rp[0] + rp[128]) + (rp[256] + rp[384]);
+                    }
+    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    if (lane == 0) {
+                        if (A.out) {
+                            // the finaliser (k_finalize), fused: same operations
+                            const int64_t b = bbase_u + b2;
+                            const bool pre = b2 == warp - kYEpiWarp0;
+                            const double coll = A.chi * (pre ? lg0_u : A.legs[2 * b]);
+                            const double dist = A.delta * (pre ? lg1_u : A.legs[2 * b + 1]);
+                            const double tran = A.alpha * acc;
+                            A.out[4 * b + 0] = coll;
+                            A.out[4 * b + 1] = tran;
+                            A.out[4 * b + 2] = dist;
+                            A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
+                        } else {
+                            A.part[bbase_u + b2] = acc;
+                        }
+                    }
+                }
+        };
+        int64_t pend_b = 0;
+        int pend_n = -1;  // a unit whose reduce is pending
+        double pend_l0 = 0.0, pend_l1 = 0.0;
         uint32_t phase = 0;
         for (int64_t j = 0; j < nslots; ++j) {
             int64_t bbase;
@@ -551,6 +653,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         }
                     }
                     ET(e_cmp);
+                    if (c == 0 && tt == 0 && pend_n >= 0) {  // the previous unit's reduce
+                        reduce_unit(pend_b, pend_n, pend_l0, pend_l1);
+                        pend_n = -1;
+                        ET(e_red);
+                    }
                 }
                 // this chunk's bins into S_T: sum_k T_b[k][l] * G_c[k][(b,l)] over
                 // k = sub, sub + 4, ... (fixed order -> deterministic); one chunk's
@@ -634,101 +741,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 epi_sync();  // bins zeroed before the next chunk's atomics (red / prod written)
                 ET(e_st);
             }
-            if (EX) {
-                // S_T = np.sum(inter * hub_dist) in numpy's pairwise order
-                // (hm/evaluation.py:117-118) over the terms in `prod`: one warp
-                // per individual, lane group g (8 lanes) runs leaf L0 + g's 8
-                // strided accumulators over its <= 16 rows (x = k*p + l; rows
-                // past the leaf add +0.0, exact for these non-negative terms),
-                // lane 0 sums the leaves up the halving tree on a stack in `red`
-                const int m = p * p, R8 = m & ~7;
-                const uint32_t pmag = (1u << 24) / (uint32_t)p + 1u;  // x / p for x < 2^16
-                const int g = lane >> 3, jl = lane & 7;
-                double* stk = red + (warp - kYEpiWarp0) * 32;
-                for (int b2 = (warp - kYEpiWarp0); b2 < nind; b2 += kYEpiThreads / 32) {
-                    const double* pb = prod + b2 * p;
-                    auto term = [&](uint32_t x) {
-                        const int k = (int)((x * pmag) >> 24);
-                        return pb[k * 128 + ((int)x - k * p)];
-                    };
-                    int depth = 0;
-                    for (int L0 = 0; L0 < A.nleaf; L0 += 4) {
-                        const int L = L0 + g;
-                        const uint32_t e = L < A.nleaf ? __ldg(A.leaves + L) : 0u;
-                        const int r0 = (int)(e & 0xffffu), nr = (int)((e >> 16) & 0xffu);
-                        double acc = 0.0;
-#pragma unroll 4
-                        for (int q = 0; q < 16; ++q) {
-                            const double v = q < nr ? term(8u * (uint32_t)(r0 + q) + jl) : 0.0;
-                            acc = q == 0 ? v : acc + v;
-                        }
-                        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
-                        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 2);
-                        acc = acc + __shfl_xor_sync(0xffffffffu, acc, 4);
-                        if (L == A.nleaf - 1 && jl == 0)  // the last leaf's partial row
-                            for (int x = R8; x < m; ++x) acc = acc + term((uint32_t)x);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const double cu = __shfl_sync(0xffffffffu, acc, 8 * u);
-                            const uint32_t eu = __shfl_sync(0xffffffffu, e, 8 * u);
-                            if (lane == 0 && L0 + u < A.nleaf) {
-                                stk[depth++] = cu;
-                                for (int c2 = L0 + u == A.nleaf - 1 ? depth - 1 : (int)(eu >> 24);
-                                     c2 > 0; --c2, --depth)
-                                    stk[depth - 2] = stk[depth - 2] + stk[depth - 1];
-                            }
-                        }
-                    }
-                    if (lane == 0) {
-                        const double st = stk[0];
-                        if (A.out) {
-                            const int64_t b = bbase + b2;
-                            const bool pre = b2 == warp - kYEpiWarp0;
-                            const double coll = A.chi * (pre ? lg0 : A.legs[2 * b]);
-                            const double dist = A.delta * (pre ? lg1 : A.legs[2 * b + 1]);
-                            const double tran = A.alpha * st;
-                            A.out[4 * b + 0] = coll;
-                            A.out[4 * b + 1] = tran;
-                            A.out[4 * b + 2] = dist;
-                            A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
-                        } else {
-                            A.part[bbase + b2] = st;
-                        }
-                    }
-                    __syncwarp();
-                }
-            } else
-            // one warp per individual: lanes stride its 4p partials, then a
-            // butterfly (fixed order -> deterministic)
-            for (int b2 = (warp - kYEpiWarp0); b2 < nind; b2 += kYEpiThreads / 32) {
-                // lane l sums column l's 4 quarter partials ((q0+q1)+(q2+q3)),
-                // columns l >= 32 folded in after (fixed order)
-                double acc = 0.0;
-                for (int ll = lane; ll < p; ll += 32) {
-                    const double* rp = red + b2 * p + ll;
-                    acc += (rp[0] + rp[128]) + (rp[256] + rp[384]);
-                }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                if (lane == 0) {
-                    if (A.out) {
-                        // the finaliser (k_finalize), fused: same operations
-                        const int64_t b = bbase + b2;
-                        const bool pre = b2 == warp - kYEpiWarp0;
-                        const double coll = A.chi * (pre ? lg0 : A.legs[2 * b]);
-                        const double dist = A.delta * (pre ? lg1 : A.legs[2 * b + 1]);
-                        const double tran = A.alpha * acc;
-                        A.out[4 * b + 0] = coll;
-                        A.out[4 * b + 1] = tran;
-                        A.out[4 * b + 2] = dist;
-                        A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
-                    } else {
-                        A.part[bbase + b2] = acc;
-                    }
-                }
-            }
+            pend_b = bbase;
+            pend_n = nind;
+            pend_l0 = lg0;
+            pend_l1 = lg1;
             ET(e_red);
         }
+        if (pend_n >= 0) reduce_unit(pend_b, pend_n, pend_l0, pend_l1);  // the last unit
         if (timed) {
             atomicAdd(A.timing + 16, e_st);
             atomicAdd(A.timing + 17, e_gen);
