@@ -44,7 +44,7 @@ POP = 8192
 HBM_FALLBACK = 6650.0
 
 
-NCU_TRAFFIC_FILE = "profiles/ncu_traffic_r1l.json"
+NCU_TRAFFIC_FILE = "profiles/ncu_traffic_r1m.json"
 
 
 def ncu_traffic(fit_kernel):
