@@ -10,9 +10,13 @@ K2 nearest-hub allocation + K3 fitness + finalise (3 kernels).  L2 is flushed
 (N > 1) every rank scores its own 8192 individuals (weak scaling); the step
 time is the max over ranks.
 
+``--gpus N`` without torchrun spawns N ranks itself (one process per GPU,
+NCCL), and fails if fewer than N devices are visible; under torchrun the
+world size comes from the environment and must equal --gpus.
+
 ``--impl reference`` times the reference's algorithm on the host cores (the
-numpy restatement in oracle/, the reference itself cannot travel to the GPU
-box) on the same instance and population: rank 0 only.
+numpy restatement in oracle/, bit-pinned to the reference's own outputs) on
+the same instance and population: rank 0 only.
 """
 
 from __future__ import annotations
@@ -35,8 +39,6 @@ sys.path.insert(0, str(ROOT))
 METRIC = "fitness evals/sec at n=1000,p=20 (1-8 B200); GA time-to-best-cost vs CPU ref"
 KERNEL_NAMES = {
     "tensor-pair": "k_fitness_tcp (K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs + integer bins + fused finalise)",
-    "tensor-tmem": "k_fitness_tcy (K3-TC/Y: u8 one-hot GEMM, one-hot in TMEM + integer bins)",
-    "tensor-smem": "k_fitness_tc (K3-TC/X: u8 one-hot GEMM, one-hot in smem + fp64 epilogue)",
     "fp64": "k_fitness (K3: fp64 smem gather)",
 }
 N, P, SEED, FACTORS = 1000, 20, 1704, (1.0, 0.75, 1.0)
@@ -57,8 +59,7 @@ def ncu_traffic(fit_kernel):
         return None
     import re
 
-    pat = {"tensor-pair": r"k_fitness_tcp\b", "tensor-tmem": r"k_fitness_tcy\b",
-           "tensor-smem": r"k_fitness_tc\b", "fp64": r"k_fitness<"}[fit_kernel]
+    pat = {"tensor-pair": r"k_fitness_tcp\b", "fp64": r"k_fitness<"}[fit_kernel]
     for name, v in ks.items():
         if re.search(pat, name):
             return v["dram_bytes"]
@@ -158,45 +159,77 @@ def cpu_model():
 
 
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons of this rank's GPU, read through NVML.
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    ``poll(done)`` samples back to back while the timed kernels run (the host
+    has queued every step and waits on the last event), so even a few-ms timed
+    region yields samples; a background thread also samples every 2 ms."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, cuda_index: int):
+        import threading
+
+        self.h = None
+        self.rows = []
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml as nv
+            import torch
+
+            nv.nvmlInit()
+            self.nv = nv
+            try:
+                pr = torch.cuda.get_device_properties(cuda_index)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = nv.nvmlDeviceGetHandleByIndex(cuda_index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.h = None
+        self._stop = threading.Event()
+        self._t = None
+        if self.h is not None:
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
+
+    def sample(self):
+        if self.h is None:
+            return
+        nv = self.nv
+        try:
+            mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            return
+        self.rows.append((mhz, r))
+
+    def _loop(self):
+        while not self._stop.wait(0.002):
+            self.sample()
+
+    def poll(self, done) -> None:
+        """Sample until done() is true (the timed region's last event)."""
+        while not done():
+            self.sample()
+            time.sleep(0.0002)
 
     def stop(self):
-        if self.proc is None:
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=1.0)
+        if self.h is None or not self.rows:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.f.flush()
-        rows = []
-        for line in Path(self.f.name).read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
-            return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+        nv = self.nv
+        reasons = sorted({name for _, r in self.rows for name, attr in self.REASONS
+                          if hasattr(nv, attr) and r & getattr(nv, attr)})
+        return {"sm_mhz": statistics.median(m for m, _ in self.rows),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML during the timed region (polled while the queued steps run)"}
 
 
 # ---------------------------------------------------------------------------
@@ -268,6 +301,11 @@ def run_gpu(args):
     import paper_1704_06258_b200 as hg
 
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, "
+                         f"{torch.cuda.device_count()} device(s) visible")
     if world > 1:
         import torch.distributed as dist
 
@@ -301,11 +339,14 @@ def run_gpu(args):
               for _ in range(args.steps)]
         barrier()
         t_wall0 = time.perf_counter()
+        launches0 = hg._lib.launch_count()
         for k in range(args.steps):  # no host sync inside: the GPU stays loaded
             flush.zero_()
             ev[k][0].record(stream)
             popd.evaluate(POP)
             ev[k][1].record(stream)
+        launches = hg._lib.launch_count() - launches0
+        clocks.poll(ev[-1][1].query)  # clocks while the queued steps run
         barrier()
         t_wall = time.perf_counter() - t_wall0
         clk = clocks.stop()
@@ -337,7 +378,7 @@ def run_gpu(args):
     tensor_ops = POP * 2.0 * N * N * P
     # every other K3 variant on the same population, for comparison
     variant_ms = {}
-    for name in ("fp64", "tensor-smem", "tensor-tmem", "tensor-pair"):
+    for name in ("fp64", "tensor-pair"):
         try:
             dinst.set_fitness(hg._lib.FIT_NAMES[name])
         except ValueError:
@@ -452,7 +493,7 @@ def run_gpu(args):
                     "h2d_bytes_per_step": int(pop_host.nbytes),
                     "d2h_bytes_per_step": int(res.nbytes),
                     "api": "paper_1704_06258_b200.evaluate_population (hg_evaluate)"},
-            "gpu_launches": (2 if fit_kernel == "tensor-pair" else 3) * args.steps,
+            "gpu_launches": launches,
             "clocks": clk,
             "ga": {"child_evals_per_s": world * 128 * 64 / (ga_ms * 1e-3),
                    "ms_per_generation": ga_ms, "config": "R=128 x pop 64 per GPU, strength 3",
@@ -509,6 +550,31 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _spawned_rank(local: int, args, world: int, port: int) -> None:
+    os.environ.update(RANK=str(local), LOCAL_RANK=str(local), WORLD_SIZE=str(world),
+                      LOCAL_WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    run_gpu(args)
+
+
+def spawn_ranks(args) -> None:
+    """--gpus N outside torchrun: one process per GPU (torch.multiprocessing,
+    NCCL), launched here; an error if fewer than N devices are visible."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.start_processes(_spawned_rank, args=(args, args.gpus, port), nprocs=args.gpus,
+                       start_method="spawn")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -521,10 +587,14 @@ def main():
     ap.add_argument("--ga-inner", type=int, default=12,
                     help="generations of the CPU-reference GA run (about 1 s each)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)
     else:
         run_gpu(args)
 

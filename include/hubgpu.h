@@ -18,7 +18,9 @@
  *     Solution encoding, hm/model.py:124-138); masks are one byte per node
  *     (numpy bool);
  *   - all device work of an instance runs on the instance's stream, in order;
- *     calls on one instance must not be made concurrently from two threads.
+ *     an instance may be shared across threads (as the reference's Instance,
+ *     hm/model.py:35): every call that uses an instance, or a population or
+ *     GA built on it, holds that instance's mutex for its duration.
  */
 #ifndef HUBGPU_H
 #define HUBGPU_H
@@ -41,16 +43,16 @@ extern "C" {
 /* instance flags reported by hg_instance_info */
 #define HG_FLAG_SYMMETRIC 1    /* dist == dist^T exactly: one matrix serves both */
 #define HG_FLAG_WEIGHTS_EXACT 2 /* out+in flow integer-valued, total < 2^53      */
-#define HG_FLAG_TENSOR_OK 4     /* flows non-negative integers < 2^32 (p <= 128):
-                                   exact u8 tensor path on 1..4 byte planes of W  */
+#define HG_FLAG_TENSOR_OK 4     /* flows non-negative integers < 2^32, p <= 128,
+                                   n <= 16384: exact u8 tensor path on 1..4 byte
+                                   planes of W                                   */
 
 /* fitness kernel choice (hg_instance_set_fitness) */
 #define HG_FIT_AUTO 0      /* tensor cores when exact, else the fp64 gather   */
 #define HG_FIT_FP64 1      /* K3: fp64 smem-gather kernel (any flows)          */
-#define HG_FIT_TENSOR 2    /* the fastest tensor-core variant this instance has */
-#define HG_FIT_TC_SMEM 3   /* K3-TC/X: one-hot B in smem, any n <= 32768       */
-#define HG_FIT_TC_TMEM 4   /* K3-TC/Y: one-hot A in TMEM, one CTA, n <= 1024  */
-#define HG_FIT_TC_PAIR 5   /* K3-TC/P: K3-TC/Y on CTA pairs (cta_group::2)   */
+#define HG_FIT_TENSOR 2    /* the tensor-core kernel (= HG_FIT_TC_PAIR)         */
+/* 3 and 4 named two superseded tensor-core variants (removed; rejected)   */
+#define HG_FIT_TC_PAIR 5   /* K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs    */
 
 typedef struct hg_inst hg_inst;
 typedef struct hg_pop hg_pop;
@@ -129,6 +131,11 @@ int hg_pop_launches_per_evaluate(const hg_pop* pop);
 /* duration (ms) of the fitness kernel K3 in the last hg_pop_evaluate,
  * measured with CUDA events on the instance stream (synchronises) */
 int hg_pop_last_fitness_ms(hg_pop* pop, float* ms);
+
+/* kernels this library has launched in the process so far (a CUDA-graph
+ * replay adds the kernels it holds); differences of two reads count the
+ * launches of a region (the bench's gpu_launches) */
+int hg_launch_count(uint64_t* count);
 
 /* tuning aid: per-phase cycle counters of K3-TC when the process runs with
  * HUBGPU_TC_TIMING=1 (32 counters, read and reset); HG_EARG otherwise */

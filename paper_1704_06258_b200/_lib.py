@@ -21,10 +21,9 @@ LIB_PATH = Path(__file__).resolve().parent / "libhubgpu.so"
 HG_OK, HG_EARG, HG_ECUDA, HG_ENODEV, HG_ESTATE = 0, 1, 2, 3, 4
 HG_HOST, HG_DEVICE = 0, 1
 FLAG_SYMMETRIC, FLAG_WEIGHTS_EXACT, FLAG_TENSOR_OK = 1, 2, 4
-FIT_AUTO, FIT_FP64, FIT_TENSOR, FIT_TC_SMEM, FIT_TC_TMEM, FIT_TC_PAIR = 0, 1, 2, 3, 4, 5
+FIT_AUTO, FIT_FP64, FIT_TENSOR, FIT_TC_PAIR = 0, 1, 2, 5
 RNG_MODES = {"replay": 0, "philox": 1}  # hg_ga_params.rng
-FIT_NAMES = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR,
-             "tensor-smem": FIT_TC_SMEM, "tensor-tmem": FIT_TC_TMEM, "tensor-pair": FIT_TC_PAIR}
+FIT_NAMES = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR, "tensor-pair": FIT_TC_PAIR}
 
 _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
@@ -71,6 +70,7 @@ SIGNATURES = {
     "hg_pop_launches_per_evaluate": (C.c_int, [_vp]),
     "hg_pop_last_fitness_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "hg_debug_tc_timing": (C.c_int, [_u64p]),
+    "hg_launch_count": (C.c_int, [_u64p]),
     "hg_correct": (C.c_int, [_vp, C.c_int64, _u8p, _i64p]),
     "hg_crossover": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _u8p, _i64p, _u8p, _u8p]),
     "hg_swap": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _i64p, _i64p, _u8p]),
@@ -131,6 +131,13 @@ def check(rc: int) -> None:
     raise HubGpuError(f"libhubgpu error {rc}: {msg}")
 
 
+def launch_count() -> int:
+    """Kernels libhubgpu has launched in this process (hg_launch_count)."""
+    v = C.c_uint64()
+    check(load().hg_launch_count(C.byref(v)))
+    return v.value
+
+
 def device_count() -> int:
     c = C.c_int(0)
     check(load().hg_device_count(C.byref(c)))
@@ -139,15 +146,15 @@ def device_count() -> int:
 
 _device = int(os.environ.get("HUBGPU_DEVICE", os.environ.get("LOCAL_RANK", "0")))
 # transfer-term kernel for new device instances: auto (tensor cores when the
-# flows allow the exact u8 GEMM), fp64 (K3 gather), tensor (the fastest K3-TC
-# variant) or one variant by name (tensor-smem / tensor-tmem / tensor-pair)
+# flows allow the exact u8 GEMM), fp64 (K3 gather) or tensor (K3-TC/P, also
+# named tensor-pair)
 _fit_default = FIT_NAMES[os.environ.get("HUBGPU_FITNESS", "auto")]
 
 
 def set_fitness_default(kind: str) -> None:
     """A FIT_NAMES key for device instances created from now on (a tensor-core
-    choice the instance cannot run -- flows not u8 integers, or n too large for
-    the TMEM variants -- leaves it on 'auto')."""
+    choice the instance cannot run -- non-integer flows, p > 128 or
+    n > 16384 -- leaves it on 'auto')."""
     global _fit_default
     _fit_default = FIT_NAMES[kind]
 
@@ -284,16 +291,26 @@ class DeviceInstance:
         return out
 
 
+_inst_lock = threading.Lock()
+
+
 def device_instance(inst, device: int | None = None) -> DeviceInstance:
+    """The instance's device copy on `device` (built once, also when several
+    threads ask at the same time: the Instance is shareable, hm/model.py:35)."""
     dev = _device if device is None else int(device)
     cache = inst.__dict__.get("_hubgpu_dev")
-    if cache is None:
-        cache = {}
-        object.__setattr__(inst, "_hubgpu_dev", cache)
-    d = cache.get(dev)
-    if d is None:
-        d = DeviceInstance(inst, dev)
-        cache[dev] = d
+    d = cache.get(dev) if cache is not None else None
+    if d is not None:
+        return d
+    with _inst_lock:
+        cache = inst.__dict__.get("_hubgpu_dev")
+        if cache is None:
+            cache = {}
+            object.__setattr__(inst, "_hubgpu_dev", cache)
+        d = cache.get(dev)
+        if d is None:
+            d = DeviceInstance(inst, dev)
+            cache[dev] = d
     return d
 
 
@@ -490,9 +507,11 @@ class _PinnedPool:
             check(load().hg_host_alloc(nbytes, C.byref(p)))
             addr = p.value
         raw = (C.c_char * nbytes).from_address(addr)
-        arr = np.frombuffer(raw, dtype=dtype).reshape(shape)
-        weakref.finalize(arr, self._give_back, nbytes, addr)
-        return arr
+        # every array over the block -- the returned one and any view or slice
+        # of it -- keeps `raw` alive (numpy's base chain ends at the buffer
+        # exporter), so the block goes back only when the last of them dies
+        weakref.finalize(raw, self._give_back, nbytes, addr)
+        return np.frombuffer(raw, dtype=dtype).reshape(shape)
 
     def _give_back(self, nbytes: int, addr: int) -> None:
         with self._lock:

@@ -64,14 +64,13 @@ struct hg_pop {
 
 struct hg_inst {
     std::atomic<int> refs{1};  // the handle itself + every hg_pop / hg_ga built on it
-    alignas(64) unsigned char wmap[128];  // CUtensorMap of W8 (K3-TC), 128-row boxes
-    alignas(64) unsigned char wmapq[128]; // same, 128/kTcyCluster-row boxes (K3-TC/Y multicast)
-    alignas(64) unsigned char wmapp[128]; // same, 64-row boxes (K3-TC/P: half a tile per CTA)
-    uint8_t* dW8 = nullptr;                // u8 copy of W, [npad_tc][npad_tc], when exact
-    bool tc_ok = false;                    // flows are integers in [0, 255] and p fits
-    bool tcx_ok = false;                   // ... and the smem one-hot kernel fits (p)
-    bool tcy_ok = false;                   // ... and n <= 1024: one-hot resident in TMEM
-    bool tcp_ok = false;                   // ... and the CTA-pair (cta_group::2) kernel
+    // serialises every call that uses the instance's stream, scratch buffers or
+    // landing slots: the reference's Instance is safe to share across threads
+    // (hm/model.py:35), and ctypes releases the GIL during each call
+    std::mutex mu;
+    alignas(64) unsigned char wmapp[128]; // CUtensorMap of W8, 64-row boxes (half a tile per CTA)
+    uint8_t* dW8 = nullptr;                // u8 byte planes of W, [P][npad_tc][npad_tc]
+    bool tc_ok = false;                    // K3-TC/P runs this instance (integer flows, p, n)
     int fit_kind = HG_FIT_AUTO;
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -96,6 +95,10 @@ struct hg_inst {
 };
 
 namespace {
+
+std::unique_lock<std::mutex> lock_of(hg_inst* inst) {
+    return inst ? std::unique_lock<std::mutex>(inst->mu) : std::unique_lock<std::mutex>();
+}
 
 int set_device(int dev) {
     HG_CUDA(cudaSetDevice(dev));
@@ -128,7 +131,7 @@ void pop_release(hg_pop* P) {
 int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     const DevInst& I = inst->I;
     P->inst = inst;
-    P->cap = cap;
+    P->cap = 0;  // set once every buffer exists (a failed allocation leaves none usable)
     HG_CUDA(cudaMalloc(&P->hubs, (size_t)cap * I.p * sizeof(int32_t)));
     HG_CUDA(cudaMalloc(&P->cl, (size_t)cap * I.npad));
     HG_CUDA(cudaMalloc(&P->co, (size_t)cap * I.npad * sizeof(uint16_t)));
@@ -139,6 +142,7 @@ int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     HG_CUDA(cudaMalloc(&P->out, (size_t)cap * 4 * sizeof(double)));
     HG_CUDA(cudaEventCreate(&P->ev0));
     HG_CUDA(cudaEventCreate(&P->ev1));
+    P->cap = cap;
     return HG_OK;
 }
 
@@ -154,7 +158,11 @@ int scratch_pop(hg_inst* inst, int64_t B, hg_pop** out) {
     if (P->cap < B) {
         pop_release(P);
         int64_t cap = B < 64 ? 64 : B;
-        HG_TRY(pop_alloc(P, inst, cap));
+        const int rc = pop_alloc(P, inst, cap);
+        if (rc) {
+            pop_release(P);
+            return rc;
+        }
     }
     *out = P;
     return HG_OK;
@@ -194,8 +202,7 @@ static std::vector<uint32_t> pw_leaf_table(int64_t m) {
 static int fitness_kernel(const hg_inst* inst) {
     int k = inst->fit_kind;
     if (k == HG_FIT_AUTO) k = inst->tc_ok ? HG_FIT_TENSOR : HG_FIT_FP64;
-    if (k == HG_FIT_TENSOR)
-        k = inst->tcp_ok ? HG_FIT_TC_PAIR : inst->tcy_ok ? HG_FIT_TC_TMEM : HG_FIT_TC_SMEM;
+    if (k == HG_FIT_TENSOR) k = HG_FIT_TC_PAIR;
     return k;
 }
 // the u16 column offsets K2 can emit are read only by the fp64 K3
@@ -212,17 +219,9 @@ int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* c
     int tiles;
     if (kind == HG_FIT_TC_PAIR)  // finaliser fused into the kernel
         return launch_fitness_tcp(I, inst->wmapp, B, cl, T, part, inst->sm_count, s, legs, out);
-    if (kind == HG_FIT_TC_TMEM) {
-        HG_TRY(launch_fitness_tcy(I, inst->wmapq, B, cl, T, part, inst->sm_count, s));
-        tiles = 1;
-    } else if (kind == HG_FIT_TC_SMEM) {
-        HG_TRY(launch_fitness_tc(I, inst->wmap, B, cl, T, part, inst->sm_count, s));
-        tiles = tc_tiles(I.n);
-    } else {
-        HG_TRY(launch_fitness(I, inst->plan, B, cl, co, T, part,
-                              inst->sm_count * inst->plan.blocks_per_sm, s));
-        tiles = inst->plan.tiles;
-    }
+    HG_TRY(launch_fitness(I, inst->plan, B, cl, co, T, part,
+                          inst->sm_count * inst->plan.blocks_per_sm, s));
+    tiles = inst->plan.tiles;
     return launch_finalize(I, tiles, B, legs, part, out, s);
 }
 
@@ -508,31 +507,13 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             chk(cudaMalloc(&inst->dW8, w8.size()), "cudaMalloc(W8)");
             chk(cudaMemcpy(inst->dW8, w8.data(), w8.size(), cudaMemcpyHostToDevice), "H2D W8");
             if (rc) break;
-            const char* var = getenv("HUBGPU_TC_VARIANT");  // tuning override: "x" | "y" | "p"
-            if (P == 1) {
-                rc = tc_make_wmap(inst->dW8, nt, 128, inst->wmap);
-                if (rc) break;
-                rc = tc_make_wmap(inst->dW8, nt, 128 / kTcyCluster, inst->wmapq);
-                if (rc) break;
-                if (tc_supported(p)) {
-                    rc = prepare_fitness_tc(p);
-                    if (rc) break;
-                    inst->tcx_ok = true;
-                }
-                if (tcy_supported(n, p, I.npad) && !(var && var[0] == 'x')) {
-                    rc = prepare_fitness_tcy(p, I.npad);
-                    if (rc) break;
-                    inst->tcy_ok = true;
-                }
-            }
-            if (tcp_supported(n, p, I.npad, P) && !(var && (var[0] == 'x' || var[0] == 'y'))) {
+            if (tcp_supported(n, p, I.npad, P)) {
                 rc = tc_make_wmap(inst->dW8, nt, 64, inst->wmapp, P * nt);
                 if (rc) break;
                 rc = prepare_fitness_tcp(p, I.npad, P);
                 if (rc) break;
-                inst->tcp_ok = true;
+                inst->tc_ok = true;
             }
-            inst->tc_ok = inst->tcx_ok || inst->tcy_ok || inst->tcp_ok;
         }
         chk(cudaStreamSynchronize(s), "sync");
     } while (0);
@@ -586,6 +567,7 @@ int hg_instance_info(const hg_inst* inst, int* n, int* p, int* flags) {
 }
 
 int hg_instance_set_exact(hg_inst* inst, int on) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     inst->I.exact = on ? 1 : 0;
     return HG_OK;
@@ -598,18 +580,14 @@ int hg_instance_exact(const hg_inst* inst, int* on) {
 }
 
 int hg_instance_set_fitness(hg_inst* inst, int kind) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
-    HG_ARG(kind >= HG_FIT_AUTO && kind <= HG_FIT_TC_PAIR, "unknown fitness kernel %d", kind);
+    HG_ARG(kind == HG_FIT_AUTO || kind == HG_FIT_FP64 || kind == HG_FIT_TENSOR ||
+               kind == HG_FIT_TC_PAIR,
+           "unknown fitness kernel %d", kind);
     HG_ARG(kind < HG_FIT_TENSOR || inst->tc_ok,
-           "tensor-core fitness needs non-negative integer flows below 2^32 and p <= 128");
-    HG_ARG(kind != HG_FIT_TC_SMEM || inst->tcx_ok,
-           "the smem one-hot tensor-core kernel does not fit p = %d (or flows >= 256)",
-           inst->I.p);
-    HG_ARG(kind != HG_FIT_TC_TMEM || inst->tcy_ok,
-           "the TMEM-resident tensor-core kernel needs n <= 1024 and flows < 256 (and was not "
-           "disabled)");
-    HG_ARG(kind != HG_FIT_TC_PAIR || inst->tcp_ok,
-           "the CTA-pair tensor-core kernel needs n <= 16384 (and was not disabled)");
+           "tensor-core fitness needs non-negative integer flows below 2^32, p <= 128 and "
+           "n <= 16384");
     inst->fit_kind = kind;
     return HG_OK;
 }
@@ -627,6 +605,7 @@ int hg_instance_stream(const hg_inst* inst, void** stream) {
 }
 
 int hg_synchronize(hg_inst* inst) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_TRY(set_device(inst->device));
     HG_CUDA(cudaStreamSynchronize(inst->stream));
@@ -634,6 +613,7 @@ int hg_synchronize(hg_inst* inst) {
 }
 
 int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_ARG(B >= 0, "negative batch");
     if (B == 0) return HG_OK;
@@ -656,6 +636,7 @@ int hg_allocate(hg_inst* inst, int64_t B, const int64_t* hubs, int64_t* alloc) {
 
 int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* alloc,
                 double* out) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_ARG(B >= 0, "negative batch");
     if (B == 0) return HG_OK;
@@ -683,6 +664,7 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
 
 int hg_evaluate_unique(hg_inst* inst, int64_t B, const int64_t* hubs, double* out,
                        int64_t* groups) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_ARG(B >= 0, "negative batch");
     if (groups) *groups = 0;
@@ -720,6 +702,7 @@ int hg_evaluate_unique(hg_inst* inst, int64_t B, const int64_t* hubs, double* ou
 }
 
 int hg_pop_create(hg_inst* inst, int64_t capacity, hg_pop** out) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst && out, "NULL argument");
     HG_ARG(capacity >= 1, "capacity must be >= 1");
     HG_TRY(set_device(inst->device));
@@ -742,14 +725,18 @@ int hg_pop_create(hg_inst* inst, int64_t capacity, hg_pop** out) {
 void hg_pop_free(hg_pop* pop) {
     if (!pop) return;
     hg_inst* inst = pop->inst;
-    cudaSetDevice(inst->device);
-    cudaStreamSynchronize(inst->stream);
-    pop_release(pop);
-    delete pop;
+    {
+        auto lk_ = lock_of(inst);
+        cudaSetDevice(inst->device);
+        cudaStreamSynchronize(inst->stream);
+        pop_release(pop);
+        delete pop;
+    }
     inst_release(inst);
 }
 
 int hg_pop_load_hubs(hg_pop* pop, int64_t B, const int32_t* hubs, int where) {
+    auto lk_ = lock_of(pop ? pop->inst : nullptr);
     HG_ARG(pop && hubs, "NULL argument");
     HG_ARG(B >= 0 && B <= pop->cap, "batch %lld outside [0, %lld]", (long long)B,
            (long long)pop->cap);
@@ -762,6 +749,7 @@ int hg_pop_load_hubs(hg_pop* pop, int64_t B, const int32_t* hubs, int where) {
 }
 
 int hg_pop_evaluate(hg_pop* pop, int64_t B) {
+    auto lk_ = lock_of(pop ? pop->inst : nullptr);
     HG_ARG(pop != nullptr, "NULL population");
     HG_ARG(B >= 0 && B <= pop->cap, "batch outside capacity");
     if (B == 0) return HG_OK;
@@ -770,6 +758,7 @@ int hg_pop_evaluate(hg_pop* pop, int64_t B) {
 }
 
 int hg_pop_read(hg_pop* pop, int64_t B, double* out, int where) {
+    auto lk_ = lock_of(pop ? pop->inst : nullptr);
     HG_ARG(pop && out, "NULL argument");
     HG_ARG(B >= 0 && B <= pop->cap, "batch outside capacity");
     HG_TRY(set_device(pop->inst->device));
@@ -777,6 +766,12 @@ int hg_pop_read(hg_pop* pop, int64_t B, double* out, int where) {
                             where == HG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                             pop->inst->stream));
     if (where != HG_DEVICE) HG_CUDA(cudaStreamSynchronize(pop->inst->stream));
+    return HG_OK;
+}
+
+int hg_launch_count(uint64_t* count) {
+    HG_ARG(count != nullptr, "NULL argument");
+    *count = launch_count();
     return HG_OK;
 }
 
@@ -790,6 +785,7 @@ int hg_pop_launches_per_evaluate(const hg_pop* pop) {
 }
 
 int hg_pop_last_fitness_ms(hg_pop* pop, float* ms) {
+    auto lk_ = lock_of(pop ? pop->inst : nullptr);
     HG_ARG(pop && ms, "NULL argument");
     HG_TRY(set_device(pop->inst->device));
     HG_CUDA(cudaEventSynchronize(pop->ev1));
@@ -798,6 +794,7 @@ int hg_pop_last_fitness_ms(hg_pop* pop, float* ms) {
 }
 
 int hg_correct(hg_inst* inst, int64_t B, const uint8_t* masks, int64_t* hubs_out) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_ARG(B >= 0, "negative batch");
     if (B == 0) return HG_OK;
@@ -927,6 +924,7 @@ struct hg_ga {
     int32_t* inc = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    int graph_kernels = 0;  // kernel launches per replay (launches captured)
     std::vector<void*> bufs;
 };
 
@@ -977,6 +975,7 @@ void ga_release(hg_ga* ga) {
 extern "C" {
 
 int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst && prm && out, "NULL argument");
     *out = nullptr;
     const DevInst& I = inst->I;
@@ -1058,8 +1057,12 @@ int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
             rc = HG_ECUDA;
             break;
         }
+        const uint64_t l0 = launch_count();
         int qrc = ga_queue_generation(ga);
         cudaError_t ce = cudaStreamEndCapture(s, &ga->graph);
+        // captured launches run on replay: count them there, not here
+        ga->graph_kernels = (int)(launch_count() - l0);
+        note_launch((uint64_t)0 - (uint64_t)ga->graph_kernels);
         if (qrc) {
             rc = qrc;
             break;
@@ -1089,14 +1092,18 @@ int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
 void hg_ga_free(hg_ga* ga) {
     if (!ga) return;
     hg_inst* inst = ga->inst;
-    cudaSetDevice(inst->device);
-    cudaStreamSynchronize(inst->stream);
-    ga_release(ga);
-    delete ga;
+    {
+        auto lk_ = lock_of(inst);
+        cudaSetDevice(inst->device);
+        cudaStreamSynchronize(inst->stream);
+        ga_release(ga);
+        delete ga;
+    }
     inst_release(inst);
 }
 
 int hg_ga_reseed(hg_ga* ga, uint64_t seed) {
+    auto lk_ = lock_of(ga ? ga->inst : nullptr);
     HG_ARG(ga != nullptr, "GA is NULL");
     hg_inst* inst = ga->inst;
     HG_TRY(set_device(inst->device));
@@ -1116,6 +1123,7 @@ int hg_ga_reseed(hg_ga* ga, uint64_t seed) {
 }
 
 int hg_ga_begin_round(hg_ga* ga, const int64_t* ancestor_hubs) {
+    auto lk_ = lock_of(ga ? ga->inst : nullptr);
     HG_ARG(ga && ancestor_hubs, "NULL argument");
     HG_TRY(set_device(ga->inst->device));
     const int p = ga->inst->I.p, n = ga->inst->I.n;
@@ -1133,14 +1141,19 @@ int hg_ga_begin_round(hg_ga* ga, const int64_t* ancestor_hubs) {
 }
 
 int hg_ga_generations(hg_ga* ga, int count) {
+    auto lk_ = lock_of(ga ? ga->inst : nullptr);
     HG_ARG(ga != nullptr, "NULL GA");
     HG_ARG(count >= 0, "negative generation count");
     HG_TRY(set_device(ga->inst->device));
-    for (int g = 0; g < count; ++g) HG_CUDA(cudaGraphLaunch(ga->exec, ga->inst->stream));
+    for (int g = 0; g < count; ++g) {
+        HG_CUDA(cudaGraphLaunch(ga->exec, ga->inst->stream));
+        note_launch((uint64_t)ga->graph_kernels);
+    }
     return HG_OK;
 }
 
 int hg_ga_round_results(hg_ga* ga, double* raw, int64_t* hubs) {
+    auto lk_ = lock_of(ga ? ga->inst : nullptr);
     HG_ARG(ga && raw && hubs, "NULL argument");
     HG_TRY(set_device(ga->inst->device));
     const GaDev& G = ga->G;
@@ -1157,6 +1170,7 @@ int hg_ga_round_results(hg_ga* ga, double* raw, int64_t* hubs) {
 }
 
 int hg_ga_last_children(hg_ga* ga, int64_t* hubs, double* raw) {
+    auto lk_ = lock_of(ga ? ga->inst : nullptr);
     HG_ARG(ga && hubs && raw, "NULL argument");
     HG_TRY(set_device(ga->inst->device));
     cudaStream_t s = ga->inst->stream;
@@ -1172,6 +1186,7 @@ int hg_ga_last_children(hg_ga* ga, int64_t* hubs, double* raw) {
 }
 
 int hg_ga_draw_counters(hg_ga* ga, uint64_t* counters) {
+    auto lk_ = lock_of(ga ? ga->inst : nullptr);
     HG_ARG(ga && counters, "NULL argument");
     HG_TRY(set_device(ga->inst->device));
     HG_CUDA(cudaMemcpyAsync(counters, ga->G.ctr, (size_t)ga->G.nloc * 3 * 8,
@@ -1259,6 +1274,7 @@ static uint64_t binom_sat(int n, int p) {
 
 int hg_restricted_optimum(hg_inst* inst, uint64_t limit, int64_t* best_hubs, double* best_raw,
                           uint64_t* count_out) {
+    auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_ARG(best_hubs && best_raw, "NULL buffer");
     HG_TRY(set_device(inst->device));

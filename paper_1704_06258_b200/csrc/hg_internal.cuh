@@ -53,6 +53,17 @@ void set_error(const char* fmt, ...);
         if (s_ != HG_OK) return s_;                                                     \
     } while (0)
 
+// kernels of this library launched by the host so far (graph replays add
+// their kernel count): the bench's gpu_launches is a difference of two reads
+void note_launch(uint64_t k = 1);
+uint64_t launch_count();
+
+#define HG_LAUNCHED()                                                                   \
+    do {                                                                                \
+        HG_CUDA(cudaGetLastError());                                                    \
+        ::hg::note_launch();                                                            \
+    } while (0)
+
 constexpr int kMaxP = 255;          // cluster ids are uint8
 constexpr int kMaxNga = 32768;      // GA mask kernels keep one mask per warp in smem
 
@@ -127,28 +138,16 @@ int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t*
 int launch_finalize(const DevInst& I, int tiles, int64_t B, const double* legs,
                     const double* part, double* out, cudaStream_t s);
 
-// ---- K3-TC (k_fitness_tc.cu): tensor-core transfer term for u8 flows ------
-bool tc_supported(int p);
-int tc_tiles(int n);
-size_t tc_smem_bytes(int p);
-int prepare_fitness_tc(int p);
+// ---- K3-TC/P helpers (tc_common.cu) ------------------------------------------
 int tc_timing_read(unsigned long long* out32);
 unsigned long long* tc_timing_buffer();  // HUBGPU_TC_TIMING=1, else nullptr
 // map_out: CUtensorMap (128 B) over the u8 W, boxes of 128 K bytes x box_rows rows
 // rows: total rows of the (plane-stacked) tensor, default npad_tc
 int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out, int rows = 0);
-#ifndef HG_TCY_CLUSTER
-#define HG_TCY_CLUSTER 1
-#endif
-constexpr int kTcyCluster = HG_TCY_CLUSTER;  // k_fitness_tcy: CTAs per cluster sharing W tiles (TMA multicast)
-int launch_fitness_tc(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
-                      const uint32_t* T, double* part, int grid, cudaStream_t s);
-// K3-TC/Y (k_fitness_tcy.cu): one-hot resident in TMEM, n <= 1024
-bool tcy_supported(int n, int p, int npad);
-size_t tcy_smem_bytes(int p, int npad);
-int prepare_fitness_tcy(int p, int npad);
-int launch_fitness_tcy(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
-                       const uint32_t* T, double* part, int grid, cudaStream_t s);
+inline int tc_tiles(int n) { return (int)((n + 127) / 128); }
+// the largest dynamic shared memory a launch of `fn` may ask for (set once:
+// the attribute is per kernel and process-wide, instances differ in size)
+int set_max_dynamic_smem(const void* fn);
 // K3-TC/P (k_fitness_tcp.cu): the same on CTA pairs (cta_group::2, M = 256)
 // P: byte planes of W (integer flows < 256^P), stacked in the u8 tensor
 bool tcp_supported(int n, int p, int npad, int P);

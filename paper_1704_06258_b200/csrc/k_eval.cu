@@ -68,7 +68,7 @@ int launch_hubs_in(const int64_t* src, int32_t* dst, int64_t B, int p, int n, in
                    cudaStream_t s) {
     if (B <= 0) return HG_OK;
     k_hubs_in<<<grid_for(B * p, 256), 256, 0, s>>>(src, dst, B, p, n, err);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -76,14 +76,14 @@ int launch_idx_in(const int64_t* src, int32_t* dst, int64_t count, int n, int* e
                   cudaStream_t s) {
     if (count <= 0) return HG_OK;
     k_idx_in<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count, n, err);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
 int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s) {
     if (count <= 0) return HG_OK;
     k_i32_to_i64<<<grid_for(count, 256), 256, 0, s>>>(src, dst, count);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -105,7 +105,7 @@ __global__ void k_transpose(const double* __restrict__ a, double* __restrict__ t
 int launch_transpose(const double* src, double* dst, int n, cudaStream_t s) {
     dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
     k_transpose<<<grid, dim3(32, 8), 0, s>>>(src, dst, n);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -140,13 +140,13 @@ __global__ void k_quantize(const double* __restrict__ Ct, uint16_t* __restrict__
 int launch_quantize(const double* Ct, uint16_t* Cq, int n, int nq, double cmin, double scale,
                     cudaStream_t s) {
     k_quantize<<<grid_for((int64_t)n * nq, 256), 256, 0, s>>>(Ct, Cq, n, nq, cmin, scale);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
 int launch_check_symmetric(const double* C, int n, int* flag, cudaStream_t s) {
     k_check_symmetric<<<grid_for((int64_t)n * n, 256), 256, 0, s>>>(C, n, flag);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -602,7 +602,7 @@ int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* c
         go(std::integral_constant<int, kLegsExact>{});
     else
         go(std::integral_constant<int, kLegsFast>{});
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -668,7 +668,7 @@ int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const in
         go(std::integral_constant<int, kLegsExact>{});
     else
         go(std::integral_constant<int, kLegsFast>{});
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -961,9 +961,8 @@ static size_t fit_smem(int rw, int cj, int g, int ps) {
 }
 
 int prepare_fitness(const FitPlan& P) {
-    HG_CUDA(cudaFuncSetAttribute(kVariants[P.variant].fn,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
-    return HG_OK;
+    (void)P.smem;  // every variant at the device maximum (instances differ in size)
+    return set_max_dynamic_smem(reinterpret_cast<const void*>(kVariants[P.variant].fn));
 }
 
 FitPlan fitness_plan(const DevInst& I, int sm_count) {
@@ -1037,7 +1036,7 @@ int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t*
     if (g > A.q_total) g = (int)A.q_total;
     FitKernel fn = kVariants[P.variant].fn;
     fn<<<g, kFitThreads, P.smem, s>>>(A);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -1071,7 +1070,7 @@ int launch_finalize(const DevInst& I, int tiles, int64_t B, const double* legs,
     const int threads = 256;
     const int64_t blocks = ceil_div(B * 32, threads);
     k_finalize<<<(unsigned)blocks, threads, 0, s>>>(I, B, tiles, legs, part, out);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 

@@ -829,15 +829,14 @@ bool tcp_supported(int n, int p, int npad, int P) {
 static int g_tcp_pairs = 0;  // co-resident clusters (cudaOccupancyMaxActiveClusters)
 
 int prepare_fitness_tcp(int p, int npad, int P) {
-    // both summation modes (the instance may switch), each at its layout
-    const bool c = p_csm(p, npad);
+    // every instantiation at the device maximum: instances of different p /
+    // planes need different sizes and the attribute is per kernel
     using KernFn = void (*)(const CUtensorMap, PArgs);
-    const KernFn fx = c ? k_fitness_tcp<true, true> : k_fitness_tcp<false, true>;
-    HG_CUDA(cudaFuncSetAttribute(fx, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tcp_smem_bytes(p, npad, P, true)));
-    const KernFn kern = c ? k_fitness_tcp<true, false> : k_fitness_tcp<false, false>;
+    const KernFn all[4] = {k_fitness_tcp<true, true>, k_fitness_tcp<false, true>,
+                           k_fitness_tcp<true, false>, k_fitness_tcp<false, false>};
+    for (KernFn f : all) HG_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(f)));
+    const KernFn kern = p_csm(p, npad) ? k_fitness_tcp<true, false> : k_fitness_tcp<false, false>;
     const size_t sm = tcp_smem_bytes(p, npad, P, false);
-    HG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kYCluster);
     cfg.blockDim = dim3(kYThreads);
@@ -922,6 +921,7 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     else
         HG_CUDA(cudaLaunchKernelEx(&cfg, A.exact ? k_fitness_tcp<false, true>
                                              : k_fitness_tcp<false, false>, map, A));
+    note_launch();
     return HG_OK;
 }
 

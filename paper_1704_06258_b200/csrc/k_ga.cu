@@ -100,7 +100,7 @@ int launch_bytes_to_bits(const uint8_t* bytes, uint32_t* bits, int64_t B, int n,
                          cudaStream_t s) {
     if (B <= 0) return HG_OK;
     k_bytes_to_bits<<<grid_for(B * nw, 256), 256, 0, s>>>(bytes, bits, B, n, nw);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -108,7 +108,7 @@ int launch_bits_to_bytes(const uint32_t* bits, uint8_t* bytes, int64_t B, int n,
                          cudaStream_t s) {
     if (B <= 0) return HG_OK;
     k_bits_to_bytes<<<grid_for(B * n, 256), 256, 0, s>>>(bits, bytes, B, n, nw);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -424,10 +424,9 @@ int launch_correct(const DevInst& I, int64_t B, const uint32_t* bits, int hmax, 
     smem = (smem + 7) & ~size_t(7);
     smem += (size_t)I.n * 4;  // cls, nxt
     if (smem > 48 * 1024)
-        HG_CUDA(cudaFuncSetAttribute(k_correct, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+        HG_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(k_correct)));
     k_correct<<<(unsigned)B, kCorrThreads, smem, s>>>(I, bits, hmax, hubs);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -459,7 +458,7 @@ int launch_splice(int64_t B, int n, int nw, const uint32_t* a, const uint32_t* b
                   const int64_t* cuts, uint32_t* c1, uint32_t* c2, cudaStream_t s) {
     if (B <= 0) return HG_OK;
     k_splice<<<grid_for(B * nw, 256), 256, 0, s>>>(B, n, nw, a, b, cuts, c1, c2);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -492,7 +491,7 @@ int launch_swap_given(int64_t B, int n, int nw, uint32_t* bits, const int64_t* r
     const unsigned blocks = (unsigned)ceil_div(B, kWarpsPerBlock);
     k_swap_given<<<blocks, kWarpsPerBlock * 32, kWarpsPerBlock * nw * 4, s>>>(B, n, nw, bits,
                                                                              r_close, r_open);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -515,7 +514,7 @@ __global__ void k_round_begin(GaDev G) {
 
 int launch_round_begin(const GaDev& G, cudaStream_t s) {
     k_round_begin<<<G.nloc, 128, 0, s>>>(G);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -553,7 +552,7 @@ int launch_build_pop(const GaDev& G, cudaStream_t s) {
     const int64_t B = (int64_t)G.nloc * G.pop;
     const unsigned blocks = (unsigned)ceil_div(B, kWarpsPerBlock);
     k_build_pop<<<blocks, kWarpsPerBlock * 32, kWarpsPerBlock * G.nw * 4, s>>>(G);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -605,7 +604,7 @@ int launch_crossover(const GaDev& G, cudaStream_t s) {
     const int64_t P = (int64_t)G.nloc * (G.pop / 2);
     const unsigned blocks = (unsigned)ceil_div(P, kWarpsPerBlock);
     k_crossover<<<blocks, kWarpsPerBlock * 32, 0, s>>>(G);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -635,7 +634,7 @@ __global__ void k_mut_scan(GaDev G) {
 
 int launch_mut_scan(const GaDev& G, cudaStream_t s) {
     k_mut_scan<<<G.nloc, kScanThreads, 0, s>>>(G);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -672,7 +671,7 @@ int launch_mutate(const GaDev& G, cudaStream_t s) {
     const int64_t B = (int64_t)G.nloc * G.pop;
     const unsigned blocks = (unsigned)ceil_div(B, kWarpsPerBlock);
     k_mutate<<<blocks, kWarpsPerBlock * 32, kWarpsPerBlock * G.nw * 4, s>>>(G);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -732,7 +731,7 @@ __global__ void k_select(GaDev G) {
 int launch_select(const GaDev& G, cudaStream_t s) {
     const int wpb = 4;
     k_select<<<(unsigned)ceil_div(G.nloc, wpb), wpb * 32, 0, s>>>(G);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 

@@ -122,12 +122,12 @@ k_batch_best(const double* __restrict__ out, int64_t B, uint64_t rank0, uint64_t
 
 int launch_gen_urand(uint64_t s, int n, double* xy, double* C, double* W, cudaStream_t st) {
     k_gen_coords<<<(2 * n + 255) / 256, 256, 0, st>>>(s, n, xy);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     const int64_t total = (int64_t)n * n;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     k_gen_matrices<<<(unsigned)blocks, 256, 0, st>>>(s, n, xy, C, W);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
@@ -136,14 +136,14 @@ int launch_unrank_combos(const uint64_t* binom, int n, int p, uint64_t rank0, in
     int64_t blocks = (B + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     k_unrank_combos<<<(unsigned)blocks, 256, 0, st>>>(binom, n, p, rank0, B, count, hubs);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 
 int launch_batch_best(const double* out, int64_t B, uint64_t rank0, uint64_t count,
                       double* best_raw, unsigned long long* best_rank, cudaStream_t st) {
     k_batch_best<<<1, kArgThreads, 0, st>>>(out, B, rank0, count, best_raw, best_rank);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 

@@ -96,14 +96,14 @@ int launch_unique_groups(const int32_t* hubs, int64_t B, int p, void* scratch, s
     void* tmp = w + off;
     size_t tmp_bytes = bytes > off ? bytes - off : 0;
     k_hash_sets<<<grid256(B), 256, 0, s>>>(hubs, B, p, kin, iin);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     HG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, iin, iout, (int)B, 0, 64,
                                             s));
     k_group_flags<<<grid256(B), 256, 0, s>>>(hubs, B, p, kout, iout, flag);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     HG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, slot, (int)B, s));
     k_compact_sets<<<grid256(B), 256, 0, s>>>(hubs, B, p, iout, flag, slot, uhubs, map);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     // group count = slot[B-1] + flag[B-1]
     HG_CUDA(cudaMemcpyAsync(d_count, slot + B - 1, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     HG_CUDA(cudaMemcpyAsync(d_count + 1, flag + B - 1, sizeof(int32_t), cudaMemcpyDeviceToDevice,
@@ -114,7 +114,7 @@ int launch_unique_groups(const int32_t* hubs, int64_t B, int p, void* scratch, s
 int launch_scatter_out(const double* uout, const int32_t* map, int64_t B, double* out,
                        cudaStream_t s) {
     k_scatter_out<<<grid256(B * 4), 256, 0, s>>>(uout, map, B, out);
-    HG_CUDA(cudaGetLastError());
+    HG_LAUNCHED();
     return HG_OK;
 }
 

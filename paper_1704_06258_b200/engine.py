@@ -18,6 +18,7 @@ order" (hm/engine.py:216-220).  Results are identical for any GPU count.
 from __future__ import annotations
 
 import enum
+import threading
 import time
 from dataclasses import dataclass
 
@@ -93,6 +94,9 @@ def island_shard(islands: int, rank: int, world: int) -> tuple[int, int]:
     return islands * rank // world, islands * (rank + 1) // world
 
 
+_ga_lock = threading.Lock()
+
+
 class DeviceIslands:
     """Islands [lo, hi) of one run on this process's GPU."""
 
@@ -101,19 +105,29 @@ class DeviceIslands:
         self.params = params
         self.lo, self.hi = lo, hi
         # one hg_ga per (instance, islands, shard, shape): a later solve() with
-        # the same shape reseeds it instead of allocating and capturing anew
+        # the same shape reseeds it instead of allocating and capturing anew.
+        # A GA is checked out of the cache for the solve (close() returns it),
+        # so concurrent solves on one shared Instance never share one
         dinst = inst.device()
-        cache = dinst.__dict__.setdefault("_ga_cache", {})
-        key = (params.islands, lo, hi, params.pop_size, strength, params.strict_paper,
-               params.rng, _lib.exact_default())
-        ga = cache.get(key)
+        self._cache = dinst.__dict__.setdefault("_ga_cache", {})
+        self._key = (params.islands, lo, hi, params.pop_size, strength, params.strict_paper,
+                     params.rng, _lib.exact_default())
+        with _ga_lock:
+            free = self._cache.get(self._key)
+            ga = free.pop() if free else None
         if ga is None:
             ga = _lib.DeviceGa(dinst, params.islands, lo, hi, params.pop_size, strength,
                                params.strict_paper, params.seed, params.rng)
-            cache[key] = ga
         else:
             ga.reseed(params.seed)
         self.ga = ga
+
+    def close(self) -> None:
+        """Return the GA object to the instance's cache."""
+        ga, self.ga = self.ga, None
+        if ga is not None:
+            with _ga_lock:
+                self._cache.setdefault(self._key, []).append(ga)
 
     def run_round(self, ancestor_hubs: np.ndarray, audit=None):
         """One outer round: N1 generations from the ancestor.  Returns the
@@ -226,6 +240,9 @@ def _solve(inst: Instance, params: GaParams, mode: FitnessMode, audit, make_shar
                 trace.append(inc[1])
     except KeyboardInterrupt:
         interrupted = True
+    finally:
+        if shard is not None and hasattr(shard, "close"):
+            shard.close()
 
     return SolveReport(
         best_solution=finish(best[2], inst),

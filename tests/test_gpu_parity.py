@@ -38,11 +38,11 @@ def _need_gpu():
         pytest.fail("no CUDA device: the gpu tests must run on a B200")
 
 
-@pytest.fixture(params=["fp64", "tensor-smem", "tensor-tmem", "tensor-pair"])
+@pytest.fixture(params=["fp64", "tensor-pair"])
 def kernel(request):
-    """Run a test with the fp64 gather kernel (K3) and with each tensor-core
-    variant (K3-TC/X, /Y, /P -- used wherever the flows are u8 integers and,
-    for /Y and /P, n <= 1024; elsewhere the instance stays on auto)."""
+    """Run a test with the fp64 gather kernel (K3) and with the tensor-core
+    kernel K3-TC/P (used wherever the flows are integers below 2^32; elsewhere
+    the instance stays on auto)."""
     from paper_1704_06258_b200 import _lib
 
     _lib.set_fitness_default(request.param)

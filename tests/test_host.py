@@ -252,3 +252,59 @@ def test_pairwise_leaf_table_replays_numpy_sum(m):
     if m == 0:
         return
     assert _replay_pairwise(a) == float(np.sum(a))
+
+
+class TestPinnedPool:
+    """The pooled page-locked result buffers (_lib._PinnedPool) with a host
+    stand-in for hg_host_alloc / hg_host_free (no GPU needed)."""
+
+    class _StubLib:
+        def __init__(self):
+            import ctypes as C
+
+            self.C = C
+            self.blocks = {}
+            self.freed = []
+
+        def hg_host_alloc(self, nbytes, out):
+            buf = (self.C.c_char * nbytes)()
+            addr = self.C.addressof(buf)
+            self.blocks[addr] = buf
+            out._obj.value = addr
+            return 0
+
+        def hg_host_free(self, addr):
+            self.freed.append(addr)
+
+    def test_view_keeps_block(self, monkeypatch):
+        import gc
+
+        stub = self._StubLib()
+        monkeypatch.setattr(_lib, "load", lambda: stub)
+        pool = _lib._PinnedPool()
+        a = pool.array((4, 4), np.float64)
+        a[:] = 1.0
+        col = a[:, 3]
+        del a
+        gc.collect()
+        b = pool.array((4, 4), np.float64)  # must not reuse the block `col` views
+        b[:] = 2.0
+        assert col.tolist() == [1.0] * 4
+        del b, col
+        gc.collect()
+        assert sum(len(v) for v in pool._free.values()) == 2
+
+    def test_block_returns_after_last_view(self, monkeypatch):
+        import gc
+
+        stub = self._StubLib()
+        monkeypatch.setattr(_lib, "load", lambda: stub)
+        pool = _lib._PinnedPool()
+        a = pool.array((8, 4), np.float64)
+        v = a.reshape(-1)[5:]
+        del a
+        gc.collect()
+        assert not pool._free.get(8 * 4 * 8)
+        del v
+        gc.collect()
+        assert len(pool._free[8 * 4 * 8]) == 1
