@@ -38,7 +38,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "fitness evals/sec at n=1000,p=20 (1-8 B200); GA time-to-best-cost vs CPU ref"
 KERNEL_NAMES = {
-    "tensor-pair": "k_fitness_tcp (K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs + integer bins + fused finalise)",
+    "tensor-pair": "k_fitness_tcp (K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs over the triangular fold of W + integer bins + fused finalise)",
+    "tensor-pair-full": "k_fitness_tcp (K3-TC/P on the full W)",
     "fp64": "k_fitness (K3: fp64 smem gather)",
 }
 N, P, SEED, FACTORS = 1000, 20, 1704, (1.0, 0.75, 1.0)
@@ -59,7 +60,8 @@ def ncu_traffic(fit_kernel):
         return None
     import re
 
-    pat = {"tensor-pair": r"k_fitness_tcp\b", "fp64": r"k_fitness<"}[fit_kernel]
+    pat = {"tensor-pair": r"k_fitness_tcp\b", "tensor-pair-full": r"k_fitness_tcp\b",
+           "fp64": r"k_fitness<"}[fit_kernel]
     for name, v in ks.items():
         if re.search(pat, name):
             return v["dram_bytes"]
@@ -378,7 +380,7 @@ def run_gpu(args):
     tensor_ops = POP * 2.0 * N * N * P
     # every other K3 variant on the same population, for comparison
     variant_ms = {}
-    for name in ("fp64", "tensor-pair"):
+    for name in ("fp64", "tensor-pair-full", "tensor-pair"):
         try:
             dinst.set_fitness(hg._lib.FIT_NAMES[name])
         except ValueError:

@@ -52,7 +52,10 @@ extern "C" {
 #define HG_FIT_FP64 1      /* K3: fp64 smem-gather kernel (any flows)          */
 #define HG_FIT_TENSOR 2    /* the tensor-core kernel (= HG_FIT_TC_PAIR)         */
 /* 3 and 4 named two superseded tensor-core variants (removed; rejected)   */
-#define HG_FIT_TC_PAIR 5   /* K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs    */
+#define HG_FIT_TC_PAIR 5   /* K3-TC/P: u8 one-hot GEMM on tcgen05 CTA pairs, on
+                              the triangular fold of W when the costs are
+                              symmetric and the sums fixed-order (half the MMAs) */
+#define HG_FIT_TC_PAIR_FULL 6 /* K3-TC/P on the full W always                  */
 
 typedef struct hg_inst hg_inst;
 typedef struct hg_pop hg_pop;

@@ -21,9 +21,10 @@ LIB_PATH = Path(__file__).resolve().parent / "libhubgpu.so"
 HG_OK, HG_EARG, HG_ECUDA, HG_ENODEV, HG_ESTATE = 0, 1, 2, 3, 4
 HG_HOST, HG_DEVICE = 0, 1
 FLAG_SYMMETRIC, FLAG_WEIGHTS_EXACT, FLAG_TENSOR_OK = 1, 2, 4
-FIT_AUTO, FIT_FP64, FIT_TENSOR, FIT_TC_PAIR = 0, 1, 2, 5
+FIT_AUTO, FIT_FP64, FIT_TENSOR, FIT_TC_PAIR, FIT_TC_PAIR_FULL = 0, 1, 2, 5, 6
 RNG_MODES = {"replay": 0, "philox": 1}  # hg_ga_params.rng
-FIT_NAMES = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR, "tensor-pair": FIT_TC_PAIR}
+FIT_NAMES = {"auto": FIT_AUTO, "fp64": FIT_FP64, "tensor": FIT_TENSOR, "tensor-pair": FIT_TC_PAIR,
+             "tensor-pair-full": FIT_TC_PAIR_FULL}
 
 _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
@@ -244,6 +245,8 @@ class DeviceInstance:
 
     @property
     def fitness_kernel(self) -> str:
+        """'fp64', 'tensor-pair' (K3-TC/P on the triangular fold of W when the
+        costs are symmetric and the sums fixed-order) or 'tensor-pair-full'."""
         k = C.c_int()
         check(load().hg_instance_fitness(self.handle, C.byref(k)))
         return {v: n for n, v in FIT_NAMES.items()}[k.value]

@@ -69,7 +69,9 @@ struct hg_inst {
     // (hm/model.py:35), and ctypes releases the GIL during each call
     std::mutex mu;
     alignas(64) unsigned char wmapp[128]; // CUtensorMap of W8, 64-row boxes (half a tile per CTA)
+    alignas(64) unsigned char wmapt[128]; // same over M8
     uint8_t* dW8 = nullptr;                // u8 byte planes of W, [P][npad_tc][npad_tc]
+    uint8_t* dM8 = nullptr;                // u8 byte planes of W's triangular fold (symmetric C)
     bool tc_ok = false;                    // K3-TC/P runs this instance (integer flows, p, n)
     int fit_kind = HG_FIT_AUTO;
     int device = 0;
@@ -203,6 +205,7 @@ static int fitness_kernel(const hg_inst* inst) {
     int k = inst->fit_kind;
     if (k == HG_FIT_AUTO) k = inst->tc_ok ? HG_FIT_TENSOR : HG_FIT_FP64;
     if (k == HG_FIT_TENSOR) k = HG_FIT_TC_PAIR;
+    if (k == HG_FIT_TC_PAIR && !inst->dM8) k = HG_FIT_TC_PAIR_FULL;  // asymmetric costs
     return k;
 }
 // the u16 column offsets K2 can emit are read only by the fp64 K3
@@ -217,8 +220,9 @@ int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* c
     cudaStream_t s = inst->stream;
     const int kind = fitness_kernel(inst);
     int tiles;
-    if (kind == HG_FIT_TC_PAIR)  // finaliser fused into the kernel
-        return launch_fitness_tcp(I, inst->wmapp, B, cl, T, part, inst->sm_count, s, legs, out);
+    if (kind == HG_FIT_TC_PAIR || kind == HG_FIT_TC_PAIR_FULL)  // finaliser fused
+        return launch_fitness_tcp(I, inst->wmapp, kind == HG_FIT_TC_PAIR ? inst->wmapt : nullptr,
+                                  B, cl, T, part, inst->sm_count, s, legs, out);
     HG_TRY(launch_fitness(I, inst->plan, B, cl, co, T, part,
                           inst->sm_count * inst->plan.blocks_per_sm, s));
     tiles = inst->plan.tiles;
@@ -390,17 +394,22 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
             "H2D");
         chk(cudaMemcpyAsync(inst->drank, rk.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s),
             "H2D");
-        int* dflag = nullptr;
-        chk(cudaMalloc(&dflag, sizeof(int)), "cudaMalloc");
+        // one device pass over C and W (K1): cost range, symmetry, flow class
+        InstanceScan* dscan = nullptr;
+        chk(cudaMalloc(&dscan, sizeof(InstanceScan)), "cudaMalloc");
         if (rc) break;
-        int one = 1;
-        chk(cudaMemcpyAsync(dflag, &one, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-        if (rc == HG_OK) rc = launch_check_symmetric(inst->dC, n, dflag, s);
-        int sym = 0;
-        chk(cudaMemcpyAsync(&sym, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+        if (rc == HG_OK) rc = launch_scan_instance(inst->dC, inst->dW, n, dscan, s);
+        InstanceScan scan{};
+        chk(cudaMemcpyAsync(&scan, dscan, sizeof(scan), cudaMemcpyDeviceToHost, s), "D2H");
         chk(cudaStreamSynchronize(s), "sync");
-        cudaFree(dflag);
+        cudaFree(dscan);
         if (rc) break;
+        auto from_bits = [](unsigned long long b) {
+            double v;
+            std::memcpy(&v, &b, sizeof(v));
+            return v;
+        };
+        const int sym = scan.symmetric;
         if (sym) {
             inst->dCt = inst->dC;
         } else {
@@ -453,11 +462,7 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         I.npad = (int)round_up(n, q);
         {
             // 16-bit monotone quantisation of Ct: exact pre-filter for allocation
-            double cmin = dist[0], cmax = dist[0];
-            for (size_t x = 1; x < nn; ++x) {
-                cmin = dist[x] < cmin ? dist[x] : cmin;
-                cmax = dist[x] > cmax ? dist[x] : cmax;
-            }
+            const double cmin = from_bits(scan.cmin_bits), cmax = from_bits(scan.cmax_bits);
             const double scale = cmax > cmin ? 65535.0 / (cmax - cmin) : 0.0;
             // rows padded with 0xFFFF to nq = npad (K2 reads whole passes of
             // nodes unguarded), one all-0xFFFF row n (the register K2's
@@ -479,41 +484,37 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         rc = prepare_allocate(I);
         if (rc) break;
         // K3-TC eligibility: every flow a non-negative integer below 2^32 ->
-        // exact u8 GEMMs on P byte planes of W (P = 1 when every flow < 256;
-        // the smem and one-CTA TMEM kernels take P = 1 only)
-        bool intw = p >= 1 && p <= 128;
-        double wmax = 0.0, wsum = 0.0;
-        for (size_t x = 0; intw && x < nn; ++x) {
-            const double v = flow[x];
-            if (!(v >= 0.0 && v < 4294967296.0 && v == std::floor(v))) intw = false;
-            wmax = v > wmax ? v : wmax;
-            wsum += v;
-        }
+        // exact u8 GEMMs on P byte planes of W (P = 1 when every flow < 256),
+        // and for symmetric costs on the triangular fold of W (its own planes)
+        const bool intw = scan.int_flows && p >= 1 && p <= 128;
+        const double wmax = from_bits(scan.wmax_bits), mmax = from_bits(scan.mmax_bits);
         // every byte plane's total below 2^32: u32 bins may accumulate over
         // all K chunks (the exact transfer sum for n > 1024)
-        I.bins_total_ok = intw && wsum < 4294967296.0 ? 1 : 0;
-        int P = 1;
+        I.bins_total_ok = intw && scan.wsum < 4294967296.0 ? 1 : 0;
+        int P = 1, Pt = 1;
         while (P < 4 && wmax >= std::ldexp(1.0, 8 * P)) ++P;
+        while (Pt < 5 && mmax >= std::ldexp(1.0, 8 * Pt)) ++Pt;
         I.wplanes = P;
-        if (intw) {
+        const bool tri = sym && Pt <= 4 && !getenv("HUBGPU_TCP_NOTRI");
+        I.wplanes_tri = tri ? Pt : 0;
+        if (intw && tcp_supported(n, p, I.npad, P) && (!tri || tcp_supported(n, p, I.npad, Pt))) {
             const int nt = (int)round_up(n, 128);
-            // planes stacked by rows: plane d holds byte d of every flow
-            std::vector<uint8_t> w8((size_t)P * nt * nt, 0);
-            for (int d = 0; d < P; ++d)
-                for (int i = 0; i < n; ++i)
-                    for (int j = 0; j < n; ++j)
-                        w8[((size_t)d * nt + i) * nt + j] =
-                            (uint8_t)((uint64_t)flow[(size_t)i * n + j] >> (8 * d));
-            chk(cudaMalloc(&inst->dW8, w8.size()), "cudaMalloc(W8)");
-            chk(cudaMemcpy(inst->dW8, w8.data(), w8.size(), cudaMemcpyHostToDevice), "H2D W8");
+            const size_t plane = (size_t)nt * nt;
+            chk(cudaMalloc(&inst->dW8, plane * P), "cudaMalloc(W8)");
+            if (tri) chk(cudaMalloc(&inst->dM8, plane * Pt), "cudaMalloc(M8)");
             if (rc) break;
-            if (tcp_supported(n, p, I.npad, P)) {
-                rc = tc_make_wmap(inst->dW8, nt, 64, inst->wmapp, P * nt);
+            rc = launch_build_planes(inst->dW, n, nt, P, Pt, inst->dW8, tri ? inst->dM8 : nullptr,
+                                     s);
+            if (rc) break;
+            rc = tc_make_wmap(inst->dW8, nt, 64, inst->wmapp, P * nt);
+            if (rc) break;
+            if (tri) {
+                rc = tc_make_wmap(inst->dM8, nt, 64, inst->wmapt, Pt * nt);
                 if (rc) break;
-                rc = prepare_fitness_tcp(p, I.npad, P);
-                if (rc) break;
-                inst->tc_ok = true;
             }
+            rc = prepare_fitness_tcp(p, I.npad, tri && Pt > P ? Pt : P);
+            if (rc) break;
+            inst->tc_ok = true;
         }
         chk(cudaStreamSynchronize(s), "sync");
     } while (0);
@@ -544,6 +545,7 @@ static void inst_destroy(hg_inst* inst) {
     cudaFree(inst->derr);
     if (inst->hflag) cudaFreeHost(inst->hflag);
     cudaFree(inst->dW8);
+    cudaFree(inst->dM8);
     inst->t1.release();
     inst->t2.release();
     inst->t3.release();
@@ -583,7 +585,7 @@ int hg_instance_set_fitness(hg_inst* inst, int kind) {
     auto lk_ = lock_of(inst);
     HG_ARG(inst != nullptr, "instance is NULL");
     HG_ARG(kind == HG_FIT_AUTO || kind == HG_FIT_FP64 || kind == HG_FIT_TENSOR ||
-               kind == HG_FIT_TC_PAIR,
+               kind == HG_FIT_TC_PAIR || kind == HG_FIT_TC_PAIR_FULL,
            "unknown fitness kernel %d", kind);
     HG_ARG(kind < HG_FIT_TENSOR || inst->tc_ok,
            "tensor-core fitness needs non-negative integer flows below 2^32, p <= 128 and "
@@ -781,7 +783,7 @@ int hg_debug_tc_timing(unsigned long long* out32) {
 }
 
 int hg_pop_launches_per_evaluate(const hg_pop* pop) {
-    return fitness_kernel(pop->inst) == HG_FIT_TC_PAIR ? 2 : 3;
+    return fitness_kernel(pop->inst) == HG_FIT_FP64 ? 3 : 2;
 }
 
 int hg_pop_last_fitness_ms(hg_pop* pop, float* ms) {
@@ -957,7 +959,7 @@ int ga_queue_generation(hg_ga* ga) {
 }
 
 // build_pop, crossover, mut_scan, mutate, correct, allocate, fitness, [finalise,] select
-int ga_launches(const hg_ga* ga) { return fitness_kernel(ga->inst) == HG_FIT_TC_PAIR ? 8 : 9; }
+int ga_launches(const hg_ga* ga) { return fitness_kernel(ga->inst) == HG_FIT_FP64 ? 9 : 8; }
 
 void ga_release(hg_ga* ga) {
     if (ga->exec) cudaGraphExecDestroy(ga->exec);

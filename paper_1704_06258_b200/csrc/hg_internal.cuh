@@ -74,6 +74,7 @@ struct DevInst {
     int npad;      // row stride (bytes) of cluster-id rows
     int weights_exact;
     int wplanes;   // byte planes of the u8 flow tensor W8 (1 when every flow < 256)
+    int wplanes_tri;  // byte planes of its triangular fold (W + W^T above the diagonal blocks)
     double chi, alpha, delta;
     const double* C;
     const double* Ct;
@@ -138,6 +139,21 @@ int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t*
 int launch_finalize(const DevInst& I, int tiles, int64_t B, const double* legs,
                     const double* part, double* out, cudaStream_t s);
 
+// ---- K1 on the device (k_load.cu) -------------------------------------------
+struct InstanceScan {
+    unsigned long long cmin_bits, cmax_bits;  // min / max cost (bit patterns, >= 0)
+    unsigned long long wmax_bits, mmax_bits;  // max flow / max entry of the triangular fold
+    double wsum;                              // total flow
+    int int_flows;                            // 1: every flow an integer in [0, 2^32)
+    int symmetric;                            // 1: C == C^T exactly
+};
+int launch_scan_instance(const double* C, const double* W, int n, InstanceScan* out,
+                         cudaStream_t s);
+// W8: P byte planes of W, M8 (optional): Ptri byte planes of the triangular
+// fold; both [planes][nt][nt] with nt = round_up(n, 128)
+int launch_build_planes(const double* W, int n, int nt, int P, int Ptri, uint8_t* W8,
+                        uint8_t* M8, cudaStream_t s);
+
 // ---- K3-TC/P helpers (tc_common.cu) ------------------------------------------
 int tc_timing_read(unsigned long long* out32);
 unsigned long long* tc_timing_buffer();  // HUBGPU_TC_TIMING=1, else nullptr
@@ -154,9 +170,10 @@ bool tcp_supported(int n, int p, int npad, int P);
 size_t tcp_smem_bytes(int p, int npad, int P, bool exact);
 int prepare_fitness_tcp(int p, int npad, int P);
 // legs / out set: the finaliser is fused (out gets the 4 cost terms, part unused)
-int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
-                       const uint32_t* T, double* part, int grid, cudaStream_t s,
-                       const double* legs = nullptr, double* out = nullptr);
+// wmap_tri: the map of the triangular fold (symmetric costs), or nullptr
+int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
+                       const uint8_t* cl, const uint32_t* T, double* part, int grid,
+                       cudaStream_t s, const double* legs = nullptr, double* out = nullptr);
 
 // ---- k_gen.cu: device generator and hub-set enumeration ---------------------
 // xy: 2n scratch; C / W: n x n (either may be null)

@@ -42,6 +42,8 @@ constexpr int kYMaxIpt = 32;
 constexpr int kYTmemCols = 512;
 constexpr int kYAcc0 = 256;                   // first accumulator column
 constexpr int kYCluster = 2;                  // the CTA pair
+constexpr int kRegsCtl = 40;                  // per thread, warpgroup 0 (setmaxnreg)
+constexpr int kRegsEpi = 104;                 // per thread, epilogue warpgroups
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -185,10 +187,17 @@ struct PArgs {
     int NC;           // K chunks of <= 8 blocks (1024 nodes): one resident one-hot each
     int stages;       // W ring depth
     int kbs;          // 128-byte K blocks per stage
+    // tri: the W tensor is the block-upper-triangular fold of a symmetric-cost
+    // instance (diagonal blocks W, blocks above W + W^T, below unused): output
+    // tile I runs K blocks J >= I only (see k_fitness_tcp's header)
+    int tri;
     int csm;          // 1: a unit's cluster rows are staged in shared memory (they fit)
     uint32_t idesc;   // kind::i8, M=256, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
-    int dbg;                     // ablation flags (tuning only): 1 = no epilogue math, 2 = no MMA
+    // ablation flags (tuning only, wrong results): 1 = no bin atomics, 2 = no
+    // MMA, 4 = no chunk fold / unit reduce, 8 = no one-hot generation, 64 = no
+    // epilogue warps at all
+    int dbg;
     // exact: one chunk and one plane, so the bins ARE the reference's
     // inter-cluster flows; S_T is then np.sum(inter * hub_dist) replayed in
     // numpy's pairwise order over the leaves of the p*p-term sum
@@ -207,7 +216,6 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int p = A.p, ipt = A.ipt, ITO = A.ITO, KBT = A.KBT, NC = A.NC;
-    const int NT = A.P * ITO;  // tiles per phase: every (plane, W row block)
     unsigned char* ring = smem;                                          // W stages
     const int NS = A.stages, KBS = A.kbs;
     unsigned char* var = smem + NS * KBS * kYStageBytes;
@@ -221,6 +229,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     var += (size_t)A.P * p * 512;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
+    // the finaliser's leg sums of each epilogue warp's first individual,
+    // fetched before the last chunk pass, used by the deferred reduce
+    double* lgs = reinterpret_cast<double*>(var);  // [16 warps][2]
+    var += (kYWarps - kYEpiWarp0) * 2 * 8;
     double* prod = reinterpret_cast<double*>(var);  // exact: [p][128] rounded terms of S_T
     var += EX ? (size_t)p * 128 * 8 : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
@@ -234,6 +246,19 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     // group: quarter h owns chunk-local blocks [kq(c,h), kq(c,h+1))
     auto nkb = [&](int c) { return KBT - c * kYChunkKB < kYChunkKB ? KBT - c * kYChunkKB : kYChunkKB; };
     auto kq = [&](int c, int h) { return h * nkb(c) / 4; };
+    // output tiles of chunk c (per plane), the first chunk-local K block of
+    // tile I, and the tile holding the last use of chunk-local block k
+    const int tri = A.tri;
+    auto ntl = [&](int c) {
+        return tri && c * kYChunkKB + nkb(c) < ITO ? c * kYChunkKB + nkb(c) : ITO;
+    };
+    auto klo = [&](int c, int I) { return tri && I > c * kYChunkKB ? I - c * kYChunkKB : 0; };
+    auto klast = [&](int c, int k) { return tri ? c * kYChunkKB + k : ntl(c) - 1; };
+    // the block whose last use frees A quarter h (an empty quarter: the block
+    // before it) -- every kbf[h] completes exactly once per phase
+    auto qrb = [&](int c, int h) {
+        return kq(c, h) < kq(c, h + 1) ? kq(c, h + 1) - 1 : (kq(c, h) > 0 ? kq(c, h) - 1 : 0);
+    };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int x = tid; x < A.P * p * 128; x += kYThreads) bins[x] = 0u;
@@ -277,39 +302,76 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     // the leader's barriers as shared::cluster addresses (remote for the peer)
     const uint32_t L_full = mapa(b_full, 0), L_acce = mapa(b_acce, 0), L_ard = mapa(b_ard, 0);
 
+    // The W stream is one flat sequence of items (slot j, chunk c, tile tt of
+    // the phase, chunk-local K block kb) -- tile tt = (plane, W row block it)
+    // runs blocks [klo(c, it), nkb(c)) -- cut into ring stages of KBS items
+    // regardless of tile boundaries, so the short tiles of the triangular
+    // fold still move full stages
+    struct Walk {
+        int64_t j;
+        int c, tt, kb;
+        uint32_t phase;
+    };
+    auto walk_first = [&](Walk& w) {
+        w.j = 0;
+        w.c = 0;
+        w.tt = 0;
+        w.kb = 0;
+        w.phase = 0;
+    };
+    auto walk_next = [&](Walk& w) {
+        if (++w.kb < nkb(w.c)) return;
+        const int T = ntl(w.c);
+        if (++w.tt == A.P * T) {
+            w.tt = 0;
+            ++w.phase;
+            if (++w.c == NC) {
+                w.c = 0;
+                ++w.j;
+            }
+        }
+        const int T2 = ntl(w.c);
+        w.kb = klo(w.c, w.tt - (w.tt / T2) * T2);
+    };
+
     if (warp == 1) {
-        // ---------------- TMA producer: W tiles (it, K-block group), same order
-        // every phase; a stage holds up to KBS consecutive 128-byte K blocks
+        // ---------------- TMA producer
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
             bool wrapped = false;
             const int q = (int)crank * 64;  // this CTA's W rows within a tile
-            for (int64_t j = 0; j < nslots; ++j)
-                for (int c = 0; c < NC; ++c)
-                    for (int tt = 0; tt < NT; ++tt)
-                        for (int kb0 = 0; kb0 < nkb(c); kb0 += KBS) {
-                            const int pl = tt / ITO, it = tt - pl * ITO;
-                            const int nk = nkb(c) - kb0 < KBS ? nkb(c) - kb0 : KBS;
-                            // stage s is free: the leader's MMAs reading it completed
-                            if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
-                            if (leader)  // both halves land on the leader's barrier
-                                mb_expect_tx(b_full + 8 * s, (uint32_t)(2 * nk * kYStageBytes));
-                            const uint32_t dst = su32(ring + s * (KBS * kYStageBytes));
-                            for (int kk = 0; kk < nk; ++kk)
-                                tma2d_pair(dst + kk * kYStageBytes, &tmW,
-                                           (c * kYChunkKB + kb0 + kk) * 128,
-                                           pl * A.nt + it * 128 + q, L_full + 8 * s);
-                            if (++s == (uint32_t)NS) {
-                                s = 0;
-                                ph ^= 1u;
-                                wrapped = true;
-                            }
-                        }
+            Walk w;
+            walk_first(w);
+            while (w.j < nslots) {
+                // items of this stage
+                Walk e = w;
+                int nk = 0;
+                while (nk < KBS && e.j < nslots) {
+                    ++nk;
+                    walk_next(e);
+                }
+                // stage s is free: the leader's MMAs reading it completed
+                if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
+                if (leader)  // both halves land on the leader's barrier
+                    mb_expect_tx(b_full + 8 * s, (uint32_t)(2 * nk * kYStageBytes));
+                const uint32_t dst = su32(ring + s * (KBS * kYStageBytes));
+                for (int kk = 0; kk < nk; ++kk) {
+                    const int T = ntl(w.c), pl = w.tt / T, it = w.tt - pl * T;
+                    tma2d_pair(dst + kk * kYStageBytes, &tmW, (w.c * kYChunkKB + w.kb) * 128,
+                               pl * A.nt + it * 128 + q, L_full + 8 * s);
+                    walk_next(w);
+                }
+                if (++s == (uint32_t)NS) {
+                    s = 0;
+                    ph ^= 1u;
+                    wrapped = true;
+                }
+            }
         }
     } else if (warp == 0) {
         // ---------------- MMA issuer (leader CTA only)
         if (lane == 0 && leader) {
-            uint32_t s = 0, ph = 0, t = 0, phase = 0;
+            uint32_t s = 0, ph = 0, t = 0;
             const bool timed = A.timing != nullptr;
             unsigned long long w_a = 0, w_e = 0, w_f = 0, w_i = 0;
             long long c0 = timed ? clock64() : 0;
@@ -321,61 +383,74 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             c0 = c1_;                               \
         }                                           \
     } while (0)
-            for (int64_t j = 0; j < nslots; ++j) {
-                for (int c = 0; c < NC; ++c, ++phase) {
-                    const int nb = nkb(c);
-                    for (int tt = 0; tt < NT; ++tt, ++t) {
-                        const int d = t & 1;
+            // per chunk-local block, 4 bits each: the A quarters whose ready
+            // barrier the block's first MMA waits on (tile 0 of a phase), and
+            // the quarters its last use frees -- rebuilt when the chunk changes
+            int qc = -1;
+            uint32_t waitq = 0u, relq = 0u;
+            uint32_t dcol = 0, d = 0;
+            Walk w;
+            walk_first(w);
+            while (w.j < nslots) {
+                mb_wait(b_full + 8 * s, ph);
+                YT(w_f);
+                fence_after();
+                const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
+                for (int kk = 0; kk < KBS && w.j < nslots; ++kk) {
+                    const int c = w.c, T = ntl(c), pl = w.tt / T, it = w.tt - pl * T;
+                    const int k0 = klo(c, it), kb = w.kb;
+                    if (c != qc) {
+                        qc = c;
+                        waitq = relq = 0u;
+                        for (int h = 0; h < 4; ++h) {
+                            if (kq(c, h) < kq(c, h + 1)) waitq |= 1u << (4 * kq(c, h) + h);
+                            relq |= 1u << (4 * qrb(c, h) + h);
+                        }
+                    }
+                    if (kb == k0) {  // a tile starts: its accumulator must be drained
+                        d = t & 1u;
                         if (t >= 2 && !(A.dbg & 64))
                             mb_wait_cl(b_acce + 8 * d, ((t >> 1) - 1) & 1);
                         YT(w_e);
                         fence_after();
-                        const uint32_t dcol = tmem + kYAcc0 + d * 128;
-                        for (int kb0 = 0; kb0 < nb; kb0 += KBS) {
-                            const int nk = nb - kb0 < KBS ? nb - kb0 : KBS;
-                            if (tt == 0 && !(A.dbg & 64)) {
-                                // first use of this phase's A: its quarters must be in TMEM
-                                for (int h = 0; h < 4; ++h)
-                                    if (kq(c, h) >= kb0 && kq(c, h) < kb0 + nk &&
-                                        kq(c, h) < kq(c, h + 1))
-                                        mb_wait_cl(b_ard + 8 * h, phase & 1u);
-                                fence_after();
-                                YT(w_a);
-                            }
-                            mb_wait(b_full + 8 * s, ph);
-                            YT(w_f);
-                            fence_after();
-                            const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
-                            if (!(A.dbg & 2)) {
-                                for (int kk = 0; kk < nk; ++kk) {
-                                    const int kb = kb0 + kk;
-                                    const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
-#pragma unroll
-                                    for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns
-                                        mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks,
-                                               A.idesc, (kb | ks) != 0);
-                                }
-                            }
-                            commit_pair(b_empty + 8 * s);
-                            if (tt == NT - 1)  // last use of this phase's A quarter: free it
-                                for (int h = 0; h < 4; ++h) {
-                                    // every kbf[h] completes exactly once per phase
-                                    // (its parity is the phase's), an empty quarter
-                                    // together with the block before it
-                                    const int rb = kq(c, h) < kq(c, h + 1)
-                                                       ? kq(c, h + 1) - 1
-                                                       : (kq(c, h) > 0 ? kq(c, h) - 1 : 0);
-                                    if (rb >= kb0 && rb < kb0 + nk) commit_pair(b_kbf + 8 * h);
-                                }
-                            if (++s == (uint32_t)NS) {
-                                s = 0;
-                                ph ^= 1u;
-                            }
-                            YT(w_i);
-                        }
-                        commit_pair(b_accf + 8 * d);
+                        dcol = tmem + kYAcc0 + d * 128;
                     }
+                    if (w.tt == 0 && !(A.dbg & 64)) {
+                        // first use of this phase's A: a quarter must be in TMEM
+                        // before its first block's MMAs (earlier blocks need not
+                        // wait for it)
+                        uint32_t wq = (waitq >> (4 * kb)) & 15u;
+                        if (wq) {
+                            for (; wq; wq &= wq - 1)
+                                mb_wait_cl(b_ard + 8 * (__ffs(wq) - 1), w.phase & 1u);
+                            fence_after();
+                        }
+                        YT(w_a);
+                    }
+                    if (!(A.dbg & 2)) {
+                        const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns
+                            mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
+                                   (kb != k0) | (ks != 0));
+                    }
+                    // last use of block kb (tri: tile 8c + kb; full W: the last
+                    // tile) frees the A quarters it ends
+                    if (pl == A.P - 1 && klast(c, kb) == it)
+                        for (uint32_t m = (relq >> (4 * kb)) & 15u; m; m &= m - 1)
+                            commit_pair(b_kbf + 8 * (__ffs(m) - 1));
+                    if (kb == nkb(c) - 1) {  // the tile's accumulator is complete
+                        commit_pair(b_accf + 8 * d);
+                        ++t;
+                    }
+                    walk_next(w);
                 }
+                commit_pair(b_empty + 8 * s);
+                if (++s == (uint32_t)NS) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+                YT(w_i);
             }
             if (timed) {
                 atomicAdd(A.timing + 0, w_a);
@@ -423,7 +498,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             const uint4* crow =
                 reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
-            for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32; c0 += 8) {
+            for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32 && !(A.dbg & 8); c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -469,8 +544,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         // a unit's S_T reduce and finaliser, run during the next unit's first
         // tile (the MMA keeps its two accumulators busy meanwhile; red and prod
         // are rewritten only after the next chunk-pass barrier)
-        auto reduce_unit = [&](const int64_t bbase_u, const int nind_u, const double lg0_u,
-                               const double lg1_u) {
+        auto reduce_unit = [&](const int64_t bbase_u, const int nind_u) {
+                const double* lgw = lgs + 2 * (warp - kYEpiWarp0);
                 if (EX) {
                     // S_T = np.sum(inter * hub_dist) in numpy's pairwise order
                     // (hm/evaluation.py:117-118) over the terms in `prod`: one warp
@@ -521,8 +596,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             if (A.out) {
                                 const int64_t b = bbase_u + b2;
                                 const bool pre = b2 == warp - kYEpiWarp0;
-                                const double coll = A.chi * (pre ? lg0_u : A.legs[2 * b]);
-                                const double dist = A.delta * (pre ? lg1_u : A.legs[2 * b + 1]);
+                                const double coll = A.chi * (pre ? lgw[0] : A.legs[2 * b]);
+                                const double dist = A.delta * (pre ? lgw[1] : A.legs[2 * b + 1]);
                                 const double tran = A.alpha * st;
                                 A.out[4 * b + 0] = coll;
                                 A.out[4 * b + 1] = tran;
@@ -552,8 +627,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             // the finaliser (k_finalize), fused: same operations
                             const int64_t b = bbase_u + b2;
                             const bool pre = b2 == warp - kYEpiWarp0;
-                            const double coll = A.chi * (pre ? lg0_u : A.legs[2 * b]);
-                            const double dist = A.delta * (pre ? lg1_u : A.legs[2 * b + 1]);
+                            const double coll = A.chi * (pre ? lgw[0] : A.legs[2 * b]);
+                            const double dist = A.delta * (pre ? lgw[1] : A.legs[2 * b + 1]);
                             const double tran = A.alpha * acc;
                             A.out[4 * b + 0] = coll;
                             A.out[4 * b + 1] = tran;
@@ -565,9 +640,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                 }
         };
-        int64_t pend_b = 0;
-        int pend_n = -1;  // a unit whose reduce is pending
-        double pend_l0 = 0.0, pend_l1 = 0.0;
+        int64_t pend_j = -1;  // the slot whose reduce is pending
         uint32_t phase = 0;
         for (int64_t j = 0; j < nslots; ++j) {
             int64_t bbase;
@@ -580,43 +653,49 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             if (CSM && j + 1 < nslots) {
                 stage(j + 1);  // the next unit's cluster rows, under this unit's MMAs
+                epi_sync();    // ... complete before any warp generates from them
                 ET(e_st);
             }
             const uint32_t* tbp = A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps + l;
             double s_acc = 0.0;  // this thread's share of S_T over the chunks
-            double lg0 = 0.0, lg1 = 0.0;  // leg sums of this warp's first individual
             for (int c = 0; c < NC; ++c, ++phase) {
                 const bool last_phase = j + 1 == nslots && c + 1 == NC;
+                const int T = ntl(c), NT = A.P * T;
+                // the next phase's one-hot quarter `sub`, generated as soon as
+                // the current A frees it.  It covers blocks [kq(cn,sub), X);
+                // every current-phase MMA on blocks < X must be done: wait on
+                // the current quarter holding block X-1 (MMAs complete in
+                // order, and a block's last use never comes after a later
+                // block's) -- chunks of different sizes (the last one) have
+                // different quarter boundaries.  tri: quarter h is free after
+                // tile 8c + its last block, early in the phase
+                int hq = -1, tt_gen = NT - 1;
+                if (!last_phase) {
+                    const int cn = c + 1 < NC ? c + 1 : 0;
+                    const int X = kq(cn, sub + 1);
+                    if (kq(cn, sub) < X) {
+                        const int need = X - 1 < nkb(c) ? X - 1 : nkb(c) - 1;
+                        hq = 3;
+                        for (int h = 0; h < 4; ++h)
+                            if (kq(c, h) <= need && need < kq(c, h + 1)) {
+                                hq = h;
+                                break;
+                            }
+                        tt_gen = (A.P - 1) * T + klast(c, qrb(c, hq));
+                    }
+                }
                 for (int tt = 0; tt < NT; ++tt, ++t) {
                     const int d = t & 1;
-                    const int pl = tt / ITO, it = tt - pl * ITO;
-                    if (!last_phase && tt == NT - 1) {
-                        // the next phase's one-hot, quarter by quarter as this
-                        // tile's MMAs release the current A.  The next quarter
-                        // covers blocks [kq(cn,sub), X); every current-phase MMA
-                        // on blocks < X must be done: wait on the current quarter
-                        // holding block X-1 (in-order MMAs, so every earlier
-                        // quarter is free too) -- chunks of different sizes
-                        // (the last one) have different quarter boundaries
-                        const int cn = c + 1 < NC ? c + 1 : 0;
-                        const int X = kq(cn, sub + 1);
-                        if (kq(cn, sub) < X) {
-                            const int need = X - 1 < nkb(c) ? X - 1 : nkb(c) - 1;
-                            int hq = 3;
-                            for (int h = 0; h < 4; ++h)
-                                if (kq(c, h) <= need && need < kq(c, h + 1)) {
-                                    hq = h;
-                                    break;
-                                }
+                    const int pl = tt / T, it = tt - pl * T;
+                    if (!last_phase && tt == tt_gen) {
+                        if (hq >= 0) {
                             mb_wait(b_kbf + 8 * hq, phase & 1u);
                             fence_after();
                         }
-                        if (c + 1 < NC) {
+                        if (c + 1 < NC)
                             gen(j, c + 1);
-                        } else {
-                            if (CSM) epi_sync();  // staging of j+1 complete
+                        else
                             gen(j + 1, 0);
-                        }
                         ET(e_gen);
                     }
                     // cluster ids of the 32 columns i = it*128 + sub*32 + k
@@ -653,9 +732,12 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         }
                     }
                     ET(e_cmp);
-                    if (c == 0 && tt == 0 && pend_n >= 0) {  // the previous unit's reduce
-                        reduce_unit(pend_b, pend_n, pend_l0, pend_l1);
-                        pend_n = -1;
+                    if (c == 0 && tt == 0 && pend_j >= 0 && !(A.dbg & 4)) {  // the previous unit's reduce
+                        int64_t pb;
+                        int pn;
+                        slot_unit(pend_j, pb, pn);
+                        reduce_unit(pb, pn);
+                        pend_j = -1;
                         ET(e_red);
                     }
                 }
@@ -675,8 +757,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     // the finaliser's leg sums, fetched now: their L2 latency
                     // hides under the barrier instead of the reduce
                     const int64_t b = bbase + (warp - kYEpiWarp0);
-                    lg0 = __ldg(A.legs + 2 * b);
-                    lg1 = __ldg(A.legs + 2 * b + 1);
+                    lgs[2 * (warp - kYEpiWarp0)] = __ldg(A.legs + 2 * b);
+                    lgs[2 * (warp - kYEpiWarp0) + 1] = __ldg(A.legs + 2 * b + 1);
                 }
                 epi_sync();  // every bin of the chunk is complete
                 if (live && EX && c + 1 == NC) {
@@ -711,7 +793,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             inter(k), __hiloint2double((int)__ldg(tbp + k * A.ps),
                                                        (int)__ldg(tbp + (p + k) * A.ps)));
                 }
-                if (live && !EX) {
+                if (live && !EX && !(A.dbg & 4)) {
                     // plane pl of W carries weight 256^pl: an exact power-of-2
                     // scaling of T, so each product is the one-plane product
                     for (int pl = 0; pl < A.P; ++pl) {
@@ -741,13 +823,15 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 epi_sync();  // bins zeroed before the next chunk's atomics (red / prod written)
                 ET(e_st);
             }
-            pend_b = bbase;
-            pend_n = nind;
-            pend_l0 = lg0;
-            pend_l1 = lg1;
+            pend_j = j;
             ET(e_red);
         }
-        if (pend_n >= 0) reduce_unit(pend_b, pend_n, pend_l0, pend_l1);  // the last unit
+        if (pend_j >= 0) {  // the last unit
+            int64_t pb;
+            int pn;
+            slot_unit(pend_j, pb, pn);
+            reduce_unit(pb, pn);
+        }
         if (timed) {
             atomicAdd(A.timing + 16, e_st);
             atomicAdd(A.timing + 17, e_gen);
@@ -787,28 +871,32 @@ static bool p_csm(int p, int npad) {
 // everything but the W ring; exact: the [p][128] fp64 terms of S_T
 static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false) {
     return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) + (size_t)P * p * 512 +
-           4 * 128 * 8 + (exact ? (size_t)p * 1024 : 0) +
+           4 * 128 * 8 + (kYWarps - kYEpiWarp0) * 2 * 8 + (exact ? (size_t)p * 1024 : 0) +
            (2 * kYMaxStages + 12) * 8 + 16;
 }
 
-// W ring depth: as deep as shared memory allows
-static int p_kbs() {
+// K blocks per W stage: 8 (one MMA-issuer loop per 1024 K) unless that
+// leaves fewer than two stages (large p / the exact mode's terms): then 4, 2, 1
+static int p_kbs(int p, int npad, int P, bool exact = false) {
     const char* e = getenv("HUBGPU_TCP_KBS");  // tuning override
-    const int k = e ? atoi(e) : 8;
-    return k >= 1 && k <= 8 ? k : 8;
+    if (e && atoi(e) >= 1 && atoi(e) <= 8) return atoi(e);
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact);
+    int k = 8;
+    while (k > 1 && room < 2 * (int64_t)k * kYStageBytes) k /= 2;
+    return k;
 }
 
 static int p_stages(int p, int npad, int P, bool exact = false) {
     const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact);
-    int64_t s = room / ((int64_t)p_kbs() * kYStageBytes);
+    int64_t s = room / ((int64_t)p_kbs(p, npad, P, exact) * kYStageBytes);
     if (s > kYMaxStages) s = kYMaxStages;
     const char* e = getenv("HUBGPU_TCP_STAGES");  // tuning override (shallower only)
     if (e && atoi(e) >= 2 && atoi(e) < s) s = atoi(e);
     return (int)s;
 }
 
-// exact sums need one chunk, one plane and room for the [p][128] terms next
-// to a W ring of >= 2 stages (p <= ~56)
+// exact sums need room for the [p][128] terms next to a W ring of >= 2
+// stages (p <= ~90 at n <= 1024)
 static bool p_exact(int p, int npad, int P) {
     return p_stages(p, npad, P, true) >= 2;
 }
@@ -816,7 +904,8 @@ static bool p_exact(int p, int npad, int P) {
 // exact: the instance asks for numpy's summation order and the terms fit
 size_t tcp_smem_bytes(int p, int npad, int P, bool exact) {
     const bool x = exact && p_exact(p, npad, P);
-    return p_fixed_bytes(p, npad, P, x) + (size_t)p_stages(p, npad, P, x) * p_kbs() * kYStageBytes;
+    return p_fixed_bytes(p, npad, P, x) +
+           (size_t)p_stages(p, npad, P, x) * p_kbs(p, npad, P, x) * kYStageBytes;
 }
 
 bool tcp_supported(int n, int p, int npad, int P) {
@@ -854,9 +943,9 @@ int prepare_fitness_tcp(int p, int npad, int P) {
     return HG_OK;
 }
 
-int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint8_t* cl,
-                       const uint32_t* T, double* part, int grid, cudaStream_t s,
-                       const double* legs, double* out) {
+int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
+                       const uint8_t* cl, const uint32_t* T, double* part, int grid,
+                       cudaStream_t s, const double* legs, double* out) {
     if (B <= 0) return HG_OK;
     PArgs A;
     A.cl = cl;
@@ -877,16 +966,19 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     A.ITO = (int)(round_up(I.n, 128) / 128);
     A.KBT = A.ITO;
     A.NC = (A.KBT + kYChunkKB - 1) / kYChunkKB;
-    A.P = I.wplanes;
     A.nt = (int)round_up(I.n, 128);
     // exact: the instance asks for numpy's order and the [p][128] terms fit
     // beside two W stages (else the fixed-order fold: tran within ~1 ulp)
     // (several K chunks or planes: the bins accumulate over all of them, exact
     // while the total flow stays below 2^32)
-    A.exact = I.exact && (A.NC == 1 && A.P == 1 || I.bins_total_ok) && p_exact(I.p, I.npad, A.P) &&
-              I.pwl != nullptr;
+    A.exact = I.exact && (A.NC == 1 && I.wplanes == 1 || I.bins_total_ok) &&
+              p_exact(I.p, I.npad, I.wplanes) && I.pwl != nullptr;
+    // the triangular fold of W (half the MMA work) whenever the bins need not
+    // be the reference's own flows: symmetric costs, fixed-order sums
+    A.tri = !A.exact && wmap_tri != nullptr && !(getenv("HUBGPU_TCP_NOTRI")) ? 1 : 0;
+    A.P = A.tri ? I.wplanes_tri : I.wplanes;
     A.stages = p_stages(I.p, I.npad, A.P, A.exact);  // as tcp_smem_bytes
-    A.kbs = p_kbs();
+    A.kbs = p_kbs(I.p, I.npad, A.P, A.exact);
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
     A.timing = tc_timing_buffer();
@@ -902,7 +994,7 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, int64_t B, const uint
     const int64_t need = round_up(A.units, kYCluster);
     if (g > need) g = (int)need;
     if (g < kYCluster) g = kYCluster;
-    CUtensorMap map = *static_cast<const CUtensorMap*>(wmap);
+    CUtensorMap map = *static_cast<const CUtensorMap*>(A.tri ? wmap_tri : wmap);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3(kYThreads);

@@ -338,11 +338,55 @@ def gen_cli():
     save("cli", **out)
 
 
+def gen_big():
+    """BASELINE shapes at full size (round 2): BIG (n=6000, p=50) cost
+    breakdowns from the reference's objective for 24 uniform hub sets, and two
+    complete solve() runs -- AP 16 x 64 x 3 x 2 and UR 128 x 64 x 1 x 1.  The
+    instances are generate_urand(...) outputs (identified by arguments and
+    SHA-256, rebuilt bit-exactly by the package's generator)."""
+    import hashlib
+
+    out = {}
+
+    def ident(label, args, inst):
+        out[f"{label}_args"] = np.array(args[:3] + list(args[3]), dtype=np.float64)
+        out[f"{label}_sha"] = np.array([hashlib.sha256(inst.dist.tobytes()).hexdigest(),
+                                        hashlib.sha256(inst.flow.tobytes()).hexdigest()])
+
+    args = [6000, 50, 1704, (1.0, 0.75, 1.0)]
+    big = hm.generate_urand(*args)
+    ident("big", args, big)
+    pop = population(big.n, big.p, 24, 1)
+    comps, ahash = [], []
+    for hubs in pop:
+        sol = hm.nearest_allocation(hubs, big)
+        bd = hm.objective(big, sol)
+        comps.append([bd.collection_cost, bd.transfer_cost, bd.distribution_cost, bd.raw_total])
+        ahash.append(hashlib.sha256(sol.alloc.astype(np.int64).tobytes()).hexdigest())
+    out["big_hubs"] = pop
+    out["big_comp"] = np.array(comps)
+    out["big_alloc_sha"] = np.array(ahash)
+    print(f"  big: {len(pop)} breakdowns")
+    for label, args, kw in [
+        ("ap", [200, 10, 1704, (3.0, 0.75, 2.0)],
+         dict(islands=16, pop_size=64, inner_iters=3, outer_iters=2, seed=0)),
+        ("ur", [1000, 20, 1704, (1.0, 0.75, 1.0)],
+         dict(islands=128, pop_size=64, inner_iters=1, outer_iters=1, seed=0)),
+    ]:
+        inst = hm.generate_urand(*args)
+        ident(label, args, inst)
+        rep = hm.solve(inst, hm.GaParams(**kw), hm.FitnessMode.STANDARD_MILLI)
+        out[f"{label}_params"] = np.array(json.dumps(kw))
+        out[f"{label}_hubs"] = rep.best_solution.hubs
+        out[f"{label}_raw"] = np.array([rep.raw_objective, rep.scaled_fitness])
+        out[f"{label}_trace"] = np.array(rep.trace)
+        out[f"{label}_evals"] = np.array([rep.evaluations])
+        print(f"  ga {label}: raw={rep.raw_objective!r} evals={rep.evaluations}")
+    save("big", **out)
+
+
 if __name__ == "__main__":
-    gen_cli()
-    gen_rng()
-    gen_instances()
-    gen_eval()
-    gen_operators()
-    gen_ga()
-    gen_restricted()
+    parts = sys.argv[1:] or ["cli", "rng", "instances", "eval", "operators", "ga", "restricted",
+                             "big"]
+    for part in parts:
+        globals()[f"gen_{part}"]()

@@ -38,11 +38,12 @@ def _need_gpu():
         pytest.fail("no CUDA device: the gpu tests must run on a B200")
 
 
-@pytest.fixture(params=["fp64", "tensor-pair"])
+@pytest.fixture(params=["fp64", "tensor-pair", "tensor-pair-full"])
 def kernel(request):
     """Run a test with the fp64 gather kernel (K3) and with the tensor-core
-    kernel K3-TC/P (used wherever the flows are integers below 2^32; elsewhere
-    the instance stays on auto)."""
+    kernel K3-TC/P, on the triangular fold of W (symmetric costs) and on the
+    full W (used wherever the flows are integers below 2^32; elsewhere the
+    instance stays on auto)."""
     from paper_1704_06258_b200 import _lib
 
     _lib.set_fitness_default(request.param)
@@ -177,8 +178,8 @@ class TestKernels:
         assert d.flags & 4 and d.fitness_kernel == "tensor-pair"
         big = hg.generate_urand(1100, 20, 3, (1.0, 0.75, 1.0))
         assert big.device().fitness_kernel == "tensor-pair"  # K chunks of 1024 nodes
-        with pytest.raises(ValueError, match="n <= 1024"):
-            big.device().set_fitness(4)  # the one-CTA TMEM kernel keeps n <= 1024
+        with pytest.raises(ValueError, match="unknown fitness kernel"):
+            big.device().set_fitness(4)  # the superseded TMEM one-CTA kernel is gone
         frac = hg.Instance(inst.n, inst.p, inst.dist, inst.flow * 0.5, 1.0, 0.75, 1.0)
         assert frac.device().fitness_kernel == "fp64"
         with pytest.raises(ValueError, match="tensor-core"):
@@ -193,13 +194,8 @@ class TestKernels:
         d = inst.device()
         d.set_fitness(1)
         fp = hg.evaluate_population(inst, pop)
-        for kind in (3, 4, 5):  # smem one-hot, TMEM one-hot, CTA pair
-            try:
-                d.set_fitness(kind)
-            except ValueError as e:  # smem one-hot: p <= ~100; TMEM one-CTA: n <= 1024
-                assert (kind == 3 and p > 64 and "does not fit" in str(e)) or (
-                    kind == 4 and n > 1024 and "n <= 1024" in str(e)), (kind, str(e))
-                continue
+        for kind in (5, 6):  # CTA pair on the triangular fold / on the full W
+            d.set_fitness(kind)
             tc = hg.evaluate_population(inst, pop)
             assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
             assert close(tc, fp, rel=1e-13), kind
@@ -572,14 +568,15 @@ class TestWidePlanes:
         inst = hg.Instance(700, 12, base.dist, flow, 1.0, 0.75, 1.0)
         d = inst.device()
         assert d.flags & 4 and d.fitness_kernel == "tensor-pair"
-        with pytest.raises(ValueError, match="flows"):
-            d.set_fitness(4)  # the one-CTA TMEM kernel takes one plane only
         pop = hg.random_population(700, 12, 999, key=2)
-        tc = hg.evaluate_population(inst, pop)
+        tc = hg.evaluate_population(inst, pop)  # triangular fold: W + W^T planes
+        d.set_fitness(6)
+        full = hg.evaluate_population(inst, pop)  # the full W's planes
         d.set_fitness(1)
         fp = hg.evaluate_population(inst, pop)
-        assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
-        assert close(tc, fp, rel=1e-13)
+        for got in (tc, full):
+            assert np.array_equal(got[:, [0, 2]], fp[:, [0, 2]])
+            assert close(got, fp, rel=1e-13)
 
     def test_flows_from_2_32_use_fp64(self):
         base = hg.generate_urand(50, 4, 5, (1.0, 0.75, 1.0))

@@ -1,0 +1,240 @@
+"""Round-2 parity and robustness on the GPU (marked gpu).
+
+* BIG (n=6000, p=50): the reference's own cost breakdowns (tests/golden/big.npz,
+  made by running hubmedian) -- within 1e-12 by default, bit-identical in
+  exact mode -- and 256 more individuals against a restatement of
+  hm/evaluation.py:103-120 within 1e-12;
+* complete solve() runs at the BASELINE GA shapes: AP 16 x 64 x 3 x 2 and
+  UR 128 x 64 x 1 x 1 (best hubs, raw, trace, evaluation count);
+* an Instance shared by 8 threads (the reference's Instance is "safe to share
+  across worker threads", hm/model.py:35);
+* instances of different p used alternately (per-kernel launch attributes);
+* the island GA across 2 and 3 processes (real DeviceIslands on the GPU,
+  champion exchange over gloo) reproducing the reference's SolveReport.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import socket
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from conftest import golden, orc
+
+import paper_1704_06258_b200 as hg
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if hg.device_count() < 1:
+        pytest.fail("no CUDA device: the gpu tests must run on a B200")
+
+
+def _rel_ok(a, b, rel=REL):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.all(np.abs(a - b) <= rel * np.abs(b))
+
+
+def _instance(g, label, device=True):
+    n, p, seed, c, a, d = g[f"{label}_args"]
+    inst = hg.generate_urand(int(n), int(p), int(seed), (c, a, d), device=device)
+    sha = g[f"{label}_sha"]
+    assert hashlib.sha256(inst.dist.tobytes()).hexdigest() == sha[0]
+    assert hashlib.sha256(inst.flow.tobytes()).hexdigest() == sha[1]
+    return inst
+
+
+@pytest.fixture(scope="module")
+def big():
+    return _instance(golden("big"), "big")
+
+
+def _costs_matrix_form(inst, hubs, alloc):
+    """(coll, tran, dist, raw) of hm/evaluation.py:103-120 in matrix form:
+    F = OneHot^T W OneHot (p x p) instead of the index-ordered bincount (the
+    same sum in another order, so the bar is 1e-12, not bits)."""
+    n, p = inst.n, inst.p
+    legs = inst.dist[np.arange(n), alloc]
+    coll = inst.chi * float(np.sum(inst.out_flow * legs))
+    dist = inst.delta * float(np.sum(inst.in_flow * legs))
+    pos = np.zeros(n, dtype=np.int64)
+    pos[hubs] = np.arange(p)
+    oh = np.zeros((n, p))
+    oh[np.arange(n), pos[alloc]] = 1.0
+    F = oh.T @ (inst.flow @ oh)
+    tran = inst.alpha * float(np.sum(F * inst.dist[np.ix_(hubs, hubs)]))
+    return np.array([coll, tran, dist, coll + tran + dist])
+
+
+class TestBig:
+    def test_reference_breakdowns(self, big):
+        g = golden("big")
+        out = hg.evaluate_population(big, g["big_hubs"])
+        assert _rel_ok(out, g["big_comp"])
+        allocs = hg.nearest_allocations(big, g["big_hubs"])
+        shas = [hashlib.sha256(a.astype(np.int64).tobytes()).hexdigest() for a in allocs]
+        assert shas == g["big_alloc_sha"].tolist()
+
+    def test_reference_breakdowns_exact(self, big):
+        # total flow 1.8e9 < 2^32: the integer bins span every K chunk, so
+        # every term is the reference's np.sum bit for bit
+        assert big.total_flow < 2**32
+        g = golden("big")
+        hg.set_exact_sums(True)
+        try:
+            out = hg.evaluate_population(big, g["big_hubs"])
+        finally:
+            hg.set_exact_sums(False)
+        assert np.array_equal(out, g["big_comp"]), np.abs(out - g["big_comp"]).max(axis=0)
+
+    def test_256_individuals(self, big):
+        pop = hg.random_population(big.n, big.p, 256, key=77)
+        out = hg.evaluate_population(big, pop)
+        allocs = hg.nearest_allocations(big, pop)
+        for b in range(256):
+            assert np.array_equal(allocs[b], orc.nearest(big.dist, pop[b])), b
+            assert _rel_ok(out[b], _costs_matrix_form(big, pop[b], allocs[b])), b
+
+    def test_fp64_kernel_agrees(self, big):
+        from paper_1704_06258_b200 import _lib
+
+        g = golden("big")
+        d = big.device()
+        tens = hg.evaluate_population(big, g["big_hubs"])
+        d.set_fitness(_lib.FIT_FP64)
+        try:
+            f64 = hg.evaluate_population(big, g["big_hubs"])
+        finally:
+            d.set_fitness(_lib.FIT_AUTO)
+        assert _rel_ok(f64, g["big_comp"])
+        assert _rel_ok(tens, f64, 1e-13)
+
+
+class TestGaFullShapes:
+    @pytest.mark.parametrize("label", ["ap", "ur"])
+    def test_solve_matches_reference(self, label):
+        g = golden("big")
+        inst = _instance(g, label)
+        params = hg.GaParams(**json.loads(str(g[f"{label}_params"])))
+        rep = hg.solve(inst, params, hg.FitnessMode.STANDARD_MILLI)
+        assert np.array_equal(rep.best_solution.hubs, g[f"{label}_hubs"])
+        assert _rel_ok([rep.raw_objective, rep.scaled_fitness], g[f"{label}_raw"])
+        assert _rel_ok(rep.trace, g[f"{label}_trace"])
+        assert rep.evaluations == int(g[f"{label}_evals"][0])
+
+
+class TestSharedInstance:
+    def test_eight_threads(self):
+        inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
+        pops = [hg.random_population(1000, 20, 64 + 8 * k, key=200 + k) for k in range(16)]
+        serial = [hg.evaluate_population(inst, pop) for pop in pops]
+        sols = [hg.nearest_allocation(pop[0], inst) for pop in pops]
+        serial_obj = [hg.objective(inst, s).raw_total for s in sols]
+
+        def work(k):
+            got = []
+            for _ in range(4):
+                got.append((hg.evaluate_population(inst, pops[k]),
+                            hg.objective(inst, sols[k]).raw_total))
+            return got
+
+        with ThreadPoolExecutor(8) as ex:
+            results = list(ex.map(work, range(16)))
+        for k, got in enumerate(results):
+            for out, raw in got:
+                assert np.array_equal(out, serial[k])
+                assert raw == serial_obj[k]
+
+    def test_concurrent_solves(self):
+        inst = hg.generate_urand(200, 10, 1704, (3.0, 0.75, 2.0))
+        params = hg.GaParams(islands=4, pop_size=16, inner_iters=3, outer_iters=2, seed=3)
+        ref = hg.solve(inst, params, hg.FitnessMode.STANDARD_MILLI)
+        with ThreadPoolExecutor(4) as ex:
+            reps = list(ex.map(lambda _: hg.solve(inst, params, hg.FitnessMode.STANDARD_MILLI),
+                               range(8)))
+        for r in reps:
+            assert np.array_equal(r.best_solution.hubs, ref.best_solution.hubs)
+            assert r.raw_objective == ref.raw_objective
+            assert r.trace == ref.trace
+
+
+class TestInstancesOfDifferentShape:
+    def test_alternating_p(self):
+        # a p=50 instance first, then p=20: each kernel's launch attribute
+        # must still admit the larger p=50 launches (and its captured graph)
+        a = hg.generate_urand(1000, 50, 5, (1.0, 0.75, 1.0))
+        pa = hg.random_population(1000, 50, 40, key=3)
+        ref_a = hg.evaluate_population(a, pa)
+        pa_ga = hg.GaParams(islands=2, pop_size=8, inner_iters=2, outer_iters=1, seed=1)
+        ga_a = hg.solve(a, pa_ga)
+        b = hg.generate_urand(1000, 20, 6, (1.0, 0.75, 1.0))
+        pb = hg.random_population(1000, 20, 40, key=4)
+        ref_b = hg.evaluate_population(b, pb)
+        for _ in range(3):
+            assert np.array_equal(hg.evaluate_population(a, pa), ref_a)
+            assert np.array_equal(hg.evaluate_population(b, pb), ref_b)
+            assert hg.solve(a, pa_ga).raw_objective == ga_a.raw_objective
+
+
+# ---------------------------------------------------------------------------
+# the island GA across processes: real device islands, gloo exchange
+# ---------------------------------------------------------------------------
+
+def _mp_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1704_06258_b200 as hg2
+
+        hg2.set_device(0)
+        g = golden("big")
+        n, p, seed, c, a, d = g["ap_args"]
+        inst = hg2.generate_urand(int(n), int(p), int(seed), (c, a, d))
+        params = hg2.GaParams(**json.loads(str(g["ap_params"])))
+        rep = hg2.solve(inst, params, hg2.FitnessMode.STANDARD_MILLI, group=dist.group.WORLD)
+        q.put((rank, rep.best_solution.hubs.tolist(), rep.raw_objective, list(rep.trace),
+               rep.evaluations))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e), None, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_islands_across_processes(world):
+    """Islands sharded over `world` processes on one GPU (each its own CUDA
+    context; the kernels never wait on another process -- the exchange is a
+    host all_gather at the round barrier) give the reference's report."""
+    import torch.multiprocessing as mp
+
+    g = golden("big")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, hubs, raw, trace, evals in res:
+        assert raw is not None, hubs
+        assert hubs == g["ap_hubs"].tolist()
+        assert _rel_ok(raw, g["ap_raw"][0])
+        assert _rel_ok(trace, g["ap_trace"])
+        assert evals == int(g["ap_evals"][0])
