@@ -76,11 +76,21 @@ def peaks():
         return HBM_FALLBACK, "fallback"
 
 
-def peaks_bf16():
+INT8_PEAK_FILE = "profiles/int8_peak_r2.json"
+
+
+def peaks_int8():
+    """Dense int8 tensor peak measured on this pool's B200 by tools/int8_peak.cu
+    (committed result), else 2x the measured bf16 burst (nominal ratio)."""
     try:
-        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+        return float(json.loads((ROOT / INT8_PEAK_FILE).read_text())["int8_tops"]), \
+            f"measured: tools/int8_peak.cu ({INT8_PEAK_FILE})"
     except Exception:
-        return 1590.0
+        try:
+            bf16 = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+        except Exception:
+            bf16 = 1590.0
+        return 2.0 * bf16, "2x measured dense bf16 (int8 microbench result missing)"
 
 
 def dist_env():
@@ -373,11 +383,14 @@ def run_gpu(args):
     fit_kernel = dinst.fitness_kernel
     fit_avg = float(np.mean(fit_ms))
     alg_bytes = POP * (8.0 * N * N + 4.0 * N)
-    achieved = alg_bytes / (fit_avg * 1e-3) / 1e9
-    # tensor view of K3-TC: useful u8 MACs 2*n^2*p ops per eval vs the dense int8
-    # peak, taken as 2x the measured dense bf16 GEMM peak (nominal ratio)
-    bf16 = peaks_bf16()
-    tensor_ops = POP * 2.0 * N * N * P
+    # K3-TC/P is bound by the int8 tensor pipe: the work is the int8 operations
+    # it issues per launch (padding, dummy slots included; on the triangular
+    # fold about half of the full contraction's), the peak the measured dense
+    # int8 rate of tools/int8_peak.cu
+    issued_ops = dinst.mma_ops(POP)
+    useful_ops = POP * 2.0 * N * N * P  # the full n x n x p contraction per eval
+    int8_peak, int8_src = peaks_int8()
+    achieved_tops = issued_ops / (fit_avg * 1e-3) / 1e12
     # every other K3 variant on the same population, for comparison
     variant_ms = {}
     for name in ("fp64", "tensor-pair-full", "tensor-pair"):
@@ -476,19 +489,25 @@ def run_gpu(args):
                        "pop_per_gpu": POP, "global_pop": POP * world,
                        "parallelism": f"population sharded, {world} rank(s)",
                        "l2": "flushed between steps (256 MiB write, untimed)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic(fit_kernel),
-                         "traffic_source": NCU_TRAFFIC_FILE,
-                         "kernel": KERNEL_NAMES[fit_kernel],
-                         "kernel_ms": fit_avg,
-                         "alg_bytes_per_launch": alg_bytes, "peak_source": hbm_src,
-                         "note": "SURVEY 8(d): 8n^2+4n bytes charged per eval; W is read "
-                                 "once per tile and reused across the population, so frac > 1 "
-                                 "-- the binding ceilings are on-chip (see tensor)",
-                         "tensor": {"achieved_tops": tensor_ops / (fit_avg * 1e-3) / 1e12,
-                                    "peak_tops": 2.0 * bf16,
-                                    "frac": tensor_ops / (fit_avg * 1e-3) / 1e12 / (2.0 * bf16),
-                                    "peak_source": "2x measured dense bf16 (nominal int8 ratio)"}},
+            "roofline": {"bound": "tensor", "operand": "int8 (tcgen05.mma kind::i8, u8 x u8 -> s32)",
+                         "achieved": achieved_tops, "peak": int8_peak, "unit": "TOP/s",
+                         "frac": achieved_tops / int8_peak,
+                         "traffic": ncu_traffic(fit_kernel), "traffic_source": NCU_TRAFFIC_FILE,
+                         "kernel": KERNEL_NAMES[fit_kernel], "kernel_ms": fit_avg,
+                         "ops_per_launch": issued_ops, "peak_source": int8_src,
+                         "useful_ops_per_launch": useful_ops,
+                         "useful_tops": useful_ops / (fit_avg * 1e-3) / 1e12,
+                         "note": "achieved = int8 ops the kernel issues per launch / its "
+                                 "event-timed duration; useful = 2 n^2 p per eval, the full "
+                                 "contraction the triangular fold halves",
+                         "hbm_view": {"alg_bytes_per_launch": alg_bytes,
+                                      "alg_gbs": alg_bytes / (fit_avg * 1e-3) / 1e9,
+                                      "hbm_peak_gbs": hbm, "peak_source": hbm_src,
+                                      "w_reuse_factor": alg_bytes / (fit_avg * 1e-3) / 1e9 / hbm,
+                                      "note": "SURVEY 8(d) charges a full fp64 W pass (8n^2+4n B) "
+                                              "per eval; W stays on chip across the population, "
+                                              "so this ratio is the W-reuse factor, not a "
+                                              "roofline fraction"}},
             "kernels_ms": {"k3_selected": fit_kernel, "k3": fit_avg,
                            "k3_variants": variant_ms, "step_total": ms_per_step},
             "e2e": {"value": e2e_value, "unit": "evals/s",

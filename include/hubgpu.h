@@ -134,6 +134,13 @@ int hg_pop_launches_per_evaluate(const hg_pop* pop);
 /* duration (ms) of the fitness kernel K3 in the last hg_pop_evaluate,
  * measured with CUDA events on the instance stream (synchronises) */
 int hg_pop_last_fitness_ms(hg_pop* pop, float* ms);
+/* duration (ms) of the allocation kernel K2 in the last hg_pop_evaluate */
+int hg_pop_last_allocate_ms(hg_pop* pop, float* ms);
+
+/* int8 tensor-core operations (2 per multiply-add) the instance's fitness
+ * kernel issues to score B hub sets, padding and dummy work included; 0 for
+ * the fp64 kernel (the bench's roofline numerator) */
+int hg_fitness_work(hg_inst* inst, int64_t B, double* mma_ops);
 
 /* kernels this library has launched in the process so far (a CUDA-graph
  * replay adds the kernels it holds); differences of two reads count the

@@ -70,8 +70,10 @@ SIGNATURES = {
     "hg_pop_read": (C.c_int, [_vp, C.c_int64, _vp, C.c_int]),
     "hg_pop_launches_per_evaluate": (C.c_int, [_vp]),
     "hg_pop_last_fitness_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "hg_pop_last_allocate_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "hg_debug_tc_timing": (C.c_int, [_u64p]),
     "hg_launch_count": (C.c_int, [_u64p]),
+    "hg_fitness_work": (C.c_int, [_vp, C.c_int64, _f64p]),
     "hg_correct": (C.c_int, [_vp, C.c_int64, _u8p, _i64p]),
     "hg_crossover": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _u8p, _i64p, _u8p, _u8p]),
     "hg_swap": (C.c_int, [C.c_int, C.c_int, C.c_int64, _u8p, _i64p, _i64p, _u8p]),
@@ -287,6 +289,12 @@ class DeviceInstance:
         check(load().hg_evaluate(self.handle, B, ptr(hubs, _i64p), ap, ptr(out, _f64p)))
         return out
 
+    def mma_ops(self, B: int) -> float:
+        """int8 tensor operations the fitness kernel issues for B hub sets."""
+        v = C.c_double()
+        check(load().hg_fitness_work(self.handle, int(B), C.byref(v)))
+        return v.value
+
     def correct(self, masks: np.ndarray) -> np.ndarray:
         masks = np.ascontiguousarray(masks, dtype=np.uint8).reshape(-1, self.n)
         out = np.empty((masks.shape[0], self.p), dtype=np.int64)
@@ -360,6 +368,11 @@ class DevicePopulation:
     def last_fitness_ms(self) -> float:
         v = C.c_float()
         check(load().hg_pop_last_fitness_ms(self.handle, C.byref(v)))
+        return v.value
+
+    def last_allocate_ms(self) -> float:
+        v = C.c_float()
+        check(load().hg_pop_last_allocate_ms(self.handle, C.byref(v)))
         return v.value
 
     @property

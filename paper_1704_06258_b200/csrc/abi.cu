@@ -59,7 +59,7 @@ struct hg_pop {
     double* part = nullptr;
     double* out = nullptr;
     DevBuf alloc;  // int32 [cap][n], on demand
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t evk = nullptr, ev0 = nullptr, ev1 = nullptr;  // before K2, K3, after K3
 };
 
 struct hg_inst {
@@ -117,6 +117,7 @@ void pop_release(hg_pop* P) {
     cudaFree(P->part);
     cudaFree(P->out);
     P->alloc.release();
+    if (P->evk) cudaEventDestroy(P->evk);
     if (P->ev0) cudaEventDestroy(P->ev0);
     if (P->ev1) cudaEventDestroy(P->ev1);
     P->hubs = nullptr;
@@ -126,7 +127,7 @@ void pop_release(hg_pop* P) {
     P->legs = nullptr;
     P->part = nullptr;
     P->out = nullptr;
-    P->ev0 = P->ev1 = nullptr;
+    P->evk = P->ev0 = P->ev1 = nullptr;
     P->cap = 0;
 }
 
@@ -142,6 +143,7 @@ int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     const int tiles = inst->plan.tiles > tc_tiles(I.n) ? inst->plan.tiles : tc_tiles(I.n);
     HG_CUDA(cudaMalloc(&P->part, (size_t)cap * tiles * sizeof(double)));
     HG_CUDA(cudaMalloc(&P->out, (size_t)cap * 4 * sizeof(double)));
+    HG_CUDA(cudaEventCreate(&P->evk));
     HG_CUDA(cudaEventCreate(&P->ev0));
     HG_CUDA(cudaEventCreate(&P->ev1));
     P->cap = cap;
@@ -235,6 +237,7 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
     hg_inst* inst = P->inst;
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
+    HG_CUDA(cudaEventRecord(P->evk, s));
     if (alloc32)
         HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, co_for(inst, P->co), P->T,
                                  P->legs, s));
@@ -771,6 +774,16 @@ int hg_pop_read(hg_pop* pop, int64_t B, double* out, int where) {
     return HG_OK;
 }
 
+int hg_fitness_work(hg_inst* inst, int64_t B, double* mma_ops) {
+    auto lk_ = lock_of(inst);
+    HG_ARG(inst != nullptr && mma_ops != nullptr, "NULL argument");
+    HG_ARG(B >= 0, "negative batch");
+    const int k = fitness_kernel(inst);
+    *mma_ops = k == HG_FIT_FP64 ? 0.0
+                                : tcp_mma_ops(inst->I, k == HG_FIT_TC_PAIR, B, inst->sm_count);
+    return HG_OK;
+}
+
 int hg_launch_count(uint64_t* count) {
     HG_ARG(count != nullptr, "NULL argument");
     *count = launch_count();
@@ -784,6 +797,15 @@ int hg_debug_tc_timing(unsigned long long* out32) {
 
 int hg_pop_launches_per_evaluate(const hg_pop* pop) {
     return fitness_kernel(pop->inst) == HG_FIT_FP64 ? 3 : 2;
+}
+
+int hg_pop_last_allocate_ms(hg_pop* pop, float* ms) {
+    auto lk_ = lock_of(pop ? pop->inst : nullptr);
+    HG_ARG(pop && ms, "NULL argument");
+    HG_TRY(set_device(pop->inst->device));
+    HG_CUDA(cudaEventSynchronize(pop->ev0));
+    HG_CUDA(cudaEventElapsedTime(ms, pop->evk, pop->ev0));
+    return HG_OK;
 }
 
 int hg_pop_last_fitness_ms(hg_pop* pop, float* ms) {

@@ -170,6 +170,8 @@ bool tcp_supported(int n, int p, int npad, int P);
 size_t tcp_smem_bytes(int p, int npad, int P, bool exact);
 int prepare_fitness_tcp(int p, int npad, int P);
 // legs / out set: the finaliser is fused (out gets the 4 cost terms, part unused)
+// int8 tensor operations one launch on B hub sets issues (the roofline's work)
+double tcp_mma_ops(const DevInst& I, bool tri_avail, int64_t B, int grid);
 // wmap_tri: the map of the triangular fold (symmetric costs), or nullptr
 int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
                        const uint8_t* cl, const uint32_t* T, double* part, int grid,

@@ -55,6 +55,17 @@ __device__ __forceinline__ void mb_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ bool mb_try(uint32_t bar, uint32_t parity) {  // non-blocking
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P;\n"
@@ -80,6 +91,17 @@ __device__ __forceinline__ void commit_pair(uint32_t bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
         " [%0], %1;" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
+}
+// the same, issued by one elected lane of a converged warp (the MMA warp runs
+// its loop warp-uniformly, so descriptors stay in uniform registers)
+__device__ __forceinline__ void commit_pair_w(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t}" ::"r"(bar),
         "h"((uint16_t)3)
         : "memory");
 }
@@ -126,6 +148,16 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ts_w(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t acc) {  // one elected lane of the warp
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
         "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
         : "memory");
 }
@@ -195,7 +227,8 @@ struct PArgs {
     uint32_t idesc;   // kind::i8, M=256, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
     // ablation flags (tuning only, wrong results): 1 = no bin atomics, 2 = no
-    // MMA, 4 = no chunk fold / unit reduce, 8 = no one-hot generation, 64 = no
+    // MMA, 4 = no chunk fold / unit reduce, 8 = no one-hot generation, 16 = the
+    // MMA issuer does not wait for W, 32 = no W stream (needs 16), 64 = no
     // epilogue warps at all
     int dbg;
     // exact: one chunk and one plane, so the bins ARE the reference's
@@ -302,76 +335,43 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     // the leader's barriers as shared::cluster addresses (remote for the peer)
     const uint32_t L_full = mapa(b_full, 0), L_acce = mapa(b_acce, 0), L_ard = mapa(b_ard, 0);
 
-    // The W stream is one flat sequence of items (slot j, chunk c, tile tt of
-    // the phase, chunk-local K block kb) -- tile tt = (plane, W row block it)
-    // runs blocks [klo(c, it), nkb(c)) -- cut into ring stages of KBS items
-    // regardless of tile boundaries, so the short tiles of the triangular
-    // fold still move full stages
-    struct Walk {
-        int64_t j;
-        int c, tt, kb;
-        uint32_t phase;
-    };
-    auto walk_first = [&](Walk& w) {
-        w.j = 0;
-        w.c = 0;
-        w.tt = 0;
-        w.kb = 0;
-        w.phase = 0;
-    };
-    auto walk_next = [&](Walk& w) {
-        if (++w.kb < nkb(w.c)) return;
-        const int T = ntl(w.c);
-        if (++w.tt == A.P * T) {
-            w.tt = 0;
-            ++w.phase;
-            if (++w.c == NC) {
-                w.c = 0;
-                ++w.j;
-            }
-        }
-        const int T2 = ntl(w.c);
-        w.kb = klo(w.c, w.tt - (w.tt / T2) * T2);
-    };
-
     if (warp == 1) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer: per phase, the W tiles (plane, row
+        // block it) in order, tile it running K blocks [klo(c, it), nkb(c));
+        // a stage holds up to KBS consecutive blocks of one tile
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
             bool wrapped = false;
             const int q = (int)crank * 64;  // this CTA's W rows within a tile
-            Walk w;
-            walk_first(w);
-            while (w.j < nslots) {
-                // items of this stage
-                Walk e = w;
-                int nk = 0;
-                while (nk < KBS && e.j < nslots) {
-                    ++nk;
-                    walk_next(e);
+            for (int64_t j = 0; j < nslots; ++j)
+                for (int c = 0; c < NC; ++c) {
+                    const int T = ntl(c), nb = nkb(c);
+                    for (int pl = 0; pl < A.P; ++pl)
+                        for (int it = 0; it < T; ++it)
+                            for (int kb0 = klo(c, it); kb0 < nb; kb0 += KBS) {
+                                const int nk = nb - kb0 < KBS ? nb - kb0 : KBS;
+                                if (A.dbg & 32) continue;  // ablation: no W stream
+                                // stage s is free: the leader's MMAs reading it completed
+                                if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
+                                if (leader)  // both halves land on the leader's barrier
+                                    mb_expect_tx(b_full + 8 * s, (uint32_t)(2 * nk * kYStageBytes));
+                                const uint32_t dst = su32(ring + s * (KBS * kYStageBytes));
+                                for (int kk = 0; kk < nk; ++kk)
+                                    tma2d_pair(dst + kk * kYStageBytes, &tmW,
+                                               (c * kYChunkKB + kb0 + kk) * 128,
+                                               pl * A.nt + it * 128 + q, L_full + 8 * s);
+                                if (++s == (uint32_t)NS) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                    wrapped = true;
+                                }
+                            }
                 }
-                // stage s is free: the leader's MMAs reading it completed
-                if (wrapped) mb_wait(b_empty + 8 * s, ph ^ 1u);
-                if (leader)  // both halves land on the leader's barrier
-                    mb_expect_tx(b_full + 8 * s, (uint32_t)(2 * nk * kYStageBytes));
-                const uint32_t dst = su32(ring + s * (KBS * kYStageBytes));
-                for (int kk = 0; kk < nk; ++kk) {
-                    const int T = ntl(w.c), pl = w.tt / T, it = w.tt - pl * T;
-                    tma2d_pair(dst + kk * kYStageBytes, &tmW, (w.c * kYChunkKB + w.kb) * 128,
-                               pl * A.nt + it * 128 + q, L_full + 8 * s);
-                    walk_next(w);
-                }
-                if (++s == (uint32_t)NS) {
-                    s = 0;
-                    ph ^= 1u;
-                    wrapped = true;
-                }
-            }
         }
     } else if (warp == 0) {
         // ---------------- MMA issuer (leader CTA only)
-        if (lane == 0 && leader) {
-            uint32_t s = 0, ph = 0, t = 0;
+        if (leader) {  // the whole warp, converged; one lane issues
+            uint32_t s = 0, ph = 0, t = 0, phase = 0;
             const bool timed = A.timing != nullptr;
             unsigned long long w_a = 0, w_e = 0, w_f = 0, w_i = 0;
             long long c0 = timed ? clock64() : 0;
@@ -383,76 +383,72 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             c0 = c1_;                               \
         }                                           \
     } while (0)
-            // per chunk-local block, 4 bits each: the A quarters whose ready
-            // barrier the block's first MMA waits on (tile 0 of a phase), and
-            // the quarters its last use frees -- rebuilt when the chunk changes
-            int qc = -1;
-            uint32_t waitq = 0u, relq = 0u;
-            uint32_t dcol = 0, d = 0;
-            Walk w;
-            walk_first(w);
-            while (w.j < nslots) {
-                mb_wait(b_full + 8 * s, ph);
-                YT(w_f);
-                fence_after();
-                const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
-                for (int kk = 0; kk < KBS && w.j < nslots; ++kk) {
-                    const int c = w.c, T = ntl(c), pl = w.tt / T, it = w.tt - pl * T;
-                    const int k0 = klo(c, it), kb = w.kb;
-                    if (c != qc) {
-                        qc = c;
-                        waitq = relq = 0u;
-                        for (int h = 0; h < 4; ++h) {
-                            if (kq(c, h) < kq(c, h + 1)) waitq |= 1u << (4 * kq(c, h) + h);
-                            relq |= 1u << (4 * qrb(c, h) + h);
-                        }
+            for (int64_t j = 0; j < nslots; ++j) {
+                for (int c = 0; c < NC; ++c, ++phase) {
+                    const int nb = nkb(c), T = ntl(c);
+                    // per chunk-local block, 4 bits each: the A quarters whose
+                    // ready barrier the block's first MMA waits on (tile 0), and
+                    // the quarters its last use frees
+                    uint32_t waitq = 0u, relq = 0u;
+                    for (int h = 0; h < 4; ++h) {
+                        if (kq(c, h) < kq(c, h + 1)) waitq |= 1u << (4 * kq(c, h) + h);
+                        relq |= 1u << (4 * qrb(c, h) + h);
                     }
-                    if (kb == k0) {  // a tile starts: its accumulator must be drained
-                        d = t & 1u;
-                        if (t >= 2 && !(A.dbg & 64))
-                            mb_wait_cl(b_acce + 8 * d, ((t >> 1) - 1) & 1);
-                        YT(w_e);
-                        fence_after();
-                        dcol = tmem + kYAcc0 + d * 128;
-                    }
-                    if (w.tt == 0 && !(A.dbg & 64)) {
-                        // first use of this phase's A: a quarter must be in TMEM
-                        // before its first block's MMAs (earlier blocks need not
-                        // wait for it)
-                        uint32_t wq = (waitq >> (4 * kb)) & 15u;
-                        if (wq) {
-                            for (; wq; wq &= wq - 1)
-                                mb_wait_cl(b_ard + 8 * (__ffs(wq) - 1), w.phase & 1u);
+                    for (int pl = 0; pl < A.P; ++pl)
+                        for (int it = 0; it < T; ++it, ++t) {
+                            const int d = t & 1, k0 = klo(c, it);
+                            const bool first = (pl | it) == 0;
+                            if (t >= 2 && !(A.dbg & 64))
+                                mb_wait_cl(b_acce + 8 * d, ((t >> 1) - 1) & 1);
+                            YT(w_e);
                             fence_after();
-                        }
-                        YT(w_a);
-                    }
-                    if (!(A.dbg & 2)) {
-                        const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
+                            const uint32_t dcol = tmem + kYAcc0 + d * 128;
+                            // the blocks this tile is the last user of (tri: its
+                            // first, block it - 8c; full W: the last tile, all)
+                            const int r0 = tri ? it - c * kYChunkKB : 0;
+                            const int r1 = tri ? r0 + 1 : (it == T - 1 ? nb : 0);
+                            for (int kb0 = k0; kb0 < nb; kb0 += KBS) {
+                                const int nk = nb - kb0 < KBS ? nb - kb0 : KBS;
+                                if (!(A.dbg & 16)) mb_wait(b_full + 8 * s, ph);
+                                YT(w_f);
+                                fence_after();
+                                const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
+                                for (int kk = 0; kk < nk; ++kk) {
+                                    const int kb = kb0 + kk;
+                                    if (first && !(A.dbg & 64)) {
+                                        // first use of this phase's A: a quarter must be
+                                        // in TMEM before its first block's MMAs
+                                        uint32_t wq = (waitq >> (4 * kb)) & 15u;
+                                        if (wq) {
+                                            for (; wq; wq &= wq - 1)
+                                                mb_wait_cl(b_ard + 8 * (__ffs(wq) - 1), phase & 1u);
+                                            fence_after();
+                                        }
+                                        YT(w_a);
+                                    }
+                                    if (A.dbg & 2) continue;
+                                    const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns
-                            mma_ts(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks, A.idesc,
-                                   (kb != k0) | (ks != 0));
-                    }
-                    // last use of block kb (tri: tile 8c + kb; full W: the last
-                    // tile) frees the A quarters it ends
-                    if (pl == A.P - 1 && klast(c, kb) == it)
-                        for (uint32_t m = (relq >> (4 * kb)) & 15u; m; m &= m - 1)
-                            commit_pair(b_kbf + 8 * (__ffs(m) - 1));
-                    if (kb == nkb(c) - 1) {  // the tile's accumulator is complete
-                        commit_pair(b_accf + 8 * d);
-                        ++t;
-                    }
-                    walk_next(w);
+                                    for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns
+                                        mma_ts_w(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks,
+                                               A.idesc, (kb != k0) | (ks != 0));
+                                }
+                                commit_pair_w(b_empty + 8 * s);
+                                if (pl == A.P - 1)  // last use of A quarters: free them
+                                    for (int rb = r0 > kb0 ? r0 : kb0; rb < r1 && rb < kb0 + nk; ++rb)
+                                        for (uint32_t m = (relq >> (4 * rb)) & 15u; m; m &= m - 1)
+                                            commit_pair_w(b_kbf + 8 * (__ffs(m) - 1));
+                                if (++s == (uint32_t)NS) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                }
+                                YT(w_i);
+                            }
+                            commit_pair_w(b_accf + 8 * d);
+                        }
                 }
-                commit_pair(b_empty + 8 * s);
-                if (++s == (uint32_t)NS) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-                YT(w_i);
             }
-            if (timed) {
+            if (timed && lane == 0) {
                 atomicAdd(A.timing + 0, w_a);
                 atomicAdd(A.timing + 1, w_e);
                 atomicAdd(A.timing + 2, w_f);
@@ -469,6 +465,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         uint32_t t = 0;
         const bool timed = A.timing != nullptr && tid == kYEpiWarp0 * 32;
         unsigned long long e_st = 0, e_gen = 0, e_wait = 0, e_cmp = 0, e_red = 0, e_ld = 0;
+        unsigned long long e_sync = 0, e_tload = 0, e_fold = 0, e_kbf = 0;
         long long c0 = timed ? clock64() : 0;
 #define ET(acc_)                                    \
     do {                                            \
@@ -653,8 +650,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             if (CSM && j + 1 < nslots) {
                 stage(j + 1);  // the next unit's cluster rows, under this unit's MMAs
-                epi_sync();    // ... complete before any warp generates from them
                 ET(e_st);
+                epi_sync();    // ... complete before any warp generates from them
+                ET(e_sync);
             }
             const uint32_t* tbp = A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps + l;
             double s_acc = 0.0;  // this thread's share of S_T over the chunks
@@ -670,6 +668,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 // different quarter boundaries.  tri: quarter h is free after
                 // tile 8c + its last block, early in the phase
                 int hq = -1, tt_gen = NT - 1;
+                bool gen_done = false;
                 if (!last_phase) {
                     const int cn = c + 1 < NC ? c + 1 : 0;
                     const int X = kq(cn, sub + 1);
@@ -687,15 +686,23 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 for (int tt = 0; tt < NT; ++tt, ++t) {
                     const int d = t & 1;
                     const int pl = tt / T, it = tt - pl * T;
-                    if (!last_phase && tt == tt_gen) {
+                    // generate as soon as the quarter is free: the MMA issuer
+                    // runs up to two tiles ahead, so poll from two tiles before
+                    // the releasing one (the next phase's first MMAs wait on it)
+                    if (!last_phase && !gen_done && tt >= tt_gen - 2 &&
+                        (tt == tt_gen ||
+                         (hq >= 0 && __shfl_sync(0xffffffffu,
+                                                 (int)mb_try(b_kbf + 8 * hq, phase & 1u), 0)))) {
                         if (hq >= 0) {
                             mb_wait(b_kbf + 8 * hq, phase & 1u);
                             fence_after();
                         }
+                        ET(e_kbf);
                         if (c + 1 < NC)
                             gen(j, c + 1);
                         else
                             gen(j + 1, 0);
+                        gen_done = true;
                         ET(e_gen);
                     }
                     // cluster ids of the 32 columns i = it*128 + sub*32 + k
@@ -760,7 +767,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     lgs[2 * (warp - kYEpiWarp0)] = __ldg(A.legs + 2 * b);
                     lgs[2 * (warp - kYEpiWarp0) + 1] = __ldg(A.legs + 2 * b + 1);
                 }
+                ET(e_tload);
                 epi_sync();  // every bin of the chunk is complete
+                ET(e_sync);
                 if (live && EX && c + 1 == NC) {
                     // the bins (every K chunk accumulated, planes weighted
                     // 256^pl) ARE the reference's inter-cluster flows, exact
@@ -820,8 +829,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                 }
                 if (c + 1 == NC && !EX) red[sub * 128 + r] = s_acc;
+                ET(e_fold);
                 epi_sync();  // bins zeroed before the next chunk's atomics (red / prod written)
-                ET(e_st);
+                ET(e_sync);
             }
             pend_j = j;
             ET(e_red);
@@ -839,6 +849,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             atomicAdd(A.timing + 19, e_cmp);
             atomicAdd(A.timing + 20, e_red);
             atomicAdd(A.timing + 21, e_ld);
+            atomicAdd(A.timing + 22, e_sync);
+            atomicAdd(A.timing + 23, e_tload);
+            atomicAdd(A.timing + 24, e_fold);
+            atomicAdd(A.timing + 25, e_kbf);
         }
     }
     fence_before();
@@ -943,16 +957,8 @@ int prepare_fitness_tcp(int p, int npad, int P) {
     return HG_OK;
 }
 
-int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
-                       const uint8_t* cl, const uint32_t* T, double* part, int grid,
-                       cudaStream_t s, const double* legs, double* out) {
-    if (B <= 0) return HG_OK;
-    PArgs A;
-    A.cl = cl;
-    A.T = T;
-    A.part = part;
-    A.legs = legs;
-    A.out = out;
+// the launch geometry and arguments (shared by the launch and the work count)
+static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArgs& A) {
     A.chi = I.chi;
     A.alpha = I.alpha;
     A.delta = I.delta;
@@ -975,7 +981,7 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri,
               p_exact(I.p, I.npad, I.wplanes) && I.pwl != nullptr;
     // the triangular fold of W (half the MMA work) whenever the bins need not
     // be the reference's own flows: symmetric costs, fixed-order sums
-    A.tri = !A.exact && wmap_tri != nullptr && !(getenv("HUBGPU_TCP_NOTRI")) ? 1 : 0;
+    A.tri = !A.exact && tri_avail && !(getenv("HUBGPU_TCP_NOTRI")) ? 1 : 0;
     A.P = A.tri ? I.wplanes_tri : I.wplanes;
     A.stages = p_stages(I.p, I.npad, A.P, A.exact);  // as tcp_smem_bytes
     A.kbs = p_kbs(I.p, I.npad, A.P, A.exact);
@@ -994,6 +1000,44 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri,
     const int64_t need = round_up(A.units, kYCluster);
     if (g > need) g = (int)need;
     if (g < kYCluster) g = kYCluster;
+    return g;
+}
+
+// int8 operations the tensor cores execute for one launch on B hub sets:
+// every (pair slot, chunk, plane, output tile) runs its K blocks as M=256 x
+// N=128 x K=128 MMAs (dummy slots of an odd unit count included)
+double tcp_mma_ops(const DevInst& I, bool tri_avail, int64_t B, int grid) {
+    if (B <= 0) return 0.0;
+    PArgs A;
+    const int g = tcp_setup(I, tri_avail, B, grid, A);
+    double blocks = 0.0;  // K blocks per pair slot
+    for (int c = 0; c < A.NC; ++c) {
+        const int nb = A.KBT - c * kYChunkKB < kYChunkKB ? A.KBT - c * kYChunkKB : kYChunkKB;
+        const int T = A.tri && c * kYChunkKB + nb < A.ITO ? c * kYChunkKB + nb : A.ITO;
+        for (int it = 0; it < T; ++it)
+            blocks += nb - (A.tri && it > c * kYChunkKB ? it - c * kYChunkKB : 0);
+    }
+    blocks *= A.P;
+    const int64_t ncl = g / kYCluster;
+    double slots = 0.0;
+    for (int64_t cid = 0; cid < ncl; ++cid) {
+        const int64_t u = A.units * (cid + 1) / ncl - A.units * cid / ncl;
+        slots += (double)((u + kYCluster - 1) / kYCluster);
+    }
+    return slots * blocks * 2.0 * 256.0 * 128.0 * 128.0;
+}
+
+int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
+                       const uint8_t* cl, const uint32_t* T, double* part, int grid,
+                       cudaStream_t s, const double* legs, double* out) {
+    if (B <= 0) return HG_OK;
+    PArgs A;
+    A.cl = cl;
+    A.T = T;
+    A.part = part;
+    A.legs = legs;
+    A.out = out;
+    const int g = tcp_setup(I, wmap_tri != nullptr, B, grid, A);
     CUtensorMap map = *static_cast<const CUtensorMap*>(A.tri ? wmap_tri : wmap);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g);

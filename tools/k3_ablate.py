@@ -50,10 +50,11 @@ def one(n: int, p: int, B: int) -> dict:
         d.synchronize()
         _lib.check(_lib.load().hg_debug_tc_timing(buf.ctypes.data_as(_lib._u64p)))
         m = buf[0:4].astype(float)
-        e = buf[16:22].astype(float)
+        e = buf[16:26].astype(float)
         out["mma_warp_pct"] = dict(zip(["waitA", "waitAccEmpty", "waitW", "issue"],
                                        (100 * m / max(m.sum(), 1)).round(1).tolist()))
-        out["epi_warp_pct"] = dict(zip(["stage", "gen", "waitAcc", "bins", "reduce", "tmemld"],
+        out["epi_warp_pct"] = dict(zip(["stage", "gen", "waitAcc", "bins", "reduce", "tmemld",
+                                        "sync", "tload", "fold", "kbfwait"],
                                        (100 * e / max(e.sum(), 1)).round(1).tolist()))
     return out
 
@@ -61,14 +62,20 @@ def one(n: int, p: int, B: int) -> dict:
 CONFIGS = [
     ("default (tri)", {}),
     ("full W", {"HUBGPU_TCP_NOTRI": "1"}),
-    ("tri, no atomics", {"HUBGPU_TCP_DBG": "1"}),
-    ("tri, no fold/reduce", {"HUBGPU_TCP_DBG": "4"}),
-    ("tri, no gen", {"HUBGPU_TCP_DBG": "8"}),
-    ("tri, no atomics/fold/gen", {"HUBGPU_TCP_DBG": "13"}),
     ("tri, no epilogue warps", {"HUBGPU_TCP_DBG": "64"}),
+    ("tri, no epilogue warps, no MMA", {"HUBGPU_TCP_DBG": "66"}),
     ("tri, no MMA", {"HUBGPU_TCP_DBG": "2"}),
+    ("epilogue alone (no MMA, no W wait)", {"HUBGPU_TCP_DBG": "18"}),
+    ("epilogue alone, no atomics", {"HUBGPU_TCP_DBG": "19"}),
+    ("epilogue alone, no fold/reduce", {"HUBGPU_TCP_DBG": "22"}),
+    ("epilogue alone, no gen", {"HUBGPU_TCP_DBG": "26"}),
+    ("epilogue alone, tile drain only", {"HUBGPU_TCP_DBG": "31"}),
+    ("epilogue alone, timing", {"HUBGPU_TCP_DBG": "18", "HUBGPU_TC_TIMING": "1"}),
+    ("MMA alone (no epilogue, no W wait)", {"HUBGPU_TCP_DBG": "80"}),
+    ("MMA issue alone (no epilogue, no W stream)", {"HUBGPU_TCP_DBG": "112"}),
+    ("MMA issue alone, full W", {"HUBGPU_TCP_DBG": "112", "HUBGPU_TCP_NOTRI": "1"}),
+    ("epilogue + MMA, no W stream", {"HUBGPU_TCP_DBG": "48"}),
     ("tri, timing", {"HUBGPU_TC_TIMING": "1"}),
-    ("full W, timing", {"HUBGPU_TC_TIMING": "1", "HUBGPU_TCP_NOTRI": "1"}),
 ]
 
 
