@@ -55,6 +55,9 @@ __device__ __forceinline__ void mb_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ bool mb_try(uint32_t bar, uint32_t parity) {  // non-blocking
     uint32_t ok;
     asm volatile(
@@ -200,6 +203,9 @@ __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
 __host__ __device__ inline size_t p_C_bytes(int ipt, int npad) {
     return ((size_t)ipt * npad + 15) & ~size_t(15);
 }
+__host__ __device__ inline size_t p_T_bytes(int ipt, int p, int ps) {
+    return (size_t)ipt * 2 * p * ps * 4;  // ps is a multiple of 4: 16-byte rows
+}
 
 struct PArgs {
     const uint8_t* cl;
@@ -224,6 +230,7 @@ struct PArgs {
     // tile I runs K blocks J >= I only (see k_fitness_tcp's header)
     int tri;
     int csm;          // 1: a unit's cluster rows are staged in shared memory (they fit)
+    int tsm;          // 1: a unit's hub-cost tables T are copied to shared memory (cp.async)
     uint32_t idesc;   // kind::i8, M=256, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
     // ablation flags (tuning only, wrong results): 1 = no bin atomics, 2 = no
@@ -262,10 +269,12 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     var += (size_t)A.P * p * 512;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
-    // the finaliser's leg sums of each epilogue warp's first individual,
-    // fetched before the last chunk pass, used by the deferred reduce
-    double* lgs = reinterpret_cast<double*>(var);  // [16 warps][2]
-    var += (kYWarps - kYEpiWarp0) * 2 * 8;
+    // the unit's spoke-leg sums (finaliser), by slot parity: [2][ipt][2]
+    double* sL = reinterpret_cast<double*>(var);
+    var += 2 * kYMaxIpt * 2 * 8;
+    // the unit's hub-cost tables T (tsm): [ipt][2][p][ps] u32, as in global memory
+    uint32_t* sT = reinterpret_cast<uint32_t*>(var);
+    var += A.tsm ? p_T_bytes(ipt, p, A.ps) : 0;
     double* prod = reinterpret_cast<double*>(var);  // exact: [p][128] rounded terms of S_T
     var += EX ? (size_t)p * 128 * 8 : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
@@ -495,6 +504,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             const uint4* crow =
                 reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
+#pragma unroll 2
             for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32 && !(A.dbg & 8); c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
@@ -541,8 +551,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         // a unit's S_T reduce and finaliser, run during the next unit's first
         // tile (the MMA keeps its two accumulators busy meanwhile; red and prod
         // are rewritten only after the next chunk-pass barrier)
-        auto reduce_unit = [&](const int64_t bbase_u, const int nind_u) {
-                const double* lgw = lgs + 2 * (warp - kYEpiWarp0);
+        auto reduce_unit = [&](const int64_t bbase_u, const int nind_u, const int64_t j_u) {
+                const double* lgw = sL + (j_u & 1) * kYMaxIpt * 2;
                 if (EX) {
                     // S_T = np.sum(inter * hub_dist) in numpy's pairwise order
                     // (hm/evaluation.py:117-118) over the terms in `prod`: one warp
@@ -592,9 +602,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             const double st = stk[0];
                             if (A.out) {
                                 const int64_t b = bbase_u + b2;
-                                const bool pre = b2 == warp - kYEpiWarp0;
-                                const double coll = A.chi * (pre ? lgw[0] : A.legs[2 * b]);
-                                const double dist = A.delta * (pre ? lgw[1] : A.legs[2 * b + 1]);
+                                const double coll = A.chi * lgw[2 * b2];
+                                const double dist = A.delta * lgw[2 * b2 + 1];
                                 const double tran = A.alpha * st;
                                 A.out[4 * b + 0] = coll;
                                 A.out[4 * b + 1] = tran;
@@ -623,9 +632,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         if (A.out) {
                             // the finaliser (k_finalize), fused: same operations
                             const int64_t b = bbase_u + b2;
-                            const bool pre = b2 == warp - kYEpiWarp0;
-                            const double coll = A.chi * (pre ? lgw[0] : A.legs[2 * b]);
-                            const double dist = A.delta * (pre ? lgw[1] : A.legs[2 * b + 1]);
+                            const double coll = A.chi * lgw[2 * b2];
+                            const double dist = A.delta * lgw[2 * b2 + 1];
                             const double tran = A.alpha * acc;
                             A.out[4 * b + 0] = coll;
                             A.out[4 * b + 1] = tran;
@@ -654,7 +662,25 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 epi_sync();    // ... complete before any warp generates from them
                 ET(e_sync);
             }
-            const uint32_t* tbp = A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps + l;
+            // this unit's T tables and leg sums into shared memory, asynchronously:
+            // read by the fold at the unit's end (after a barrier) and by its
+            // deferred reduce; the previous unit's fold finished with them
+            {
+                const int etid = tid - kYEpiWarp0 * 32;
+                if (A.tsm) {
+                    const char* src = reinterpret_cast<const char*>(A.T + bbase * 2 * p * (int64_t)A.ps);
+                    const int chunks = nind * 2 * p * A.ps / 4;
+                    for (int x = etid; x < chunks; x += kYEpiThreads)
+                        cp_async16(su32(sT) + 16u * x, src + 16 * (int64_t)x);
+                }
+                if (A.out && etid < nind)
+                    cp_async16(su32(sL + (j & 1) * kYMaxIpt * 2 + 2 * etid),
+                               A.legs + 2 * (bbase + etid));
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+            const uint32_t* tbp =
+                (A.tsm ? sT + (live ? bl : 0) * 2 * p * A.ps
+                       : A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps) + l;
             double s_acc = 0.0;  // this thread's share of S_T over the chunks
             for (int c = 0; c < NC; ++c, ++phase) {
                 const bool last_phase = j + 1 == nslots && c + 1 == NC;
@@ -743,7 +769,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         int64_t pb;
                         int pn;
                         slot_unit(pend_j, pb, pn);
-                        reduce_unit(pb, pn);
+                        reduce_unit(pb, pn, pend_j);
                         pend_j = -1;
                         ET(e_red);
                     }
@@ -752,21 +778,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 // k = sub, sub + 4, ... (fixed order -> deterministic); one chunk's
                 // bins stay below 2^32 (<= 255 * 1024 * n, n <= 16384).  The first
                 // 8 T values are fetched before the barrier.
-                uint32_t th[8], tl[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int k = sub + 4 * u;
-                    const bool ok = live && k < p;
-                    th[u] = ok ? __ldg(tbp + k * A.ps) : 0u;
-                    tl[u] = ok ? __ldg(tbp + (p + k) * A.ps) : 0u;
-                }
-                if (c + 1 == NC && A.out && lane == 0 && warp - kYEpiWarp0 < nind) {
-                    // the finaliser's leg sums, fetched now: their L2 latency
-                    // hides under the barrier instead of the reduce
-                    const int64_t b = bbase + (warp - kYEpiWarp0);
-                    lgs[2 * (warp - kYEpiWarp0)] = __ldg(A.legs + 2 * b);
-                    lgs[2 * (warp - kYEpiWarp0) + 1] = __ldg(A.legs + 2 * b + 1);
-                }
+                asm volatile("cp.async.wait_all;" ::: "memory");  // T, legs: this thread's part
+                auto tval = [&](int k) {
+                    return __hiloint2double((int)tbp[k * A.ps], (int)tbp[(p + k) * A.ps]);
+                };
                 ET(e_tload);
                 epi_sync();  // every bin of the chunk is complete
                 ET(e_sync);
@@ -791,40 +806,18 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         return (double)g;
                     };
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int k = sub + 4 * u;
-                        if (k < p)
-                            prod[k * 128 + r] =
-                                __dmul_rn(inter(k), __hiloint2double((int)th[u], (int)tl[u]));
-                    }
-                    for (int k = sub + 32; k < p; k += 4)
-                        prod[k * 128 + r] = __dmul_rn(
-                            inter(k), __hiloint2double((int)__ldg(tbp + k * A.ps),
-                                                       (int)__ldg(tbp + (p + k) * A.ps)));
+                    for (int k = sub; k < p; k += 4) prod[k * 128 + r] = __dmul_rn(inter(k), tval(k));
                 }
                 if (live && !EX && !(A.dbg & 4)) {
                     // plane pl of W carries weight 256^pl: an exact power-of-2
                     // scaling of T, so each product is the one-plane product
                     for (int pl = 0; pl < A.P; ++pl) {
                         uint32_t* bp = binsj + (size_t)pl * p * 128;
-                        const double sc = ldexp(1.0, 8 * pl);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int k = sub + 4 * u;
-                            if (k < p) {
-                                const uint32_t g = bp[k * 128 + r];
-                                bp[k * 128 + r] = 0u;
-                                s_acc = fma((double)g,
-                                            __hiloint2double((int)th[u], (int)tl[u]) * sc, s_acc);
-                            }
-                        }
-                        for (int k = sub + 32; k < p; k += 4) {
+                        const double sc = __longlong_as_double((long long)(1023 + 8 * pl) << 52);
+                        for (int k = sub; k < p; k += 4) {
                             const uint32_t g = bp[k * 128 + r];
                             bp[k * 128 + r] = 0u;
-                            s_acc = fma((double)g,
-                                        __hiloint2double((int)__ldg(tbp + k * A.ps),
-                                                         (int)__ldg(tbp + (p + k) * A.ps)) * sc,
-                                        s_acc);
+                            s_acc = fma((double)g, tval(k) * sc, s_acc);
                         }
                     }
                 }
@@ -840,7 +833,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             int64_t pb;
             int pn;
             slot_unit(pend_j, pb, pn);
-            reduce_unit(pb, pn);
+            reduce_unit(pb, pn, pend_j);
         }
         if (timed) {
             atomicAdd(A.timing + 16, e_st);
@@ -883,10 +876,25 @@ static bool p_csm(int p, int npad) {
 }
 
 // everything but the W ring; exact: the [p][128] fp64 terms of S_T
-static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false) {
+static size_t p_base_bytes(int p, int npad, int P, bool exact) {
     return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) + (size_t)P * p * 512 +
-           4 * 128 * 8 + (kYWarps - kYEpiWarp0) * 2 * 8 + (exact ? (size_t)p * 1024 : 0) +
+           4 * 128 * 8 + 2 * kYMaxIpt * 2 * 8 + (exact ? (size_t)p * 1024 : 0) +
            (2 * kYMaxStages + 12) * 8 + 16;
+}
+
+// the unit's T tables in shared memory when they leave room for two full W
+// stages (p <= ~36 at n <= 1024)
+static bool p_tsm(int p, int npad, int P, bool exact) {
+    const char* e = getenv("HUBGPU_TCP_TSM");  // tuning override: 0 disables
+    if (e && atoi(e) == 0) return false;
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_base_bytes(p, npad, P, exact) -
+                         (int64_t)p_T_bytes(p_ipt(p), p, (p + 3) & ~3);
+    return room >= 2 * 8 * (int64_t)kYStageBytes;
+}
+
+static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false) {
+    return p_base_bytes(p, npad, P, exact) +
+           (p_tsm(p, npad, P, exact) ? p_T_bytes(p_ipt(p), p, (p + 3) & ~3) : 0);
 }
 
 // K blocks per W stage: 8 (one MMA-issuer loop per 1024 K) unless that
@@ -986,6 +994,7 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     A.stages = p_stages(I.p, I.npad, A.P, A.exact);  // as tcp_smem_bytes
     A.kbs = p_kbs(I.p, I.npad, A.P, A.exact);
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;
+    A.tsm = p_tsm(I.p, I.npad, A.P, A.exact) ? 1 : 0;
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
     A.timing = tc_timing_buffer();
     {

@@ -61,21 +61,11 @@ def one(n: int, p: int, B: int) -> dict:
 
 CONFIGS = [
     ("default (tri)", {}),
-    ("full W", {"HUBGPU_TCP_NOTRI": "1"}),
-    ("tri, no epilogue warps", {"HUBGPU_TCP_DBG": "64"}),
-    ("tri, no epilogue warps, no MMA", {"HUBGPU_TCP_DBG": "66"}),
-    ("tri, no MMA", {"HUBGPU_TCP_DBG": "2"}),
-    ("epilogue alone (no MMA, no W wait)", {"HUBGPU_TCP_DBG": "18"}),
-    ("epilogue alone, no atomics", {"HUBGPU_TCP_DBG": "19"}),
-    ("epilogue alone, no fold/reduce", {"HUBGPU_TCP_DBG": "22"}),
-    ("epilogue alone, no gen", {"HUBGPU_TCP_DBG": "26"}),
-    ("epilogue alone, tile drain only", {"HUBGPU_TCP_DBG": "31"}),
-    ("epilogue alone, timing", {"HUBGPU_TCP_DBG": "18", "HUBGPU_TC_TIMING": "1"}),
-    ("MMA alone (no epilogue, no W wait)", {"HUBGPU_TCP_DBG": "80"}),
-    ("MMA issue alone (no epilogue, no W stream)", {"HUBGPU_TCP_DBG": "112"}),
-    ("MMA issue alone, full W", {"HUBGPU_TCP_DBG": "112", "HUBGPU_TCP_NOTRI": "1"}),
-    ("epilogue + MMA, no W stream", {"HUBGPU_TCP_DBG": "48"}),
+    ("tri, T from global", {"HUBGPU_TCP_TSM": "0"}),
     ("tri, timing", {"HUBGPU_TC_TIMING": "1"}),
+    ("epilogue alone (no MMA, no W wait)", {"HUBGPU_TCP_DBG": "18"}),
+    ("epilogue alone, timing", {"HUBGPU_TCP_DBG": "18", "HUBGPU_TC_TIMING": "1"}),
+    ("full W", {"HUBGPU_TCP_NOTRI": "1"}),
 ]
 
 
