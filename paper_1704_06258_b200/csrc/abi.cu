@@ -486,28 +486,48 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         if (rc) break;
         rc = prepare_allocate(I);
         if (rc) break;
-        // K3-TC eligibility: every flow a non-negative integer below 2^32 ->
-        // exact u8 GEMMs on P byte planes of W (P = 1 when every flow < 256),
-        // and for symmetric costs on the triangular fold of W (its own planes)
-        const bool intw = scan.int_flows && p >= 1 && p <= 128;
+        // K3-TC eligibility.  Integer flows below 2^32: exact u8 GEMMs on P
+        // byte planes of W (P = 1 when every flow < 256).  Other flows: the
+        // planes of Q = rint(W / q), q a power of two small enough that every
+        // nonzero flow keeps 2^-41 relative precision (each term W_ij * T of
+        // the non-negative transfer sum then within 2^-41, so the sum too),
+        // when that takes at most 8 planes.  Symmetric costs: also the planes
+        // of the triangular fold of Q.
+        const bool intw = scan.int_flows != 0;
         const double wmax = from_bits(scan.wmax_bits), mmax = from_bits(scan.mmax_bits);
+        const double wmin = scan.wmin_bits == ~0ull ? wmax : from_bits(scan.wmin_bits);
         // every byte plane's total below 2^32: u32 bins may accumulate over
         // all K chunks (the exact transfer sum for n > 1024)
         I.bins_total_ok = intw && scan.wsum < 4294967296.0 ? 1 : 0;
+        I.int_flows = intw ? 1 : 0;
         int P = 1, Pt = 1;
-        while (P < 4 && wmax >= std::ldexp(1.0, 8 * P)) ++P;
-        while (Pt < 5 && mmax >= std::ldexp(1.0, 8 * Pt)) ++Pt;
+        double qscale = 1.0;
+        bool planes_ok = p >= 1 && p <= 128 && wmax > 0.0;
+        if (intw) {
+            while (P < 4 && wmax >= std::ldexp(1.0, 8 * P)) ++P;
+        } else if (planes_ok) {
+            const int E = std::ilogb(wmax) + 1;                       // wmax < 2^E
+            const double range = std::log2(wmax / wmin);
+            P = (int)std::ceil((range + 42.0) / 8.0);
+            if (P < 1) P = 1;
+            planes_ok = P <= 8;
+            qscale = std::ldexp(1.0, E - 8 * P);                    // max Q < 2^(8P)
+        }
+        const double mq = mmax / qscale + 2.0;  // bound on the fold's quantised entries
+        while (Pt < 9 && mq >= std::ldexp(1.0, 8 * Pt)) ++Pt;
         I.wplanes = P;
-        const bool tri = sym && Pt <= 4 && !getenv("HUBGPU_TCP_NOTRI");
+        I.wscale = qscale;
+        const bool tri = sym && Pt <= 8 && !getenv("HUBGPU_TCP_NOTRI");
         I.wplanes_tri = tri ? Pt : 0;
-        if (intw && tcp_supported(n, p, I.npad, P) && (!tri || tcp_supported(n, p, I.npad, Pt))) {
+        if (planes_ok && tcp_supported(n, p, I.npad, P) &&
+            (!tri || tcp_supported(n, p, I.npad, Pt))) {
             const int nt = (int)round_up(n, 128);
             const size_t plane = (size_t)nt * nt;
             chk(cudaMalloc(&inst->dW8, plane * P), "cudaMalloc(W8)");
             if (tri) chk(cudaMalloc(&inst->dM8, plane * Pt), "cudaMalloc(M8)");
             if (rc) break;
-            rc = launch_build_planes(inst->dW, n, nt, P, Pt, inst->dW8, tri ? inst->dM8 : nullptr,
-                                     s);
+            rc = launch_build_planes(inst->dW, n, nt, qscale, P, Pt, inst->dW8,
+                                     tri ? inst->dM8 : nullptr, s);
             if (rc) break;
             rc = tc_make_wmap(inst->dW8, nt, 64, inst->wmapp, P * nt);
             if (rc) break;
@@ -591,8 +611,8 @@ int hg_instance_set_fitness(hg_inst* inst, int kind) {
                kind == HG_FIT_TC_PAIR || kind == HG_FIT_TC_PAIR_FULL,
            "unknown fitness kernel %d", kind);
     HG_ARG(kind < HG_FIT_TENSOR || inst->tc_ok,
-           "tensor-core fitness needs non-negative integer flows below 2^32, p <= 128 and "
-           "n <= 16384");
+           "tensor-core fitness needs p <= 128, n <= 16384 and flows whose nonzero range "
+           "fits 8 byte planes at 2^-41 relative precision");
     inst->fit_kind = kind;
     return HG_OK;
 }

@@ -75,6 +75,8 @@ struct DevInst {
     int weights_exact;
     int wplanes;   // byte planes of the u8 flow tensor W8 (1 when every flow < 256)
     int wplanes_tri;  // byte planes of its triangular fold (W + W^T above the diagonal blocks)
+    int int_flows;    // every flow an integer below 2^32 (the planes hold W exactly)
+    double wscale;    // the planes hold Q = rint(W / wscale), wscale a power of two (1: integers)
     double chi, alpha, delta;
     const double* C;
     const double* Ct;
@@ -143,16 +145,17 @@ int launch_finalize(const DevInst& I, int tiles, int64_t B, const double* legs,
 struct InstanceScan {
     unsigned long long cmin_bits, cmax_bits;  // min / max cost (bit patterns, >= 0)
     unsigned long long wmax_bits, mmax_bits;  // max flow / max entry of the triangular fold
+    unsigned long long wmin_bits;             // smallest nonzero flow
     double wsum;                              // total flow
     int int_flows;                            // 1: every flow an integer in [0, 2^32)
     int symmetric;                            // 1: C == C^T exactly
 };
 int launch_scan_instance(const double* C, const double* W, int n, InstanceScan* out,
                          cudaStream_t s);
-// W8: P byte planes of W, M8 (optional): Ptri byte planes of the triangular
-// fold; both [planes][nt][nt] with nt = round_up(n, 128)
-int launch_build_planes(const double* W, int n, int nt, int P, int Ptri, uint8_t* W8,
-                        uint8_t* M8, cudaStream_t s);
+// W8: P byte planes of Q = rint(W / wscale), M8 (optional): Ptri byte planes of
+// Q's triangular fold; both [planes][nt][nt] with nt = round_up(n, 128)
+int launch_build_planes(const double* W, int n, int nt, double wscale, int P, int Ptri,
+                        uint8_t* W8, uint8_t* M8, cudaStream_t s);
 
 // ---- K3-TC/P helpers (tc_common.cu) ------------------------------------------
 int tc_timing_read(unsigned long long* out32);

@@ -231,6 +231,11 @@ struct PArgs {
     int tri;
     int csm;          // 1: a unit's cluster rows are staged in shared memory (they fit)
     int tsm;          // 1: a unit's hub-cost tables T are copied to shared memory (cp.async)
+    // pfold: planes > 4 (fractional flows): the bins hold one plane and each
+    // plane is folded into S_T after its last tile; wscale: the flows' common
+    // power-of-two quantum (1 for integer flows) -- plane pl weighs 256^pl * wscale
+    int pfold;
+    double wscale;
     uint32_t idesc;   // kind::i8, M=256, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
     // ablation flags (tuning only, wrong results): 1 = no bin atomics, 2 = no
@@ -265,8 +270,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     const size_t cb = CSM ? p_C_bytes(ipt, A.npad) : 0;
     unsigned char* sC0 = var;
     var += 2 * cb;
-    uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [P][p][128] cluster-pair flow bins
-    var += (size_t)A.P * p * 512;
+    const int PB = A.pfold ? 1 : A.P;  // planes of bins
+    uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [PB][p][128] cluster-pair flow bins
+    var += (size_t)PB * p * 512;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
     var += 4 * 128 * 8;
     // the unit's spoke-leg sums (finaliser), by slot parity: [2][ipt][2]
@@ -303,7 +309,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int x = tid; x < A.P * p * 128; x += kYThreads) bins[x] = 0u;
+    for (int x = tid; x < PB * p * 128; x += kYThreads) bins[x] = 0u;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mb_init(b_full + 8 * s, 1);
@@ -504,7 +510,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             const uint4* crow =
                 reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
-#pragma unroll 2
+#pragma unroll 1
             for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32 && !(A.dbg & 8); c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
@@ -682,6 +688,18 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 (A.tsm ? sT + (live ? bl : 0) * 2 * p * A.ps
                        : A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps) + l;
             double s_acc = 0.0;  // this thread's share of S_T over the chunks
+            // plane pl of the flows carries weight 256^pl * wscale (an exact power
+            // of two): each product is the one-plane product, scaled exactly
+            auto fold_plane = [&](int pl, uint32_t* bp) {
+                const double sc = A.wscale * __longlong_as_double((long long)(1023 + 8 * pl) << 52);
+                for (int k = sub; k < p; k += 4) {
+                    const uint32_t g = bp[k * 128 + r];
+                    bp[k * 128 + r] = 0u;
+                    s_acc = fma((double)g,
+                                __hiloint2double((int)tbp[k * A.ps], (int)tbp[(p + k) * A.ps]) * sc,
+                                s_acc);
+                }
+            };
             for (int c = 0; c < NC; ++c, ++phase) {
                 const bool last_phase = j + 1 == nslots && c + 1 == NC;
                 const int T = ntl(c), NT = A.P * T;
@@ -759,12 +777,20 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             const uint32_t cc = __byte_perm(cw[k >> 2], 0u, 0x4440u + (k & 3));
                             const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
                             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(
-                                             bin_r + (uint32_t)pl * (uint32_t)p * 512u + cc * 512u),
+                                             bin_r + (uint32_t)(A.pfold ? 0 : pl) * (uint32_t)p * 512u +
+                                                 cc * 512u),
                                          "r"(dv)
                                          : "memory");
                         }
                     }
                     ET(e_cmp);
+                    if (A.pfold && it == T - 1 && pl + 1 < A.P) {
+                        // plane pl complete: into S_T now, the bins serve the next plane
+                        asm volatile("cp.async.wait_all;" ::: "memory");
+                        epi_sync();
+                        if (live) fold_plane(pl, binsj);
+                        epi_sync();
+                    }
                     if (c == 0 && tt == 0 && pend_j >= 0 && !(A.dbg & 4)) {  // the previous unit's reduce
                         int64_t pb;
                         int pn;
@@ -809,17 +835,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     for (int k = sub; k < p; k += 4) prod[k * 128 + r] = __dmul_rn(inter(k), tval(k));
                 }
                 if (live && !EX && !(A.dbg & 4)) {
-                    // plane pl of W carries weight 256^pl: an exact power-of-2
-                    // scaling of T, so each product is the one-plane product
-                    for (int pl = 0; pl < A.P; ++pl) {
-                        uint32_t* bp = binsj + (size_t)pl * p * 128;
-                        const double sc = __longlong_as_double((long long)(1023 + 8 * pl) << 52);
-                        for (int k = sub; k < p; k += 4) {
-                            const uint32_t g = bp[k * 128 + r];
-                            bp[k * 128 + r] = 0u;
-                            s_acc = fma((double)g, tval(k) * sc, s_acc);
-                        }
-                    }
+                    // every plane (pfold: the last; the others were folded as
+                    // they completed)
+                    for (int pl = A.pfold ? A.P - 1 : 0; pl < A.P; ++pl)
+                        fold_plane(pl, binsj + (size_t)(A.pfold ? 0 : pl) * p * 128);
                 }
                 if (c + 1 == NC && !EX) red[sub * 128 + r] = s_acc;
                 ET(e_fold);
@@ -876,8 +895,12 @@ static bool p_csm(int p, int npad) {
 }
 
 // everything but the W ring; exact: the [p][128] fp64 terms of S_T
+// planes beyond 4 (fractional flows) are folded one at a time: one plane of bins
+static int p_bin_planes(int P) { return P > 4 ? 1 : P; }
+
 static size_t p_base_bytes(int p, int npad, int P, bool exact) {
-    return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) + (size_t)P * p * 512 +
+    return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) +
+           (size_t)p_bin_planes(P) * p * 512 +
            4 * 128 * 8 + 2 * kYMaxIpt * 2 * 8 + (exact ? (size_t)p * 1024 : 0) +
            (2 * kYMaxStages + 12) * 8 + 16;
 }
@@ -934,7 +957,7 @@ bool tcp_supported(int n, int p, int npad, int P) {
     // p <= 128: a unit's one-hot rows fit the 128 TMEM lanes; n <= 16384: a
     // chunk's u32 bins cannot overflow
     return p >= 1 && p <= 128 && n >= 1 && n <= 16384 && npad % 128 == 0 &&
-           P >= 1 && P <= 4 && p_stages(p, npad, P) >= 2;
+           P >= 1 && P <= 8 && p_stages(p, npad, P) >= 2;
 }
 
 static int g_tcp_pairs = 0;  // co-resident clusters (cudaOccupancyMaxActiveClusters)
@@ -985,7 +1008,7 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     // beside two W stages (else the fixed-order fold: tran within ~1 ulp)
     // (several K chunks or planes: the bins accumulate over all of them, exact
     // while the total flow stays below 2^32)
-    A.exact = I.exact && (A.NC == 1 && I.wplanes == 1 || I.bins_total_ok) &&
+    A.exact = I.exact && I.int_flows && (A.NC == 1 && I.wplanes == 1 || I.bins_total_ok) &&
               p_exact(I.p, I.npad, I.wplanes) && I.pwl != nullptr;
     // the triangular fold of W (half the MMA work) whenever the bins need not
     // be the reference's own flows: symmetric costs, fixed-order sums
@@ -995,6 +1018,8 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     A.kbs = p_kbs(I.p, I.npad, A.P, A.exact);
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;
     A.tsm = p_tsm(I.p, I.npad, A.P, A.exact) ? 1 : 0;
+    A.pfold = p_bin_planes(A.P) < A.P ? 1 : 0;
+    A.wscale = I.wscale;
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
     A.timing = tc_timing_buffer();
     {

@@ -37,7 +37,7 @@ __device__ __forceinline__ double fold_at(const double* __restrict__ W, int n, i
 
 __global__ void k_scan_instance(const double* __restrict__ C, const double* __restrict__ W, int n,
                                 InstanceScan* out) {
-    unsigned long long cmin = ~0ull, cmax = 0ull, wmax = 0ull, mmax = 0ull;
+    unsigned long long cmin = ~0ull, cmax = 0ull, wmax = 0ull, mmax = 0ull, wmin = ~0ull;
     int intw = 1, sym = 1;
     double wsum = 0.0;
     const int64_t total = (int64_t)n * n;
@@ -53,6 +53,7 @@ __global__ void k_scan_instance(const double* __restrict__ C, const double* __re
         if (!(w >= 0.0 && w < 4294967296.0 && w == floor(w))) intw = 0;
         const unsigned long long wb = pos_bits(w >= 0.0 ? w : 0.0);
         wmax = wb > wmax ? wb : wmax;
+        if (w > 0.0) wmin = wb < wmin ? wb : wmin;
         const double m = fold_at(W, n, i, j);
         const unsigned long long mb = pos_bits(m >= 0.0 ? m : 0.0);
         mmax = mb > mmax ? mb : mmax;
@@ -64,6 +65,7 @@ __global__ void k_scan_instance(const double* __restrict__ C, const double* __re
         cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
         wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+        wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
         wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
     }
     intw = __all_sync(0xffffffffu, intw);
@@ -73,6 +75,7 @@ __global__ void k_scan_instance(const double* __restrict__ C, const double* __re
         atomicMax(&out->cmax_bits, cmax);
         atomicMax(&out->wmax_bits, wmax);
         atomicMax(&out->mmax_bits, mmax);
+        atomicMin(&out->wmin_bits, wmin);
         if (!intw) atomicAnd(&out->int_flows, 0);
         if (!sym) atomicAnd(&out->symmetric, 0);
         // integer flows: every partial sum is an exact integer below 2^53 for
@@ -81,18 +84,28 @@ __global__ void k_scan_instance(const double* __restrict__ C, const double* __re
     }
 }
 
-// plane d of W8 / M8 = byte d of the (integer) flow, zero in the padding
-__global__ void k_build_planes(const double* __restrict__ W, int n, int nt, int P, int Ptri,
-                               uint8_t* __restrict__ W8, uint8_t* __restrict__ M8) {
+// the flow as an integer multiple of the quantum: rint(w / wscale), exact for
+// integer flows (wscale = 1); wscale is a power of two, so the division is exact
+__device__ __forceinline__ uint64_t quant(double w, double inv) {
+    return (uint64_t)rint(w * inv);
+}
+
+// plane d of W8 / M8 = byte d of Q (and of Q's triangular fold), zero in the padding
+__global__ void k_build_planes(const double* __restrict__ W, int n, int nt, double inv, int P,
+                               int Ptri, uint8_t* __restrict__ W8, uint8_t* __restrict__ M8) {
     const int64_t per = (int64_t)nt * nt;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < per;
          x += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(x / nt), j = (int)(x - (int64_t)i * nt);
         const bool in = i < n && j < n;
-        const uint64_t w = in ? (uint64_t)W[(size_t)i * n + j] : 0ull;
-        for (int d = 0; d < P; ++d) W8[d * per + x] = (uint8_t)(w >> (8 * d));
+        const uint64_t q = in ? quant(W[(size_t)i * n + j], inv) : 0ull;
+        for (int d = 0; d < P; ++d) W8[d * per + x] = (uint8_t)(q >> (8 * d));
         if (M8) {
-            const uint64_t m = in ? (uint64_t)fold_at(W, n, i, j) : 0ull;
+            uint64_t m = 0ull;
+            if (in) {
+                const int bi = i / kTriBlock, bj = j / kTriBlock;
+                m = bi == bj ? q : (bj > bi ? q + quant(W[(size_t)j * n + i], inv) : 0ull);
+            }
             for (int d = 0; d < Ptri; ++d) M8[d * per + x] = (uint8_t)(m >> (8 * d));
         }
     }
@@ -107,7 +120,7 @@ unsigned grid_of(int64_t work) {
 
 int launch_scan_instance(const double* C, const double* W, int n, InstanceScan* out,
                          cudaStream_t s) {
-    const InstanceScan init = {~0ull, 0ull, 0ull, 0ull, 0.0, 1, 1};
+    const InstanceScan init = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0.0, 1, 1};
     HG_CUDA(cudaMemcpyAsync(out, &init, sizeof(init), cudaMemcpyHostToDevice, s));
     k_scan_instance<<<grid_of((int64_t)n * n), 256, 0, s>>>(C, W, n, out);
     HG_LAUNCHED();
@@ -115,9 +128,10 @@ int launch_scan_instance(const double* C, const double* W, int n, InstanceScan* 
     return HG_OK;
 }
 
-int launch_build_planes(const double* W, int n, int nt, int P, int Ptri, uint8_t* W8,
-                        uint8_t* M8, cudaStream_t s) {
-    k_build_planes<<<grid_of((int64_t)nt * nt), 256, 0, s>>>(W, n, nt, P, Ptri, W8, M8);
+int launch_build_planes(const double* W, int n, int nt, double wscale, int P, int Ptri,
+                        uint8_t* W8, uint8_t* M8, cudaStream_t s) {
+    k_build_planes<<<grid_of((int64_t)nt * nt), 256, 0, s>>>(W, n, nt, 1.0 / wscale, P, Ptri, W8,
+                                                             M8);
     HG_LAUNCHED();
     return HG_OK;
 }

@@ -238,3 +238,70 @@ def test_islands_across_processes(world):
         assert _rel_ok(raw, g["ap_raw"][0])
         assert _rel_ok(trace, g["ap_trace"])
         assert evals == int(g["ap_evals"][0])
+
+
+class TestFractionalFlows:
+    """Non-integer flows on the tensor cores: Q = rint(W / q) on up to 8 byte
+    planes, q a power of two keeping every nonzero flow to 2^-41 relative, so
+    every cost term (and the non-negative transfer sum) is within 2^-41 of the
+    reference's -- the test bar stays 1e-12 relative."""
+
+    @staticmethod
+    def _instance(n, p, flows, symmetric=True, seed=3):
+        base = hg.generate_urand(n, p, seed, (3.0, 0.75, 2.0))
+        dist = base.dist
+        if not symmetric:
+            dist = dist.copy()
+            dist[np.triu_indices(n, 1)] *= 1.0 + 1e-3
+        return hg.Instance(n, p, dist, flows, 3.0, 0.75, 2.0)
+
+    @pytest.mark.parametrize("case", ["decimals", "wide", "asymmetric", "bigger"])
+    def test_tensor_path_matches_oracle(self, case):
+        rng = np.random.default_rng(11)
+        n, p = (1100, 12) if case == "bigger" else (300, 10)
+        if case == "wide":  # flows over six decades: the one-plane-at-a-time fold
+            flows = 10.0 ** rng.uniform(-3.0, 3.0, (n, n))
+        else:
+            flows = rng.integers(0, 100, (n, n)) * 0.37 + rng.random((n, n))
+        np.fill_diagonal(flows, 0.0)
+        inst = self._instance(n, p, flows, symmetric=case != "asymmetric")
+        d = inst.device()
+        assert d.flags & 4
+        assert d.fitness_kernel == ("tensor-pair-full" if case == "asymmetric" else "tensor-pair")
+        pop = hg.random_population(n, p, 200, key=5)
+        tc = hg.evaluate_population(inst, pop)
+        from paper_1704_06258_b200 import _lib
+
+        d.set_fitness(_lib.FIT_FP64)
+        try:
+            fp = hg.evaluate_population(inst, pop)
+        finally:
+            d.set_fitness(_lib.FIT_AUTO)
+        assert np.array_equal(tc[:, [0, 2]], fp[:, [0, 2]])
+        assert _rel_ok(tc, fp)
+        pr = orc.Problem(n, p, inst.dist, inst.flow, 3.0, 0.75, 2.0)
+        for b in range(0, 200, 23):
+            a = orc.nearest(pr.C, pop[b])
+            c, t, dd = orc.cost_terms(pr, pop[b], a)
+            assert _rel_ok(tc[b], [c, t, dd, c + t + dd]), b
+
+    def test_range_beyond_eight_planes_uses_fp64(self):
+        rng = np.random.default_rng(2)
+        flows = 10.0 ** rng.uniform(-9.0, 9.0, (200, 200))
+        np.fill_diagonal(flows, 0.0)
+        inst = self._instance(200, 8, flows)
+        assert inst.device().fitness_kernel == "fp64"
+        assert not inst.device().flags & 4
+
+    def test_ga_replays_on_fractional_flows(self):
+        rng = np.random.default_rng(4)
+        flows = rng.integers(0, 100, (200, 200)) * 0.5 + rng.random((200, 200))
+        np.fill_diagonal(flows, 0.0)
+        inst = self._instance(200, 10, flows)
+        assert inst.device().fitness_kernel == "tensor-pair"
+        pr = orc.Problem(200, 10, inst.dist, inst.flow, 3.0, 0.75, 2.0)
+        rep = hg.solve(inst, hg.GaParams(islands=4, pop_size=16, inner_iters=3, outer_iters=2),
+                       hg.FitnessMode.STANDARD_MILLI)
+        ref = orc.island_ga(pr, 4, 16, 3, 2, 0, None, False, "milli")
+        assert np.array_equal(rep.best_solution.hubs, ref.hubs)
+        assert _rel_ok(rep.raw_objective, ref.raw)
