@@ -140,7 +140,9 @@ int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     HG_CUDA(cudaMalloc(&P->co, (size_t)cap * I.npad * sizeof(uint16_t)));
     HG_CUDA(cudaMalloc(&P->T, (size_t)cap * 2 * I.p * I.ps * sizeof(uint32_t)));
     HG_CUDA(cudaMalloc(&P->legs, (size_t)cap * 2 * sizeof(double)));
-    const int tiles = inst->plan.tiles > tc_tiles(I.n) ? inst->plan.tiles : tc_tiles(I.n);
+    // per-individual partials: fp64 K3 tiles, or the byte planes of K3-TC/P (<= 8)
+    int tiles = inst->plan.tiles > tc_tiles(I.n) ? inst->plan.tiles : tc_tiles(I.n);
+    if (tiles < 8) tiles = 8;
     HG_CUDA(cudaMalloc(&P->part, (size_t)cap * tiles * sizeof(double)));
     HG_CUDA(cudaMalloc(&P->out, (size_t)cap * 4 * sizeof(double)));
     HG_CUDA(cudaEventCreate(&P->evk));
@@ -486,25 +488,33 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         if (rc) break;
         rc = prepare_allocate(I);
         if (rc) break;
-        // K3-TC eligibility.  Integer flows below 2^32: exact u8 GEMMs on P
-        // byte planes of W (P = 1 when every flow < 256).  Other flows: the
+        // K3-TC eligibility.  Integer flows below 2^32 (or such integers times
+        // a power of two): exact u8 GEMMs on P byte planes of W (P = 1 when
+        // every flow < 256).  Other flows: the
         // planes of Q = rint(W / q), q a power of two small enough that every
         // nonzero flow keeps 2^-41 relative precision (each term W_ij * T of
         // the non-negative transfer sum then within 2^-41, so the sum too),
         // when that takes at most 8 planes.  Symmetric costs: also the planes
         // of the triangular fold of Q.
-        const bool intw = scan.int_flows != 0;
         const double wmax = from_bits(scan.wmax_bits), mmax = from_bits(scan.mmax_bits);
         const double wmin = scan.wmin_bits == ~0ull ? wmax : from_bits(scan.wmin_bits);
-        // every byte plane's total below 2^32: u32 bins may accumulate over
-        // all K chunks (the exact transfer sum for n > 1024)
-        I.bins_total_ok = intw && scan.wsum < 4294967296.0 ? 1 : 0;
-        I.int_flows = intw ? 1 : 0;
+        // flows that are integer multiples of 2^e (e = the lowest set bit over
+        // all of them) below 2^32 * 2^e: exact integers Q = W / 2^e
         int P = 1, Pt = 1;
         double qscale = 1.0;
+        bool intw = scan.int_flows != 0;
+        if (!intw && scan.lsb_exp < 0 && wmax > 0.0 &&
+            wmax < std::ldexp(4294967296.0, scan.lsb_exp)) {
+            intw = true;
+            qscale = std::ldexp(1.0, scan.lsb_exp);
+        }
+        // every byte plane's total below 2^32: u32 bins may accumulate over
+        // all K chunks (the exact transfer sum for n > 1024)
+        I.bins_total_ok = intw && scan.wsum / qscale < 4294967296.0 ? 1 : 0;
+        I.int_flows = intw ? 1 : 0;
         bool planes_ok = p >= 1 && p <= 128 && wmax > 0.0;
         if (intw) {
-            while (P < 4 && wmax >= std::ldexp(1.0, 8 * P)) ++P;
+            while (P < 4 && wmax / qscale >= std::ldexp(1.0, 8 * P)) ++P;
         } else if (planes_ok) {
             const int E = std::ilogb(wmax) + 1;                       // wmax < 2^E
             const double range = std::log2(wmax / wmin);

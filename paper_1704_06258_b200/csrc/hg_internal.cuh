@@ -149,6 +149,7 @@ struct InstanceScan {
     double wsum;                              // total flow
     int int_flows;                            // 1: every flow an integer in [0, 2^32)
     int symmetric;                            // 1: C == C^T exactly
+    int lsb_exp;                              // min over nonzero flows of e in w = odd * 2^e
 };
 int launch_scan_instance(const double* C, const double* W, int n, InstanceScan* out,
                          cudaStream_t s);

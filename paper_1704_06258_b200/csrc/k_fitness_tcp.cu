@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <cmath>
 
 #include "hg_internal.cuh"
 
@@ -32,18 +33,20 @@ namespace hg {
 
 namespace {
 
+// warp 0 issues the MMAs, warp 1 the W loads, warps 2-3 idle, warps 4..19 are
+// the epilogue (warp w reaches TMEM lanes 32 (w % 4) ..).  Registers: 96 per
+// thread -- each SM sub-partition holds 5 of the 20 warps (16384 / 5 / 32)
 constexpr int kYThreads = 640;
 constexpr int kYWarps = kYThreads / 32;
-constexpr int kYEpiWarp0 = 4;                 // first epilogue warp
-constexpr int kYEpiThreads = kYThreads - 128; // 512
+constexpr int kYEpiWarp0 = 4;                                 // first epilogue warp
+constexpr int kYEpiThreads = kYThreads - 32 * kYEpiWarp0;     // 512
 constexpr int kYMaxStages = 16;               // W ring depth bound (runtime: PArgs::stages)
 constexpr int kYStageBytes = 64 * 128;        // this CTA's 64 W rows x 128 K (u8)
 constexpr int kYMaxIpt = 32;
 constexpr int kYTmemCols = 512;
 constexpr int kYAcc0 = 256;                   // first accumulator column
 constexpr int kYCluster = 2;                  // the CTA pair
-constexpr int kRegsCtl = 40;                  // per thread, warpgroup 0 (setmaxnreg)
-constexpr int kRegsEpi = 104;                 // per thread, epilogue warpgroups
+constexpr int kYMaxPlanes = 4;                // byte planes one launch folds together
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -198,6 +201,19 @@ __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
     return (~t & 0x80808080u) >> 7;
 }
 
+// one row's share of a plane's fold: s += sum_k G[k] * T[k][l] * sc over
+// k = sub, sub + 4, ... (fixed order), zeroing the bins; out of line -- the
+// epilogue's tile loop is register-bound
+__device__ __noinline__ double fold_bins(uint32_t* bp, const uint32_t* tbp, int p, int ps, int sub,
+                                         double sc, double s) {
+    for (int k = sub; k < p; k += 4) {
+        const uint32_t g = bp[k * 128];
+        bp[k * 128] = 0u;
+        s = fma((double)g, __hiloint2double((int)tbp[k * ps], (int)tbp[(p + k) * ps]) * sc, s);
+    }
+    return s;
+}
+
 }  // namespace
 
 __host__ __device__ inline size_t p_C_bytes(int ipt, int npad) {
@@ -231,10 +247,11 @@ struct PArgs {
     int tri;
     int csm;          // 1: a unit's cluster rows are staged in shared memory (they fit)
     int tsm;          // 1: a unit's hub-cost tables T are copied to shared memory (cp.async)
-    // pfold: planes > 4 (fractional flows): the bins hold one plane and each
-    // plane is folded into S_T after its last tile; wscale: the flows' common
-    // power-of-two quantum (1 for integer flows) -- plane pl weighs 256^pl * wscale
-    int pfold;
+    // plane0: the first byte plane this launch reads (instances with more than
+    // 4 planes run one launch per plane, each writing its partial S_T to part
+    // with stride pstride); wscale: the weight of plane plane0 -- the flows'
+    // power-of-two quantum times 256^plane0 (plane pl weighs 256^pl * that)
+    int plane0, pstride;
     double wscale;
     uint32_t idesc;   // kind::i8, M=256, N=128, K-major both
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
@@ -270,7 +287,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     const size_t cb = CSM ? p_C_bytes(ipt, A.npad) : 0;
     unsigned char* sC0 = var;
     var += 2 * cb;
-    const int PB = A.pfold ? 1 : A.P;  // planes of bins
+    const int PB = A.P;  // planes of bins
     uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [PB][p][128] cluster-pair flow bins
     var += (size_t)PB * p * 512;
     double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
@@ -374,7 +391,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                 for (int kk = 0; kk < nk; ++kk)
                                     tma2d_pair(dst + kk * kYStageBytes, &tmW,
                                                (c * kYChunkKB + kb0 + kk) * 128,
-                                               pl * A.nt + it * 128 + q, L_full + 8 * s);
+                                               (A.plane0 + pl) * A.nt + it * 128 + q,
+                                               L_full + 8 * s);
                                 if (++s == (uint32_t)NS) {
                                     s = 0;
                                     ph ^= 1u;
@@ -510,7 +528,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             const uint4* crow =
                 reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
-#pragma unroll 1
+#pragma unroll 2
             for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32 && !(A.dbg & 8); c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
@@ -616,7 +634,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                 A.out[4 * b + 2] = dist;
                                 A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
                             } else {
-                                A.part[bbase_u + b2] = st;
+                                A.part[(bbase_u + b2) * A.pstride] = st;
                             }
                         }
                         __syncwarp();
@@ -646,13 +664,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             A.out[4 * b + 2] = dist;
                             A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
                         } else {
-                            A.part[bbase_u + b2] = acc;
+                            A.part[(bbase_u + b2) * A.pstride] = acc;
                         }
                     }
                 }
         };
-        int64_t pend_j = -1;  // the slot whose reduce is pending
-        uint32_t phase = 0;
+        // (slot j's first tile runs slot j-1's reduce; phase = j * NC + c is
+        // recomputed rather than carried: the loop is register-bound)
         for (int64_t j = 0; j < nslots; ++j) {
             int64_t bbase;
             int nind;
@@ -692,15 +710,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             // of two): each product is the one-plane product, scaled exactly
             auto fold_plane = [&](int pl, uint32_t* bp) {
                 const double sc = A.wscale * __longlong_as_double((long long)(1023 + 8 * pl) << 52);
-                for (int k = sub; k < p; k += 4) {
-                    const uint32_t g = bp[k * 128 + r];
-                    bp[k * 128 + r] = 0u;
-                    s_acc = fma((double)g,
-                                __hiloint2double((int)tbp[k * A.ps], (int)tbp[(p + k) * A.ps]) * sc,
-                                s_acc);
-                }
+                s_acc = fold_bins(bp + r, tbp, p, A.ps, sub, sc, s_acc);
             };
-            for (int c = 0; c < NC; ++c, ++phase) {
+            for (int c = 0; c < NC; ++c) {
+                const uint32_t phase = (uint32_t)(j * NC + c);
                 const bool last_phase = j + 1 == nslots && c + 1 == NC;
                 const int T = ntl(c), NT = A.P * T;
                 // the next phase's one-hot quarter `sub`, generated as soon as
@@ -777,26 +790,17 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             const uint32_t cc = __byte_perm(cw[k >> 2], 0u, 0x4440u + (k & 3));
                             const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
                             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(
-                                             bin_r + (uint32_t)(A.pfold ? 0 : pl) * (uint32_t)p * 512u +
-                                                 cc * 512u),
+                                             bin_r + (uint32_t)pl * (uint32_t)p * 512u + cc * 512u),
                                          "r"(dv)
                                          : "memory");
                         }
                     }
                     ET(e_cmp);
-                    if (A.pfold && it == T - 1 && pl + 1 < A.P) {
-                        // plane pl complete: into S_T now, the bins serve the next plane
-                        asm volatile("cp.async.wait_all;" ::: "memory");
-                        epi_sync();
-                        if (live) fold_plane(pl, binsj);
-                        epi_sync();
-                    }
-                    if (c == 0 && tt == 0 && pend_j >= 0 && !(A.dbg & 4)) {  // the previous unit's reduce
+                    if (c == 0 && tt == 0 && j > 0 && !(A.dbg & 4)) {  // the previous unit's reduce
                         int64_t pb;
                         int pn;
-                        slot_unit(pend_j, pb, pn);
-                        reduce_unit(pb, pn, pend_j);
-                        pend_j = -1;
+                        slot_unit(j - 1, pb, pn);
+                        reduce_unit(pb, pn, j - 1);
                         ET(e_red);
                     }
                 }
@@ -832,27 +836,25 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         return (double)g;
                     };
 #pragma unroll
-                    for (int k = sub; k < p; k += 4) prod[k * 128 + r] = __dmul_rn(inter(k), tval(k));
+                    // (the bins count Q = W / wscale, wscale a power of two: exact)
+                    for (int k = sub; k < p; k += 4)
+                        prod[k * 128 + r] = __dmul_rn(inter(k) * A.wscale, tval(k));
                 }
                 if (live && !EX && !(A.dbg & 4)) {
-                    // every plane (pfold: the last; the others were folded as
-                    // they completed)
-                    for (int pl = A.pfold ? A.P - 1 : 0; pl < A.P; ++pl)
-                        fold_plane(pl, binsj + (size_t)(A.pfold ? 0 : pl) * p * 128);
+                    for (int pl = 0; pl < A.P; ++pl) fold_plane(pl, binsj + (size_t)pl * p * 128);
                 }
                 if (c + 1 == NC && !EX) red[sub * 128 + r] = s_acc;
                 ET(e_fold);
                 epi_sync();  // bins zeroed before the next chunk's atomics (red / prod written)
                 ET(e_sync);
             }
-            pend_j = j;
             ET(e_red);
         }
-        if (pend_j >= 0) {  // the last unit
+        if (nslots > 0 && !(A.dbg & 4)) {  // the last unit
             int64_t pb;
             int pn;
-            slot_unit(pend_j, pb, pn);
-            reduce_unit(pb, pn, pend_j);
+            slot_unit(nslots - 1, pb, pn);
+            reduce_unit(pb, pn, nslots - 1);
         }
         if (timed) {
             atomicAdd(A.timing + 16, e_st);
@@ -895,8 +897,8 @@ static bool p_csm(int p, int npad) {
 }
 
 // everything but the W ring; exact: the [p][128] fp64 terms of S_T
-// planes beyond 4 (fractional flows) are folded one at a time: one plane of bins
-static int p_bin_planes(int P) { return P > 4 ? 1 : P; }
+// planes of bins one launch holds (more planes: a launch per plane)
+static int p_bin_planes(int P) { return P > kYMaxPlanes ? 1 : P; }
 
 static size_t p_base_bytes(int p, int npad, int P, bool exact) {
     return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) +
@@ -1018,8 +1020,10 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     A.kbs = p_kbs(I.p, I.npad, A.P, A.exact);
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;
     A.tsm = p_tsm(I.p, I.npad, A.P, A.exact) ? 1 : 0;
-    A.pfold = p_bin_planes(A.P) < A.P ? 1 : 0;
+    A.plane0 = 0;
+    A.pstride = 1;
     A.wscale = I.wscale;
+    if (A.P > kYMaxPlanes) A.P = 1;  // one launch per plane (launch_fitness_tcp)
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
     A.timing = tc_timing_buffer();
     {
@@ -1051,7 +1055,7 @@ double tcp_mma_ops(const DevInst& I, bool tri_avail, int64_t B, int grid) {
         for (int it = 0; it < T; ++it)
             blocks += nb - (A.tri && it > c * kYChunkKB ? it - c * kYChunkKB : 0);
     }
-    blocks *= A.P;
+    blocks *= A.tri ? I.wplanes_tri : I.wplanes;  // every plane, one launch or several
     const int64_t ncl = g / kYCluster;
     double slots = 0.0;
     for (int64_t cid = 0; cid < ncl; ++cid) {
@@ -1060,6 +1064,8 @@ double tcp_mma_ops(const DevInst& I, bool tri_avail, int64_t B, int grid) {
     }
     return slots * blocks * 2.0 * 256.0 * 128.0 * 128.0;
 }
+
+static int tcp_launch(const DevInst& I, const PArgs& A, int g, const void* wmap, cudaStream_t s);
 
 int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
                        const uint8_t* cl, const uint32_t* T, double* part, int grid,
@@ -1072,7 +1078,27 @@ int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri,
     A.legs = legs;
     A.out = out;
     const int g = tcp_setup(I, wmap_tri != nullptr, B, grid, A);
-    CUtensorMap map = *static_cast<const CUtensorMap*>(A.tri ? wmap_tri : wmap);
+    const int planes = A.tri ? I.wplanes_tri : I.wplanes;
+    if (planes > kYMaxPlanes) {
+        // fractional flows on more than 4 planes: a launch per plane writes its
+        // partial S_T (weight 256^pl * quantum), the finaliser sums them in
+        // plane order
+        for (int pl = 0; pl < planes; ++pl) {
+            PArgs Ap = A;
+            Ap.plane0 = pl;
+            Ap.wscale = I.wscale * std::ldexp(1.0, 8 * pl);
+            Ap.out = nullptr;
+            Ap.part = part + pl;
+            Ap.pstride = planes;
+            HG_TRY(tcp_launch(I, Ap, g, A.tri ? wmap_tri : wmap, s));
+        }
+        return launch_finalize(I, planes, B, legs, part, out, s);
+    }
+    return tcp_launch(I, A, g, A.tri ? wmap_tri : wmap, s);
+}
+
+static int tcp_launch(const DevInst& I, const PArgs& A, int g, const void* wmap, cudaStream_t s) {
+    CUtensorMap map = *static_cast<const CUtensorMap*>(wmap);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3(kYThreads);

@@ -38,7 +38,7 @@ __device__ __forceinline__ double fold_at(const double* __restrict__ W, int n, i
 __global__ void k_scan_instance(const double* __restrict__ C, const double* __restrict__ W, int n,
                                 InstanceScan* out) {
     unsigned long long cmin = ~0ull, cmax = 0ull, wmax = 0ull, mmax = 0ull, wmin = ~0ull;
-    int intw = 1, sym = 1;
+    int intw = 1, sym = 1, glsb = 1 << 30;
     double wsum = 0.0;
     const int64_t total = (int64_t)n * n;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
@@ -53,7 +53,14 @@ __global__ void k_scan_instance(const double* __restrict__ C, const double* __re
         if (!(w >= 0.0 && w < 4294967296.0 && w == floor(w))) intw = 0;
         const unsigned long long wb = pos_bits(w >= 0.0 ? w : 0.0);
         wmax = wb > wmax ? wb : wmax;
-        if (w > 0.0) wmin = wb < wmin ? wb : wmin;
+        if (w > 0.0) {
+            wmin = wb < wmin ? wb : wmin;
+            // exponent of the flow's lowest set bit (w = odd * 2^e)
+            const int ex = (int)((wb >> 52) & 0x7ff);
+            const unsigned long long man = (wb & 0xfffffffffffffull) | (ex ? 1ull << 52 : 0ull);
+            const int e = (ex ? ex : 1) - 1075 + __ffsll((long long)man) - 1;
+            glsb = e < glsb ? e : glsb;
+        }
         const double m = fold_at(W, n, i, j);
         const unsigned long long mb = pos_bits(m >= 0.0 ? m : 0.0);
         mmax = mb > mmax ? mb : mmax;
@@ -66,6 +73,7 @@ __global__ void k_scan_instance(const double* __restrict__ C, const double* __re
         wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
         wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+        glsb = min(glsb, __shfl_xor_sync(0xffffffffu, glsb, o));
         wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
     }
     intw = __all_sync(0xffffffffu, intw);
@@ -76,6 +84,7 @@ __global__ void k_scan_instance(const double* __restrict__ C, const double* __re
         atomicMax(&out->wmax_bits, wmax);
         atomicMax(&out->mmax_bits, mmax);
         atomicMin(&out->wmin_bits, wmin);
+        atomicMin(&out->lsb_exp, glsb);
         if (!intw) atomicAnd(&out->int_flows, 0);
         if (!sym) atomicAnd(&out->symmetric, 0);
         // integer flows: every partial sum is an exact integer below 2^53 for
@@ -120,7 +129,7 @@ unsigned grid_of(int64_t work) {
 
 int launch_scan_instance(const double* C, const double* W, int n, InstanceScan* out,
                          cudaStream_t s) {
-    const InstanceScan init = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0.0, 1, 1};
+    const InstanceScan init = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0.0, 1, 1, 1 << 30};
     HG_CUDA(cudaMemcpyAsync(out, &init, sizeof(init), cudaMemcpyHostToDevice, s));
     k_scan_instance<<<grid_of((int64_t)n * n), 256, 0, s>>>(C, W, n, out);
     HG_LAUNCHED();

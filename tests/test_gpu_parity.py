@@ -180,7 +180,10 @@ class TestKernels:
         assert big.device().fitness_kernel == "tensor-pair"  # K chunks of 1024 nodes
         with pytest.raises(ValueError, match="unknown fitness kernel"):
             big.device().set_fitness(4)  # the superseded TMEM one-CTA kernel is gone
-        frac = hg.Instance(inst.n, inst.p, inst.dist, inst.flow * 0.5, 1.0, 0.75, 1.0)
+        half = hg.Instance(inst.n, inst.p, inst.dist, inst.flow * 0.5, 1.0, 0.75, 1.0)
+        assert half.device().fitness_kernel == "tensor-pair"  # quantum 2^-1: exact
+        wide = np.where(inst.flow > 50, inst.flow * 1e12, inst.flow * 1e-9)  # 2^70 range
+        frac = hg.Instance(inst.n, inst.p, inst.dist, wide, 1.0, 0.75, 1.0)
         assert frac.device().fitness_kernel == "fp64"
         with pytest.raises(ValueError, match="tensor-core"):
             frac.device().set_fitness(2)

@@ -259,10 +259,10 @@ class TestFractionalFlows:
     def test_tensor_path_matches_oracle(self, case):
         rng = np.random.default_rng(11)
         n, p = (1100, 12) if case == "bigger" else (300, 10)
-        if case == "wide":  # flows over six decades: the one-plane-at-a-time fold
-            flows = 10.0 ** rng.uniform(-3.0, 3.0, (n, n))
-        else:
-            flows = rng.integers(0, 100, (n, n)) * 0.37 + rng.random((n, n))
+        if case == "wide":  # flows over four decades: 7 planes, folded one at a time
+            flows = 10.0 ** rng.uniform(-2.0, 2.0, (n, n))
+        else:  # decimals in [0.1, 37.6): 6 planes (the fold of W + W^T: 7)
+            flows = rng.integers(0, 100, (n, n)) * 0.37 + 0.1 + 0.9 * rng.random((n, n))
         np.fill_diagonal(flows, 0.0)
         inst = self._instance(n, p, flows, symmetric=case != "asymmetric")
         d = inst.device()
@@ -295,7 +295,7 @@ class TestFractionalFlows:
 
     def test_ga_replays_on_fractional_flows(self):
         rng = np.random.default_rng(4)
-        flows = rng.integers(0, 100, (200, 200)) * 0.5 + rng.random((200, 200))
+        flows = rng.integers(0, 100, (200, 200)) * 0.5 + 0.1 + 0.9 * rng.random((200, 200))
         np.fill_diagonal(flows, 0.0)
         inst = self._instance(200, 10, flows)
         assert inst.device().fitness_kernel == "tensor-pair"
@@ -305,3 +305,21 @@ class TestFractionalFlows:
         ref = orc.island_ga(pr, 4, 16, 3, 2, 0, None, False, "milli")
         assert np.array_equal(rep.best_solution.hubs, ref.hubs)
         assert _rel_ok(rep.raw_objective, ref.raw)
+
+    def test_power_of_two_multiples_are_exact(self):
+        # flows in quarter units: exact integers Q = 4 W on the byte planes,
+        # so even the exact mode is bit-identical to the reference's sums
+        base = hg.generate_urand(300, 10, 7, (3.0, 0.75, 2.0))
+        inst = hg.Instance(300, 10, base.dist, base.flow * 0.25, 3.0, 0.75, 2.0)
+        assert inst.device().fitness_kernel == "tensor-pair"
+        pop = hg.random_population(300, 10, 64, key=9)
+        pr = orc.Problem(300, 10, inst.dist, inst.flow, 3.0, 0.75, 2.0)
+        hg.set_exact_sums(True)
+        try:
+            ex = hg.evaluate_population(inst, pop)
+        finally:
+            hg.set_exact_sums(False)
+        for b in range(0, 64, 7):
+            a = orc.nearest(pr.C, pop[b])
+            c, t, d = orc.cost_terms(pr, pop[b], a)
+            assert np.array_equal(ex[b], [c, t, d, c + t + d]), b
