@@ -364,11 +364,12 @@ def run_gpu(args):
         clk = clocks.stop()
         step_ms = [a.elapsed_time(b) for a, b in ev]
         # per-launch duration of the dominant kernel (K3), events inside the library
-        fit_ms = []
+        fit_ms, k2_ms = [], []
         for _ in range(20):
             flush.zero_()
             popd.evaluate(POP)
             fit_ms.append(popd.last_fitness_ms())
+            k2_ms.append(popd.last_allocate_ms())
 
     total_ms = float(sum(step_ms))
     if world > 1:
@@ -509,6 +510,7 @@ def run_gpu(args):
                                               "so this ratio is the W-reuse factor, not a "
                                               "roofline fraction"}},
             "kernels_ms": {"k3_selected": fit_kernel, "k3": fit_avg,
+                           "k2": float(np.mean(k2_ms)),
                            "k3_variants": variant_ms, "step_total": ms_per_step},
             "e2e": {"value": e2e_value, "unit": "evals/s",
                     "h2d_bytes_per_step": int(pop_host.nbytes),

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdarg>
+#include <cstdio>
 
 #include "../../include/hubgpu.h"
 
@@ -63,6 +64,23 @@ uint64_t launch_count();
         HG_CUDA(cudaGetLastError());                                                    \
         ::hg::note_launch();                                                            \
     } while (0)
+
+// device-side invariant checks of the checked build (make EXTRA=-DHG_CHECKS):
+// a failed check prints and traps (compute-sanitizer is closed on this pool,
+// tools/checked_tests.sh runs the GPU tests on this build instead)
+#ifdef HG_CHECKS
+#define HG_DCHECK(cond, fmt, ...)                                                        \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("HG_DCHECK %s:%d " fmt "\n", __FILE__, __LINE__, ##__VA_ARGS__);     \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define HG_DCHECK(cond, fmt, ...) \
+    do {                          \
+    } while (0)
+#endif
 
 constexpr int kMaxP = 255;          // cluster ids are uint8
 constexpr int kMaxNga = 32768;      // GA mask kernels keep one mask per warp in smem

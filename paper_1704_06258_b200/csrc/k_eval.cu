@@ -347,7 +347,13 @@ __device__ __forceinline__ void alloc_chunk_out(const DevInst& I, const int32_t*
     }
     uint8_t* clb = cl + b * I.npad + c0 + lane;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) clb[32 * t] = (uint8_t)c4[t];
+    for (int t = 0; t < 4; ++t) {
+        HG_DCHECK(c4[t] >= 0 && c4[t] < p, "K2 cluster %d of node %d outside [0, %d)", c4[t],
+                  c0 + 32 * t + lane, p);
+        HG_DCHECK(c0 + 32 * t + lane < I.npad, "K2 node %d past npad %d", c0 + 32 * t + lane,
+                  I.npad);
+        clb[32 * t] = (uint8_t)c4[t];
+    }
     if (co)  // byte offsets of the columns in a T plane row (fp64 K3 only)
 #pragma unroll
         for (int t = 0; t < 4; ++t) co[b * I.npad + c0 + 32 * t + lane] = (uint16_t)(c4[t] * 4);

@@ -355,6 +355,17 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     fence_after();
     cluster_sync_all();  // the peer's barriers are initialised before any remote signal
     const uint32_t tmem = *tmem_slot;
+#ifdef HG_CHECKS
+    if (tid == 0) {
+        uint32_t dyn;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        const size_t used = (size_t)(reinterpret_cast<unsigned char*>(tmem_slot + 1) - smem_raw);
+        HG_DCHECK(used <= dyn, "K3 shared layout %llu B past the %u B launched",
+                  (unsigned long long)used, dyn);
+        HG_DCHECK(PB * p * 128 * 4 + (size_t)(reinterpret_cast<unsigned char*>(bins) - smem) <=
+                      (size_t)dyn, "K3 bins past the launched shared memory");
+    }
+#endif
 
     // units of this pair, interleaved over its 2 CTAs; both run the same number
     // of slots (a slot past the end is a dummy unit): one MMA stream serves both.
@@ -788,6 +799,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
 #pragma unroll
                         for (int k = 0; k < 32; ++k) {
                             const uint32_t cc = __byte_perm(cw[k >> 2], 0u, 0x4440u + (k & 3));
+                            HG_DCHECK(cc < (uint32_t)p, "K3 cluster %u of column %d outside [0, %d)",
+                                      cc, it * 128 + sub * 32 + k, p);
                             const uint32_t dv = k < 16 ? v0[k] : v1[k - 16];
                             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(
                                              bin_r + (uint32_t)pl * (uint32_t)p * 512u + cc * 512u),

@@ -413,7 +413,12 @@ k_correct(DevInst I, const uint32_t* __restrict__ bits, int hmax, int32_t* __res
         __syncthreads();
         --h;
     }
-    for (int k = threadIdx.x; k < p; k += kCorrThreads) hubs_out[b * p + k] = H[k];
+    HG_DCHECK(h == p, "K4c left %d hubs, p = %d", h, p);
+    for (int k = threadIdx.x; k < p; k += kCorrThreads) {
+        HG_DCHECK(H[k] >= 0 && H[k] < n && (k == 0 || H[k] > H[k - 1]),
+                  "K4c hub %d of child %lld: %d (n = %d)", k, (long long)b, H[k], n);
+        hubs_out[b * p + k] = H[k];
+    }
 }
 
 int launch_correct(const DevInst& I, int64_t B, const uint32_t* bits, int hmax, int32_t* hubs,
