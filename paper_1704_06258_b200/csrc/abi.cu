@@ -217,16 +217,24 @@ static uint16_t* co_for(const hg_inst* inst, uint16_t* co) {
     return fitness_kernel(inst) == HG_FIT_FP64 ? co : nullptr;
 }
 
+// the hub-cost tables K2 must write: none when K3-TC/P gathers them from C
+static uint32_t* T_for(const hg_inst* inst, int64_t B, uint32_t* T) {
+    const int k = fitness_kernel(inst);
+    if (k == HG_FIT_FP64) return T;
+    return tcp_gathers_T(inst->I, k == HG_FIT_TC_PAIR, B, inst->sm_count) ? nullptr : T;
+}
+
 // K3 (fp64 gather) or K3-TC (tensor cores) + finalise, by the instance's choice
-int queue_fitness(hg_inst* inst, int64_t B, const uint8_t* cl, const uint16_t* co,
-                  const uint32_t* T, double* part, const double* legs, double* out) {
+int queue_fitness(hg_inst* inst, int64_t B, const int32_t* hubs, const uint8_t* cl,
+                  const uint16_t* co, const uint32_t* T, double* part, const double* legs,
+                  double* out) {
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
     const int kind = fitness_kernel(inst);
     int tiles;
     if (kind == HG_FIT_TC_PAIR || kind == HG_FIT_TC_PAIR_FULL)  // finaliser fused
         return launch_fitness_tcp(I, inst->wmapp, kind == HG_FIT_TC_PAIR ? inst->wmapt : nullptr,
-                                  B, cl, T, part, inst->sm_count, s, legs, out);
+                                  B, cl, T, part, inst->sm_count, s, legs, out, hubs);
     HG_TRY(launch_fitness(I, inst->plan, B, cl, co, T, part,
                           inst->sm_count * inst->plan.blocks_per_sm, s));
     tiles = inst->plan.tiles;
@@ -241,14 +249,13 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
     cudaStream_t s = inst->stream;
     HG_CUDA(cudaEventRecord(P->evk, s));
     if (alloc32)
-        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, co_for(inst, P->co), P->T,
-                                 P->legs, s));
+        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, co_for(inst, P->co),
+                                 T_for(inst, B, P->T), P->legs, s));
     else
-        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, co_for(inst, P->co), P->T,
-                               P->legs, nullptr,
-                               s));
+        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, co_for(inst, P->co), T_for(inst, B, P->T),
+                               P->legs, nullptr, s));
     HG_CUDA(cudaEventRecord(P->ev0, s));
-    HG_TRY(queue_fitness(inst, B, P->cl, P->co, P->T, P->part, P->legs, P->out));
+    HG_TRY(queue_fitness(inst, B, P->hubs, P->cl, P->co, P->T, P->part, P->legs, P->out));
     HG_CUDA(cudaEventRecord(P->ev1, s));
     return HG_OK;
 }
@@ -1003,9 +1010,9 @@ int ga_queue_generation(hg_ga* ga) {
     HG_TRY(launch_mutate(G, s));
     HG_TRY(launch_correct(inst->I, ga->B, G.kids, 2 * G.p, G.khubs, s));
     HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, co_for(inst, ga->pop->co),
-                           ga->pop->T, ga->pop->legs, nullptr, s));
-    HG_TRY(queue_fitness(inst, ga->B, ga->pop->cl, ga->pop->co, ga->pop->T, ga->pop->part,
-                         ga->pop->legs, ga->pop->out));
+                           T_for(inst, ga->B, ga->pop->T), ga->pop->legs, nullptr, s));
+    HG_TRY(queue_fitness(inst, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->co, ga->pop->T,
+                         ga->pop->part, ga->pop->legs, ga->pop->out));
     HG_TRY(launch_select(G, s));
     return HG_OK;
 }

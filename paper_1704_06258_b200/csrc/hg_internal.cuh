@@ -197,7 +197,9 @@ double tcp_mma_ops(const DevInst& I, bool tri_avail, int64_t B, int grid);
 // wmap_tri: the map of the triangular fold (symmetric costs), or nullptr
 int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
                        const uint8_t* cl, const uint32_t* T, double* part, int grid,
-                       cudaStream_t s, const double* legs = nullptr, double* out = nullptr);
+                       cudaStream_t s, const double* legs, double* out, const int32_t* hubs);
+// true: the launch gathers the hub-cost tables from C itself (K2 need not write T)
+bool tcp_gathers_T(const DevInst& I, bool tri_avail, int64_t B, int grid);
 
 // ---- k_gen.cu: device generator and hub-set enumeration ---------------------
 // xy: 2n scratch; C / W: n x n (either may be null)

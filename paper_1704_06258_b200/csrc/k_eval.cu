@@ -373,8 +373,8 @@ __device__ __forceinline__ void alloc_finish(const DevInst& I, const int32_t* hs
                                              int lane, double so, double sd, const double* st,
                                              uint32_t* __restrict__ T, double* __restrict__ legs) {
     const int p = I.p, n = I.n;
-    uint32_t* Tb = T + b * 2 * (int64_t)p * I.ps;
-    for (int k0 = 0; k0 < p; k0 += 8) {
+    uint32_t* Tb = T ? T + b * 2 * (int64_t)p * I.ps : nullptr;
+    for (int k0 = 0; T && k0 < p; k0 += 8) {  // T null: the fitness kernel gathers it
         for (int l = lane; l < p; l += 32) {
             const int hl = hs[l];
             double v[8];

@@ -47,6 +47,13 @@ constexpr int kYTmemCols = 512;
 constexpr int kYAcc0 = 256;                   // first accumulator column
 constexpr int kYCluster = 2;                  // the CTA pair
 constexpr int kYMaxPlanes = 4;                // byte planes one launch folds together
+// phase counters (HUBGPU_TC_TIMING=1) only in a timing build
+// (make EXTRA=-DHG_TCP_TIMING): their accumulators cost registers
+#ifdef HG_TCP_TIMING
+constexpr bool kTimingBuild = true;
+#else
+constexpr bool kTimingBuild = false;
+#endif
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -60,6 +67,12 @@ __device__ __forceinline__ void mb_expect_tx(uint32_t bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ bool mb_try(uint32_t bar, uint32_t parity) {  // non-blocking
     uint32_t ok;
@@ -204,12 +217,14 @@ __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
 // one row's share of a plane's fold: s += sum_k G[k] * T[k][l] * sc over
 // k = sub, sub + 4, ... (fixed order), zeroing the bins; out of line -- the
 // epilogue's tile loop is register-bound
-__device__ __noinline__ double fold_bins(uint32_t* bp, const uint32_t* tbp, int p, int ps, int sub,
-                                         double sc, double s) {
+__device__ __noinline__ double fold_bins(uint32_t* bp, const double* tbd, const uint32_t* tbp,
+                                         int p, int ps, int sub, double sc, double s) {
     for (int k = sub; k < p; k += 4) {
         const uint32_t g = bp[k * 128];
         bp[k * 128] = 0u;
-        s = fma((double)g, __hiloint2double((int)tbp[k * ps], (int)tbp[(p + k) * ps]) * sc, s);
+        const double t = tbd ? tbd[k * p]
+                             : __hiloint2double((int)tbp[k * ps], (int)tbp[(p + k) * ps]);
+        s = fma((double)g, t * sc, s);
     }
     return s;
 }
@@ -219,13 +234,19 @@ __device__ __noinline__ double fold_bins(uint32_t* bp, const uint32_t* tbp, int 
 __host__ __device__ inline size_t p_C_bytes(int ipt, int npad) {
     return ((size_t)ipt * npad + 15) & ~size_t(15);
 }
-__host__ __device__ inline size_t p_T_bytes(int ipt, int p, int ps) {
-    return (size_t)ipt * 2 * p * ps * 4;  // ps is a multiple of 4: 16-byte rows
+__host__ __device__ inline size_t p_T_bytes(int ipt, int p) {
+    return (size_t)ipt * p * p * 8;
+}
+__host__ __device__ inline size_t p_H_bytes(int ipt, int p) {
+    return ((size_t)2 * ipt * p * 4 + 15) & ~size_t(15);
 }
 
 struct PArgs {
     const uint8_t* cl;
-    const uint32_t* T;
+    const uint32_t* T;   // K2's hub-cost tables (read when !tsm)
+    const int32_t* hubs; // [B][p] sorted hubs (tsm: T_b gathered from C here)
+    const double* C;     // the cost matrix, n x n
+    int nC;
     double* part;     // [B][1]: S_T complete per individual (when out is null)
     const double* legs;  // [B][2] spoke-leg sums from K2 (finalise fused when out is set)
     double* out;         // [B][4] collection, transfer, distribution, raw
@@ -246,7 +267,8 @@ struct PArgs {
     // tile I runs K blocks J >= I only (see k_fitness_tcp's header)
     int tri;
     int csm;          // 1: a unit's cluster rows are staged in shared memory (they fit)
-    int tsm;          // 1: a unit's hub-cost tables T are copied to shared memory (cp.async)
+    int tsm;          // 1: a unit's hub-cost tables T_b[k][l] = C[h_k][h_l] are gathered
+                      // from C into shared memory by cp.async (K2 writes none)
     // plane0: the first byte plane this launch reads (instances with more than
     // 4 planes run one launch per plane, each writing its partial S_T to part
     // with stride pstride); wscale: the weight of plane plane0 -- the flows'
@@ -257,8 +279,8 @@ struct PArgs {
     unsigned long long* timing;  // optional phase counters (HUBGPU_TC_TIMING=1)
     // ablation flags (tuning only, wrong results): 1 = no bin atomics, 2 = no
     // MMA, 4 = no chunk fold / unit reduce, 8 = no one-hot generation, 16 = the
-    // MMA issuer does not wait for W, 32 = no W stream (needs 16), 64 = no
-    // epilogue warps at all
+    // MMA issuer does not wait for W (only together with 32: the ring's
+    // barriers race otherwise), 32 = no W stream, 64 = no epilogue warps at all
     int dbg;
     // exact: one chunk and one plane, so the bins ARE the reference's
     // inter-cluster flows; S_T is then np.sum(inter * hub_dist) replayed in
@@ -295,9 +317,12 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     // the unit's spoke-leg sums (finaliser), by slot parity: [2][ipt][2]
     double* sL = reinterpret_cast<double*>(var);
     var += 2 * kYMaxIpt * 2 * 8;
-    // the unit's hub-cost tables T (tsm): [ipt][2][p][ps] u32, as in global memory
-    uint32_t* sT = reinterpret_cast<uint32_t*>(var);
-    var += A.tsm ? p_T_bytes(ipt, p, A.ps) : 0;
+    // the unit's hub-cost tables T (tsm): [ipt][p][p] fp64, and its hubs (and
+    // the next unit's: double buffer) [2][ipt][p] int32
+    double* sT = reinterpret_cast<double*>(var);
+    var += A.tsm ? p_T_bytes(ipt, p) : 0;
+    int32_t* sH = reinterpret_cast<int32_t*>(var);
+    var += A.tsm ? p_H_bytes(ipt, p) : 0;
     double* prod = reinterpret_cast<double*>(var);  // exact: [p][128] rounded terms of S_T
     var += EX ? (size_t)p * 128 * 8 : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
@@ -378,6 +403,14 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     // the leader's barriers as shared::cluster addresses (remote for the peer)
     const uint32_t L_full = mapa(b_full, 0), L_acce = mapa(b_acce, 0), L_ard = mapa(b_ard, 0);
 
+    // per-slot unit geometry: the first individual and the count (0: a dummy
+    // slot past the pair's units)
+    auto slot_unit = [&](int64_t j, int64_t& bbase, int& nind) {
+        const int64_t u = cs0 + j * kYCluster + crank;
+        bbase = u * ipt;
+        nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
+    };
+
     if (warp == 1) {
         // ---------------- TMA producer: per phase, the W tiles (plane, row
         // block it) in order, tile it running K blocks [klo(c, it), nkb(c));
@@ -416,7 +449,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         // ---------------- MMA issuer (leader CTA only)
         if (leader) {  // the whole warp, converged; one lane issues
             uint32_t s = 0, ph = 0, t = 0, phase = 0;
-            const bool timed = A.timing != nullptr;
+            const bool timed = kTimingBuild && A.timing != nullptr;
             unsigned long long w_a = 0, w_e = 0, w_f = 0, w_i = 0;
             long long c0 = timed ? clock64() : 0;
 #define YT(acc_)                                    \
@@ -507,7 +540,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         const int bl = r / p, l = r - bl * p;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         uint32_t t = 0;
-        const bool timed = A.timing != nullptr && tid == kYEpiWarp0 * 32;
+        const bool timed = kTimingBuild && A.timing != nullptr && tid == kYEpiWarp0 * 32;
         unsigned long long e_st = 0, e_gen = 0, e_wait = 0, e_cmp = 0, e_red = 0, e_ld = 0;
         unsigned long long e_sync = 0, e_tload = 0, e_fold = 0, e_kbf = 0;
         long long c0 = timed ? clock64() : 0;
@@ -520,11 +553,6 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         }                                           \
     } while (0)
         // per-slot unit geometry
-        auto slot_unit = [&](int64_t j, int64_t& bbase, int& nind) {
-            const int64_t u = cs0 + j * kYCluster + crank;
-            bbase = u * ipt;
-            nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
-        };
         // one-hot A of phase (j, c) into TMEM (row r = (bl, l), K = the chunk's
         // nodes); this warp writes chunk blocks [kq(c,sub), kq(c,sub+1)) of its
         // lane quadrant, reading the cluster rows straight from global memory
@@ -539,7 +567,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             const uint4* crow =
                 reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
-#pragma unroll 2
+#pragma unroll 4
             for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32 && !(A.dbg & 8); c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
@@ -574,6 +602,16 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             }
         };
         if (nslots > 0) {
+            if (A.tsm) {  // unit 0's hubs (each unit's T gather reads them)
+                int64_t nb;
+                int nn;
+                slot_unit(0, nb, nn);
+                for (int x = tid - kYEpiWarp0 * 32; x < nn * p; x += kYEpiThreads)
+                    cp_async4(su32(sH + x), A.hubs + nb * p + x);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                epi_sync();
+            }
             if (CSM) {
                 stage(0);
                 epi_sync();
@@ -697,31 +735,45 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 epi_sync();    // ... complete before any warp generates from them
                 ET(e_sync);
             }
-            // this unit's T tables and leg sums into shared memory, asynchronously:
-            // read by the fold at the unit's end (after a barrier) and by its
-            // deferred reduce; the previous unit's fold finished with them
+            // this unit's leg sums and (tsm) hub-cost tables T_b[k][l] = C[h_k][h_l]
+            // into shared memory by cp.async: the tables gathered from C (row
+            // (b2, k) per warp, column l per lane) off the unit's hubs, staged one
+            // unit ahead; read by the fold at the unit's end (after a barrier)
+            // and the deferred reduce; the previous unit's fold is done with them
             {
                 const int etid = tid - kYEpiWarp0 * 32;
                 if (A.tsm) {
-                    const char* src = reinterpret_cast<const char*>(A.T + bbase * 2 * p * (int64_t)A.ps);
-                    const int chunks = nind * 2 * p * A.ps / 4;
-                    for (int x = etid; x < chunks; x += kYEpiThreads)
-                        cp_async16(su32(sT) + 16u * x, src + 16 * (int64_t)x);
+                    const int32_t* hsj = sH + (j & 1) * ipt * p;
+                    const int pp = p * p;
+                    for (int x = etid; x < nind * pp; x += kYEpiThreads) {
+                        const int b2 = x / pp, kl = x - b2 * pp, k = kl / p, l2 = kl - k * p;
+                        const int32_t* hs = hsj + b2 * p;
+                        cp_async8(su32(sT) + 8u * x, A.C + (size_t)hs[k] * A.nC + hs[l2]);
+                    }
+                    if (j + 1 < nslots) {
+                        int64_t nb;
+                        int nn;
+                        slot_unit(j + 1, nb, nn);
+                        for (int x = etid; x < nn * p; x += kYEpiThreads)
+                            cp_async4(su32(sH + ((j + 1) & 1) * ipt * p + x), A.hubs + nb * p + x);
+                    }
                 }
                 if (A.out && etid < nind)
                     cp_async16(su32(sL + (j & 1) * kYMaxIpt * 2 + 2 * etid),
                                A.legs + 2 * (bbase + etid));
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
+            // this row's T column: fp64 T_b[k][l] at tbd[k * p] (tsm), else K2's
+            // hi / lo planes at tbp[k * ps], tbp[(p + k) * ps]
+            const double* tbd = A.tsm ? sT + (live ? bl : 0) * p * p + l : nullptr;
             const uint32_t* tbp =
-                (A.tsm ? sT + (live ? bl : 0) * 2 * p * A.ps
-                       : A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps) + l;
+                A.tsm ? nullptr : A.T + (bbase + (live ? bl : 0)) * 2 * p * (int64_t)A.ps + l;
             double s_acc = 0.0;  // this thread's share of S_T over the chunks
             // plane pl of the flows carries weight 256^pl * wscale (an exact power
             // of two): each product is the one-plane product, scaled exactly
             auto fold_plane = [&](int pl, uint32_t* bp) {
                 const double sc = A.wscale * __longlong_as_double((long long)(1023 + 8 * pl) << 52);
-                s_acc = fold_bins(bp + r, tbp, p, A.ps, sub, sc, s_acc);
+                s_acc = fold_bins(bp + r, tbd, tbp, p, A.ps, sub, sc, s_acc);
             };
             for (int c = 0; c < NC; ++c) {
                 const uint32_t phase = (uint32_t)(j * NC + c);
@@ -819,11 +871,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 }
                 // this chunk's bins into S_T: sum_k T_b[k][l] * G_c[k][(b,l)] over
                 // k = sub, sub + 4, ... (fixed order -> deterministic); one chunk's
-                // bins stay below 2^32 (<= 255 * 1024 * n, n <= 16384).  The first
-                // 8 T values are fetched before the barrier.
+                // bins stay below 2^32 (<= 255 * 1024 * n, n <= 16384).
                 asm volatile("cp.async.wait_all;" ::: "memory");  // T, legs: this thread's part
                 auto tval = [&](int k) {
-                    return __hiloint2double((int)tbp[k * A.ps], (int)tbp[(p + k) * A.ps]);
+                    return tbd ? tbd[k * p]
+                               : __hiloint2double((int)tbp[k * A.ps], (int)tbp[(p + k) * A.ps]);
                 };
                 ET(e_tload);
                 epi_sync();  // every bin of the chunk is complete
@@ -926,13 +978,13 @@ static bool p_tsm(int p, int npad, int P, bool exact) {
     const char* e = getenv("HUBGPU_TCP_TSM");  // tuning override: 0 disables
     if (e && atoi(e) == 0) return false;
     const int64_t room = (int64_t)227 * 1024 - (int64_t)p_base_bytes(p, npad, P, exact) -
-                         (int64_t)p_T_bytes(p_ipt(p), p, (p + 3) & ~3);
+                         (int64_t)(p_T_bytes(p_ipt(p), p) + p_H_bytes(p_ipt(p), p));
     return room >= 2 * 8 * (int64_t)kYStageBytes;
 }
 
 static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false) {
     return p_base_bytes(p, npad, P, exact) +
-           (p_tsm(p, npad, P, exact) ? p_T_bytes(p_ipt(p), p, (p + 3) & ~3) : 0);
+           (p_tsm(p, npad, P, exact) ? p_T_bytes(p_ipt(p), p) + p_H_bytes(p_ipt(p), p) : 0);
 }
 
 // K blocks per W stage: 8 (one MMA-issuer loop per 1024 K) unless that
@@ -1054,6 +1106,12 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     return g;
 }
 
+bool tcp_gathers_T(const DevInst& I, bool tri_avail, int64_t B, int grid) {
+    PArgs A;
+    tcp_setup(I, tri_avail, B > 0 ? B : 1, grid, A);
+    return A.tsm != 0;
+}
+
 // int8 operations the tensor cores execute for one launch on B hub sets:
 // every (pair slot, chunk, plane, output tile) runs its K blocks as M=256 x
 // N=128 x K=128 MMAs (dummy slots of an odd unit count included)
@@ -1082,11 +1140,14 @@ static int tcp_launch(const DevInst& I, const PArgs& A, int g, const void* wmap,
 
 int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
                        const uint8_t* cl, const uint32_t* T, double* part, int grid,
-                       cudaStream_t s, const double* legs, double* out) {
+                       cudaStream_t s, const double* legs, double* out, const int32_t* hubs) {
     if (B <= 0) return HG_OK;
     PArgs A;
     A.cl = cl;
     A.T = T;
+    A.hubs = hubs;
+    A.C = I.C;
+    A.nC = I.n;
     A.part = part;
     A.legs = legs;
     A.out = out;

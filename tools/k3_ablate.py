@@ -42,7 +42,14 @@ def one(n: int, p: int, B: int) -> dict:
             pop.evaluate(B)
             if k >= 3:
                 ms.append(pop.last_fitness_ms())
-    out = {"k3_ms": float(np.median(ms)), "kernel": d.fitness_kernel}
+    k2 = []
+    with torch.cuda.stream(st):
+        for _ in range(5):
+            flush.zero_()
+            pop.evaluate(B)
+            k2.append(pop.last_allocate_ms())
+    out = {"k3_ms": float(np.median(ms)), "k2_ms": float(np.median(k2)),
+           "kernel": d.fitness_kernel}
     if os.environ.get("HUBGPU_TC_TIMING") == "1":
         buf = np.zeros(32, dtype=np.uint64)
         _lib.check(_lib.load().hg_debug_tc_timing(buf.ctypes.data_as(_lib._u64p)))
@@ -61,12 +68,13 @@ def one(n: int, p: int, B: int) -> dict:
 
 CONFIGS = [
     ("default (tri)", {}),
-    ("tri, T from global", {"HUBGPU_TCP_TSM": "0"}),
-    ("tri, timing", {"HUBGPU_TC_TIMING": "1"}),
-    ("epilogue alone (no MMA, no W wait)", {"HUBGPU_TCP_DBG": "18"}),
-    ("epilogue alone, timing", {"HUBGPU_TCP_DBG": "18", "HUBGPU_TC_TIMING": "1"}),
     ("full W", {"HUBGPU_TCP_NOTRI": "1"}),
+    ("tri, T from K2 via global", {"HUBGPU_TCP_TSM": "0"}),
+    ("tri, no epilogue warps", {"HUBGPU_TCP_DBG": "64"}),
+    ("epilogue, no MMA", {"HUBGPU_TCP_DBG": "2"}),
+    ("MMA issue alone (no epilogue, no W stream)", {"HUBGPU_TCP_DBG": "112"}),
 ]
+# (phase counters, HUBGPU_TC_TIMING=1, need a timing build: make EXTRA=-DHG_TCP_TIMING)
 
 
 def main() -> None:
