@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -58,9 +59,13 @@ struct hg_pop {
     double* legs = nullptr;
     double* part = nullptr;
     double* out = nullptr;
+    int tiles = 0;  // per-individual partials (the row stride of part)
     DevBuf alloc;  // int32 [cap][n], on demand
     cudaEvent_t evk = nullptr, ev0 = nullptr, ev1 = nullptr;  // before K2, K3, after K3
 };
+
+constexpr int kEvalChunks = 2;          // hg_evaluate pipelines batches in this many chunks
+constexpr int64_t kEvalChunkMin = 2048; // ... each at least this many hub sets
 
 struct hg_inst {
     std::atomic<int> refs{1};  // the handle itself + every hg_pop / hg_ga built on it
@@ -94,6 +99,9 @@ struct hg_inst {
     int* hflag = nullptr;  // page-locked landing slots for small device->host reads
     hg_pop* scratch = nullptr;
     DevBuf t1, t2, t3, t4;
+    // hg_evaluate's copy stream and per-chunk events (copies overlap compute)
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_in[kEvalChunks] = {}, ev_done[kEvalChunks] = {};
 };
 
 namespace {
@@ -144,6 +152,7 @@ int pop_alloc(hg_pop* P, hg_inst* inst, int64_t cap) {
     int tiles = inst->plan.tiles > tc_tiles(I.n) ? inst->plan.tiles : tc_tiles(I.n);
     if (tiles < 8) tiles = 8;
     HG_CUDA(cudaMalloc(&P->part, (size_t)cap * tiles * sizeof(double)));
+    P->tiles = tiles;
     HG_CUDA(cudaMalloc(&P->out, (size_t)cap * 4 * sizeof(double)));
     HG_CUDA(cudaEventCreate(&P->evk));
     HG_CUDA(cudaEventCreate(&P->ev0));
@@ -241,22 +250,88 @@ int queue_fitness(hg_inst* inst, int64_t B, const int32_t* hubs, const uint8_t* 
     return launch_finalize(I, tiles, B, legs, part, out, s);
 }
 
-// queue K2 + K3 + finalise for B individuals whose int32 hubs are in P->hubs
-// (alloc32 == nullptr: nearest allocation; otherwise the given allocation)
-int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
+// queue K2 + K3 + finalise for individuals [b0, b0 + B) of P whose int32 hubs
+// are in P->hubs (alloc32 == nullptr: nearest allocation; otherwise the given
+// allocation, rows from b0); events: time K2 and K3 (hg_pop_last_*_ms)
+int pop_eval_range(hg_pop* P, int64_t b0, int64_t B, const int32_t* alloc32, bool events) {
     hg_inst* inst = P->inst;
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
-    HG_CUDA(cudaEventRecord(P->evk, s));
+    const int tiles = P->tiles;
+    int32_t* hubs = P->hubs + b0 * I.p;
+    uint8_t* cl = P->cl + b0 * I.npad;
+    uint16_t* co = co_for(inst, P->co) ? P->co + b0 * I.npad : nullptr;
+    uint32_t* T = P->T + b0 * 2 * I.p * (int64_t)I.ps;
+    double* legs = P->legs + 2 * b0;
+    if (events) HG_CUDA(cudaEventRecord(P->evk, s));
     if (alloc32)
-        HG_TRY(launch_from_alloc(I, B, P->hubs, alloc32, P->cl, co_for(inst, P->co),
-                                 T_for(inst, B, P->T), P->legs, s));
+        HG_TRY(launch_from_alloc(I, B, hubs, alloc32 + b0 * I.n, cl, co, T_for(inst, B, T), legs,
+                                 s));
     else
-        HG_TRY(launch_allocate(I, B, P->hubs, P->cl, co_for(inst, P->co), T_for(inst, B, P->T),
-                               P->legs, nullptr, s));
-    HG_CUDA(cudaEventRecord(P->ev0, s));
-    HG_TRY(queue_fitness(inst, B, P->hubs, P->cl, P->co, P->T, P->part, P->legs, P->out));
-    HG_CUDA(cudaEventRecord(P->ev1, s));
+        HG_TRY(launch_allocate(I, B, hubs, cl, co, T_for(inst, B, T), legs, nullptr, s));
+    if (events) HG_CUDA(cudaEventRecord(P->ev0, s));
+    HG_TRY(queue_fitness(inst, B, hubs, cl, co, T, P->part + b0 * tiles, legs, P->out + 4 * b0));
+    if (events) HG_CUDA(cudaEventRecord(P->ev1, s));
+    return HG_OK;
+}
+
+int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
+    return pop_eval_range(P, 0, B, alloc32, true);
+}
+
+// hg_evaluate's pipeline: chunk c's int64 hub sets cross PCIe on the copy
+// stream while chunk c-1 is scored on the instance stream; chunk c's costs go
+// back on the copy stream once scored.  The caller reads the flag and
+// synchronises the instance stream, which waits for the last copy.
+int eval_pipelined(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, double* out) {
+    const DevInst& I = inst->I;
+    cudaStream_t s = inst->stream;
+    if (!inst->cstream) {
+        HG_CUDA(cudaStreamCreateWithFlags(&inst->cstream, cudaStreamNonBlocking));
+        for (int c = 0; c < kEvalChunks; ++c) {
+            HG_CUDA(cudaEventCreateWithFlags(&inst->ev_in[c], cudaEventDisableTiming));
+            HG_CUDA(cudaEventCreateWithFlags(&inst->ev_done[c], cudaEventDisableTiming));
+        }
+    }
+    HG_TRY(inst->t1.ensure((size_t)B * I.p * sizeof(int64_t)));
+    int64_t* dsrc = inst->t1.as<int64_t>();
+    // the copy stream starts after everything queued before this call
+    HG_CUDA(cudaEventRecord(inst->ev_done[kEvalChunks - 1], s));
+    HG_CUDA(cudaStreamWaitEvent(inst->cstream, inst->ev_done[kEvalChunks - 1], 0));
+    // equal chunks (a first chunk of one K3 wave -- 128/p hub sets per SM,
+    // HUBGPU_EVAL_WAVE=1 -- measured 3 % slower end to end: two short launches)
+    int64_t lo[kEvalChunks + 1];
+    const int64_t ipt = I.p <= 128 ? 128 / I.p : 1;
+    static const int wave_first = env_int("HUBGPU_EVAL_WAVE", 0);  // tuning override
+    const int64_t first = wave_first ? (int64_t)inst->sm_count * ipt : B / 2;
+    lo[0] = 0;
+    lo[1] = first < B / 2 ? first : B / 2;
+    for (int c = 2; c <= kEvalChunks; ++c) lo[c] = lo[1] + (B - lo[1]) * (c - 1) / (kEvalChunks - 1);
+    for (int c = 0; c < kEvalChunks; ++c) {
+        const int64_t b0 = lo[c], nb = lo[c + 1] - lo[c];
+        HG_CUDA(cudaMemcpyAsync(dsrc + b0 * I.p, hubs + b0 * I.p, (size_t)nb * I.p * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, inst->cstream));
+        HG_CUDA(cudaEventRecord(inst->ev_in[c], inst->cstream));
+    }
+    for (int c = 0; c < kEvalChunks; ++c) {
+        const int64_t b0 = lo[c], nb = lo[c + 1] - lo[c];
+        HG_CUDA(cudaStreamWaitEvent(s, inst->ev_in[c], 0));
+        HG_TRY(launch_hubs_in(dsrc + b0 * I.p, P->hubs + b0 * I.p, nb, I.p, I.n, inst->derr, s,
+                              b0));
+        HG_TRY(pop_eval_range(P, b0, nb, nullptr, false));
+        HG_CUDA(cudaEventRecord(inst->ev_done[c], s));
+    }
+    // (every kernel is queued before the first copy back: a pageable `out`
+    // makes that copy synchronous for the host)
+    for (int c = 0; c < kEvalChunks; ++c) {
+        const int64_t b0 = lo[c], nb = lo[c + 1] - lo[c];
+        HG_CUDA(cudaStreamWaitEvent(inst->cstream, inst->ev_done[c], 0));
+        HG_CUDA(cudaMemcpyAsync(out + 4 * b0, P->out + 4 * b0, (size_t)nb * 4 * sizeof(double),
+                                cudaMemcpyDeviceToHost, inst->cstream));
+    }
+    // the instance stream (and its synchronisation) covers the copies back
+    HG_CUDA(cudaEventRecord(inst->ev_in[0], inst->cstream));
+    HG_CUDA(cudaStreamWaitEvent(s, inst->ev_in[0], 0));
     return HG_OK;
 }
 
@@ -534,7 +609,7 @@ int hg_instance_create(int device, int n, int p, const double* dist, const doubl
         while (Pt < 9 && mq >= std::ldexp(1.0, 8 * Pt)) ++Pt;
         I.wplanes = P;
         I.wscale = qscale;
-        const bool tri = sym && Pt <= 8 && !getenv("HUBGPU_TCP_NOTRI");
+        const bool tri = sym && Pt <= 8 && !env_int("HUBGPU_TCP_NOTRI", 0);
         I.wplanes_tri = tri ? Pt : 0;
         if (planes_ok && tcp_supported(n, p, I.npad, P) &&
             (!tri || tcp_supported(n, p, I.npad, Pt))) {
@@ -586,6 +661,14 @@ static void inst_destroy(hg_inst* inst) {
     if (inst->hflag) cudaFreeHost(inst->hflag);
     cudaFree(inst->dW8);
     cudaFree(inst->dM8);
+    if (inst->cstream) {
+        cudaStreamSynchronize(inst->cstream);
+        cudaStreamDestroy(inst->cstream);
+        for (int c = 0; c < kEvalChunks; ++c) {
+            cudaEventDestroy(inst->ev_in[c]);
+            cudaEventDestroy(inst->ev_done[c]);
+        }
+    }
     inst->t1.release();
     inst->t2.release();
     inst->t3.release();
@@ -687,19 +770,56 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
     hg_pop* P;
     HG_TRY(scratch_pop(inst, B, &P));
     const DevInst& I = inst->I;
-    HG_TRY(h2d_hubs_checked(inst, inst->t1, hubs, B, P->hubs));
-    const int32_t* a32 = nullptr;
-    if (alloc) {
-        HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
-        HG_TRY(h2d_alloc_checked(inst, inst->t2, alloc, B, P->alloc.as<int32_t>()));
-        a32 = P->alloc.as<int32_t>();
+    // HUBGPU_E2E_TRACE=1: device phase times of this call on stderr (tuning)
+    static const bool trace = getenv("HUBGPU_E2E_TRACE") != nullptr;
+    cudaEvent_t te[3] = {nullptr, nullptr, nullptr};
+    const auto h0 = std::chrono::steady_clock::now();
+    if (trace)
+        for (auto& e : te) cudaEventCreate(&e);
+    if (trace) cudaEventRecord(te[0], inst->stream);
+    static const int chunked = env_int("HUBGPU_EVAL_CHUNKS", 1);  // tuning override: 0 = off
+    const bool piped = !alloc && chunked && B >= kEvalChunks * kEvalChunkMin;
+    if (piped) {
+        // the hub sets in chunks on the copy stream, each chunk scored as soon
+        // as it lands and its costs copied back while the next one is scored
+        // (the PCIe transfers hide under the kernels)
+        HG_TRY(eval_pipelined(inst, P, B, hubs, out));
+    } else {
+        HG_TRY(h2d_hubs_checked(inst, inst->t1, hubs, B, P->hubs));
+        const int32_t* a32 = nullptr;
+        if (alloc) {
+            HG_TRY(P->alloc.ensure((size_t)B * I.n * sizeof(int32_t)));
+            HG_TRY(h2d_alloc_checked(inst, inst->t2, alloc, B, P->alloc.as<int32_t>()));
+            a32 = P->alloc.as<int32_t>();
+        }
+        HG_TRY(pop_eval_queue(P, B, a32));
+        if (trace) cudaEventRecord(te[1], inst->stream);
+        HG_CUDA(cudaMemcpyAsync(out, P->out, (size_t)B * 4 * sizeof(double),
+                                cudaMemcpyDeviceToHost, inst->stream));
     }
-    HG_TRY(pop_eval_queue(P, B, a32));
-    HG_CUDA(cudaMemcpyAsync(out, P->out, (size_t)B * 4 * sizeof(double), cudaMemcpyDeviceToHost,
-                            inst->stream));
     HG_CUDA(cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,
                             inst->stream));
+    if (trace) cudaEventRecord(te[2], inst->stream);
+    const auto h1 = std::chrono::steady_clock::now();
     HG_CUDA(cudaStreamSynchronize(inst->stream));
+    if (trace) {
+        const auto h2 = std::chrono::steady_clock::now();
+        float in_ms = 0, k2_ms = 0, k3_ms = 0, tot_ms = 0, out_ms = 0;
+        if (!piped) {
+            cudaEventElapsedTime(&in_ms, te[0], P->evk);
+            cudaEventElapsedTime(&k2_ms, P->evk, P->ev0);
+            cudaEventElapsedTime(&k3_ms, P->ev0, P->ev1);
+            cudaEventElapsedTime(&out_ms, te[1], te[2]);
+        }
+        cudaEventElapsedTime(&tot_ms, te[0], te[2]);
+        fprintf(stderr,
+                "hg_evaluate B=%lld: device: in %.1f us, K2 %.1f, K3 %.1f, out %.1f, total %.1f; "
+                "host: queue %.1f us, wait %.1f us\n",
+                (long long)B, in_ms * 1e3, k2_ms * 1e3, k3_ms * 1e3, out_ms * 1e3, tot_ms * 1e3,
+                std::chrono::duration<double, std::micro>(h1 - h0).count(),
+                std::chrono::duration<double, std::micro>(h2 - h1).count());
+        for (auto& e : te) cudaEventDestroy(e);
+    }
     const int flag = inst->hflag[0];
     return check_input_flag(inst, flag, alloc ? "solution" : "hub set");
 }

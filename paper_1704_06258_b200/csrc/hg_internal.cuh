@@ -30,6 +30,10 @@ namespace hg {
 
 void set_error(const char* fmt, ...);
 
+// a tuning variable of the environment as an int (absent: dflt; present but
+// not a number: 1), read once per process -- launch paths call this often
+int env_int(const char* name, int dflt);
+
 #define HG_CUDA(call)                                                                   \
     do {                                                                                \
         cudaError_t e_ = (call);                                                        \
@@ -141,7 +145,7 @@ int prepare_fitness(const FitPlan& P);
 
 // ---- launchers (k_eval.cu) -------------------------------------------------
 int launch_hubs_in(const int64_t* src, int32_t* dst, int64_t B, int p, int n, int* err,
-                   cudaStream_t s);
+                   cudaStream_t s, int64_t row0 = 0);
 int launch_idx_in(const int64_t* src, int32_t* dst, int64_t count, int n, int* err,
                   cudaStream_t s);
 int launch_i32_to_i64(const int32_t* src, int64_t* dst, int64_t count, cudaStream_t s);

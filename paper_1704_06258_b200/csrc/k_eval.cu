@@ -37,18 +37,21 @@ static int grid_for(int64_t m, int block) {
 
 // hub sets in (int64, B x p) -> int32, validated: each row strictly increasing
 // within [0, n).  *err (0 = ok) records the FIRST bad row as 0x7ffffffe - row
-// via atomicMax; K2 then treats the whole batch as hubs 0..p-1 (stays in bounds)
+// via atomicMax; K2 then treats the whole batch as hubs 0..p-1 (stays in bounds);
+// row0 offsets the row numbers of a batch queued in chunks
 __global__ void k_hubs_in(const int64_t* __restrict__ s, int32_t* __restrict__ d, int64_t B,
-                          int p, int n, int* err) {
+                          int p, int n, int* err, int64_t row0) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < B * p;
          x += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = x / p;
-        const int k = (int)(x - b * p);
+        const int64_t b = row0 + x / p;
+        const int k = (int)(x - (b - row0) * p);
         const int64_t v = s[x];
         bool ok = v >= 0 && v < n;
         if (k > 0) ok = ok && s[x - 1] < v;
         if (!ok) atomicMax(err, (int)(0x7ffffffe - (b < 0x7ffffffe ? b : 0x7ffffffd)));
-        d[x] = (int32_t)v;
+        // out-of-range entries become 0: kernels that index with the hubs
+        // before seeing *err (K3-TC/P's table gather) stay in bounds
+        d[x] = v >= 0 && v < n ? (int32_t)v : 0;
     }
 }
 
@@ -65,9 +68,9 @@ __global__ void k_idx_in(const int64_t* __restrict__ s, int32_t* __restrict__ d,
 }
 
 int launch_hubs_in(const int64_t* src, int32_t* dst, int64_t B, int p, int n, int* err,
-                   cudaStream_t s) {
+                   cudaStream_t s, int64_t row0) {
     if (B <= 0) return HG_OK;
-    k_hubs_in<<<grid_for(B * p, 256), 256, 0, s>>>(src, dst, B, p, n, err);
+    k_hubs_in<<<grid_for(B * p, 256), 256, 0, s>>>(src, dst, B, p, n, err, row0);
     HG_LAUNCHED();
     return HG_OK;
 }

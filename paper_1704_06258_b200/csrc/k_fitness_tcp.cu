@@ -956,8 +956,7 @@ static int p_ipt(int p) {
 
 // stage a unit's cluster rows in shared memory when the double buffer is small
 static bool p_csm(int p, int npad) {
-    const char* e = getenv("HUBGPU_TCP_CSM");  // tuning override: 0 disables
-    if (e && atoi(e) == 0) return false;
+    if (env_int("HUBGPU_TCP_CSM", 1) == 0) return false;  // tuning override
     return 2 * p_C_bytes(p_ipt(p), npad) <= 48 * 1024;
 }
 
@@ -975,8 +974,7 @@ static size_t p_base_bytes(int p, int npad, int P, bool exact) {
 // the unit's T tables in shared memory when they leave room for two full W
 // stages (p <= ~36 at n <= 1024)
 static bool p_tsm(int p, int npad, int P, bool exact) {
-    const char* e = getenv("HUBGPU_TCP_TSM");  // tuning override: 0 disables
-    if (e && atoi(e) == 0) return false;
+    if (env_int("HUBGPU_TCP_TSM", 1) == 0) return false;  // tuning override
     const int64_t room = (int64_t)227 * 1024 - (int64_t)p_base_bytes(p, npad, P, exact) -
                          (int64_t)(p_T_bytes(p_ipt(p), p) + p_H_bytes(p_ipt(p), p));
     return room >= 2 * 8 * (int64_t)kYStageBytes;
@@ -990,8 +988,8 @@ static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false) {
 // K blocks per W stage: 8 (one MMA-issuer loop per 1024 K) unless that
 // leaves fewer than two stages (large p / the exact mode's terms): then 4, 2, 1
 static int p_kbs(int p, int npad, int P, bool exact = false) {
-    const char* e = getenv("HUBGPU_TCP_KBS");  // tuning override
-    if (e && atoi(e) >= 1 && atoi(e) <= 8) return atoi(e);
+    const int ek = env_int("HUBGPU_TCP_KBS", 0);  // tuning override
+    if (ek >= 1 && ek <= 8) return ek;
     const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact);
     int k = 8;
     while (k > 1 && room < 2 * (int64_t)k * kYStageBytes) k /= 2;
@@ -1002,8 +1000,8 @@ static int p_stages(int p, int npad, int P, bool exact = false) {
     const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact);
     int64_t s = room / ((int64_t)p_kbs(p, npad, P, exact) * kYStageBytes);
     if (s > kYMaxStages) s = kYMaxStages;
-    const char* e = getenv("HUBGPU_TCP_STAGES");  // tuning override (shallower only)
-    if (e && atoi(e) >= 2 && atoi(e) < s) s = atoi(e);
+    const int es = env_int("HUBGPU_TCP_STAGES", 0);  // tuning override (shallower only)
+    if (es >= 2 && es < s) s = es;
     return (int)s;
 }
 
@@ -1079,7 +1077,7 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
               p_exact(I.p, I.npad, I.wplanes) && I.pwl != nullptr;
     // the triangular fold of W (half the MMA work) whenever the bins need not
     // be the reference's own flows: symmetric costs, fixed-order sums
-    A.tri = !A.exact && tri_avail && !(getenv("HUBGPU_TCP_NOTRI")) ? 1 : 0;
+    A.tri = !A.exact && tri_avail && !env_int("HUBGPU_TCP_NOTRI", 0) ? 1 : 0;
     A.P = A.tri ? I.wplanes_tri : I.wplanes;
     A.stages = p_stages(I.p, I.npad, A.P, A.exact);  // as tcp_smem_bytes
     A.kbs = p_kbs(I.p, I.npad, A.P, A.exact);
@@ -1091,10 +1089,7 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     if (A.P > kYMaxPlanes) A.P = 1;  // one launch per plane (launch_fitness_tcp)
     A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
     A.timing = tc_timing_buffer();
-    {
-        const char* e = getenv("HUBGPU_TCP_DBG");
-        A.dbg = e ? atoi(e) : 0;
-    }
+    A.dbg = env_int("HUBGPU_TCP_DBG", 0);
     A.leaves = I.pwl;
     A.nleaf = I.npwl;
     // whole clusters only, all co-resident (one wave): the GPCs need not hold a

@@ -3,6 +3,9 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <mutex>
+#include <string>
+#include <unordered_map>
 #include <cstdlib>
 
 #include "hg_internal.cuh"
@@ -69,6 +72,23 @@ int tc_make_wmap(const uint8_t* W8, int npad_tc, int box_rows, void* map_out, in
 }  // namespace hg
 
 namespace hg {
+
+int env_int(const char* name, int dflt) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(name);
+    if (it != cache.end()) return it->second;
+    const char* e = getenv(name);
+    int v = dflt;
+    if (e) {
+        char* end = nullptr;
+        const long x = strtol(e, &end, 10);
+        v = end != e ? (int)x : 1;
+    }
+    cache.emplace(name, v);
+    return v;
+}
 
 static std::atomic<uint64_t> g_launches{0};
 

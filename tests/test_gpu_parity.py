@@ -111,7 +111,9 @@ class TestObjective:
         good = hg.evaluate_population(inst, pop)
         for bad_row, mutate in ((17, lambda h: h.__setitem__(2, h[1])),      # repeat
                                 (3, lambda h: h.__setitem__(0, -1)),         # negative
-                                (40, lambda h: h.__setitem__(6, 300))):      # >= n
+                                (40, lambda h: h.__setitem__(6, 300)),       # >= n
+                                (41, lambda h: h.__setitem__(6, 10**12)),    # far out
+                                (49, lambda h: h.__setitem__(0, -10**12))):
             bad = pop.copy()
             mutate(bad[bad_row])
             with pytest.raises(ValueError, match=f"hub set {bad_row}:"):
