@@ -47,7 +47,7 @@ POP = 8192
 HBM_FALLBACK = 6650.0
 
 
-NCU_TRAFFIC_FILE = "profiles/ncu_traffic_r1m.json"
+NCU_TRAFFIC_FILE = "profiles/ncu_traffic_r2.json"
 
 
 def ncu_traffic(fit_kernel):
@@ -65,6 +65,21 @@ def ncu_traffic(fit_kernel):
     for name, v in ks.items():
         if re.search(pat, name):
             return v["dram_bytes"]
+    return None
+
+
+def ncu_kernel_record(pattern):
+    """The committed ncu record of the first kernel matching `pattern`."""
+    import re
+
+    try:
+        with open(ROOT / NCU_TRAFFIC_FILE) as f:
+            ks = json.load(f)["kernels"]
+    except (OSError, ValueError, KeyError):
+        return None
+    for name, v in ks.items():
+        if re.search(pattern, name):
+            return v
     return None
 
 
@@ -307,6 +322,22 @@ def ga_time_to_target(hg, inst, args):
 # ---------------------------------------------------------------------------
 
 
+def k2_roofline(k2_ms):
+    """K2 (nearest-hub allocation) is bound by L1/TEX: its Cq rows (p*n*2 B
+    per eval, coalesced) and the fp64 leg gathers (one sector per node);
+    frac = ncu's l1tex throughput of the committed capture."""
+    rec = ncu_kernel_record(r"k_allocate")
+    out = {"kernel": "k_allocate_r (K2: 16-bit pre-filtered argmin, legs, cluster ids)",
+           "kernel_ms": k2_ms, "bound": "L1/TEX (gather)",
+           "cq_bytes_per_launch": POP * P * N * 2.0}
+    if rec:
+        out.update({"frac": rec["l1tex_throughput_pct"] / 100.0,
+                    "frac_source": f"ncu l1tex__throughput.avg.pct_of_peak_sustained_active, "
+                                   f"{NCU_TRAFFIC_FILE}",
+                    "traffic": rec["dram_bytes"]})
+    return out
+
+
 def run_gpu(args):
     import torch
 
@@ -501,6 +532,7 @@ def run_gpu(args):
                          "note": "achieved = int8 ops the kernel issues per launch / its "
                                  "event-timed duration; useful = 2 n^2 p per eval, the full "
                                  "contraction the triangular fold halves",
+                         "k2": k2_roofline(float(np.mean(k2_ms))),
                          "hbm_view": {"alg_bytes_per_launch": alg_bytes,
                                       "alg_gbs": alg_bytes / (fit_avg * 1e-3) / 1e9,
                                       "hbm_peak_gbs": hbm, "peak_source": hbm_src,

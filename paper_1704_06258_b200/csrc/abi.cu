@@ -236,14 +236,15 @@ static uint32_t* T_for(const hg_inst* inst, int64_t B, uint32_t* T) {
 // K3 (fp64 gather) or K3-TC (tensor cores) + finalise, by the instance's choice
 int queue_fitness(hg_inst* inst, int64_t B, const int32_t* hubs, const uint8_t* cl,
                   const uint16_t* co, const uint32_t* T, double* part, const double* legs,
-                  double* out) {
+                  double* out, const int32_t* dynB = nullptr) {
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
     const int kind = fitness_kernel(inst);
     int tiles;
     if (kind == HG_FIT_TC_PAIR || kind == HG_FIT_TC_PAIR_FULL)  // finaliser fused
         return launch_fitness_tcp(I, inst->wmapp, kind == HG_FIT_TC_PAIR ? inst->wmapt : nullptr,
-                                  B, cl, T, part, inst->sm_count, s, legs, out, hubs);
+                                  B, cl, T, part, inst->sm_count, s, legs, out, hubs, dynB);
+    HG_ARG(dynB == nullptr, "a device-side batch bound needs the tensor kernel");
     HG_TRY(launch_fitness(I, inst->plan, B, cl, co, T, part,
                           inst->sm_count * inst->plan.blocks_per_sm, s));
     tiles = inst->plan.tiles;
@@ -1099,6 +1100,15 @@ int hg_swap(int device, int n, int64_t B, const uint8_t* masks, const int64_t* r
 struct hg_ga {
     hg_inst* inst = nullptr;
     hg_pop* pop = nullptr;
+    // per-generation duplicate grouping (the reference's memo
+    // hm/engine.py:102-129): each distinct child hub set scored once
+    bool dedupe = false;
+    int32_t* uhubs = nullptr;  // [B][p] one representative per group
+    int32_t* umap = nullptr;   // [B] group of child b
+    int32_t* ucount = nullptr; // [3] slot[B-1], flag[B-1], groups
+    double* uout = nullptr;    // [B][4] the groups' costs
+    unsigned char* uscratch = nullptr;
+    size_t uscratch_bytes = 0;
     hg_ga_params prm{};
     GaDev G{};
     int64_t B = 0;
@@ -1110,6 +1120,20 @@ struct hg_ga {
 };
 
 namespace {
+
+// C(n, p) saturated at 2^63
+uint64_t binom_sat(int n, int p) {
+    const uint64_t cap = 1ull << 63;
+    uint64_t c = 1;
+    for (int i = 1; i <= p; ++i) {
+        // c * (n - p + i) / i stays an integer at every step
+        const unsigned __int128 t = (unsigned __int128)c * (uint64_t)(n - p + i) / (uint64_t)i;
+        if (t >= cap) return cap;
+        c = (uint64_t)t;
+    }
+    return c;
+}
+
 
 template <class T>
 int ga_alloc(hg_ga* ga, T** p, size_t count) {
@@ -1129,16 +1153,32 @@ int ga_queue_generation(hg_ga* ga) {
     HG_TRY(launch_mut_scan(G, s));
     HG_TRY(launch_mutate(G, s));
     HG_TRY(launch_correct(inst->I, ga->B, G.kids, 2 * G.p, G.khubs, s));
-    HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl, co_for(inst, ga->pop->co),
-                           T_for(inst, ga->B, ga->pop->T), ga->pop->legs, nullptr, s));
-    HG_TRY(queue_fitness(inst, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->co, ga->pop->T,
-                         ga->pop->part, ga->pop->legs, ga->pop->out));
+    if (ga->dedupe) {
+        // group the children's hub sets, score one per group (K2 and K3 bounded
+        // by the device-side group count), copy each group's costs to its
+        // members: the selection sees exactly the costs of scoring them all
+        HG_TRY(launch_unique_groups(ga->pop->hubs, ga->B, G.p, ga->uscratch, ga->uscratch_bytes,
+                                    ga->uhubs, ga->umap, ga->ucount, s, ga->ucount + 2));
+        HG_TRY(launch_allocate(inst->I, ga->B, ga->uhubs, ga->pop->cl, co_for(inst, ga->pop->co),
+                               T_for(inst, ga->B, ga->pop->T), ga->pop->legs, nullptr, s,
+                               ga->ucount + 2));
+        HG_TRY(queue_fitness(inst, ga->B, ga->uhubs, ga->pop->cl, ga->pop->co, ga->pop->T,
+                             ga->pop->part, ga->pop->legs, ga->uout, ga->ucount + 2));
+        HG_TRY(launch_scatter_out(ga->uout, ga->umap, ga->B, ga->pop->out, s));
+    } else {
+        HG_TRY(launch_allocate(inst->I, ga->B, ga->pop->hubs, ga->pop->cl,
+                               co_for(inst, ga->pop->co), T_for(inst, ga->B, ga->pop->T),
+                               ga->pop->legs, nullptr, s));
+        HG_TRY(queue_fitness(inst, ga->B, ga->pop->hubs, ga->pop->cl, ga->pop->co, ga->pop->T,
+                             ga->pop->part, ga->pop->legs, ga->pop->out));
+    }
     HG_TRY(launch_select(G, s));
     return HG_OK;
 }
 
 // build_pop, crossover, mut_scan, mutate, correct, allocate, fitness, [finalise,] select
-int ga_launches(const hg_ga* ga) { return fitness_kernel(ga->inst) == HG_FIT_FP64 ? 9 : 8; }
+// (+ hash, group flags, compact, count, scatter and two CUB passes when deduplicating)
+int ga_launches(const hg_ga* ga) { return ga->graph_kernels; }
 
 void ga_release(hg_ga* ga) {
     if (ga->exec) cudaGraphExecDestroy(ga->exec);
@@ -1214,6 +1254,25 @@ int hg_ga_create(hg_inst* inst, const hg_ga_params* prm, hg_ga** out) {
         if ((rc = ga_alloc(ga, &G.st, (size_t)nloc * 3))) break;
         if ((rc = ga_alloc(ga, &G.ctr, (size_t)nloc * 3))) break;
         if ((rc = ga_alloc(ga, &ga->inc, p))) break;
+        // per-generation duplicate grouping: off unless HUBGPU_GA_DEDUPE=1.
+        // Measured (tools/ga_dedupe_probe.py, profiles/ga_dedupe_r2.json): the
+        // grouping (hash, CUB sort, scan, compact, scatter) costs more than
+        // scoring the duplicates at every BASELINE shape, CAB's 4x duplication
+        // included -- the memo pays on the CPU, not here.  Tensor kernel only
+        // (it takes the device-side group count as its batch bound).
+        {
+            const int fk = fitness_kernel(inst);
+            ga->dedupe = (fk == HG_FIT_TC_PAIR || fk == HG_FIT_TC_PAIR_FULL) &&
+                         env_int("HUBGPU_GA_DEDUPE", 0) > 0;
+        }
+        if (ga->dedupe) {
+            ga->uscratch_bytes = unique_scratch_bytes(ga->B);
+            if ((rc = ga_alloc(ga, &ga->uscratch, ga->uscratch_bytes))) break;
+            if ((rc = ga_alloc(ga, &ga->uhubs, B * p))) break;
+            if ((rc = ga_alloc(ga, &ga->umap, B))) break;
+            if ((rc = ga_alloc(ga, &ga->ucount, 3))) break;
+            if ((rc = ga_alloc(ga, &ga->uout, B * 4))) break;
+        }
         G.khubs = ga->pop->hubs;
         G.kraw = ga->pop->out;
         G.inc = ga->inc;
@@ -1440,18 +1499,6 @@ int hg_generate_urand(int device, int n, int p, uint64_t seed, double* dist, dou
     return rc;
 }
 
-// C(n, p) saturated at 2^63
-static uint64_t binom_sat(int n, int p) {
-    const uint64_t cap = 1ull << 63;
-    uint64_t c = 1;
-    for (int i = 1; i <= p; ++i) {
-        // c * (n - p + i) / i stays an integer at every step
-        const unsigned __int128 t = (unsigned __int128)c * (uint64_t)(n - p + i) / (uint64_t)i;
-        if (t >= cap) return cap;
-        c = (uint64_t)t;
-    }
-    return c;
-}
 
 int hg_restricted_optimum(hg_inst* inst, uint64_t limit, int64_t* best_hubs, double* best_raw,
                           uint64_t* count_out) {

@@ -125,6 +125,9 @@ struct DevInst {
     // reference); 0: fixed-order sums (deterministic, ~1 ulp apart)
     int exact;
     int bins_total_ok;  // total flow < 2^32: integer bins can span every K chunk
+    // a device-side batch size (the GA's distinct-hub-set count) bounding a
+    // launch sized for the host batch; nullptr: the host batch
+    const int32_t* dynB;
 };
 
 constexpr int kPwStack = 16;  // tree depth bound (n < 2^21)
@@ -155,7 +158,8 @@ int launch_quantize(const double* Ct, uint16_t* Cq, int n, int nq, double cmin, 
                     cudaStream_t s);
 int prepare_allocate(const DevInst& I);
 int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
-                    uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s);
+                    uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s,
+                    const int32_t* dynB = nullptr);
 int launch_from_alloc(const DevInst& I, int64_t B, const int32_t* hubs, const int32_t* alloc,
                       uint8_t* cl, uint16_t* co, uint32_t* T, double* legs, cudaStream_t s);
 int launch_fitness(const DevInst& I, const FitPlan& P, int64_t B, const uint8_t* cl,
@@ -201,7 +205,8 @@ double tcp_mma_ops(const DevInst& I, bool tri_avail, int64_t B, int grid);
 // wmap_tri: the map of the triangular fold (symmetric costs), or nullptr
 int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
                        const uint8_t* cl, const uint32_t* T, double* part, int grid,
-                       cudaStream_t s, const double* legs, double* out, const int32_t* hubs);
+                       cudaStream_t s, const double* legs, double* out, const int32_t* hubs,
+                       const int32_t* dynB = nullptr);
 // true: the launch gathers the hub-cost tables from C itself (K2 need not write T)
 bool tcp_gathers_T(const DevInst& I, bool tri_avail, int64_t B, int grid);
 
@@ -219,8 +224,10 @@ size_t unique_scratch_bytes(int64_t B);
 // groups the B hub sets (int32 [B][p]); writes one representative per group to
 // uhubs (dense, in sorted-hash order), map[b] = group of set b, and
 // d_count[0] + d_count[1] = number of groups
+// d_total (optional): the group count itself, written on the device
 int launch_unique_groups(const int32_t* hubs, int64_t B, int p, void* scratch, size_t bytes,
-                         int32_t* uhubs, int32_t* map, int32_t* d_count, cudaStream_t s);
+                         int32_t* uhubs, int32_t* map, int32_t* d_count, cudaStream_t s,
+                         int32_t* d_total = nullptr);
 int launch_scatter_out(const double* uout, const int32_t* map, int64_t B, double* out,
                        cudaStream_t s);
 

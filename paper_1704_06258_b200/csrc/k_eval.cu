@@ -418,7 +418,7 @@ k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __re
     __shared__ double pwst[K2<LM>::warps][K2<LM>::stack];   // the two tree stacks
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * K2<LM>::warps + warp;
-    if (b >= B) return;
+    if (b >= B || (I.dynB && b >= *I.dynB)) return;
     const int p = I.p, nq = I.nq;
     int32_t* hs = hs_all[warp];
     double* ring = pwring[warp];
@@ -523,7 +523,7 @@ k_allocate_r(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __
     __shared__ double pwst[K2<LM>::warps][K2<LM>::stack];   // the two tree stacks
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * K2<LM>::warps + warp;
-    if (b >= B) return;
+    if (b >= B || (I.dynB && b >= *I.dynB)) return;
     const int n = I.n, p = I.p, nq = I.nq;
     int32_t* hs = hs_all[warp];
     uint32_t* ro = ro_all[warp];
@@ -583,9 +583,12 @@ static bool k2_scalar() {
     return v;
 }
 
-int launch_allocate(const DevInst& I, int64_t B, const int32_t* hubs, uint8_t* cl, uint16_t* co,
-                    uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s) {
+int launch_allocate(const DevInst& Iin, int64_t B, const int32_t* hubs, uint8_t* cl,
+                    uint16_t* co, uint32_t* T, double* legs, int32_t* alloc, cudaStream_t s,
+                    const int32_t* dynB) {
     if (B <= 0) return HG_OK;
+    DevInst I = Iin;
+    I.dynB = dynB;
     // legs == nullptr: the fitness kernel computes the leg sums itself
     // legs == nullptr: allocation only; else the instance's summation mode
     auto go = [&](auto mode) {
@@ -629,7 +632,7 @@ k_from_alloc(DevInst I, int64_t B, const int32_t* __restrict__ hubs,
     __shared__ double pwst[K2<LM>::warps][K2<LM>::stack];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * K2<LM>::warps + warp;
-    if (b >= B) return;
+    if (b >= B || (I.dynB && b >= *I.dynB)) return;
     const int n = I.n, p = I.p;
     int32_t* hs = hs_all[warp];
     double* ring = pwring[warp];

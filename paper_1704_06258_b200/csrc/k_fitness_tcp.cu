@@ -242,6 +242,7 @@ __host__ __device__ inline size_t p_H_bytes(int ipt, int p) {
 }
 
 struct PArgs {
+    const int32_t* dB;   // device-side batch size bounding B (nullptr: B)
     const uint8_t* cl;
     const uint32_t* T;   // K2's hub-cost tables (read when !tsm)
     const int32_t* hubs; // [B][p] sorted hubs (tsm: T_b gathered from C here)
@@ -397,7 +398,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     // A phase is (slot, chunk): one resident one-hot, ITO output tiles.
     const uint32_t crank = cluster_rank();
     const int64_t ncl = gridDim.x / kYCluster, cid = blockIdx.x / kYCluster;
-    const int64_t cs0 = A.units * cid / ncl, cs1 = A.units * (cid + 1) / ncl;
+    // the batch: the host's, or a device-side count bounding it (the GA's
+    // distinct hub sets); units of ipt individuals
+    const int64_t Bk = A.dB ? (int64_t)*A.dB : A.B;
+    const int64_t units = A.dB ? (Bk + ipt - 1) / ipt : A.units;
+    const int64_t cs0 = units * cid / ncl, cs1 = units * (cid + 1) / ncl;
     const int64_t nslots = (cs1 - cs0 + kYCluster - 1) / kYCluster;
     const bool leader = crank == 0;
     // the leader's barriers as shared::cluster addresses (remote for the peer)
@@ -408,7 +413,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     auto slot_unit = [&](int64_t j, int64_t& bbase, int& nind) {
         const int64_t u = cs0 + j * kYCluster + crank;
         bbase = u * ipt;
-        nind = u < cs1 ? (int)(A.B - bbase < ipt ? A.B - bbase : ipt) : 0;
+        nind = u < cs1 ? (int)(Bk - bbase < ipt ? Bk - bbase : ipt) : 0;
     };
 
     if (warp == 1) {
@@ -542,7 +547,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         uint32_t t = 0;
         const bool timed = kTimingBuild && A.timing != nullptr && tid == kYEpiWarp0 * 32;
         unsigned long long e_st = 0, e_gen = 0, e_wait = 0, e_cmp = 0, e_red = 0, e_ld = 0;
-        unsigned long long e_sync = 0, e_tload = 0, e_fold = 0, e_kbf = 0;
+        unsigned long long e_sync = 0, e_tload = 0, e_fold = 0, e_kbf = 0, e_drain = 0;
         long long c0 = timed ? clock64() : 0;
 #define ET(acc_)                                    \
     do {                                            \
@@ -880,6 +885,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 ET(e_tload);
                 epi_sync();  // every bin of the chunk is complete
                 ET(e_sync);
+                if (timed) {  // the shared-memory pipe behind the atomics (timing build only)
+                    uint32_t x0;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x0) : "r"(bin_r0) : "memory");
+                    asm volatile("add.u32 %0, %0, 1;" : "+r"(x0));
+                    if (x0 == 0xFFFFFFFFu) A.timing[31] = 1;
+                    ET(e_drain);
+                }
                 if (live && EX && c + 1 == NC) {
                     // the bins (every K chunk accumulated, planes weighted
                     // 256^pl) ARE the reference's inter-cluster flows, exact
@@ -932,6 +944,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             atomicAdd(A.timing + 23, e_tload);
             atomicAdd(A.timing + 24, e_fold);
             atomicAdd(A.timing + 25, e_kbf);
+            atomicAdd(A.timing + 26, e_drain);
         }
     }
     fence_before();
@@ -1103,6 +1116,7 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
 
 bool tcp_gathers_T(const DevInst& I, bool tri_avail, int64_t B, int grid) {
     PArgs A;
+    A.dB = nullptr;
     tcp_setup(I, tri_avail, B > 0 ? B : 1, grid, A);
     return A.tsm != 0;
 }
@@ -1113,6 +1127,7 @@ bool tcp_gathers_T(const DevInst& I, bool tri_avail, int64_t B, int grid) {
 double tcp_mma_ops(const DevInst& I, bool tri_avail, int64_t B, int grid) {
     if (B <= 0) return 0.0;
     PArgs A;
+    A.dB = nullptr;
     const int g = tcp_setup(I, tri_avail, B, grid, A);
     double blocks = 0.0;  // K blocks per pair slot
     for (int c = 0; c < A.NC; ++c) {
@@ -1135,9 +1150,11 @@ static int tcp_launch(const DevInst& I, const PArgs& A, int g, const void* wmap,
 
 int launch_fitness_tcp(const DevInst& I, const void* wmap, const void* wmap_tri, int64_t B,
                        const uint8_t* cl, const uint32_t* T, double* part, int grid,
-                       cudaStream_t s, const double* legs, double* out, const int32_t* hubs) {
+                       cudaStream_t s, const double* legs, double* out, const int32_t* hubs,
+                       const int32_t* dynB) {
     if (B <= 0) return HG_OK;
     PArgs A;
+    A.dB = dynB;
     A.cl = cl;
     A.T = T;
     A.hubs = hubs;

@@ -62,6 +62,11 @@ __global__ void k_scatter_out(const double* __restrict__ uout, const int32_t* __
         out[x] = uout[(int64_t)map[x >> 2] * 4 + (x & 3)];
 }
 
+__global__ void k_group_total(const int32_t* __restrict__ slot, const int32_t* __restrict__ flag,
+                              int64_t B, int32_t* __restrict__ total) {
+    *total = slot[B - 1] + flag[B - 1];
+}
+
 int grid256(int64_t count) {
     int64_t g = (count + 255) / 256;
     return (int)(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -83,7 +88,8 @@ size_t unique_scratch_bytes(int64_t B) {
 }
 
 int launch_unique_groups(const int32_t* hubs, int64_t B, int p, void* scratch, size_t bytes,
-                         int32_t* uhubs, int32_t* map, int32_t* d_count, cudaStream_t s) {
+                         int32_t* uhubs, int32_t* map, int32_t* d_count, cudaStream_t s,
+                         int32_t* d_total) {
     HG_ARG(B < (1ll << 31), "batch too large for duplicate grouping");
     unsigned char* w = static_cast<unsigned char*>(scratch);
     uint64_t* kin = reinterpret_cast<uint64_t*>(w);
@@ -108,6 +114,10 @@ int launch_unique_groups(const int32_t* hubs, int64_t B, int p, void* scratch, s
     HG_CUDA(cudaMemcpyAsync(d_count, slot + B - 1, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     HG_CUDA(cudaMemcpyAsync(d_count + 1, flag + B - 1, sizeof(int32_t), cudaMemcpyDeviceToDevice,
                             s));
+    if (d_total) {
+        k_group_total<<<1, 1, 0, s>>>(slot, flag, B, d_total);
+        HG_LAUNCHED();
+    }
     return HG_OK;
 }
 

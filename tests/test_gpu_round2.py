@@ -19,7 +19,10 @@ import hashlib
 import json
 import os
 import socket
+import subprocess
+import sys
 from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -27,6 +30,8 @@ import pytest
 from conftest import golden, orc
 
 import paper_1704_06258_b200 as hg
+
+ROOT = Path(__file__).resolve().parent.parent
 
 pytestmark = pytest.mark.gpu
 
@@ -323,3 +328,17 @@ class TestFractionalFlows:
             a = orc.nearest(pr.C, pop[b])
             c, t, d = orc.cost_terms(pr, pop[b], a)
             assert np.array_equal(ex[b], [c, t, d, c + t + d]), b
+
+
+@pytest.mark.gpu
+def test_ga_replays_with_duplicate_grouping_forced():
+    """The GA's per-generation duplicate grouping must leave the
+    trajectory unchanged: rerun the GA replay tests with it forced on for every
+    tensor-kernel GA (the switch is read once per process, hence the child)."""
+    env = dict(os.environ, HUBGPU_GA_DEDUPE="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p",
+                        "no:cacheprovider", "tests/test_gpu_parity.py::TestGa",
+                        "tests/test_gpu_round2.py::TestGaFullShapes",
+                        "tests/test_gpu_round2.py::TestFractionalFlows"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -68,12 +68,18 @@ def one(n: int, p: int, B: int) -> dict:
 
 CONFIGS = [
     ("default (tri)", {}),
-    ("full W", {"HUBGPU_TCP_NOTRI": "1"}),
-    ("tri, T from K2 via global", {"HUBGPU_TCP_TSM": "0"}),
-    ("tri, no epilogue warps", {"HUBGPU_TCP_DBG": "64"}),
-    ("epilogue, no MMA", {"HUBGPU_TCP_DBG": "2"}),
+    ("no bin atomics", {"HUBGPU_TCP_DBG": "1"}),
+    ("no fold/reduce", {"HUBGPU_TCP_DBG": "4"}),
+    ("no one-hot generation", {"HUBGPU_TCP_DBG": "8"}),
+    ("no MMA", {"HUBGPU_TCP_DBG": "2"}),
+    ("no MMA, no atomics", {"HUBGPU_TCP_DBG": "3"}),
+    ("no MMA: drain + W only", {"HUBGPU_TCP_DBG": "15"}),
+    ("no epilogue warps", {"HUBGPU_TCP_DBG": "64"}),
+    ("no epilogue, no MMA: W stream", {"HUBGPU_TCP_DBG": "66"}),
     ("MMA issue alone (no epilogue, no W stream)", {"HUBGPU_TCP_DBG": "112"}),
+    ("full W", {"HUBGPU_TCP_NOTRI": "1"}),
 ]
+# (phase counters, HUBGPU_TC_TIMING=1, need a timing build: make EXTRA=-DHG_TCP_TIMING)
 # (phase counters, HUBGPU_TC_TIMING=1, need a timing build: make EXTRA=-DHG_TCP_TIMING)
 
 
