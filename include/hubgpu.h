@@ -150,6 +150,8 @@ int hg_launch_count(uint64_t* count);
 /* tuning aid: per-phase cycle counters of K3-TC when the process runs with
  * HUBGPU_TC_TIMING=1 (32 counters, read and reset); HG_EARG otherwise */
 int hg_debug_tc_timing(unsigned long long* out32);
+/* Timing build only: K3-TC/P's event trace of CTA 0 (3 x 8192 words). */
+int hg_debug_tc_trace(unsigned long long* out);
 
 /* K4c -- correction.  Replaces correct_hub_set (hm/operators.py:69-101) for
  * B raw hub masks (B x n bytes): deficit opens closed nodes in middle-rank

@@ -18,6 +18,9 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libhubgpu.so"
+# tuning only (tools/ab_k3.py): another in-tree build of the same library
+if os.environ.get("HUBGPU_LIB_VARIANT"):
+    LIB_PATH = LIB_PATH.with_name(f"libhubgpu_{os.environ['HUBGPU_LIB_VARIANT']}.so")
 
 HG_OK, HG_EARG, HG_ECUDA, HG_ENODEV, HG_ESTATE = 0, 1, 2, 3, 4
 HG_HOST, HG_DEVICE = 0, 1
@@ -73,6 +76,7 @@ SIGNATURES = {
     "hg_pop_last_fitness_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "hg_pop_last_allocate_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "hg_debug_tc_timing": (C.c_int, [_u64p]),
+    "hg_debug_tc_trace": (C.c_int, [_u64p]),
     "hg_launch_count": (C.c_int, [_u64p]),
     "hg_fitness_work": (C.c_int, [_vp, C.c_int64, _f64p]),
     "hg_correct": (C.c_int, [_vp, C.c_int64, _u8p, _i64p]),

@@ -953,6 +953,11 @@ int hg_debug_tc_timing(unsigned long long* out32) {
     return tc_timing_read(out32);
 }
 
+int hg_debug_tc_trace(unsigned long long* out) {
+    HG_ARG(out != nullptr, "NULL buffer");
+    return tc_trace_read(out);
+}
+
 int hg_pop_launches_per_evaluate(const hg_pop* pop) {
     return fitness_kernel(pop->inst) == HG_FIT_FP64 ? 3 : 2;
 }

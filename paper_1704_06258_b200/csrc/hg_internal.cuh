@@ -186,6 +186,7 @@ int launch_build_planes(const double* W, int n, int nt, double wscale, int P, in
 
 // ---- K3-TC/P helpers (tc_common.cu) ------------------------------------------
 int tc_timing_read(unsigned long long* out32);
+int tc_trace_read(unsigned long long* out);
 unsigned long long* tc_timing_buffer();  // HUBGPU_TC_TIMING=1, else nullptr
 // map_out: CUtensorMap (128 B) over the u8 W, boxes of 128 K bytes x box_rows rows
 // rows: total rows of the (plane-stacked) tensor, default npad_tc

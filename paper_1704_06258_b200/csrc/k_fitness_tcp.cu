@@ -54,6 +54,16 @@ constexpr bool kTimingBuild = true;
 #else
 constexpr bool kTimingBuild = false;
 #endif
+// timing build: an event trace of CTA 0 (clock64 stamps, code in the top
+// byte) at timing[64 + role * kTraceLen ..]; roles 0 = MMA issuer, 1 = epilogue
+// warp 4 (lane quadrant 0, column quarter 0), 2 = epilogue warp 19 (3, 3)
+constexpr int kTraceLen = 8192;
+#define TRC(role_, code_)                                                                   \
+    do {                                                                                    \
+        if (kTimingBuild && tr_on && tr_n < kTraceLen)                                      \
+            A.timing[64 + (role_) * kTraceLen + tr_n++] =                                   \
+                ((unsigned long long)(code_) << 56) | ((unsigned long long)clock64() & ((1ull << 56) - 1)); \
+    } while (0)
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -219,12 +229,28 @@ __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
 // epilogue's tile loop is register-bound
 __device__ __noinline__ double fold_bins(uint32_t* bp, const double* tbd, const uint32_t* tbp,
                                          int p, int ps, int sub, double sc, double s) {
-    for (int k = sub; k < p; k += 4) {
+    auto tv = [&](int k) {
+        return tbd ? tbd[k * p] : __hiloint2double((int)tbp[k * ps], (int)tbp[(p + k) * ps]);
+    };
+    int k = sub;
+    // four bins at a time, their loads issued together (same summation order)
+    for (; k + 12 < p; k += 16) {
+        const uint32_t g0 = bp[k * 128], g1 = bp[(k + 4) * 128], g2 = bp[(k + 8) * 128],
+                       g3 = bp[(k + 12) * 128];
+        const double t0 = tv(k), t1 = tv(k + 4), t2 = tv(k + 8), t3 = tv(k + 12);
+        bp[k * 128] = 0u;
+        bp[(k + 4) * 128] = 0u;
+        bp[(k + 8) * 128] = 0u;
+        bp[(k + 12) * 128] = 0u;
+        s = fma((double)g0, t0 * sc, s);
+        s = fma((double)g1, t1 * sc, s);
+        s = fma((double)g2, t2 * sc, s);
+        s = fma((double)g3, t3 * sc, s);
+    }
+    for (; k < p; k += 4) {
         const uint32_t g = bp[k * 128];
         bp[k * 128] = 0u;
-        const double t = tbd ? tbd[k * p]
-                             : __hiloint2double((int)tbp[k * ps], (int)tbp[(p + k) * ps]);
-        s = fma((double)g, t * sc, s);
+        s = fma((double)g, tv(k) * sc, s);
     }
     return s;
 }
@@ -455,6 +481,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         if (leader) {  // the whole warp, converged; one lane issues
             uint32_t s = 0, ph = 0, t = 0, phase = 0;
             const bool timed = kTimingBuild && A.timing != nullptr;
+            const bool tr_on = timed && blockIdx.x == 0 && lane == 0;
+            int tr_n = 0;
             unsigned long long w_a = 0, w_e = 0, w_f = 0, w_i = 0;
             long long c0 = timed ? clock64() : 0;
 #define YT(acc_)                                    \
@@ -480,8 +508,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         for (int it = 0; it < T; ++it, ++t) {
                             const int d = t & 1, k0 = klo(c, it);
                             const bool first = (pl | it) == 0;
+                            TRC(0, 1);
                             if (t >= 2 && !(A.dbg & 64))
                                 mb_wait_cl(b_acce + 8 * d, ((t >> 1) - 1) & 1);
+                            TRC(0, 2);
                             YT(w_e);
                             fence_after();
                             const uint32_t dcol = tmem + kYAcc0 + d * 128;
@@ -492,6 +522,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                             for (int kb0 = k0; kb0 < nb; kb0 += KBS) {
                                 const int nk = nb - kb0 < KBS ? nb - kb0 : KBS;
                                 if (!(A.dbg & 16)) mb_wait(b_full + 8 * s, ph);
+                                TRC(0, 3);
                                 YT(w_f);
                                 fence_after();
                                 const uint64_t bd0 = sw128(su32(ring + s * (KBS * kYStageBytes)));
@@ -502,9 +533,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                         // in TMEM before its first block's MMAs
                                         uint32_t wq = (waitq >> (4 * kb)) & 15u;
                                         if (wq) {
+                                            TRC(0, 4);
                                             for (; wq; wq &= wq - 1)
                                                 mb_wait_cl(b_ard + 8 * (__ffs(wq) - 1), phase & 1u);
                                             fence_after();
+                                            TRC(0, 5);
                                         }
                                         YT(w_a);
                                     }
@@ -527,6 +560,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                 YT(w_i);
                             }
                             commit_pair_w(b_accf + 8 * d);
+                            TRC(0, 8);
                         }
                 }
             }
@@ -548,6 +582,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         const bool timed = kTimingBuild && A.timing != nullptr && tid == kYEpiWarp0 * 32;
         unsigned long long e_st = 0, e_gen = 0, e_wait = 0, e_cmp = 0, e_red = 0, e_ld = 0;
         unsigned long long e_sync = 0, e_tload = 0, e_fold = 0, e_kbf = 0, e_drain = 0;
+        const bool tr_on = kTimingBuild && A.timing != nullptr && blockIdx.x == 0 && lane == 0 &&
+                           (warp == kYEpiWarp0 || warp == kYWarps - 1);
+        const int tr_role = warp == kYEpiWarp0 ? 1 : 2;
+        int tr_n = 0;
         long long c0 = timed ? clock64() : 0;
 #define ET(acc_)                                    \
     do {                                            \
@@ -734,6 +772,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             uint32_t* const binsj = bins;
             const uint8_t* crow = CSM ? sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
+            TRC(tr_role, 24);
             if (CSM && j + 1 < nslots) {
                 stage(j + 1);  // the next unit's cluster rows, under this unit's MMAs
                 ET(e_st);
@@ -748,10 +787,16 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             {
                 const int etid = tid - kYEpiWarp0 * 32;
                 if (A.tsm) {
+                    // element x = (b2, k, l2) per thread; x / (p*p) and x / p as
+                    // (x * m) >> 32, m = floor((2^32 - 1) / d) + 1 (exact while
+                    // x * d < 2^32: x < 128 p here)
                     const int32_t* hsj = sH + (j & 1) * ipt * p;
                     const int pp = p * p;
+                    const uint64_t mpp = 0xFFFFFFFFull / (uint64_t)pp + 1u;
+                    const uint64_t mp = 0xFFFFFFFFull / (uint64_t)p + 1u;
                     for (int x = etid; x < nind * pp; x += kYEpiThreads) {
-                        const int b2 = x / pp, kl = x - b2 * pp, k = kl / p, l2 = kl - k * p;
+                        const int b2 = (int)(((uint64_t)x * mpp) >> 32), kl = x - b2 * pp;
+                        const int k = (int)(((uint64_t)kl * mp) >> 32), l2 = kl - k * p;
                         const int32_t* hs = hsj + b2 * p;
                         cp_async8(su32(sT) + 8u * x, A.C + (size_t)hs[k] * A.nC + hs[l2]);
                     }
@@ -768,6 +813,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                A.legs + 2 * (bbase + etid));
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
+            TRC(tr_role, 26);
             // this row's T column: fp64 T_b[k][l] at tbd[k * p] (tsm), else K2's
             // hi / lo planes at tbp[k * ps], tbp[(p + k) * ps]
             const double* tbd = A.tsm ? sT + (live ? bl : 0) * p * p + l : nullptr;
@@ -810,7 +856,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 }
                 for (int tt = 0; tt < NT; ++tt, ++t) {
                     const int d = t & 1;
-                    const int pl = tt / T, it = tt - pl * T;
+                    const int pl = A.P == 1 ? 0 : tt / T, it = tt - pl * T;
                     // generate as soon as the quarter is free: the MMA issuer
                     // runs up to two tiles ahead, so poll from two tiles before
                     // the releasing one (the next phase's first MMAs wait on it)
@@ -818,16 +864,19 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         (tt == tt_gen ||
                          (hq >= 0 && __shfl_sync(0xffffffffu,
                                                  (int)mb_try(b_kbf + 8 * hq, phase & 1u), 0)))) {
+                        TRC(tr_role, 11);
                         if (hq >= 0) {
                             mb_wait(b_kbf + 8 * hq, phase & 1u);
                             fence_after();
                         }
+                        TRC(tr_role, 12);
                         ET(e_kbf);
                         if (c + 1 < NC)
                             gen(j, c + 1);
                         else
                             gen(j + 1, 0);
                         gen_done = true;
+                        TRC(tr_role, 13);
                         ET(e_gen);
                     }
                     // cluster ids of the 32 columns i = it*128 + sub*32 + k
@@ -837,7 +886,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         ca = cp[0];
                         cz = cp[1];
                     }
+                    TRC(tr_role, 14);
                     mb_wait(b_accf + 8 * d, (t >> 1) & 1);
+                    TRC(tr_role, 15);
                     ET(e_wait);
                     fence_after();
                     const uint32_t dcol = tmem + lane_base + kYAcc0 + d * 128 + sub * 32;
@@ -849,6 +900,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     fence_before();
                     __syncwarp();
                     if (lane == 0) arrive_remote(L_acce + 8 * d);  // accumulator may be overwritten
+                    TRC(tr_role, 16);
                     if (live && !(A.dbg & 1)) {
                         // G[c_i][r] += D[r][i]: exact integer bins, this row's own
                         // (4 column-quarter warps share a row, hence the atomics)
@@ -865,18 +917,21 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                          : "memory");
                         }
                     }
+                    TRC(tr_role, 17);
                     ET(e_cmp);
                     if (c == 0 && tt == 0 && j > 0 && !(A.dbg & 4)) {  // the previous unit's reduce
                         int64_t pb;
                         int pn;
                         slot_unit(j - 1, pb, pn);
                         reduce_unit(pb, pn, j - 1);
+                        TRC(tr_role, 18);
                         ET(e_red);
                     }
                 }
                 // this chunk's bins into S_T: sum_k T_b[k][l] * G_c[k][(b,l)] over
                 // k = sub, sub + 4, ... (fixed order -> deterministic); one chunk's
                 // bins stay below 2^32 (<= 255 * 1024 * n, n <= 16384).
+                TRC(tr_role, 20);
                 asm volatile("cp.async.wait_all;" ::: "memory");  // T, legs: this thread's part
                 auto tval = [&](int k) {
                     return tbd ? tbd[k * p]
@@ -884,6 +939,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 };
                 ET(e_tload);
                 epi_sync();  // every bin of the chunk is complete
+                TRC(tr_role, 21);
                 ET(e_sync);
                 if (timed) {  // the shared-memory pipe behind the atomics (timing build only)
                     uint32_t x0;
@@ -921,8 +977,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     for (int pl = 0; pl < A.P; ++pl) fold_plane(pl, binsj + (size_t)pl * p * 128);
                 }
                 if (c + 1 == NC && !EX) red[sub * 128 + r] = s_acc;
+                TRC(tr_role, 22);
                 ET(e_fold);
                 epi_sync();  // bins zeroed before the next chunk's atomics (red / prod written)
+                TRC(tr_role, 23);
                 ET(e_sync);
             }
             ET(e_red);

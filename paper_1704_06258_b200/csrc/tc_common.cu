@@ -19,8 +19,10 @@ unsigned long long* tc_timing_buffer() {
     if (on < 0) {
         const char* e = getenv("HUBGPU_TC_TIMING");
         on = (e && e[0] == '1') ? 1 : 0;
-        if (on && cudaMalloc(&buf, 32 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(buf, 0, 32 * sizeof(unsigned long long));
+        // 32 counters, 32 spare, then the K3 event trace (3 roles x 8192)
+        const size_t words = 64 + 3 * 8192;
+        if (on && cudaMalloc(&buf, words * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(buf, 0, words * sizeof(unsigned long long));
         else
             buf = nullptr;
     }
@@ -32,6 +34,15 @@ int tc_timing_read(unsigned long long* out32) {
     if (!b) return HG_EARG;
     HG_CUDA(cudaMemcpy(out32, b, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     HG_CUDA(cudaMemset(b, 0, 32 * sizeof(unsigned long long)));
+    return HG_OK;
+}
+
+// the K3 event trace (timing build): 3 x 8192 words, cleared after the read
+int tc_trace_read(unsigned long long* out) {
+    unsigned long long* b = tc_timing_buffer();
+    if (!b) return HG_EARG;
+    HG_CUDA(cudaMemcpy(out, b + 64, 3 * 8192 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    HG_CUDA(cudaMemset(b + 64, 0, 3 * 8192 * sizeof(unsigned long long)));
     return HG_OK;
 }
 

@@ -81,6 +81,33 @@ __global__ void __launch_bounds__(128, 1) k_peak(int iters, uint32_t idesc, int*
     if (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
     if (threadIdx.x == 0 && crank == 0) {
         const uint64_t ad = sw128(su32(a)), bd = sw128(su32(b));
+        if (MODE >= 3) {
+            // K3-TC/P's triangular unit (MODE 3: tiles of 8, 7, .., 1 K blocks)
+            // or full-W unit (MODE 4: 8 tiles of 8 blocks): accumulators
+            // alternate per tile, the tile's first MMA overwrites, a commit per
+            // tile; A = the one-hot columns 0..255, accumulators at 256 / 384
+            int done = 0, t = 0;
+            while (done < iters) {
+                for (int I = 0; I < 8 && done < iters; ++I, ++t) {
+                    const uint32_t d = tmem + 256 + (t & 1) * 128;
+                    const int k0 = MODE == 3 ? I : 0;
+                    for (int kb = k0; kb < 8; ++kb, ++done)
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                                "r"(tmem + kb * 32 + ks * 8), "l"(bd + 2 * ks), "r"(idesc),
+                                "r"((int)(kb != k0 || ks))
+                                : "memory");
+                    asm volatile(
+                        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                        " [%0], %1;" ::"r"(su32(&bar2)),
+                        "h"((uint16_t)3)
+                        : "memory");
+                }
+            }
+        } else
         for (int it = 0; it < iters; ++it) {
             const uint32_t d = MODE ? tmem + 256 + ((it >> 3) & 1) * 128
                                     : tmem + (it & 1) * (ATMEM ? 128 : 256);
@@ -292,6 +319,11 @@ int main() {
     if (run<2, true, 1>(sms, iters, &t5, &m5)) return 1;
     if (run<2, true, 2>(sms, iters, &t6, &m6)) return 1;
     fprintf(stderr, "a_tmem K3 layout: %.1f TOPS; + commit per K block: %.1f TOPS\n", t5, t6);
+    double t7, t8;
+    float m7, m8;
+    if (run<2, true, 3>(sms, iters, &t7, &m7)) return 1;
+    if (run<2, true, 4>(sms, iters, &t8, &m8)) return 1;
+    fprintf(stderr, "K3 unit pattern: triangular tiles %.1f TOPS; full tiles %.1f TOPS\n", t7, t8);
     int clk = 0;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     printf("{\"what\": \"dense int8 tensor peak, tcgen05.mma kind::i8 (u8 x u8 -> s32), operands "

@@ -80,7 +80,6 @@ CONFIGS = [
     ("full W", {"HUBGPU_TCP_NOTRI": "1"}),
 ]
 # (phase counters, HUBGPU_TC_TIMING=1, need a timing build: make EXTRA=-DHG_TCP_TIMING)
-# (phase counters, HUBGPU_TC_TIMING=1, need a timing build: make EXTRA=-DHG_TCP_TIMING)
 
 
 def main() -> None:
