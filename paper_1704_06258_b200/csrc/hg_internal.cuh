@@ -198,7 +198,7 @@ int set_max_dynamic_smem(const void* fn);
 // K3-TC/P (k_fitness_tcp.cu): the same on CTA pairs (cta_group::2, M = 256)
 // P: byte planes of W (integer flows < 256^P), stacked in the u8 tensor
 bool tcp_supported(int n, int p, int npad, int P);
-size_t tcp_smem_bytes(int p, int npad, int P, bool exact);
+size_t tcp_smem_bytes(int p, int npad, int P, bool exact, bool df = false);
 int prepare_fitness_tcp(int p, int npad, int P);
 // legs / out set: the finaliser is fused (out gets the 4 cost terms, part unused)
 // int8 tensor operations one launch on B hub sets issues (the roofline's work)

@@ -140,6 +140,14 @@ __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
+__device__ __forceinline__ void mb_arrive(uint32_t bar) {  // release.cta
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// arrive once every cp.async this thread issued so far has landed (the
+// barrier counts one arrival per thread: .noinc)
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void arrive_remote(uint32_t bar_cluster) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
@@ -263,8 +271,8 @@ __host__ __device__ inline size_t p_C_bytes(int ipt, int npad) {
 __host__ __device__ inline size_t p_T_bytes(int ipt, int p) {
     return (size_t)ipt * p * p * 8;
 }
-__host__ __device__ inline size_t p_H_bytes(int ipt, int p) {
-    return ((size_t)2 * ipt * p * 4 + 15) & ~size_t(15);
+__host__ __device__ inline size_t p_H_bytes(int ipt, int p) {  // 3 buffers (defer)
+    return ((size_t)3 * ipt * p * 4 + 15) & ~size_t(15);
 }
 
 struct PArgs {
@@ -313,15 +321,21 @@ struct PArgs {
     // inter-cluster flows; S_T is then np.sum(inter * hub_dist) replayed in
     // numpy's pairwise order over the leaves of the p*p-term sum
     int exact;
+    // defer (one K chunk, >= 4 output tiles, !exact): a unit's bins, partials,
+    // T tables are double-buffered and its fold / reduce run during the next
+    // unit's tiles, ordered by mbarriers instead of epilogue-wide barriers; the
+    // cluster rows are triple-buffered and staged by cp.async
+    int defer;
     const uint32_t* leaves;  // per leaf: first row | rows << 16 | tree sums << 24
     int nleaf;
 };
 
 constexpr int kYChunkKB = 8;  // K blocks per chunk: 8 x 128 nodes = 256 TMEM columns of A
+constexpr int kYDeferBars = 11;  // binsdone[2] folded[2] tready[2] cready[3] reduced[2]
 
 // CSM: a unit's cluster rows staged in shared memory (known address space ->
 // LDS) rather than read from global memory
-template <bool CSM, bool EX>
+template <bool CSM, bool EX, bool DFT = false>
 __global__ void __launch_bounds__(kYThreads, 1)
 k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -333,31 +347,36 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     // cluster rows of the current / next unit, when they fit (CSM); a double
     // buffer addressed arithmetically (a runtime-indexed pointer array would
     // drop to local memory)
+    constexpr bool DF = !EX && DFT;  // (launched only with A.defer)
+    const int NB = DF ? 2 : 1;  // bins / partials / T-table buffers
     const size_t cb = CSM ? p_C_bytes(ipt, A.npad) : 0;
     unsigned char* sC0 = var;
-    var += 2 * cb;
+    var += (DF ? 3 : 2) * cb;
     const int PB = A.P;  // planes of bins
-    uint32_t* bins = reinterpret_cast<uint32_t*>(var);  // [PB][p][128] cluster-pair flow bins
-    var += (size_t)PB * p * 512;
-    double* red = reinterpret_cast<double*>(var);  // [4 subs][128 rows]
-    var += 4 * 128 * 8;
+    // [NB][PB][p][128] cluster-pair flow bins
+    uint32_t* bins = reinterpret_cast<uint32_t*>(var);
+    var += (size_t)NB * PB * p * 512;
+    double* red = reinterpret_cast<double*>(var);  // [NB][4 subs][128 rows]
+    var += (size_t)NB * 4 * 128 * 8;
     // the unit's spoke-leg sums (finaliser), by slot parity: [2][ipt][2]
     double* sL = reinterpret_cast<double*>(var);
     var += 2 * kYMaxIpt * 2 * 8;
     // the unit's hub-cost tables T (tsm): [ipt][p][p] fp64, and its hubs (and
-    // the next unit's: double buffer) [2][ipt][p] int32
-    double* sT = reinterpret_cast<double*>(var);
-    var += A.tsm ? p_T_bytes(ipt, p) : 0;
+    // the next units': 2 buffers, defer 3) [3][ipt][p] int32
+    double* sT = reinterpret_cast<double*>(var);  // [NB][ipt][p][p]
+    var += A.tsm ? NB * p_T_bytes(ipt, p) : 0;
     int32_t* sH = reinterpret_cast<int32_t*>(var);
     var += A.tsm ? p_H_bytes(ipt, p) : 0;
     double* prod = reinterpret_cast<double*>(var);  // exact: [p][128] rounded terms of S_T
     var += EX ? (size_t)p * 128 * 8 : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(var);
-    // bars: full[16] empty[16] accfull[2] accempty[2] kbfree[4] aready[4]
+    // bars: full[16] empty[16] accfull[2] accempty[2] kbfree[4] aready[4], and
+    // (defer) binsdone[2] folded[2] tready[2] cready[3] reduced[2]
     const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kYMaxStages,
                    b_accf = b_empty + 8 * kYMaxStages, b_acce = b_accf + 16, b_kbf = b_acce + 16,
-                   b_ard = b_kbf + 32;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kYMaxStages + 12);
+                   b_ard = b_kbf + 32, b_bdone = b_ard + 32, b_fold = b_bdone + 16,
+                   b_tready = b_fold + 16, b_cready = b_tready + 16, b_rdone = b_cready + 24;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kYMaxStages + 12 + kYDeferBars);
     // chunk c of the K dimension: K blocks [c*8, c*8 + nkb(c)); its one-hot is
     // generated in 4 contiguous ranges of K blocks, one per column-quarter warp
     // group: quarter h owns chunk-local blocks [kq(c,h), kq(c,h+1))
@@ -378,7 +397,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int x = tid; x < PB * p * 128; x += kYThreads) bins[x] = 0u;
+    for (int x = tid; x < NB * PB * p * 128; x += kYThreads) bins[x] = 0u;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mb_init(b_full + 8 * s, 1);
@@ -392,6 +411,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             mb_init(b_kbf + 8 * h, 1);
             mb_init(b_ard + 8 * h, 8);  // the 4 lane-quadrant warps of quarter h, both CTAs
         }
+        for (int x = 0; x < 2; ++x) {
+            mb_init(b_bdone + 8 * x, kYEpiThreads / 32);  // a warp's last atomics of a unit
+            mb_init(b_fold + 8 * x, kYEpiThreads / 32);   // a warp's fold of a unit
+            mb_init(b_tready + 8 * x, kYEpiThreads);      // every thread's cp.async (noinc)
+        }
+        for (int x = 0; x < 3; ++x) mb_init(b_cready + 8 * x, kYEpiThreads);
+        for (int x = 0; x < 2; ++x) mb_init(b_rdone + 8 * x, 2);  // warps 2-3
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
     }
@@ -442,7 +468,53 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         nind = u < cs1 ? (int)(Bk - bbase < ipt ? Bk - bbase : ipt) : 0;
     };
 
-    if (warp == 1) {
+    // a unit's S_T reduce + the finaliser (fixed order): one warp per
+    // individual b2 = first, first + step, ..; lane l sums column l's 4 quarter
+    // partials ((q0+q1)+(q2+q3)), columns l >= 32 folded in after, then a
+    // butterfly (deterministic)
+    auto reduce_rows = [&](const int64_t bbase_u, const int nind_u, const int64_t j_u, int first,
+                           int step) {
+        const double* lgw = sL + (j_u & 1) * kYMaxIpt * 2;
+        const double* redu = red + (DF ? (j_u & 1) * 512 : 0);
+        for (int b2 = first; b2 < nind_u; b2 += step) {
+            double acc = 0.0;
+            for (int ll = lane; ll < p; ll += 32) {
+                const double* rp = redu + b2 * p + ll;
+                acc += (rp[0] + rp[128]) + (rp[256] + rp[384]);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) {
+                if (A.out) {
+                    // the finaliser (k_finalize), fused: same operations
+                    const int64_t b = bbase_u + b2;
+                    const double coll = A.chi * lgw[2 * b2];
+                    const double dist = A.delta * lgw[2 * b2 + 1];
+                    const double tran = A.alpha * acc;
+                    A.out[4 * b + 0] = coll;
+                    A.out[4 * b + 1] = tran;
+                    A.out[4 * b + 2] = dist;
+                    A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
+                } else {
+                    A.part[(bbase_u + b2) * A.pstride] = acc;
+                }
+            }
+        }
+    };
+
+    if (DF && (warp == 2 || warp == 3)) {
+        // ---------------- (defer) the units' reduces, each once its folds are
+        // in: the epilogue warps never stop draining for them
+        for (int64_t j = 0; j < nslots; ++j) {
+            mb_wait(b_fold + 8 * (uint32_t)(j & 1), (uint32_t)((j >> 1) & 1));
+            int64_t pb;
+            int pn;
+            slot_unit(j, pb, pn);
+            reduce_rows(pb, pn, j, warp - 2, 2);
+            __syncwarp();
+            if (lane == 0) mb_arrive(b_rdone + 8 * (uint32_t)(j & 1));
+        }
+    } else if (warp == 1) {
         // ---------------- TMA producer: per phase, the W tiles (plane, row
         // block it) in order, tile it running K blocks [klo(c, it), nkb(c));
         // a stage holds up to KBS consecutive blocks of one tile
@@ -600,13 +672,16 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         // nodes); this warp writes chunk blocks [kq(c,sub), kq(c,sub+1)) of its
         // lane quadrant, reading the cluster rows straight from global memory
         // (lanes of one individual read the same bytes: L1 broadcasts)
+        // the cluster-row buffer of unit j (defer: 3, staged by cp.async)
+        auto cbuf = [&](int64_t j) { return DF ? (int)(j % 3) : (int)(j & 1); };
         auto gen = [&](int64_t j, int c) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
             const bool live = r < ipt * p && bl < nind;
             const uint32_t lrep = (uint32_t)l * 0x01010101u;
-            const uint8_t* rowp = CSM ? sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad
+            if (CSM && DF) mb_wait(b_cready + 8 * (uint32_t)(j % 3), (uint32_t)((j / 3) & 1));
+            const uint8_t* rowp = CSM ? sC0 + cbuf(j) * cb + (size_t)(live ? bl : 0) * A.npad
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             const uint4* crow =
                 reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
@@ -630,12 +705,22 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         };
 
         // stage a unit's cluster rows into double buffer j & 1 (CSM)
+        // (defer: by cp.async, rows of live individuals only -- nothing reads
+        // the others -- completion tracked by cready[j % 3])
         auto stage = [&](int64_t j) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
-            uint8_t* Cs = sC0 + (j & 1) * cb;
+            uint8_t* Cs = sC0 + cbuf(j) * cb;
             const int chunks = A.npad / 16;
+            if (DF) {
+                for (int x = tid - kYEpiWarp0 * 32; x < nind * chunks; x += kYEpiThreads)
+                    cp_async16(su32(Cs) + 16u * (uint32_t)x,
+                               A.cl + bbase * A.npad + (size_t)x * 16);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                cp_async_arrive(b_cready + 8 * (uint32_t)(j % 3));
+                return;
+            }
             for (int x = tid - kYEpiWarp0 * 32; x < ipt * chunks; x += kYEpiThreads) {
                 const int b2 = x / chunks, k = x - b2 * chunks;
                 uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -657,7 +742,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             }
             if (CSM) {
                 stage(0);
-                epi_sync();
+                if (!DF) epi_sync();
             }
             gen(0, 0);
         }
@@ -731,35 +816,56 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         }
                         __syncwarp();
                     }
-                } else
-                // one warp per individual: lanes stride its 4p partials, then a
-                // butterfly (fixed order -> deterministic)
-                for (int b2 = (warp - kYEpiWarp0); b2 < nind_u; b2 += kYEpiThreads / 32) {
-                    // lane l sums column l's 4 quarter partials ((q0+q1)+(q2+q3)),
-                    // columns l >= 32 folded in after (fixed order)
-                    double acc = 0.0;
-                    for (int ll = lane; ll < p; ll += 32) {
-                        const double* rp = red + b2 * p + ll;
-                        acc += (rp[0] + rp[128]) + (rp[256] + rp[384]);
-                    }
-    #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                    if (lane == 0) {
-                        if (A.out) {
-                            // the finaliser (k_finalize), fused: same operations
-                            const int64_t b = bbase_u + b2;
-                            const double coll = A.chi * lgw[2 * b2];
-                            const double dist = A.delta * lgw[2 * b2 + 1];
-                            const double tran = A.alpha * acc;
-                            A.out[4 * b + 0] = coll;
-                            A.out[4 * b + 1] = tran;
-                            A.out[4 * b + 2] = dist;
-                            A.out[4 * b + 3] = __dadd_rn(__dadd_rn(coll, tran), dist);
-                        } else {
-                            A.part[(bbase_u + b2) * A.pstride] = acc;
-                        }
-                    }
+                } else {
+                    reduce_rows(bbase_u, nind_u, j_u, warp - kYEpiWarp0, kYEpiThreads / 32);
                 }
+        };
+        // defer: unit jp's bins (all its warps' atomics done) into this
+        // row's partial red[jp & 1][sub][r], zeroing them; then folded[jp & 1]
+        auto fold_unit = [&](const int64_t jp) {
+            int64_t pb;
+            int pn;
+            slot_unit(jp, pb, pn);
+            const bool livep = r < ipt * p && bl < pn;
+            const uint32_t bx = (uint32_t)(jp & 1), par = (uint32_t)((jp >> 1) & 1);
+            mb_wait(b_bdone + 8 * bx, par);
+            mb_wait(b_tready + 8 * bx, par);
+            double sp = 0.0;
+            if (livep && !(A.dbg & 4)) {
+                const double* tb =
+                    A.tsm ? sT + (size_t)bx * ipt * p * p + bl * p * p + l : nullptr;
+                const uint32_t* tp =
+                    A.tsm ? nullptr : A.T + (pb + bl) * 2 * p * (int64_t)A.ps + l;
+                for (int pl = 0; pl < A.P; ++pl) {
+                    const double sc =
+                        A.wscale * __longlong_as_double((long long)(1023 + 8 * pl) << 52);
+                    sp = fold_bins(bins + (size_t)(bx * PB + pl) * p * 128 + r, tb, tp, p,
+                                   A.ps, sub, sc, sp);
+                }
+            }
+            red[bx * 512 + sub * 128 + r] = sp;
+            __syncwarp();
+            if (lane == 0) mb_arrive(b_fold + 8 * bx);
+        };
+        // unit j's hub-cost tables T_b[k][l] = C[h_k][h_l] into sT (defer: its
+        // buffer j & 1) by cp.async, off the unit's hubs in sH[j & 1]: this
+        // thread's elements x = etid + 512 m for m = part, part + parts, ..
+        // ((b2, k, l2) = x by multiply-high: (x * m) >> 32 with m =
+        // floor((2^32 - 1) / d) + 1 is x / d exactly while x * d < 2^32)
+        auto gather_T = [&](const int64_t j, const int nind, const int part, const int parts) {
+            const int etid = tid - kYEpiWarp0 * 32;
+            const uint32_t sTj =
+                su32(sT) + (DF ? (uint32_t)(j & 1) * (uint32_t)p_T_bytes(ipt, p) : 0u);
+            const int32_t* hsj = sH + (DF ? (int)(j % 3) : (int)(j & 1)) * ipt * p;
+            const int pp = p * p;
+            const uint64_t mpp = 0xFFFFFFFFull / (uint64_t)pp + 1u;
+            const uint64_t mp = 0xFFFFFFFFull / (uint64_t)p + 1u;
+            for (int x = etid + part * kYEpiThreads; x < nind * pp; x += parts * kYEpiThreads) {
+                const int b2 = (int)(((uint64_t)x * mpp) >> 32), kl = x - b2 * pp;
+                const int k = (int)(((uint64_t)kl * mp) >> 32), l2 = kl - k * p;
+                const int32_t* hs = hsj + b2 * p;
+                cp_async8(sTj + 8u * x, A.C + (size_t)hs[k] * A.nC + hs[l2]);
+            }
         };
         // (slot j's first tile runs slot j-1's reduce; phase = j * NC + c is
         // recomputed rather than carried: the loop is register-bound)
@@ -768,15 +874,16 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             int nind;
             slot_unit(j, bbase, nind);
             const bool live = r < ipt * p && bl < nind;
-            const uint32_t bin_r = bin_r0;
+            // defer: unit j's bins are buffer j & 1
+            const uint32_t bin_r = bin_r0 + (DF ? (uint32_t)(j & 1) * (uint32_t)(PB * p * 512) : 0u);
             uint32_t* const binsj = bins;
-            const uint8_t* crow = CSM ? sC0 + (j & 1) * cb + (size_t)(live ? bl : 0) * A.npad
+            const uint8_t* crow = CSM ? sC0 + cbuf(j) * cb + (size_t)(live ? bl : 0) * A.npad
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             TRC(tr_role, 24);
             if (CSM && j + 1 < nslots) {
                 stage(j + 1);  // the next unit's cluster rows, under this unit's MMAs
                 ET(e_st);
-                epi_sync();    // ... complete before any warp generates from them
+                if (!DF) epi_sync();  // ... complete before any warp generates from them
                 ET(e_sync);
             }
             // this unit's leg sums and (tsm) hub-cost tables T_b[k][l] = C[h_k][h_l]
@@ -787,27 +894,20 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             {
                 const int etid = tid - kYEpiWarp0 * 32;
                 if (A.tsm) {
-                    // element x = (b2, k, l2) per thread; x / (p*p) and x / p as
-                    // (x * m) >> 32, m = floor((2^32 - 1) / d) + 1 (exact while
-                    // x * d < 2^32: x < 128 p here)
-                    const int32_t* hsj = sH + (j & 1) * ipt * p;
-                    const int pp = p * p;
-                    const uint64_t mpp = 0xFFFFFFFFull / (uint64_t)pp + 1u;
-                    const uint64_t mp = 0xFFFFFFFFull / (uint64_t)p + 1u;
-                    for (int x = etid; x < nind * pp; x += kYEpiThreads) {
-                        const int b2 = (int)(((uint64_t)x * mpp) >> 32), kl = x - b2 * pp;
-                        const int k = (int)(((uint64_t)kl * mp) >> 32), l2 = kl - k * p;
-                        const int32_t* hs = hsj + b2 * p;
-                        cp_async8(su32(sT) + 8u * x, A.C + (size_t)hs[k] * A.nC + hs[l2]);
-                    }
+                    // (defer: spread over the unit's tiles instead, gather_T)
+                    if (!DF) gather_T(j, nind, 0, 1);
                     if (j + 1 < nslots) {
                         int64_t nb;
                         int nn;
                         slot_unit(j + 1, nb, nn);
                         for (int x = etid; x < nn * p; x += kYEpiThreads)
-                            cp_async4(su32(sH + ((j + 1) & 1) * ipt * p + x), A.hubs + nb * p + x);
+                            cp_async4(su32(sH + (DF ? (int)((j + 1) % 3) : (int)((j + 1) & 1)) * ipt * p + x),
+                                      A.hubs + nb * p + x);
                     }
                 }
+                // defer: unit j - 2's reduce (warps 2-3) is done with sL / red
+                if (DF && j >= 2)
+                    mb_wait(b_rdone + 8 * (uint32_t)(j & 1), (uint32_t)(((j - 2) >> 1) & 1));
                 if (A.out && etid < nind)
                     cp_async16(su32(sL + (j & 1) * kYMaxIpt * 2 + 2 * etid),
                                A.legs + 2 * (bbase + etid));
@@ -901,6 +1001,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     __syncwarp();
                     if (lane == 0) arrive_remote(L_acce + 8 * d);  // accumulator may be overwritten
                     TRC(tr_role, 16);
+                    // defer: bins j & 1 were folded (zeroed) for unit j - 2
+                    if (DF && tt == 0 && j >= 2)
+                        mb_wait(b_fold + 8 * (uint32_t)(j & 1), (uint32_t)(((j - 2) >> 1) & 1));
                     if (live && !(A.dbg & 1)) {
                         // G[c_i][r] += D[r][i]: exact integer bins, this row's own
                         // (4 column-quarter warps share a row, hence the atomics)
@@ -919,7 +1022,16 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                     TRC(tr_role, 17);
                     ET(e_cmp);
-                    if (c == 0 && tt == 0 && j > 0 && !(A.dbg & 4)) {  // the previous unit's reduce
+                    if (DF && tt >= 1) {
+                        // the previous unit's fold after this unit's tile 1 (its
+                        // reduce: warps 2-3), then a share of this unit's T
+                        // gather after every later tile (its hubs arrived with
+                        // the previous unit's batch, which the fold waited for)
+                        if (tt == 1 && j > 0) fold_unit(j - 1);
+                        if (A.tsm) gather_T(j, nind, tt - 1, NT - 1);
+                        TRC(tr_role, 18);
+                    }
+                    if (!DF && c == 0 && tt == 0 && j > 0 && !(A.dbg & 4)) {  // the previous unit's reduce
                         int64_t pb;
                         int pn;
                         slot_unit(j - 1, pb, pn);
@@ -927,6 +1039,14 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         TRC(tr_role, 18);
                         ET(e_red);
                     }
+                }
+                if (DF) {  // this warp's atomics of unit j are done; fold + reduce deferred
+                    // (the unit's T gather, next hubs and legs: tready[j & 1])
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    cp_async_arrive(b_tready + 8 * (uint32_t)(j & 1));
+                    __syncwarp();
+                    if (lane == 0) mb_arrive(b_bdone + 8 * (uint32_t)(j & 1));
+                    continue;  // (one chunk)
                 }
                 // this chunk's bins into S_T: sum_k T_b[k][l] * G_c[k][(b,l)] over
                 // k = sub, sub + 4, ... (fixed order -> deterministic); one chunk's
@@ -985,7 +1105,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             }
             ET(e_red);
         }
-        if (nslots > 0 && !(A.dbg & 4)) {  // the last unit
+        if (nslots > 0 && DF) fold_unit(nslots - 1);  // the last unit's (reduce: warps 2-3)
+        if (nslots > 0 && !DF && !(A.dbg & 4)) {  // the last unit
             int64_t pb;
             int pn;
             slot_unit(nslots - 1, pb, pn);
@@ -1035,41 +1156,46 @@ static bool p_csm(int p, int npad) {
 // planes of bins one launch holds (more planes: a launch per plane)
 static int p_bin_planes(int P) { return P > kYMaxPlanes ? 1 : P; }
 
-static size_t p_base_bytes(int p, int npad, int P, bool exact) {
-    return 1024 + (p_csm(p, npad) ? 2 * p_C_bytes(p_ipt(p), npad) : 0) +
-           (size_t)p_bin_planes(P) * p * 512 +
-           4 * 128 * 8 + 2 * kYMaxIpt * 2 * 8 + (exact ? (size_t)p * 1024 : 0) +
-           (2 * kYMaxStages + 12) * 8 + 16;
+// df: the deferred-fold layout (cluster rows x3, bins / partials / T x2)
+static size_t p_base_bytes(int p, int npad, int P, bool exact, bool df = false) {
+    const int nb = df ? 2 : 1;
+    return 1024 + (p_csm(p, npad) ? (df ? 3 : 2) * p_C_bytes(p_ipt(p), npad) : 0) +
+           (size_t)nb * p_bin_planes(P) * p * 512 +
+           (size_t)nb * 4 * 128 * 8 + 2 * kYMaxIpt * 2 * 8 + (exact ? (size_t)p * 1024 : 0) +
+           (2 * kYMaxStages + 12 + kYDeferBars) * 8 + 16;
 }
 
 // the unit's T tables in shared memory when they leave room for two full W
 // stages (p <= ~36 at n <= 1024)
-static bool p_tsm(int p, int npad, int P, bool exact) {
+static size_t p_tsm_bytes(int p, bool df) {
+    return (df ? 2 : 1) * p_T_bytes(p_ipt(p), p) + p_H_bytes(p_ipt(p), p);
+}
+static bool p_tsm(int p, int npad, int P, bool exact, bool df = false) {
     if (env_int("HUBGPU_TCP_TSM", 1) == 0) return false;  // tuning override
-    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_base_bytes(p, npad, P, exact) -
-                         (int64_t)(p_T_bytes(p_ipt(p), p) + p_H_bytes(p_ipt(p), p));
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_base_bytes(p, npad, P, exact, df) -
+                         (int64_t)p_tsm_bytes(p, df);
     return room >= 2 * 8 * (int64_t)kYStageBytes;
 }
 
-static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false) {
-    return p_base_bytes(p, npad, P, exact) +
-           (p_tsm(p, npad, P, exact) ? p_T_bytes(p_ipt(p), p) + p_H_bytes(p_ipt(p), p) : 0);
+static size_t p_fixed_bytes(int p, int npad, int P, bool exact = false, bool df = false) {
+    return p_base_bytes(p, npad, P, exact, df) +
+           (p_tsm(p, npad, P, exact, df) ? p_tsm_bytes(p, df) : 0);
 }
 
 // K blocks per W stage: 8 (one MMA-issuer loop per 1024 K) unless that
 // leaves fewer than two stages (large p / the exact mode's terms): then 4, 2, 1
-static int p_kbs(int p, int npad, int P, bool exact = false) {
+static int p_kbs(int p, int npad, int P, bool exact = false, bool df = false) {
     const int ek = env_int("HUBGPU_TCP_KBS", 0);  // tuning override
     if (ek >= 1 && ek <= 8) return ek;
-    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact);
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact, df);
     int k = 8;
     while (k > 1 && room < 2 * (int64_t)k * kYStageBytes) k /= 2;
     return k;
 }
 
-static int p_stages(int p, int npad, int P, bool exact = false) {
-    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact);
-    int64_t s = room / ((int64_t)p_kbs(p, npad, P, exact) * kYStageBytes);
+static int p_stages(int p, int npad, int P, bool exact = false, bool df = false) {
+    const int64_t room = (int64_t)227 * 1024 - (int64_t)p_fixed_bytes(p, npad, P, exact, df);
+    int64_t s = room / ((int64_t)p_kbs(p, npad, P, exact, df) * kYStageBytes);
     if (s > kYMaxStages) s = kYMaxStages;
     const int es = env_int("HUBGPU_TCP_STAGES", 0);  // tuning override (shallower only)
     if (es >= 2 && es < s) s = es;
@@ -1083,10 +1209,22 @@ static bool p_exact(int p, int npad, int P) {
 }
 
 // exact: the instance asks for numpy's summation order and the terms fit
-size_t tcp_smem_bytes(int p, int npad, int P, bool exact) {
+size_t tcp_smem_bytes(int p, int npad, int P, bool exact, bool df) {
     const bool x = exact && p_exact(p, npad, P);
-    return p_fixed_bytes(p, npad, P, x) +
-           (size_t)p_stages(p, npad, P, x) * p_kbs(p, npad, P, x) * kYStageBytes;
+    df = df && !x;
+    return p_fixed_bytes(p, npad, P, x, df) +
+           (size_t)p_stages(p, npad, P, x, df) * p_kbs(p, npad, P, x, df) * kYStageBytes;
+}
+
+// the deferred fold (K3's unit-to-unit hand-off without epilogue barriers):
+// one K chunk, >= 4 output tiles per plane pass (the unit-drift bound its
+// buffer reuse relies on), and its layout keeps the full 8-block W stages
+// and the T tables in shared memory
+static bool p_defer(int p, int npad, int P, int NC, int ITO, bool exact) {
+    if (exact || NC != 1 || ITO < 4 || env_int("HUBGPU_TCP_DEFER", 1) == 0) return false;
+    return p_kbs(p, npad, P, false, true) == p_kbs(p, npad, P, false, false) &&
+           p_stages(p, npad, P, false, true) >= 2 &&
+           p_tsm(p, npad, P, false, true) == p_tsm(p, npad, P, false, false);
 }
 
 bool tcp_supported(int n, int p, int npad, int P) {
@@ -1102,8 +1240,9 @@ int prepare_fitness_tcp(int p, int npad, int P) {
     // every instantiation at the device maximum: instances of different p /
     // planes need different sizes and the attribute is per kernel
     using KernFn = void (*)(const CUtensorMap, PArgs);
-    const KernFn all[4] = {k_fitness_tcp<true, true>, k_fitness_tcp<false, true>,
-                           k_fitness_tcp<true, false>, k_fitness_tcp<false, false>};
+    const KernFn all[6] = {k_fitness_tcp<true, true>,  k_fitness_tcp<false, true>,
+                           k_fitness_tcp<true, false>, k_fitness_tcp<false, false>,
+                           k_fitness_tcp<true, false, true>, k_fitness_tcp<false, false, true>};
     for (KernFn f : all) HG_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(f)));
     const KernFn kern = p_csm(p, npad) ? k_fitness_tcp<true, false> : k_fitness_tcp<false, false>;
     const size_t sm = tcp_smem_bytes(p, npad, P, false);
@@ -1150,10 +1289,11 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     // be the reference's own flows: symmetric costs, fixed-order sums
     A.tri = !A.exact && tri_avail && !env_int("HUBGPU_TCP_NOTRI", 0) ? 1 : 0;
     A.P = A.tri ? I.wplanes_tri : I.wplanes;
-    A.stages = p_stages(I.p, I.npad, A.P, A.exact);  // as tcp_smem_bytes
-    A.kbs = p_kbs(I.p, I.npad, A.P, A.exact);
+    A.defer = p_defer(I.p, I.npad, A.P, A.NC, A.ITO, A.exact) ? 1 : 0;
+    A.stages = p_stages(I.p, I.npad, A.P, A.exact, A.defer);  // as tcp_smem_bytes
+    A.kbs = p_kbs(I.p, I.npad, A.P, A.exact, A.defer);
     A.csm = p_csm(I.p, I.npad) ? 1 : 0;
-    A.tsm = p_tsm(I.p, I.npad, A.P, A.exact) ? 1 : 0;
+    A.tsm = p_tsm(I.p, I.npad, A.P, A.exact, A.defer) ? 1 : 0;
     A.plane0 = 0;
     A.pstride = 1;
     A.wscale = I.wscale;
@@ -1246,7 +1386,7 @@ static int tcp_launch(const DevInst& I, const PArgs& A, int g, const void* wmap,
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3(kYThreads);
-    cfg.dynamicSmemBytes = tcp_smem_bytes(I.p, I.npad, A.P, A.exact);
+    cfg.dynamicSmemBytes = tcp_smem_bytes(I.p, I.npad, A.P, A.exact, A.defer);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1255,12 +1395,12 @@ static int tcp_launch(const DevInst& I, const PArgs& A, int g, const void* wmap,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (A.csm)
-        HG_CUDA(cudaLaunchKernelEx(&cfg, A.exact ? k_fitness_tcp<true, true>
-                                             : k_fitness_tcp<true, false>, map, A));
-    else
-        HG_CUDA(cudaLaunchKernelEx(&cfg, A.exact ? k_fitness_tcp<false, true>
-                                             : k_fitness_tcp<false, false>, map, A));
+    using KernFn = void (*)(const CUtensorMap, PArgs);
+    const KernFn kern = A.exact ? (A.csm ? k_fitness_tcp<true, true> : k_fitness_tcp<false, true>)
+                        : A.defer ? (A.csm ? k_fitness_tcp<true, false, true>
+                                           : k_fitness_tcp<false, false, true>)
+                                  : (A.csm ? k_fitness_tcp<true, false> : k_fitness_tcp<false, false>);
+    HG_CUDA(cudaLaunchKernelEx(&cfg, kern, map, A));
     note_launch();
     return HG_OK;
 }
