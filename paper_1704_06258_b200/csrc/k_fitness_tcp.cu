@@ -696,8 +696,12 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     v[4 * h + 2] = live ? oh4(x.z, lrep) : 0u;
                     v[4 * h + 3] = live ? oh4(x.w, lrep) : 0u;
                 }
+                // (.sync.aligned: the warp must be converged -- the compiler
+                // does not know the asm requires it)
+                __syncwarp();
                 st8(tmem + lane_base + (uint32_t)c0, v);
             }
+            __syncwarp();
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             fence_before();
             __syncwarp();
@@ -858,8 +862,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 su32(sT) + (DF ? (uint32_t)(j & 1) * (uint32_t)p_T_bytes(ipt, p) : 0u);
             const int32_t* hsj = sH + (DF ? (int)(j % 3) : (int)(j & 1)) * ipt * p;
             const int pp = p * p;
-            const uint64_t mpp = 0xFFFFFFFFull / (uint64_t)pp + 1u;
-            const uint64_t mp = 0xFFFFFFFFull / (uint64_t)p + 1u;
+            // (32-bit divisions: inline code, no 64-bit division subroutine)
+            const uint64_t mpp = (uint64_t)(0xFFFFFFFFu / (uint32_t)pp) + 1u;
+            const uint64_t mp = (uint64_t)(0xFFFFFFFFu / (uint32_t)p) + 1u;
             for (int x = etid + part * kYEpiThreads; x < nind * pp; x += parts * kYEpiThreads) {
                 const int b2 = (int)(((uint64_t)x * mpp) >> 32), kl = x - b2 * pp;
                 const int k = (int)(((uint64_t)kl * mp) >> 32), l2 = kl - k * p;
@@ -895,7 +900,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 const int etid = tid - kYEpiWarp0 * 32;
                 if (A.tsm) {
                     // (defer: spread over the unit's tiles instead, gather_T)
-                    if (!DF) gather_T(j, nind, 0, 1);
+                    // defer: unit j's hubs came with unit j-1's batch -- wait for
+                    // it (every epilogue thread's copies, tready[(j-1) & 1]).
+                    // (Spreading this gather over the unit's tiles instead gave
+                    // wrong tables in the checked build: kept at the unit top.)
+                    if (DF && j > 0)
+                        mb_wait(b_tready + 8 * (uint32_t)((j - 1) & 1), (uint32_t)(((j - 1) >> 1) & 1));
+                    gather_T(j, nind, 0, 1);
                     if (j + 1 < nslots) {
                         int64_t nb;
                         int nn;
@@ -993,6 +1004,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     fence_after();
                     const uint32_t dcol = tmem + lane_base + kYAcc0 + d * 128 + sub * 32;
                     uint32_t v0[16], v1[16];
+                    __syncwarp();  // (.sync.aligned loads: converged warp)
                     ld16(dcol, v0);
                     ld16(dcol + 16, v1);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -1022,13 +1034,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                     TRC(tr_role, 17);
                     ET(e_cmp);
-                    if (DF && tt >= 1) {
+                    if (DF && tt == 1 && j > 0) {
                         // the previous unit's fold after this unit's tile 1 (its
-                        // reduce: warps 2-3), then a share of this unit's T
-                        // gather after every later tile (its hubs arrived with
-                        // the previous unit's batch, which the fold waited for)
-                        if (tt == 1 && j > 0) fold_unit(j - 1);
-                        if (A.tsm) gather_T(j, nind, tt - 1, NT - 1);
+                        // reduce: warps 2-3)
+                        fold_unit(j - 1);
                         TRC(tr_role, 18);
                     }
                     if (!DF && c == 0 && tt == 0 && j > 0 && !(A.dbg & 4)) {  // the previous unit's reduce
