@@ -102,6 +102,26 @@ struct hg_inst {
     // hg_evaluate's copy stream and per-chunk events (copies overlap compute)
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_in[kEvalChunks] = {}, ev_done[kEvalChunks] = {};
+    // hg_evaluate's pipeline captured once per (batch, buffers, kernel choice)
+    // and replayed with the call's host pointers patched into its copy nodes
+    struct EvalGraph {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        int64_t B = -1;
+        const void* P = nullptr;  // the scratch population's buffers it was captured on
+        const void* Ph = nullptr;
+        const void* dsrc = nullptr;
+        int kind = -1, exact = -1, kernels = 0;
+        cudaGraphNode_t h2d[kEvalChunks] = {}, d2h[kEvalChunks] = {};
+        int64_t lo[kEvalChunks + 1] = {};
+        void release() {
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+            exec = nullptr;
+            graph = nullptr;
+            B = -1;
+        }
+    } eg;
 };
 
 namespace {
@@ -308,6 +328,7 @@ int eval_pipelined(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, dou
     lo[0] = 0;
     lo[1] = first < B / 2 ? first : B / 2;
     for (int c = 2; c <= kEvalChunks; ++c) lo[c] = lo[1] + (B - lo[1]) * (c - 1) / (kEvalChunks - 1);
+    for (int c = 0; c <= kEvalChunks; ++c) inst->eg.lo[c] = lo[c];
     for (int c = 0; c < kEvalChunks; ++c) {
         const int64_t b0 = lo[c], nb = lo[c + 1] - lo[c];
         HG_CUDA(cudaMemcpyAsync(dsrc + b0 * I.p, hubs + b0 * I.p, (size_t)nb * I.p * sizeof(int64_t),
@@ -334,6 +355,134 @@ int eval_pipelined(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, dou
     HG_CUDA(cudaEventRecord(inst->ev_in[0], inst->cstream));
     HG_CUDA(cudaStreamWaitEvent(s, inst->ev_in[0], 0));
     return HG_OK;
+}
+
+// hg_evaluate without copies: K2 reads the caller's page-locked int64 hub
+// sets over PCIe while it computes (validating them: the fused k_hubs_in) and
+// the fused finaliser writes the costs straight into the caller's page-locked
+// result buffer.  hubs_d / out_d are the buffers' device addresses.
+int eval_zero_copy(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs_d, double* out_d) {
+    DevInst I = inst->I;
+    cudaStream_t s = inst->stream;
+    I.hubs64 = hubs_d;
+    I.hubs_w = P->hubs;
+    I.hrow0 = 0;
+    HG_CUDA(cudaEventRecord(P->evk, s));
+    HG_TRY(launch_allocate(I, B, P->hubs, P->cl, co_for(inst, P->co), T_for(inst, B, P->T),
+                           P->legs, nullptr, s));
+    HG_CUDA(cudaEventRecord(P->ev0, s));
+    HG_TRY(queue_fitness(inst, B, P->hubs, P->cl, P->co, P->T, P->part, P->legs, out_d));
+    HG_CUDA(cudaEventRecord(P->ev1, s));
+    return HG_OK;
+}
+
+// the device address of a page-locked host buffer (nullptr: pageable)
+const void* host_mapped(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+// the pipeline of eval_pipelined (+ the error-flag read) as a CUDA graph:
+// captured on first use for this batch size / scratch buffers / kernel
+// choice, then replayed with the call's host pointers set into its four copy
+// nodes -- one graph launch instead of ~20 stream operations (host queueing
+// dominated the end-to-end overhead).  Page-locked host buffers only.
+int eval_graph_run(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, double* out) {
+    const DevInst& I = inst->I;
+    cudaStream_t s = inst->stream;
+    auto& G = inst->eg;
+    HG_TRY(inst->t1.ensure((size_t)B * I.p * sizeof(int64_t)));  // no allocation under capture
+    const int64_t* dsrc = inst->t1.as<int64_t>();
+    const int kind = fitness_kernel(inst);
+    if (!G.exec || G.B != B || G.P != P->out || G.Ph != P->hubs || G.dsrc != dsrc ||
+        G.kind != kind || G.exact != I.exact) {
+        G.release();
+        if (!inst->cstream) {  // created outside the capture
+            HG_CUDA(cudaStreamCreateWithFlags(&inst->cstream, cudaStreamNonBlocking));
+            for (int c = 0; c < kEvalChunks; ++c) {
+                HG_CUDA(cudaEventCreateWithFlags(&inst->ev_in[c], cudaEventDisableTiming));
+                HG_CUDA(cudaEventCreateWithFlags(&inst->ev_done[c], cudaEventDisableTiming));
+            }
+        }
+        HG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const uint64_t l0 = launch_count();
+        int rc = eval_pipelined(inst, P, B, hubs, out);
+        if (!rc && cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,
+                                   s) != cudaSuccess)
+            rc = HG_ECUDA;
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        G.kernels = (int)(launch_count() - l0);  // counted again at every replay
+        note_launch((uint64_t)0 - (uint64_t)G.kernels);
+        if (rc || ce != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            if (!rc) set_error("evaluate graph capture: %s", cudaGetErrorString(ce));
+            return rc ? rc : HG_ECUDA;
+        }
+        G.graph = g;
+        // the copy nodes, by device-side address: chunk c's hub sets land at
+        // dsrc + lo[c] p, its costs leave from P->out + 4 lo[c]
+        size_t nn = 0;
+        HG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        HG_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        int found = 0;
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            HG_CUDA(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeMemcpy) continue;
+            cudaMemcpy3DParms mp = {};
+            HG_CUDA(cudaGraphMemcpyNodeGetParams(nd, &mp));
+            for (int c = 0; c < kEvalChunks; ++c) {
+                if (mp.dstPtr.ptr == (void*)(dsrc + G.lo[c] * I.p)) {
+                    G.h2d[c] = nd;
+                    ++found;
+                }
+                if (mp.srcPtr.ptr == (void*)(P->out + 4 * G.lo[c])) {
+                    G.d2h[c] = nd;
+                    ++found;
+                }
+            }
+        }
+        if (found != 2 * kEvalChunks) {
+            G.release();
+            set_error("evaluate graph: %d of %d copy nodes found", found, 2 * kEvalChunks);
+            return HG_ECUDA;
+        }
+        HG_CUDA(cudaGraphInstantiate(&G.exec, g, 0));
+        G.B = B;
+        G.P = P->out;
+        G.Ph = P->hubs;
+        G.dsrc = dsrc;
+        G.kind = kind;
+        G.exact = I.exact;
+    } else {
+        for (int c = 0; c < kEvalChunks; ++c) {
+            const int64_t b0 = G.lo[c], nb = G.lo[c + 1] - G.lo[c];
+            HG_CUDA(cudaGraphExecMemcpyNodeSetParams1D(
+                G.exec, G.h2d[c], (void*)(dsrc + b0 * I.p), hubs + b0 * I.p,
+                (size_t)nb * I.p * sizeof(int64_t), cudaMemcpyHostToDevice));
+            HG_CUDA(cudaGraphExecMemcpyNodeSetParams1D(
+                G.exec, G.d2h[c], out + 4 * b0, P->out + 4 * b0, (size_t)nb * 4 * sizeof(double),
+                cudaMemcpyDeviceToHost));
+        }
+    }
+    HG_CUDA(cudaGraphLaunch(G.exec, s));
+    note_launch((uint64_t)G.kernels);
+    return HG_OK;
+}
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
 }
 
 // host hub sets / allocations in, validated on the device (see k_hubs_in)
@@ -662,6 +811,7 @@ static void inst_destroy(hg_inst* inst) {
     if (inst->hflag) cudaFreeHost(inst->hflag);
     cudaFree(inst->dW8);
     cudaFree(inst->dM8);
+    inst->eg.release();
     if (inst->cstream) {
         cudaStreamSynchronize(inst->cstream);
         cudaStreamDestroy(inst->cstream);
@@ -780,7 +930,26 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
     if (trace) cudaEventRecord(te[0], inst->stream);
     static const int chunked = env_int("HUBGPU_EVAL_CHUNKS", 1);  // tuning override: 0 = off
     const bool piped = !alloc && chunked && B >= kEvalChunks * kEvalChunkMin;
-    if (piped) {
+    static const int graphed = env_int("HUBGPU_EVAL_GRAPH", 1);  // tuning override: 0 = off
+    // HUBGPU_EVAL_ZEROCOPY=1: no copies (measured slower end to end: K2's
+    // warps all start on a PCIe read of their hub set, 313 vs 258 us per 8192)
+    static const int zcopy = env_int("HUBGPU_EVAL_ZEROCOPY", 0);
+    const int64_t* hubs_d = nullptr;
+    double* out_d = nullptr;
+    if (!alloc && zcopy) {
+        hubs_d = static_cast<const int64_t*>(host_mapped(hubs));
+        out_d = hubs_d ? static_cast<double*>(const_cast<void*>(host_mapped(out))) : nullptr;
+    }
+    const bool use_zc = hubs_d && out_d;
+    const bool use_graph =
+        !use_zc && piped && graphed && !trace && host_pinned(hubs) && host_pinned(out);
+    if (use_zc) {
+        // page-locked hub sets and results: no copies at all
+        HG_TRY(eval_zero_copy(inst, P, B, hubs_d, out_d));
+    } else if (use_graph) {
+        // (the same pipeline, replayed as one graph; it reads the error flag too)
+        HG_TRY(eval_graph_run(inst, P, B, hubs, out));
+    } else if (piped) {
         // the hub sets in chunks on the copy stream, each chunk scored as soon
         // as it lands and its costs copied back while the next one is scored
         // (the PCIe transfers hide under the kernels)
@@ -798,8 +967,9 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
         HG_CUDA(cudaMemcpyAsync(out, P->out, (size_t)B * 4 * sizeof(double),
                                 cudaMemcpyDeviceToHost, inst->stream));
     }
-    HG_CUDA(cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,
-                            inst->stream));
+    if (!use_graph)
+        HG_CUDA(cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,
+                                inst->stream));
     if (trace) cudaEventRecord(te[2], inst->stream);
     const auto h1 = std::chrono::steady_clock::now();
     HG_CUDA(cudaStreamSynchronize(inst->stream));

@@ -128,6 +128,14 @@ struct DevInst {
     // a device-side batch size (the GA's distinct-hub-set count) bounding a
     // launch sized for the host batch; nullptr: the host batch
     const int32_t* dynB;
+    // K2 reads the batch's int64 hub sets itself (nullptr: the int32 `hubs`):
+    // rows hrow0.. of the caller's batch -- typically page-locked host memory
+    // read over PCIe while K2 computes, k_hubs_in fused: each row validated
+    // (in [0, n), ascending) with the bad row recorded in *err, and written
+    // as int32 to hubs_w for K3
+    const int64_t* hubs64 = nullptr;
+    int32_t* hubs_w = nullptr;
+    int64_t hrow0 = 0;
 };
 
 constexpr int kPwStack = 16;  // tree depth bound (n < 2^21)

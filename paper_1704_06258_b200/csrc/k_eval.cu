@@ -407,6 +407,41 @@ __device__ __forceinline__ void alloc_finish(const DevInst& I, const int32_t* hs
 // and hub the argmin is 4 integer ops: key = (q << 8) | k by one byte
 // permute, then the two smallest keys (m1, m2) by min/max; m1's low byte is
 // the first hub at the minimal q, and m2 at the same q is a tie.  The
+// a warp's hub set into hs[0, p): the int32 batch, or (I.hubs64) the
+// caller's int64 row read and validated here -- the fused k_hubs_in: a bad
+// row records itself in *err (the first bad row wins) and runs on hubs 0..p-1
+// so that every later index stays in bounds; each entry goes to I.hubs_w as
+// k_hubs_in writes it (out of range -> 0) for K3
+__device__ __forceinline__ void k2_load_hubs(const DevInst& I, const int32_t* __restrict__ hubs,
+                                             int64_t b, int lane, int32_t* hs) {
+    const int p = I.p, n = I.n;
+    if (!I.hubs64) {
+        const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
+        for (int k = lane; k < p; k += 32) hs[k] = bad ? k : hubs[b * p + k];
+        return;
+    }
+    const int64_t* row = I.hubs64 + b * p;
+    bool rowbad = false;
+    for (int k0 = 0; k0 < p; k0 += 32) {
+        const int k = k0 + lane;
+        const int64_t v = k < p ? row[k] : 0;
+        int64_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+        if (lane == 0 && k0 > 0) prev = row[k0 - 1];
+        const bool inr = v >= 0 && v < n;
+        const bool ok = k >= p || (inr && (k == 0 || prev < v));
+        rowbad |= __any_sync(0xffffffffu, !ok);
+        if (k < p) I.hubs_w[b * p + k] = inr ? (int32_t)v : 0;
+        if (k < p) hs[k] = (int32_t)v;
+    }
+    if (rowbad) {
+        for (int k = lane; k < p; k += 32) hs[k] = k;
+        if (lane == 0) {
+            const int64_t r = I.hrow0 + b;
+            atomicMax(const_cast<int*>(I.err), (int)(0x7ffffffe - (r < 0x7ffffffe ? r : 0x7ffffffd)));
+        }
+    }
+}
+
 // per-node (slot, tie) codes move to the strided layout by 8 shuffles.
 template <int LM>
 __global__ void __launch_bounds__(K2<LM>::threads)
@@ -423,8 +458,7 @@ k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __re
     int32_t* hs = hs_all[warp];
     double* ring = pwring[warp];
     double* st = pwst[warp];
-    const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
-    for (int k = lane; k < p; k += 32) hs[k] = bad ? k : hubs[b * p + k];
+    k2_load_hubs(I, hubs, b, lane, hs);
     __syncwarp();
 
     PwState S;
@@ -529,8 +563,7 @@ k_allocate_r(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __
     uint32_t* ro = ro_all[warp];
     double* ring = pwring[warp];
     double* st = pwst[warp];
-    const bool bad = I.err != nullptr && *I.err != 0;  // rejected input: stay in bounds
-    if (lane < p) hs[lane] = bad ? lane : hubs[b * p + lane];
+    k2_load_hubs(I, hubs, b, lane, hs);
     __syncwarp();
     if (lane < PM) ro[lane] = (uint32_t)(lane < p ? hs[lane] : n) * (uint32_t)nq;
     __syncwarp();

@@ -342,3 +342,74 @@ def test_ga_replays_with_duplicate_grouping_forced():
                         "tests/test_gpu_round2.py::TestFractionalFlows"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+class TestEvaluateGraph:
+    """hg_evaluate replays its pipelined copies + kernels as one CUDA graph
+    when the hub sets and the results are page-locked, patching each call's
+    host pointers into the graph's copy nodes: results must equal the stream
+    path's (pageable hub sets) bit for bit, for alternating buffers and batch
+    sizes, and a bad row must still be reported."""
+
+    def test_replays_match_stream_path(self):
+        from paper_1704_06258_b200 import _lib
+
+        inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
+        pops = [hg.random_population(1000, 20, B, key=40 + k)
+                for k, B in enumerate((8192, 8192, 4096, 8192))]
+        ref = [hg.evaluate_population(inst, pop) for pop in pops]  # pageable: stream path
+        pinned = []
+        for pop in pops:
+            buf = _lib.pinned_array(pop.shape, np.int64)
+            buf[...] = pop
+            pinned.append(buf)
+        for rnd in range(3):
+            for k, buf in enumerate(pinned):
+                assert np.array_equal(hg.evaluate_population(inst, buf), ref[k]), (rnd, k)
+        bad = _lib.pinned_array(pops[0].shape, np.int64)
+        bad[...] = pops[0]
+        bad[77, 3] = bad[77, 2]
+        with pytest.raises(ValueError, match="hub set 77:"):
+            hg.evaluate_population(inst, bad)
+        assert np.array_equal(hg.evaluate_population(inst, pinned[0]), ref[0])
+
+
+@pytest.mark.gpu
+def test_zero_copy_evaluate_matches():
+    """HUBGPU_EVAL_ZEROCOPY=1 (opt-in): K2 reads the page-locked int64 hub sets
+    over PCIe and validates them itself (the fused k_hubs_in), K3 writes the
+    costs into the page-locked result buffer.  Same results as the default
+    path, same bad-row report (child process: the switch is read once)."""
+    code = r'''
+import numpy as np, pytest, sys
+sys.path.insert(0, ".")
+import paper_1704_06258_b200 as hg
+from paper_1704_06258_b200 import _lib
+inst = hg.generate_urand(1000, 20, 1704, (1.0, 0.75, 1.0))
+inst2 = hg.generate_urand(300, 40, 9, (1.0, 0.5, 2.0))
+for ins, B in ((inst, 8192), (inst, 300), (inst2, 777)):
+    pop = hg.random_population(ins.n, ins.p, B, key=B)
+    buf = _lib.pinned_array(pop.shape, np.int64)
+    buf[...] = pop
+    np.save(sys.stdout.buffer, hg.evaluate_population(ins, buf))
+bad = _lib.pinned_array((64, 20), np.int64)
+bad[...] = hg.random_population(1000, 20, 64, key=3)
+bad[41, 5] = 5000
+try:
+    hg.evaluate_population(inst, bad)
+    print("NOERROR")
+except ValueError as e:
+    assert "hub set 41:" in str(e), e
+'''
+    outs = []
+    for zc in ("0", "1"):
+        env = dict(os.environ, HUBGPU_EVAL_ZEROCOPY=zc)
+        r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr.decode()[-3000:]
+        assert b"NOERROR" not in r.stdout
+        import io
+        f = io.BytesIO(r.stdout)
+        outs.append([np.load(f) for _ in range(3)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
