@@ -413,3 +413,30 @@ except ValueError as e:
         outs.append([np.load(f) for _ in range(3)])
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+class TestDeferredFoldShapes:
+    """K3-TC/P's deferred fold (one K chunk, >= 4 output tiles) at the shapes
+    around its edges -- 4..8 tiles, ragged last tiles, odd unit counts (a
+    dummy slot in one CTA of a pair), p from 5 to 37 -- against the fp64
+    kernel, within the 1e-12 bar; and the pair path (HUBGPU_TCP_DEFER=0 is
+    covered by the shapes below 4 tiles)."""
+
+    @pytest.mark.parametrize("n,p,B", [(385, 5, 1001), (500, 13, 777), (640, 20, 2049),
+                                       (700, 37, 333), (1024, 20, 4097), (900, 8, 65)])
+    def test_vs_fp64_kernel(self, n, p, B):
+        from paper_1704_06258_b200 import _lib
+
+        inst = hg.generate_urand(n, p, 11 + n, (1.0, 0.75, 1.0))
+        pop = hg.random_population(n, p, B, key=n + p)
+        d = inst.device()
+        tens = hg.evaluate_population(inst, pop)
+        d.set_fitness(_lib.FIT_FP64)
+        try:
+            f64 = hg.evaluate_population(inst, pop)
+        finally:
+            d.set_fitness(_lib.FIT_AUTO)
+        assert _rel_ok(tens, f64, 1e-12)
+        # and batch invariance across the slot partition
+        part = hg.evaluate_population(inst, pop[B // 3:B // 3 + 17])
+        assert np.array_equal(part, tens[B // 3:B // 3 + 17])
