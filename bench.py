@@ -322,6 +322,59 @@ def ga_time_to_target(hg, inst, args):
 # ---------------------------------------------------------------------------
 
 
+SWEEP_NS, SWEEP_PS, SWEEP_BS = (200, 1000, 6000), (5, 20, 50), (4096, 65536)
+
+
+def sweep(hg, world, rank, barrier):
+    """BASELINE configs[4]: fitness-eval throughput over n x p x population per
+    GPU (device-resident hub sets, L2 flushed before every evaluation, K2 + K3
+    + finalise timed by CUDA events on the instance stream, the max over
+    ranks); whole-job evals/s = ranks x B / time, weak scaling."""
+    import torch
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    out = []
+    for n in SWEEP_NS:
+        for p in SWEEP_PS:
+            inst = hg.generate_urand(n, p, SEED, FACTORS, device=True)
+            d = inst.device()
+            st = torch.cuda.ExternalStream(d.stream)
+            for B in SWEEP_BS:
+                pop = hg._lib.DevicePopulation(d, B)
+                pop.load_hubs(hg.random_population(n, p, B, key=7, start=rank * B)
+                              .astype(np.int32))
+                reps = 5
+                with torch.cuda.stream(st):
+                    for _ in range(2):
+                        flush.zero_()
+                        pop.evaluate(B)
+                    barrier()
+                    ev = [(torch.cuda.Event(enable_timing=True),
+                           torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+                    k3 = []
+                    for k in range(reps):
+                        flush.zero_()
+                        ev[k][0].record(st)
+                        pop.evaluate(B)
+                        ev[k][1].record(st)
+                    barrier()
+                    for _ in range(2):
+                        flush.zero_()
+                        pop.evaluate(B)
+                        k3.append(pop.last_fitness_ms())
+                ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+                if world > 1:
+                    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+                    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                    ms = float(t.item())
+                out.append({"n": n, "p": p, "pop_per_gpu": B, "ms": ms,
+                            "evals_per_s": world * B / (ms * 1e-3),
+                            "k3_ms": float(np.median(k3)), "kernel": d.fitness_kernel})
+                del pop
+            del inst, d
+    return out
+
+
 def k2_roofline(k2_ms):
     """K2 (nearest-hub allocation) is bound by L1/TEX: its Cq rows (p*n*2 B
     per eval, coalesced) and the fp64 leg gathers (one sector per node);
@@ -499,6 +552,8 @@ def run_gpu(args):
     if rank == 0 and not args.no_cpu:
         ga_ttt = ga_time_to_target(hg, inst, args)
 
+    sweep_pts = sweep(hg, world, rank, barrier) if not args.no_sweep else None
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         cb = CpuBaseline()
@@ -558,6 +613,11 @@ def run_gpu(args):
         }
         if ga_ttt:
             line["ga_time_to_target"] = ga_ttt
+        if sweep_pts:
+            line["sweep"] = {"what": "BASELINE configs[4]: fitness evals/s over n x p x population "
+                                     "per GPU (weak scaling), median of 5 CUDA-event-timed "
+                                     "evaluations, L2 flushed before each, max over ranks",
+                             "points": sweep_pts}
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -639,6 +699,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] sweep")
     ap.add_argument("--ga-inner", type=int, default=12,
                     help="generations of the CPU-reference GA run (about 1 s each)")
     args = ap.parse_args()
