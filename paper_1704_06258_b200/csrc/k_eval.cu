@@ -458,6 +458,9 @@ k_allocate(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __re
     int32_t* hs = hs_all[warp];
     double* ring = pwring[warp];
     double* st = pwst[warp];
+    // the fitness kernel (launched programmatically dependent) may start its
+    // own set-up now; it waits for this grid before reading what it writes
+    asm volatile("griddepcontrol.launch_dependents;");
     k2_load_hubs(I, hubs, b, lane, hs);
     __syncwarp();
 
@@ -563,6 +566,9 @@ k_allocate_r(DevInst I, int64_t B, const int32_t* __restrict__ hubs, uint8_t* __
     uint32_t* ro = ro_all[warp];
     double* ring = pwring[warp];
     double* st = pwst[warp];
+    // the fitness kernel (launched programmatically dependent) may start its
+    // own set-up now; it waits for this grid before reading what it writes
+    asm volatile("griddepcontrol.launch_dependents;");
     k2_load_hubs(I, hubs, b, lane, hs);
     __syncwarp();
     if (lane < PM) ro[lane] = (uint32_t)(lane < p ? hs[lane] : n) * (uint32_t)nq;

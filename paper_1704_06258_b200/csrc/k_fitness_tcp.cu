@@ -645,6 +645,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         }
     } else if (warp >= kYEpiWarp0 && !(A.dbg & 64)) {
         // ---------------- generators + epilogue (16 warps)
+        // (K3 is launched programmatically dependent on K2: its set-up and the
+        // first W stages overlap K2's tail; everything K2 writes -- cluster
+        // ids, legs, T planes -- is read only after this)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const int q = warp & 3;                         // TMEM lane quadrant
         const int sub = (warp - kYEpiWarp0) >> 2;       // 0..3: column quarter
         const int r = q * 32 + lane;                    // A row / accumulator lane
@@ -1397,13 +1401,17 @@ static int tcp_launch(const DevInst& I, const PArgs& A, int g, const void* wmap,
     cfg.blockDim = dim3(kYThreads);
     cfg.dynamicSmemBytes = tcp_smem_bytes(I.p, I.npad, A.P, A.exact, A.defer);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kYCluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch on the preceding kernel (K2): see the
+    // epilogue's griddepcontrol.wait (HUBGPU_TCP_PDL=0: plain serialisation)
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = env_int("HUBGPU_TCP_PDL", 1) ? 2 : 1;
     using KernFn = void (*)(const CUtensorMap, PArgs);
     const KernFn kern = A.exact ? (A.csm ? k_fitness_tcp<true, true> : k_fitness_tcp<false, true>)
                         : A.defer ? (A.csm ? k_fitness_tcp<true, false, true>
