@@ -1,4 +1,4 @@
-"""Small driver for ncu: a few island-GA generations on the UR config.
+"""Small driver for ncu: a few GA generations (128 islands x 64, UR).
 
     python tools/prof_ga.py [generations]
 """
@@ -17,4 +17,4 @@ ga = hg._lib.DeviceGa(d, 128, 0, 128, 64, 3, False, 0)
 ga.begin_round(np.sort(inst.middle_rank[:20]))
 ga.generations(gens)
 d.synchronize()
-print("done")
+print("ok")
