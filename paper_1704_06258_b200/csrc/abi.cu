@@ -112,6 +112,7 @@ struct hg_inst {
         const void* Ph = nullptr;
         const void* dsrc = nullptr;
         int kind = -1, exact = -1, kernels = 0;
+        bool broken = false;  // capture failed once: stream path from then on
         cudaGraphNode_t h2d[kEvalChunks] = {}, d2h[kEvalChunks] = {};
         int64_t lo[kEvalChunks + 1] = {};
         void release() {
@@ -941,14 +942,23 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
         out_d = hubs_d ? static_cast<double*>(const_cast<void*>(host_mapped(out))) : nullptr;
     }
     const bool use_zc = hubs_d && out_d;
-    const bool use_graph =
-        !use_zc && piped && graphed && !trace && host_pinned(hubs) && host_pinned(out);
+    const bool use_graph = !use_zc && piped && graphed && !trace && !inst->eg.broken &&
+                           host_pinned(hubs) && host_pinned(out);
     if (use_zc) {
         // page-locked hub sets and results: no copies at all
         HG_TRY(eval_zero_copy(inst, P, B, hubs_d, out_d));
     } else if (use_graph) {
         // (the same pipeline, replayed as one graph; it reads the error flag too)
-        HG_TRY(eval_graph_run(inst, P, B, hubs, out));
+        if (eval_graph_run(inst, P, B, hubs, out) != HG_OK) {
+            // a pipeline that cannot be captured (or replayed) here: the stream
+            // path, for this and every later call on the instance
+            inst->eg.release();
+            inst->eg.broken = true;
+            cudaGetLastError();
+            HG_TRY(eval_pipelined(inst, P, B, hubs, out));
+            HG_CUDA(cudaMemcpyAsync(inst->hflag, inst->derr, sizeof(int), cudaMemcpyDeviceToHost,
+                                    inst->stream));
+        }
     } else if (piped) {
         // the hub sets in chunks on the copy stream, each chunk scored as soon
         // as it lands and its costs copied back while the next one is scored
