@@ -188,13 +188,22 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
         "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
         : "memory");
 }
-__device__ __forceinline__ void mma_ts_w(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t acc) {  // one elected lane of the warp
+// a K block's four K=32 MMAs (A columns a, a+8, a+16, a+24; B descriptors
+// bdesc + 0, 2, 4, 6 -- 32 bytes apart in the 128-byte swizzled rows) from one
+// elected lane: one election and one descriptor set-up for the four
+__device__ __forceinline__ void mma4_ts_w(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {  // acc: the first MMA accumulates
     asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "setp.eq.b32 t, %4, %4;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [a1], b1, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [a2], b2, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [a3], b3, %3, t;\n\t}" ::"r"(d),
         "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
         : "memory");
 }
@@ -331,6 +340,9 @@ struct PArgs {
 };
 
 constexpr int kYChunkKB = 8;  // K blocks per chunk: 8 x 128 nodes = 256 TMEM columns of A
+// instruction descriptor: kind::i8, u8 x u8 -> s32, M = 256 (the pair), N = 128,
+// both operands K-major (a compile-time constant: no per-MMA constant loads)
+constexpr uint32_t kIdescI8 = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 constexpr int kYDeferBars = 11;  // binsdone[2] folded[2] tready[2] cready[3] reduced[2]
 
 // CSM: a unit's cluster rows staged in shared memory (known address space ->
@@ -615,10 +627,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                                     }
                                     if (A.dbg & 2) continue;
                                     const uint64_t bd = bd0 + (uint64_t)((kk * kYStageBytes) >> 4);
-#pragma unroll
-                                    for (int ks = 0; ks < 4; ++ks)  // K step 32 = 8 TMEM columns
-                                        mma_ts_w(dcol, tmem + kb * 32 + ks * 8, bd + 2 * ks,
-                                               A.idesc, (kb != k0) | (ks != 0));
+                                    // K steps of 32 = 8 TMEM columns of A each
+                                    mma4_ts_w(dcol, tmem + kb * 32, bd, kIdescI8, kb != k0);
                                 }
                                 commit_pair_w(b_empty + 8 * s);
                                 if (pl == A.P - 1)  // last use of A quarters: free them
@@ -1311,7 +1321,7 @@ static int tcp_setup(const DevInst& I, bool tri_avail, int64_t B, int grid, PArg
     A.pstride = 1;
     A.wscale = I.wscale;
     if (A.P > kYMaxPlanes) A.P = 1;  // one launch per plane (launch_fitness_tcp)
-    A.idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    A.idesc = kIdescI8;
     A.timing = tc_timing_buffer();
     A.dbg = env_int("HUBGPU_TCP_DBG", 0);
     A.leaves = I.pwl;
