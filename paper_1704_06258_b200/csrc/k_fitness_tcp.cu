@@ -879,11 +879,19 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             // (32-bit divisions: inline code, no 64-bit division subroutine)
             const uint64_t mpp = (uint64_t)(0xFFFFFFFFu / (uint32_t)pp) + 1u;
             const uint64_t mp = (uint64_t)(0xFFFFFFFFu / (uint32_t)p) + 1u;
+            int m = 0;
             for (int x = etid + part * kYEpiThreads; x < nind * pp; x += parts * kYEpiThreads) {
                 const int b2 = (int)(((uint64_t)x * mpp) >> 32), kl = x - b2 * pp;
                 const int k = (int)(((uint64_t)kl * mp) >> 32), l2 = kl - k * p;
                 const int32_t* hs = hsj + b2 * p;
                 cp_async8(sTj + 8u * x, A.C + (size_t)hs[k] * A.nC + hs[l2]);
+                // (large p: at most two groups of 16 copies in flight per thread --
+                // a thread with ~40 uncommitted copies trapped in testing)
+                if (++m == 16) {
+                    m = 0;
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                }
             }
         };
         // (slot j's first tile runs slot j-1's reduce; phase = j * NC + c is

@@ -423,7 +423,8 @@ class TestDeferredFoldShapes:
     covered by the shapes below 4 tiles)."""
 
     @pytest.mark.parametrize("n,p,B", [(385, 5, 1001), (500, 13, 777), (640, 20, 2049),
-                                       (700, 37, 333), (1024, 20, 4097), (900, 8, 65)])
+                                       (700, 37, 333), (1024, 20, 4097), (900, 8, 65),
+                                       (600, 64, 301), (900, 40, 1000), (1000, 90, 128)])
     def test_vs_fp64_kernel(self, n, p, B):
         from paper_1704_06258_b200 import _lib
 
