@@ -325,7 +325,10 @@ int eval_pipelined(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, dou
     int64_t lo[kEvalChunks + 1];
     const int64_t ipt = I.p <= 128 ? 128 / I.p : 1;
     static const int wave_first = env_int("HUBGPU_EVAL_WAVE", 0);  // tuning override
-    const int64_t first = wave_first ? (int64_t)inst->sm_count * ipt : B / 2;
+    // HUBGPU_EVAL_FIRST=k: a first chunk of B / k (tuning override; default 2)
+    static const int first_div = env_int("HUBGPU_EVAL_FIRST", 2);
+    const int64_t first = wave_first ? (int64_t)inst->sm_count * ipt
+                                     : B / (first_div >= 2 ? first_div : 2);
     lo[0] = 0;
     lo[1] = first < B / 2 ? first : B / 2;
     for (int c = 2; c <= kEvalChunks; ++c) lo[c] = lo[1] + (B - lo[1]) * (c - 1) / (kEvalChunks - 1);
