@@ -275,7 +275,8 @@ int queue_fitness(hg_inst* inst, int64_t B, const int32_t* hubs, const uint8_t* 
 // queue K2 + K3 + finalise for individuals [b0, b0 + B) of P whose int32 hubs
 // are in P->hubs (alloc32 == nullptr: nearest allocation; otherwise the given
 // allocation, rows from b0); events: time K2 and K3 (hg_pop_last_*_ms)
-int pop_eval_range(hg_pop* P, int64_t b0, int64_t B, const int32_t* alloc32, bool events) {
+int pop_eval_range(hg_pop* P, int64_t b0, int64_t B, const int32_t* alloc32, bool events,
+                   double* out_all = nullptr) {
     hg_inst* inst = P->inst;
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
@@ -292,7 +293,8 @@ int pop_eval_range(hg_pop* P, int64_t b0, int64_t B, const int32_t* alloc32, boo
     else
         HG_TRY(launch_allocate(I, B, hubs, cl, co, T_for(inst, B, T), legs, nullptr, s));
     if (events) HG_CUDA(cudaEventRecord(P->ev0, s));
-    HG_TRY(queue_fitness(inst, B, hubs, cl, co, T, P->part + b0 * tiles, legs, P->out + 4 * b0));
+    HG_TRY(queue_fitness(inst, B, hubs, cl, co, T, P->part + b0 * tiles, legs,
+                         (out_all ? out_all : P->out) + 4 * b0));
     if (events) HG_CUDA(cudaEventRecord(P->ev1, s));
     return HG_OK;
 }
@@ -305,7 +307,10 @@ int pop_eval_queue(hg_pop* P, int64_t B, const int32_t* alloc32) {
 // stream while chunk c-1 is scored on the instance stream; chunk c's costs go
 // back on the copy stream once scored.  The caller reads the flag and
 // synchronises the instance stream, which waits for the last copy.
-int eval_pipelined(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, double* out) {
+// out_d: the device address of a page-locked `out` -- the finaliser then writes
+// the costs straight into it (no copies back)
+int eval_pipelined(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, double* out,
+                   double* out_d = nullptr) {
     const DevInst& I = inst->I;
     cudaStream_t s = inst->stream;
     if (!inst->cstream) {
@@ -344,9 +349,10 @@ int eval_pipelined(hg_inst* inst, hg_pop* P, int64_t B, const int64_t* hubs, dou
         HG_CUDA(cudaStreamWaitEvent(s, inst->ev_in[c], 0));
         HG_TRY(launch_hubs_in(dsrc + b0 * I.p, P->hubs + b0 * I.p, nb, I.p, I.n, inst->derr, s,
                               b0));
-        HG_TRY(pop_eval_range(P, b0, nb, nullptr, false));
+        HG_TRY(pop_eval_range(P, b0, nb, nullptr, false, out_d));
         HG_CUDA(cudaEventRecord(inst->ev_done[c], s));
     }
+    if (out_d) return HG_OK;  // nothing to copy back
     // (every kernel is queued before the first copy back: a pageable `out`
     // makes that copy synchronous for the host)
     for (int c = 0; c < kEvalChunks; ++c) {
@@ -965,8 +971,11 @@ int hg_evaluate(hg_inst* inst, int64_t B, const int64_t* hubs, const int64_t* al
     } else if (piped) {
         // the hub sets in chunks on the copy stream, each chunk scored as soon
         // as it lands and its costs copied back while the next one is scored
-        // (the PCIe transfers hide under the kernels)
-        HG_TRY(eval_pipelined(inst, P, B, hubs, out));
+        // (the PCIe transfers hide under the kernels).  HUBGPU_EVAL_ZCOUT=1:
+        // costs written by the finaliser into a page-locked `out` directly
+        static const int zcout = env_int("HUBGPU_EVAL_ZCOUT", 0);
+        double* od = zcout ? static_cast<double*>(const_cast<void*>(host_mapped(out))) : nullptr;
+        HG_TRY(eval_pipelined(inst, P, B, hubs, out, od));
     } else {
         HG_TRY(h2d_hubs_checked(inst, inst->t1, hubs, B, P->hubs));
         const int32_t* a32 = nullptr;
