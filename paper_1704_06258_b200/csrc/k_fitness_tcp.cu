@@ -921,9 +921,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             {
                 const int etid = tid - kYEpiWarp0 * 32;
                 if (A.tsm) {
-                    // (defer: spread over the unit's tiles instead, gather_T)
                     // defer: unit j's hubs came with unit j-1's batch -- wait for
-                    // it (every epilogue thread's copies, tready[(j-1) & 1]).
+                    // it (every epilogue thread's copies issued at unit j-1's
+                    // top, tready[(j-1) & 1]).
                     // (Spreading this gather over the unit's tiles instead gave
                     // wrong tables in the checked build: kept at the unit top.)
                     if (DF && j > 0)
@@ -945,6 +945,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     cp_async16(su32(sL + (j & 1) * kYMaxIpt * 2 + 2 * etid),
                                A.legs + 2 * (bbase + etid));
                 asm volatile("cp.async.commit_group;" ::: "memory");
+                // defer: this unit's T tables and legs and the next unit's hubs,
+                // all issued above, land on tready[j & 1] -- no wait for the
+                // unit's end (the next unit's gather and this unit's fold wait)
+                if (DF) cp_async_arrive(b_tready + 8 * (uint32_t)(j & 1));
             }
             TRC(tr_role, 26);
             // this row's T column: fp64 T_b[k][l] at tbd[k * p] (tsm), else K2's
@@ -1072,9 +1076,6 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                 }
                 if (DF) {  // this warp's atomics of unit j are done; fold + reduce deferred
-                    // (the unit's T gather, next hubs and legs: tready[j & 1])
-                    asm volatile("cp.async.commit_group;" ::: "memory");
-                    cp_async_arrive(b_tready + 8 * (uint32_t)(j & 1));
                     __syncwarp();
                     if (lane == 0) mb_arrive(b_bdone + 8 * (uint32_t)(j & 1));
                     continue;  // (one chunk)
