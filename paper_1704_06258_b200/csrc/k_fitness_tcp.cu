@@ -928,6 +928,14 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     // wrong tables in the checked build: kept at the unit top.)
                     if (DF && j > 0)
                         mb_wait(b_tready + 8 * (uint32_t)((j - 1) & 1), (uint32_t)(((j - 1) >> 1) & 1));
+                    // ... and every warp's fold of unit j-2 is done with sT[j & 1].
+                    // With >= 5 tiles per unit the accumulator hand-off already
+                    // orders it (a warp here has drained unit j-1's last tile, so
+                    // every warp released unit j-1's tile NT-3 >= 2, after its
+                    // tile-1 fold); with 4 a slow warp may still be between its
+                    // tile 1 and its fold
+                    if (DF && j >= 2 && A.P * ntl(0) < 5)
+                        mb_wait(b_fold + 8 * (uint32_t)(j & 1), (uint32_t)(((j - 2) >> 1) & 1));
                     gather_T(j, nind, 0, 1);
                     if (j + 1 < nslots) {
                         int64_t nb;
