@@ -244,10 +244,16 @@ __device__ __forceinline__ uint32_t oh4(uint32_t x, uint32_t lrep) {
 // one row's share of a plane's fold: s += sum_k G[k] * T[k][l] * sc over
 // k = sub, sub + 4, ... (fixed order), zeroing the bins; out of line -- the
 // epilogue's tile loop is register-bound
+// lsym >= 0 (symmetric costs, the table's upper triangle only): T[k][l] for
+// k > lsym = l is read as T[l][k]
 __device__ __noinline__ double fold_bins(uint32_t* bp, const double* tbd, const uint32_t* tbp,
-                                         int p, int ps, int sub, double sc, double s) {
+                                         int p, int ps, int sub, double sc, double s,
+                                         int lsym = -1) {
+    const double* trow = tbd && lsym >= 0 ? tbd - lsym + lsym * p : nullptr;
     auto tv = [&](int k) {
-        return tbd ? tbd[k * p] : __hiloint2double((int)tbp[k * ps], (int)tbp[(p + k) * ps]);
+        return trow && k > lsym ? trow[k]
+               : tbd        ? tbd[k * p]
+                            : __hiloint2double((int)tbp[k * ps], (int)tbp[(p + k) * ps]);
     };
     int k = sub;
     // four bins at a time, their loads issued together (same summation order)
@@ -858,7 +864,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     const double sc =
                         A.wscale * __longlong_as_double((long long)(1023 + 8 * pl) << 52);
                     sp = fold_bins(bins + (size_t)(bx * PB + pl) * p * 128 + r, tb, tp, p,
-                                   A.ps, sub, sc, sp);
+                                   A.ps, sub, sc, sp, A.tri && A.tsm ? l : -1);
                 }
             }
             red[bx * 512 + sub * 128 + r] = sp;
@@ -883,6 +889,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             for (int x = etid + part * kYEpiThreads; x < nind * pp; x += parts * kYEpiThreads) {
                 const int b2 = (int)(((uint64_t)x * mpp) >> 32), kl = x - b2 * pp;
                 const int k = (int)(((uint64_t)kl * mp) >> 32), l2 = kl - k * p;
+                // (defer on symmetric costs: the upper triangle only -- the
+                // fold reads T[l][k] for T[k][l] below the diagonal)
+                if (DF && A.tri && k > l2) continue;
                 const int32_t* hs = hsj + b2 * p;
                 cp_async8(sTj + 8u * x, A.C + (size_t)hs[k] * A.nC + hs[l2]);
                 // (large p: at most two groups of 16 copies in flight per thread --
