@@ -349,7 +349,7 @@ constexpr int kYChunkKB = 8;  // K blocks per chunk: 8 x 128 nodes = 256 TMEM co
 // instruction descriptor: kind::i8, u8 x u8 -> s32, M = 256 (the pair), N = 128,
 // both operands K-major (a compile-time constant: no per-MMA constant loads)
 constexpr uint32_t kIdescI8 = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-constexpr int kYDeferBars = 11;  // binsdone[2] folded[2] tready[2] cready[3] reduced[2]
+constexpr int kYDeferBars = 13;  // binsdone[2] folded[2] tready[2] cready[3] reduced[2] tgath[2]
 
 // CSM: a unit's cluster rows staged in shared memory (known address space ->
 // LDS) rather than read from global memory
@@ -393,7 +393,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kYMaxStages,
                    b_accf = b_empty + 8 * kYMaxStages, b_acce = b_accf + 16, b_kbf = b_acce + 16,
                    b_ard = b_kbf + 32, b_bdone = b_ard + 32, b_fold = b_bdone + 16,
-                   b_tready = b_fold + 16, b_cready = b_tready + 16, b_rdone = b_cready + 24;
+                   b_tready = b_fold + 16, b_cready = b_tready + 16, b_rdone = b_cready + 24,
+                   b_tgath = b_rdone + 16;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kYMaxStages + 12 + kYDeferBars);
     // chunk c of the K dimension: K blocks [c*8, c*8 + nkb(c)); its one-hot is
     // generated in 4 contiguous ranges of K blocks, one per column-quarter warp
@@ -435,7 +436,10 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             mb_init(b_tready + 8 * x, kYEpiThreads);      // every thread's cp.async (noinc)
         }
         for (int x = 0; x < 3; ++x) mb_init(b_cready + 8 * x, kYEpiThreads);
-        for (int x = 0; x < 2; ++x) mb_init(b_rdone + 8 * x, 2);  // warps 2-3
+        for (int x = 0; x < 2; ++x) {
+            mb_init(b_rdone + 8 * x, 2);   // warps 2-3
+            mb_init(b_tgath + 8 * x, 64);  // warps 2-3's cp.async (noinc), a unit's T
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
     }
@@ -522,7 +526,56 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
 
     if (DF && (warp == 2 || warp == 3)) {
         // ---------------- (defer) the units' reduces, each once its folds are
-        // in: the epilogue warps never stop draining for them
+        // in, and (T in smem) the units' hubs + hub-cost tables two units
+        // ahead: the epilogue warps never stop draining for them
+        const int t2 = tid - 64;  // 0..63
+        auto sync2 = [&]() {
+            __syncwarp();
+            asm volatile("bar.sync 2, 64;" ::: "memory");
+        };
+        // unit u's hubs into sH[u % 3] (own copies awaited, then both warps)
+        auto hubs_of = [&](int64_t u) {
+            int64_t nb;
+            int nn;
+            slot_unit(u, nb, nn);
+            for (int x = t2; x < nn * p; x += 64)
+                cp_async4(su32(sH + (int)((uint32_t)u % 3u) * ipt * p + x), A.hubs + nb * p + x);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            sync2();
+        };
+        // unit u's tables T_b[k][l] = C[h_k][h_l] into sT[u & 1] (symmetric
+        // costs: the upper triangle), landing on tgath[u & 1]
+        auto gather_of = [&](int64_t u) {
+            int64_t nb;
+            int nn;
+            slot_unit(u, nb, nn);
+            const uint32_t sTu = su32(sT) + (uint32_t)(u & 1) * (uint32_t)p_T_bytes(ipt, p);
+            const int32_t* hsu = sH + (int)((uint32_t)u % 3u) * ipt * p;
+            const int pp = p * p;
+            const uint64_t mpp = (uint64_t)(0xFFFFFFFFu / (uint32_t)pp) + 1u;
+            const uint64_t mp = (uint64_t)(0xFFFFFFFFu / (uint32_t)p) + 1u;
+            int m = 0;
+            for (int x = t2; x < nn * pp; x += 64) {
+                const int b2 = (int)(((uint64_t)x * mpp) >> 32), kl = x - b2 * pp;
+                const int k = (int)(((uint64_t)kl * mp) >> 32), l2 = kl - k * p;
+                if (A.tri && k > l2) continue;
+                const int32_t* hs = hsu + b2 * p;
+                cp_async8(sTu + 8u * x, A.C + (size_t)hs[k] * A.nC + hs[l2]);
+                if (++m == 16) {  // (bounded groups of copies in flight)
+                    m = 0;
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            cp_async_arrive(b_tgath + 8 * (uint32_t)(u & 1));
+        };
+        if (A.tsm)
+            for (int64_t u = 0; u < 2 && u < nslots; ++u) {
+                hubs_of(u);
+                gather_of(u);
+            }
         for (int64_t j = 0; j < nslots; ++j) {
             mb_wait(b_fold + 8 * (uint32_t)(j & 1), (uint32_t)((j >> 1) & 1));
             int64_t pb;
@@ -531,6 +584,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             reduce_rows(pb, pn, j, warp - 2, 2);
             __syncwarp();
             if (lane == 0) mb_arrive(b_rdone + 8 * (uint32_t)(j & 1));
+            // unit j+2's tables go where unit j's were (its fold is done)
+            if (A.tsm && j + 2 < nslots) {
+                hubs_of(j + 2);
+                gather_of(j + 2);
+            }
         }
     } else if (warp == 1) {
         // ---------------- TMA producer: per phase, the W tiles (plane, row
@@ -754,7 +812,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             }
         };
         if (nslots > 0) {
-            if (A.tsm) {  // unit 0's hubs (each unit's T gather reads them)
+            if (A.tsm && !DF) {  // unit 0's hubs (each unit's T gather reads them; defer: warps 2-3)
                 int64_t nb;
                 int nn;
                 slot_unit(0, nb, nn);
@@ -854,6 +912,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             const uint32_t bx = (uint32_t)(jp & 1), par = (uint32_t)((jp >> 1) & 1);
             mb_wait(b_bdone + 8 * bx, par);
             mb_wait(b_tready + 8 * bx, par);
+            if (A.tsm) mb_wait(b_tgath + 8 * bx, par);  // its tables (warps 2-3)
             double sp = 0.0;
             if (livep && !(A.dbg & 4)) {
                 const double* tb =
@@ -929,30 +988,14 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             // and the deferred reduce; the previous unit's fold is done with them
             {
                 const int etid = tid - kYEpiWarp0 * 32;
-                if (A.tsm) {
-                    // defer: unit j's hubs came with unit j-1's batch -- wait for
-                    // it (every epilogue thread's copies issued at unit j-1's
-                    // top, tready[(j-1) & 1]).
-                    // (Spreading this gather over the unit's tiles instead gave
-                    // wrong tables in the checked build: kept at the unit top.)
-                    if (DF && j > 0)
-                        mb_wait(b_tready + 8 * (uint32_t)((j - 1) & 1), (uint32_t)(((j - 1) >> 1) & 1));
-                    // ... and every warp's fold of unit j-2 is done with sT[j & 1].
-                    // With >= 5 tiles per unit the accumulator hand-off already
-                    // orders it (a warp here has drained unit j-1's last tile, so
-                    // every warp released unit j-1's tile NT-3 >= 2, after its
-                    // tile-1 fold); with 4 a slow warp may still be between its
-                    // tile 1 and its fold
-                    if (DF && j >= 2 && A.P * ntl(0) < 5)
-                        mb_wait(b_fold + 8 * (uint32_t)(j & 1), (uint32_t)(((j - 2) >> 1) & 1));
+                if (A.tsm && !DF) {  // (defer: hubs and tables by warps 2-3)
                     gather_T(j, nind, 0, 1);
                     if (j + 1 < nslots) {
                         int64_t nb;
                         int nn;
                         slot_unit(j + 1, nb, nn);
                         for (int x = etid; x < nn * p; x += kYEpiThreads)
-                            cp_async4(su32(sH + (DF ? (int)((j + 1) % 3) : (int)((j + 1) & 1)) * ipt * p + x),
-                                      A.hubs + nb * p + x);
+                            cp_async4(su32(sH + ((j + 1) & 1) * ipt * p + x), A.hubs + nb * p + x);
                     }
                 }
                 // defer: unit j - 2's reduce (warps 2-3) is done with sL / red
