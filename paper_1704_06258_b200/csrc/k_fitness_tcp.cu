@@ -759,6 +759,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             const bool live = r < ipt * p && bl < nind;
             const uint32_t lrep = (uint32_t)l * 0x01010101u;
             if (CSM && DF) mb_wait(b_cready + 8 * (uint32_t)(j % 3), (uint32_t)((j / 3) & 1));
+            TRC(tr_role, 19);
             const uint8_t* rowp = CSM ? sC0 + cbuf(j) * cb + (size_t)(live ? bl : 0) * A.npad
                                         : A.cl + (bbase + (live ? bl : 0)) * A.npad;
             const uint4* crow =
@@ -779,6 +780,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 __syncwarp();
                 st8(tmem + lane_base + (uint32_t)c0, v);
             }
+            TRC(tr_role, 25);
             __syncwarp();
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             fence_before();

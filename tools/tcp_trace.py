@@ -8,7 +8,8 @@ in clock64 cycles relative to the first event of the first chosen slot, and a
 per-tile summary (MMA issue window, accumulator hand-off, epilogue drain).
 Codes: MMA 1 wait acc-empty, 2 acc free, 3 W stage ready, 4/5 A-quarter wait
 begin/end, 8 tile committed; epilogue 24 slot top, 26 T gather issued,
-11/12 kbf wait begin/end, 13 one-hot generated, 14 acc-full wait, 15 acc full,
+11/12 kbf wait begin/end, 19 cluster rows ready (deferred fold), 25 one-hot
+stores issued, 13 one-hot generated, 14 acc-full wait, 15 acc full,
 16 released, 17 bins done, 18 reduce done, 20 chunk end, 21 after sync 1,
 22 fold done, 23 after sync 2.
 """
@@ -81,5 +82,6 @@ print("MMA: total", tot, "wait acc-empty", spans(mma, 1, 2), "wait A", spans(mma
 for name, ev in (("epi4", roles[1]), ("epi19", roles[2])):
     print(name, "wait acc-full", spans(ev, 14, 15), "drain", spans(ev, 15, 16),
           "bins", spans(ev, 16, 17), "kbf wait", spans(ev, 11, 12), "gen", spans(ev, 12, 13),
+          "gen cready wait", spans(ev, 12, 19), "gen st wait", spans(ev, 25, 13),
           "sync1", spans(ev, 20, 21), "fold", spans(ev, 21, 22), "sync2", spans(ev, 22, 23),
           "reduce", spans(ev, 17, 18), "top", spans(ev, 24, 26))
