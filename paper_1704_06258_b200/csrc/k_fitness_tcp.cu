@@ -751,6 +751,15 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         // lane quadrant, reading the cluster rows straight from global memory
         // (lanes of one individual read the same bytes: L1 broadcasts)
         // the cluster-row buffer of unit j (defer: 3, staged by cp.async)
+// the tile after which column quarter s folds the previous unit (nibble s):
+// quarter 0 generates the next unit's first one-hot quarter at tile 1, so it
+// folds at tile 3, the others at tile 1 (tools/ab_k3.py: 0.1229 vs 0.1249 ms
+// with every quarter at tile 1)
+#ifndef HG_FOLD_TS
+#define HG_FOLD_TS 0x1113
+#endif
+        static_assert((HG_FOLD_TS & 0xcccc) == 0, "the deferred fold runs with >= 4 tiles");
+        const int ftile = (HG_FOLD_TS >> (4 * sub)) & 15;
         auto cbuf = [&](int64_t j) { return DF ? (int)(j % 3) : (int)(j & 1); };
         auto gen = [&](int64_t j, int c) {
             int64_t bbase;
@@ -1122,9 +1131,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                     TRC(tr_role, 17);
                     ET(e_cmp);
-                    if (DF && tt == 1 && j > 0) {
-                        // the previous unit's fold after this unit's tile 1 (its
-                        // reduce: warps 2-3)
+                    if (DF && tt == ftile && j > 0) {
+                        // the previous unit's fold after this unit's tile 1, 3
+                        // for column quarter 0 (its reduce: warps 2-3)
                         fold_unit(j - 1);
                         TRC(tr_role, 18);
                     }
