@@ -1068,10 +1068,15 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     // generate as soon as the quarter is free: the MMA issuer
                     // runs up to two tiles ahead, so poll from two tiles before
                     // the releasing one (the next phase's first MMAs wait on it)
-                    if (!last_phase && !gen_done && tt >= tt_gen - 2 &&
-                        (tt == tt_gen ||
-                         (hq >= 0 && __shfl_sync(0xffffffffu,
-                                                 (int)mb_try(b_kbf + 8 * hq, phase & 1u), 0)))) {
+// where a warp generates its quarter of the next one-hot (deferred fold; the
+// other instantiations keep 0): 2 (default) after
+// the releasing tile's drain and bin atomics -- the freed accumulator goes back
+// to the MMA first; 0 at the top of that tile, before its drain, polling from
+// two tiles earlier (tools/ab_k3.py: 0.1208 vs 0.1238 ms)
+#ifndef HG_GEN_POS
+#define HG_GEN_POS 2
+#endif
+                    auto gen_next = [&]() {
                         TRC(tr_role, 11);
                         if (hq >= 0) {
                             mb_wait(b_kbf + 8 * hq, phase & 1u);
@@ -1086,7 +1091,12 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         gen_done = true;
                         TRC(tr_role, 13);
                         ET(e_gen);
-                    }
+                    };
+                    if ((HG_GEN_POS == 0 || !DF) && !last_phase && !gen_done && tt >= tt_gen - 2 &&
+                        (tt == tt_gen ||
+                         (hq >= 0 && __shfl_sync(0xffffffffu,
+                                                 (int)mb_try(b_kbf + 8 * hq, phase & 1u), 0))))
+                        gen_next();
                     // cluster ids of the 32 columns i = it*128 + sub*32 + k
                     uint4 ca = make_uint4(0, 0, 0, 0), cz = ca;
                     if (live) {
@@ -1131,6 +1141,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                     TRC(tr_role, 17);
                     ET(e_cmp);
+                    if (HG_GEN_POS == 2 && DF && !last_phase && !gen_done && tt == tt_gen) gen_next();
                     if (DF && tt == ftile && j > 0) {
                         // the previous unit's fold after this unit's tile 1, 3
                         // for column quarter 0 (its reduce: warps 2-3)
