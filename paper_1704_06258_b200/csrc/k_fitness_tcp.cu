@@ -778,11 +778,15 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 uint32_t v[8];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const uint4 x = live ? crow[(c0 >> 2) + h] : make_uint4(0, 0, 0, 0);
-                    v[4 * h + 0] = live ? oh4(x.x, lrep) : 0u;
-                    v[4 * h + 1] = live ? oh4(x.y, lrep) : 0u;
-                    v[4 * h + 2] = live ? oh4(x.z, lrep) : 0u;
-                    v[4 * h + 3] = live ? oh4(x.w, lrep) : 0u;
+                    // (CSM: a dead row -- padding, or past the batch -- encodes
+                    // the staged row 0 or stale bytes: harmless, it only feeds
+                    // its own accumulator row, which nothing reads)
+                    const bool ld = CSM || live;
+                    const uint4 x = ld ? crow[(c0 >> 2) + h] : make_uint4(0, 0, 0, 0);
+                    v[4 * h + 0] = ld ? oh4(x.x, lrep) : 0u;
+                    v[4 * h + 1] = ld ? oh4(x.y, lrep) : 0u;
+                    v[4 * h + 2] = ld ? oh4(x.z, lrep) : 0u;
+                    v[4 * h + 3] = ld ? oh4(x.w, lrep) : 0u;
                 }
                 // (.sync.aligned: the warp must be converged -- the compiler
                 // does not know the asm requires it)
