@@ -414,6 +414,21 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
     auto qrb = [&](int c, int h) {
         return kq(c, h) < kq(c, h + 1) ? kq(c, h + 1) - 1 : (kq(c, h) > 0 ? kq(c, h) - 1 : 0);
     };
+    // HG_QSPLIT=1 (deferred fold, triangular fold): the last quarter -- freed
+    // only by a unit's last tile, needed soon after by the next unit's first --
+    // generated by the four column-quarter warps of a lane quadrant, 1/4 each,
+    // its ready barrier counting 4x.  Parity-green but measured slower (0.1178
+    // vs 0.1167 ms, tools/ab_k3.py): off
+#ifndef HG_QSPLIT
+#define HG_QSPLIT 0
+#endif
+    const bool qsplit = HG_QSPLIT && DF && tri && NC == 1 && kq(0, 3) < kq(0, 4);
+    // 32-bit TMEM columns [lo, hi) of part s_ of the last quarter
+    auto q3part = [&](int s_, int& lo, int& hi) {
+        const int base = kq(0, 3) * 32, n8 = (kq(0, 4) - kq(0, 3)) * 4;
+        lo = base + 8 * (n8 * s_ / 4);
+        hi = base + 8 * (n8 * (s_ + 1) / 4);
+    };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int x = tid; x < NB * PB * p * 128; x += kYThreads) bins[x] = 0u;
@@ -428,7 +443,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         }
         for (int h = 0; h < 4; ++h) {
             mb_init(b_kbf + 8 * h, 1);
-            mb_init(b_ard + 8 * h, 8);  // the 4 lane-quadrant warps of quarter h, both CTAs
+            // the 4 lane-quadrant warps of quarter h, both CTAs (qsplit: all 16 for the last)
+            mb_init(b_ard + 8 * h, h == 3 && qsplit ? 32 : 8);
         }
         for (int x = 0; x < 2; ++x) {
             mb_init(b_bdone + 8 * x, kYEpiThreads / 32);  // a warp's last atomics of a unit
@@ -761,7 +777,8 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         static_assert((HG_FOLD_TS & 0xcccc) == 0, "the deferred fold runs with >= 4 tiles");
         const int ftile = (HG_FOLD_TS >> (4 * sub)) & 15;
         auto cbuf = [&](int64_t j) { return DF ? (int)(j % 3) : (int)(j & 1); };
-        auto gen = [&](int64_t j, int c) {
+        // one-hot columns [lo, hi) of phase (j, c), then quarter ha's ready arrive
+        auto gen = [&](int64_t j, int c, int lo, int hi, int ha) {
             int64_t bbase;
             int nind;
             slot_unit(j, bbase, nind);
@@ -774,7 +791,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             const uint4* crow =
                 reinterpret_cast<const uint4*>(rowp + (size_t)c * kYChunkKB * 128);
 #pragma unroll 4
-            for (int c0 = kq(c, sub) * 32; c0 < kq(c, sub + 1) * 32 && !(A.dbg & 8); c0 += 8) {
+            for (int c0 = lo; c0 < hi && !(A.dbg & 8); c0 += 8) {
                 uint32_t v[8];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -798,7 +815,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             fence_before();
             __syncwarp();
-            if (lane == 0) arrive_remote(L_ard + 8 * sub);
+            if (lane == 0) arrive_remote(L_ard + 8 * ha);
         };
 
         // stage a unit's cluster rows into double buffer j & 1 (CSM)
@@ -841,7 +858,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                 stage(0);
                 if (!DF) epi_sync();
             }
-            gen(0, 0);
+            int lo = kq(0, sub) * 32, hi = kq(0, sub + 1) * 32;
+            if (qsplit && sub == 3) q3part(3, lo, hi);
+            gen(0, 0, lo, hi, sub);
+            if (qsplit && sub < 3) {
+                q3part(sub, lo, hi);
+                gen(0, 0, lo, hi, 3);
+            }
         }
         ET(e_gen);
         // this thread's bin row: bins[k][r] at byte k * 512 + r * 4
@@ -1080,27 +1103,28 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
 #ifndef HG_GEN_POS
 #define HG_GEN_POS 2
 #endif
-                    auto gen_next = [&]() {
+                    // columns [lo, hi) of the next phase's one-hot once this
+                    // phase's quarter hw is free; ready arrive on quarter ha
+                    auto gen_next = [&](int lo, int hi, int ha, int hw) {
                         TRC(tr_role, 11);
-                        if (hq >= 0) {
-                            mb_wait(b_kbf + 8 * hq, phase & 1u);
+                        if (hw >= 0) {
+                            mb_wait(b_kbf + 8 * hw, phase & 1u);
                             fence_after();
                         }
                         TRC(tr_role, 12);
                         ET(e_kbf);
-                        if (c + 1 < NC)
-                            gen(j, c + 1);
-                        else
-                            gen(j + 1, 0);
-                        gen_done = true;
+                        gen(c + 1 < NC ? j : j + 1, c + 1 < NC ? c + 1 : 0, lo, hi, ha);
                         TRC(tr_role, 13);
                         ET(e_gen);
                     };
+                    const int cn = c + 1 < NC ? c + 1 : 0;
                     if ((HG_GEN_POS == 0 || !DF) && !last_phase && !gen_done && tt >= tt_gen - 2 &&
                         (tt == tt_gen ||
                          (hq >= 0 && __shfl_sync(0xffffffffu,
-                                                 (int)mb_try(b_kbf + 8 * hq, phase & 1u), 0))))
-                        gen_next();
+                                                 (int)mb_try(b_kbf + 8 * hq, phase & 1u), 0)))) {
+                        gen_next(kq(cn, sub) * 32, kq(cn, sub + 1) * 32, sub, hq);
+                        gen_done = true;
+                    }
                     // cluster ids of the 32 columns i = it*128 + sub*32 + k
                     uint4 ca = make_uint4(0, 0, 0, 0), cz = ca;
                     if (live) {
@@ -1145,7 +1169,22 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     }
                     TRC(tr_role, 17);
                     ET(e_cmp);
-                    if (HG_GEN_POS == 2 && DF && !last_phase && !gen_done && tt == tt_gen) gen_next();
+                    if (HG_GEN_POS == 2 && DF && !last_phase) {
+                        // this warp's quarter at its releasing tile; qsplit: its
+                        // part of the last quarter at the last tile
+                        int lo = -1, hi = 0, ha = 3, hw = 3;
+                        if (!gen_done && tt == tt_gen) {
+                            lo = kq(cn, sub) * 32;
+                            hi = kq(cn, sub + 1) * 32;
+                            if (qsplit && sub == 3) q3part(3, lo, hi);
+                            ha = sub;
+                            hw = hq;
+                            gen_done = true;
+                        } else if (qsplit && sub < 3 && tt == NT - 1) {
+                            q3part(sub, lo, hi);
+                        }
+                        if (lo >= 0) gen_next(lo, hi, ha, hw);
+                    }
                     if (DF && tt == ftile && j > 0) {
                         // the previous unit's fold after this unit's tile 1, 3
                         // for column quarter 0 (its reduce: warps 2-3)
