@@ -806,8 +806,12 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                     v[4 * h + 3] = ld ? oh4(x.w, lrep) : 0u;
                 }
                 // (.sync.aligned: the warp must be converged -- the compiler
-                // does not know the asm requires it)
-                __syncwarp();
+                // does not know the asm requires it; CSM: the loop body has no
+                // per-lane branch)
+#ifndef HG_GEN_SYNC
+#define HG_GEN_SYNC 0
+#endif
+                if (HG_GEN_SYNC || !CSM) __syncwarp();
                 st8(tmem + lane_base + (uint32_t)c0, v);
             }
             TRC(tr_role, 25);
