@@ -1130,8 +1130,9 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         gen_done = true;
                     }
                     // cluster ids of the 32 columns i = it*128 + sub*32 + k
+                    // (CSM: a dead row reads staged bytes too; its atomics are skipped)
                     uint4 ca = make_uint4(0, 0, 0, 0), cz = ca;
-                    if (live) {
+                    if (CSM || live) {
                         const uint4* cp = reinterpret_cast<const uint4*>(crow + it * 128 + sub * 32);
                         ca = cp[0];
                         cz = cp[1];
