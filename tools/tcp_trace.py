@@ -85,3 +85,24 @@ for name, ev in (("epi4", roles[1]), ("epi19", roles[2])):
           "gen cready wait", spans(ev, 12, 19), "gen st wait", spans(ev, 25, 13),
           "sync1", spans(ev, 20, 21), "fold", spans(ev, 21, 22), "sync2", spans(ev, 22, 23),
           "reduce", spans(ev, 17, 18), "top", spans(ev, 24, 26))
+
+# per-tile MMA waits of the first two traced slots: accumulator, W stage, A quarters
+tiles, cur = [], None
+for c, t in mma:
+    if c == 1:
+        if cur:
+            tiles.append(cur)
+        cur = {1: t, "A": 0}
+    elif cur is not None:
+        if c == 4:
+            cur[4] = t
+        elif c == 5:
+            cur["A"] += t - cur[4]
+        elif c not in cur:
+            cur[c] = t
+if cur:
+    tiles.append(cur)
+for i, x in enumerate(tiles[u0 * tiles_per_slot:(u0 + 2) * tiles_per_slot]):
+    if 2 in x and 3 in x:
+        print(f"tile {i % tiles_per_slot}: wait acc {x[2] - x[1]}, wait W {x[3] - x[2]}, "
+              f"wait A {x['A']}, issue {x.get(8, x[3]) - x[3]}")
