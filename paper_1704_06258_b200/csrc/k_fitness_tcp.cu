@@ -768,11 +768,11 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
         // (lanes of one individual read the same bytes: L1 broadcasts)
         // the cluster-row buffer of unit j (defer: 3, staged by cp.async)
 // the tile after which column quarter s folds the previous unit (nibble s):
-// quarter 0 generates the next unit's first one-hot quarter at tile 1, so it
-// folds at tile 3, the others at tile 1 (tools/ab_k3.py: 0.1229 vs 0.1249 ms
-// with every quarter at tile 1)
+// quarter 0 generates the next unit's first one-hot quarter after tile 1, so
+// it folds after tile 0, the others after tile 1 (tools/ab_k3.py: tile 3 for
+// quarter 0 0.1137, tile 0 0.1130, every quarter at tile 1 0.1142 ms)
 #ifndef HG_FOLD_TS
-#define HG_FOLD_TS 0x1113
+#define HG_FOLD_TS 0x1110
 #endif
         static_assert((HG_FOLD_TS & 0xcccc) == 0, "the deferred fold runs with >= 4 tiles");
         const int ftile = (HG_FOLD_TS >> (4 * sub)) & 15;
@@ -1191,7 +1191,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         if (lo >= 0) gen_next(lo, hi, ha, hw);
                     }
                     if (DF && tt == ftile && j > 0) {
-                        // the previous unit's fold after this unit's tile 1, 3
+                        // the previous unit's fold after this unit's tile 1, 0
                         // for column quarter 0 (its reduce: warps 2-3)
                         fold_unit(j - 1);
                         TRC(tr_role, 18);
