@@ -1093,6 +1093,13 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
                         tt_gen = (A.P - 1) * T + klast(c, qrb(c, hq));
                     }
                 }
+#ifndef HG_GEN_T0
+#define HG_GEN_T0 2
+#endif
+                // (deferred fold: column quarter 0 folds after tile 0, so its
+                // generation waits until after tile HG_GEN_T0 <= 3: 2, tools/ab_k3.py 0.1116
+                // vs 0.1127 ms at its releasing tile 1)
+                if (DF && HG_GEN_T0 > 0 && sub == 0 && tt_gen < HG_GEN_T0) tt_gen = HG_GEN_T0;
                 for (int tt = 0; tt < NT; ++tt, ++t) {
                     const int d = t & 1;
                     const int pl = A.P == 1 ? 0 : tt / T, it = tt - pl * T;
