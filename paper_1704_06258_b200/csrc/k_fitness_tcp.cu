@@ -811,7 +811,7 @@ k_fitness_tcp(const __grid_constant__ CUtensorMap tmW, PArgs A) {
 #ifndef HG_GEN_SYNC
 #define HG_GEN_SYNC 0
 #endif
-                if (HG_GEN_SYNC || !CSM) __syncwarp();
+                if (HG_GEN_SYNC || !CSM || !DF) __syncwarp();
                 st8(tmem + lane_base + (uint32_t)c0, v);
             }
             TRC(tr_role, 25);
